@@ -1,0 +1,235 @@
+/*
+ * adapmoe.h — C ABI of the B200-native AdapMoE offloaded-MoE decode path.
+ *
+ * The reference (moesim, header-only C++20; `inc/` = /root/reference/proj/include/moesim) exposes
+ * this path as a C++ header API + file formats + CLI flags and has no C ABI/FFI of its own
+ * (SURVEY.md §8(b)).  Every entry point below replaces one reference function or CLI step; the
+ * replaced interface is cited on each declaration.  A C++ facade with the reference's own names
+ * (adapmoe::simulate_trace, adapmoe::dp_allocate, ...) sits above this ABI in
+ * paper_2408_10284_b200/csrc/host/ (C++ headers); the Python mirror is paper_2408_10284_b200/moesim.py.
+ *
+ * Conventions
+ *   - Every call returns an int status in the reference CLI's exit-code classes
+ *     (proj/tools/moesim_main.cpp:26-40) plus MOE_E_DEVICE for CUDA failures; exceptions never
+ *     cross the ABI.  moe_last_error() returns the calling thread's last message.
+ *   - Plain pointers and sizes only.  Arrays are row-major, C-contiguous, host memory unless the
+ *     name says `d_`.  The caller owns every buffer it passes; the engine owns device memory, the
+ *     pinned host expert store, streams, events and its copy thread.
+ *   - An engine handle is re-entrant per handle and must not be shared across threads
+ *     concurrently (inc/simulator.hpp:329 is single-threaded).
+ *   - Functions marked [host] need no GPU; all others need the CUDA device the engine was
+ *     created on and fail with MOE_E_DEVICE (never fall back to CPU) when it is absent.
+ */
+#ifndef ADAPMOE_H
+#define ADAPMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (proj/tools/moesim_main.cpp:26-31) ---------------------------------------- */
+#define MOE_OK 0
+#define MOE_E_USAGE 1        /* std::invalid_argument / std::domain_error / out_of_range  */
+#define MOE_E_IO 2           /* io_error (inc/io.hpp:23)                                   */
+#define MOE_E_FORMAT 3       /* parse_error / schema_error / version_error (inc/io.hpp:28-37) */
+#define MOE_E_VALIDATION 4   /* inputs fail cross-validation (validate_trace, inc/core.hpp:249) */
+#define MOE_E_INFEASIBLE 5   /* infeasible budget / allocation                             */
+#define MOE_E_DEVICE 6       /* CUDA error or no device (extension; the reference has no GPU) */
+#define MOE_E_INTERNAL 7     /* std::logic_error (internal invariant)                     */
+
+/* [host] thread-local message of the last failing call ("" if none) */
+const char* moe_last_error(void);
+/* [host] library version string */
+const char* moe_version(void);
+
+/* ---- value types -------------------------------------------------------------------------- */
+/* ModelSpec (inc/core.hpp:22-37) */
+typedef struct {
+    int32_t num_layers;        /* L */
+    int32_t experts_per_layer; /* N (2..64) */
+    int32_t top_k;             /* K */
+    int32_t hidden_dim;        /* d */
+} moe_model_spec;
+
+/* SimConfig + PolicyFlags (inc/simulator.hpp:26-50) */
+typedef struct {
+    int32_t tile_count_per_expert;
+    int64_t tile_transfer_time;
+    int64_t tile_compute_time;
+    int64_t attention_compute_time;
+    int64_t gate_compute_time;
+    int32_t lookahead_depth; /* 0..3 */
+    int32_t adaptive_gating;
+    int32_t prefetch;
+    int32_t adaptive_cache;
+} moe_sim_config;
+
+/* SimMetrics scalars (inc/simulator.hpp:149-166); per-token/per-layer vectors are separate args */
+typedef struct {
+    int64_t total_latency;
+    int64_t stall_time;
+    int64_t on_demand_loads;
+    int64_t cache_hits;
+    int64_t prefetch_hits;
+    int64_t single_expert_decisions;
+    int64_t experts_activated_total;
+} moe_metrics;
+
+/* TimelineEvent (inc/simulator.hpp:130-141): stream 0=compute 1=comm; kind 0 attention, 1 gate,
+ * 2 expert_compute, 3 tile_compute, 4 tile_transfer. */
+typedef struct {
+    int64_t stream, kind, start, end, token, layer, expert, tile;
+} moe_event;
+
+/* SynthConfig + LayerScales (inc/workload.hpp:14-49) */
+typedef struct {
+    moe_model_spec spec;
+    int32_t tokens;
+    double dirichlet_concentration;
+    double residual_drift;
+    uint64_t gate_seed;
+    uint64_t token_seed;
+    int32_t shared_gates;
+    const double* fisher_scales; /* [L] or NULL (all ones) */
+    const double* drift_scales;  /* [L] or NULL (all ones) */
+} moe_synth_config;
+
+/* ---- [host] policy tools ------------------------------------------------------------------- */
+/* calibrate_threshold (inc/gating.hpp:85-122; CLI `calibrate`, moesim_main.cpp:160):
+ * scores [T][L][N] post-softmax, fisher [L]; writes tau and the realized single ratio. */
+int moe_calibrate_threshold(const moe_model_spec* spec, const double* scores, int32_t tokens,
+                            const double* fisher, double target_single_ratio, double* tau,
+                            double* realized_single_ratio);
+
+/* build_cost_table (inc/cache_model.hpp:189-204): alpha/beta [L] -> table [L][N+1] */
+int moe_build_cost_table(const moe_model_spec* spec, const double* alpha, const double* beta, double* table);
+
+/* dp_allocate (inc/allocator.hpp:66-88; CLI `allocate`, moesim_main.cpp:232): knapsack over the
+ * cost table.  budget is clamped to L*N like the reference; capacities [L]. */
+int moe_dp_allocate(const moe_model_spec* spec, const double* table, int32_t budget, int32_t* capacities,
+                    double* total_cost);
+
+/* uniform_allocation (inc/allocator.hpp:140-153) */
+int moe_uniform_allocation(const moe_model_spec* spec, int32_t budget, int32_t* capacities);
+
+/* expected_cost (inc/cache_model.hpp:71-74) */
+int moe_expected_cost(int32_t t, int32_t n, double alpha, double beta, double* cost);
+
+/* tile_pipeline_latency (inc/simulator.hpp:55-60) */
+int moe_tile_pipeline_latency(int32_t tiles, int64_t transfer, int64_t compute, int64_t* latency);
+
+/* Tick-model policy engine replay over router outputs already computed (by moe_route_trace):
+ * the cache/transfer half of simulate_trace (inc/simulator.hpp:343-468).  decisions [T][L][K]
+ * (-1 padded), predictions [T][L][3][2+K] rows (target, count, experts..., -1 padded).
+ * events may be NULL; *n_events always receives the event count. */
+int moe_replay_policy(const moe_model_spec* spec, int32_t tokens, const int32_t* capacities,
+                      const moe_sim_config* cfg, uint64_t seed, const int32_t* decisions,
+                      const int32_t* decision_single, const int32_t* predictions, moe_metrics* metrics,
+                      int64_t* latency_per_token, int64_t* on_demand_per_layer, moe_event* events,
+                      int64_t events_capacity, int64_t* n_events);
+
+/* ---- device engine ------------------------------------------------------------------------ */
+typedef struct moe_engine* moe_engine_t;
+
+/* Creates the per-GPU engine: streams, events, router workspace.  No weights yet. */
+int moe_engine_create(const moe_model_spec* spec, int32_t device, moe_engine_t* out);
+int moe_engine_destroy(moe_engine_t engine);
+
+/* Upload the per-layer gate matrices (GateMatrix, inc/prefetch.hpp:13-38; io `load_gates`,
+ * inc/io.hpp:227) as row-major fp64 [L][d][N], plus the optional trained first-layer gate
+ * (PredictiveGate, inc/prefetch.hpp:146) [d][N] or NULL. */
+int moe_load_gates(moe_engine_t engine, const double* gates, const double* first_gate);
+
+/* K1 batched router over a whole trace (replaces the reference's per-call GateMatrix::logits +
+ * softmax + top_k + gate_decide_sensitivity inside simulate_trace, inc/simulator.hpp:368-444,
+ * and the stored-score decision at :390-396).  acts [T][L][d] fp64, scores [T][L][N] fp64, fisher
+ * [L].  Writes decisions [T][L][K], decision_single [T][L], perturbation [T][L] (NULL ok) and
+ * predictions [T][L][3][2+K] exactly as simulate_trace would evaluate them. */
+int moe_route_trace(moe_engine_t engine, const double* acts, const double* scores, int32_t tokens,
+                    const double* fisher, double tau, const moe_sim_config* cfg, int32_t* decisions,
+                    int32_t* decision_single, double* perturbation, int32_t* predictions);
+
+/* simulate_trace (inc/simulator.hpp:329-468) with the router on the GPU (K1) and the tick-model
+ * cache/transfer engine on the host.  Bit-exact drop-in for the reference's metrics + timeline. */
+int moe_simulate_trace(moe_engine_t engine, const double* acts, const double* scores, int32_t tokens,
+                       const double* fisher, const int32_t* capacities, double tau, const moe_sim_config* cfg,
+                       uint64_t seed, moe_metrics* metrics, int64_t* latency_per_token,
+                       int64_t* on_demand_per_layer, moe_event* events, int64_t events_capacity,
+                       int64_t* n_events);
+
+/* generate_trace (inc/workload.hpp:60-112): host mt19937_64 stream (bit-identical draws), gate
+ * logits on the GPU via K1 (fp64, reference summation order).  Outputs: gates [L][d][N], acts
+ * [T][L][d], scores [T][L][N], selected [T][L][K], fisher [L]. Also loads the gates into the engine. */
+int moe_generate_trace(moe_engine_t engine, const moe_synth_config* cfg, double* gates, double* acts,
+                       double* scores, int32_t* selected, double* fisher);
+
+/* generate_profiles (inc/workload.hpp:133-181): alpha (single-expert ratio at tau) and beta
+ * (reuse-predict top-1 accuracy) per layer; the T*L reuse GEMVs run batched on the GPU.  Uses the
+ * engine's gates and first-layer gate. */
+int moe_generate_profiles(moe_engine_t engine, const double* acts, const double* scores, int32_t tokens,
+                          const double* fisher, double tau, double* alpha, double* beta);
+
+/* ---- physical offloaded decode (expert FFN + HBM expert cache + copy engine) -------------- */
+/* Expert FFN shape: SwiGLU with ffn_dim F, bf16 weights, F % tiles == 0, tiles = the
+ * SimConfig tile_count_per_expert.  Creates the pinned host expert store (all L*N experts,
+ * tile-major) and fills it with the deterministic counter-based init (same values as the oracle's
+ * orc_expert_init).  host_alias > 0 stores only that many distinct experts and maps
+ * (l, e) -> (l*N + e) % host_alias (for hosts without L*N*expert_bytes of RAM); 0 = all distinct. */
+int moe_experts_init(moe_engine_t engine, int32_t ffn_dim, int32_t tiles, uint64_t seed, int32_t host_alias);
+
+/* Bytes of one expert (3 * F * d * 2) in the store. */
+int moe_expert_bytes(moe_engine_t engine, int64_t* bytes);
+
+/* Copy one expert's tile-major bf16 weights out of the pinned store (for parity tests). */
+int moe_expert_read(moe_engine_t engine, int32_t layer, int32_t expert, uint16_t* out);
+
+/* Begin a decode session: per-layer HBM slot pool sized by `capacities` (the DP allocation) plus
+ * `staging_slots` transfer slots, LRU initial fill from SeededRng(seed) (inc/simulator.hpp:352-360),
+ * fisher [L], tau, config.  total_tokens is the trace length (the last-layer first-gate
+ * prediction needs tok + 1 < T, inc/simulator.hpp:431). staging_slots <= 0 sizes the staging pool
+ * automatically with a logical dry run of the session inputs when those are given to
+ * moe_decode_tokens for the first time. */
+int moe_decode_begin(moe_engine_t engine, const int32_t* capacities, int32_t staging_slots, const double* fisher,
+                     double tau, const moe_sim_config* cfg, uint64_t seed, int32_t total_tokens);
+
+/* Decode `count` tokens (trace-replay: layer l's router/FFN input is the trace activation).
+ * acts [count][L][d] fp64 and scores [count][L][N] fp64 are HOST buffers if inputs_on_device == 0,
+ * else device pointers.  hidden_out [count][L][d] fp32 receives x_l + sum_e w_e * E_e(x_l) per
+ * layer (host buffer, or device if inputs_on_device; NULL skips the readback).  gpu_ms receives
+ * the CUDA-event time of the call on the compute stream. */
+int moe_decode_tokens(moe_engine_t engine, const double* acts, const double* scores, int32_t count,
+                      int32_t inputs_on_device, float* hidden_out, double* gpu_ms);
+
+/* Physical counters of the session so far. */
+typedef struct {
+    int64_t tokens;
+    int64_t kernels_launched;     /* our kernels (router, ffn phases, combine) */
+    int64_t tile_copies;          /* H2D tile copies issued */
+    int64_t h2d_bytes;            /* expert bytes moved host -> HBM */
+    int64_t ffn_bytes;            /* algorithmic expert bytes streamed by the FFN kernels */
+    double copy_busy_ms;          /* sum of tile-copy durations (CUDA events) */
+    double ffn_ms;                /* sum of FFN kernel durations (CUDA events, per launch group) */
+    double router_ms;             /* sum of router kernel durations */
+    double stall_ms;              /* compute-stream time spent waiting on copies (events) */
+    int32_t slots_total;
+    int32_t staging_high_water;
+} moe_decode_stats;
+
+/* End the session: logical metrics/timeline (bit-exact with simulate_trace on the same inputs),
+ * physical stats.  Any pointer may be NULL. */
+int moe_decode_end(moe_engine_t engine, moe_metrics* metrics, int64_t* latency_per_token,
+                   int64_t* on_demand_per_layer, moe_event* events, int64_t events_capacity, int64_t* n_events,
+                   moe_decode_stats* stats);
+
+/* Single-expert SwiGLU (parity/profiling entry): y[d] fp32 = W2 (silu(W1 x) * (W3 x)) for expert
+ * (layer, expert) of the store, x [d] fp64 host buffer, y [d] fp32 host buffer.  Runs the same
+ * K2 passes and tile-order reduction as the decode path. */
+int moe_expert_ffn(moe_engine_t engine, int32_t layer, int32_t expert, const double* x, float* y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADAPMOE_H */

@@ -883,3 +883,13 @@ int orc_swiglu(const uint16_t* w, int D, int F, int tiles, const float* x, doubl
     free(h);
     return 0;
 }
+
+/* FNV-1a over raw bytes (fixture hashing; same as inc/io.hpp:80-87 over a byte string). */
+uint64_t orc_fnv1a(const void* data, size_t n, uint64_t h) {
+    const unsigned char* p = (const unsigned char*)data;
+    for (size_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}

@@ -110,6 +110,10 @@ int orc_expert_init(uint64_t seed, int layer, int expert, int D, int F, int tile
 /* y[D] = W2 (silu(W1 x) * (W3 x)), fp64 accumulation over bf16 weights, x fp32. */
 int orc_swiglu(const uint16_t* w, int D, int F, int tiles, const float* x, double* y);
 
+/* FNV-1a (inc/io.hpp:80-87) over raw bytes, for fixture hashes; start with 0xcbf29ce484222325 */
+#include <stddef.h>
+uint64_t orc_fnv1a(const void* data, size_t n, uint64_t h);
+
 #ifdef __cplusplus
 }
 #endif

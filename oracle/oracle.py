@@ -86,6 +86,8 @@ def _declare(L):
     L.orc_swiglu.argtypes = [_u16, C.c_int, C.c_int, C.c_int, _f, _d]
     L.orc_init_scale.argtypes = [C.c_int]
     L.orc_init_scale.restype = C.c_float
+    L.orc_fnv1a.argtypes = [C.c_void_p, C.c_size_t, C.c_uint64]
+    L.orc_fnv1a.restype = C.c_uint64
 
 
 def _p(a, t):
@@ -94,13 +96,8 @@ def _p(a, t):
 
 def fnv1a(arr: np.ndarray, h: int = 0xcbf29ce484222325) -> str:
     """FNV-1a over the raw little-endian bytes (same hash the reference driver prints)."""
-    data = np.ascontiguousarray(arr).view(np.uint8)
-    # vectorised FNV is awkward; bytes are small enough for a python loop on fixtures only
-    hh = h
-    for b in data.tobytes():
-        hh ^= b
-        hh = (hh * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
-    return f"{hh:016x}"
+    data = np.ascontiguousarray(arr)
+    return f"{lib().orc_fnv1a(data.ctypes.data, data.nbytes, h):016x}"
 
 
 @dataclass

@@ -1,0 +1,473 @@
+// C ABI (include/adapmoe.h) over the C++ engine.  Exceptions are caught at this boundary and
+// turned into the reference CLI's exit-code classes (proj/tools/moesim_main.cpp:26-40, :738-757).
+#include "../../include/adapmoe.h"
+
+#include <cuda_runtime_api.h>
+
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "host/policy.hpp"
+#include "host/policy_engine.hpp"
+#include "runtime/decode.hpp"
+#include "runtime/engine.hpp"
+#include "runtime/experts.hpp"
+#include "kernels/expert_ffn.hpp"
+
+using namespace adapmoe;
+
+struct moe_engine {
+    Engine* impl;
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        g_last_error.clear();
+        f();
+        return MOE_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return static_cast<int>(e.status);
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return MOE_E_USAGE;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return MOE_E_USAGE;
+    }
+}
+
+ModelSpec to_spec(const moe_model_spec* s) {
+    if (!s) fail(Status::Usage, "null model spec");
+    ModelSpec m{s->num_layers, s->experts_per_layer, s->top_k, s->hidden_dim};
+    m.validate();
+    return m;
+}
+
+SimConfig to_cfg(const moe_sim_config* c) {
+    if (!c) fail(Status::Usage, "null sim config");
+    SimConfig s;
+    s.tile_count_per_expert = c->tile_count_per_expert;
+    s.tile_transfer_time = c->tile_transfer_time;
+    s.tile_compute_time = c->tile_compute_time;
+    s.attention_compute_time = c->attention_compute_time;
+    s.gate_compute_time = c->gate_compute_time;
+    s.lookahead_depth = c->lookahead_depth;
+    s.policy = PolicyFlags{c->adaptive_gating != 0, c->prefetch != 0, c->adaptive_cache != 0};
+    s.validate();
+    return s;
+}
+
+Engine& eng(moe_engine_t h) {
+    if (!h || !h->impl) fail(Status::Usage, "null engine handle");
+    return *h->impl;
+}
+
+void require(const void* p, const char* what) {
+    if (!p) fail(Status::Usage, std::string("null pointer: ") + what);
+}
+
+void export_metrics(const SimMetrics& m, moe_metrics* out, int64_t* lat, int64_t* odl) {
+    if (out) {
+        out->total_latency = m.total_latency;
+        out->stall_time = m.stall_time;
+        out->on_demand_loads = m.on_demand_loads;
+        out->cache_hits = m.cache_hits;
+        out->prefetch_hits = m.prefetch_hits;
+        out->single_expert_decisions = m.single_expert_decisions;
+        out->experts_activated_total = m.experts_activated_total;
+    }
+    if (lat) std::memcpy(lat, m.latency_per_token.data(), m.latency_per_token.size() * sizeof(int64_t));
+    if (odl)
+        for (size_t l = 0; l < m.on_demand_loads_per_layer.size(); ++l) odl[l] = m.on_demand_loads_per_layer[l];
+}
+
+void export_events(const std::vector<TimelineEvent>& ev, long long total, moe_event* out, int64_t cap, int64_t* n) {
+    if (n) *n = total;
+    if (!out) return;
+    if (static_cast<int64_t>(ev.size()) > cap) fail(Status::Usage, "events buffer too small (need " + std::to_string(ev.size()) + ")");
+    for (size_t i = 0; i < ev.size(); ++i)
+        out[i] = moe_event{static_cast<int64_t>(ev[i].stream), static_cast<int64_t>(ev[i].kind), ev[i].start, ev[i].end,
+                           ev[i].token, ev[i].layer, ev[i].expert, ev[i].tile};
+}
+
+// Replays router outputs through the logical engine (simulate_trace's cache/transfer half).
+void replay(const ModelSpec& spec, int T, const int32_t* caps, const SimConfig& cfg, uint64_t seed, const int32_t* sel,
+            const int32_t* single, const int32_t* preds, moe_metrics* metrics, int64_t* lat, int64_t* odl,
+            moe_event* events, int64_t cap, int64_t* n_events) {
+    const int L = spec.num_layers, K = spec.top_k, PW = 2 + K;
+    std::vector<int> c(caps, caps + L);
+    Allocation a{c, 0};
+    for (int t : c) a.budget += t;
+    a.validate(spec);
+    PolicyEngine pe(spec, cfg, c, seed, T, nullptr, events != nullptr);
+    RouteDecision d;
+    RoutePrediction p[3];
+    for (int tok = 0; tok < T; ++tok)
+        for (int l = 0; l < L; ++l) {
+            const size_t tl = static_cast<size_t>(tok) * L + l;
+            d.count = 0;
+            for (int k = 0; k < K; ++k) {
+                const int e = sel[tl * K + k];
+                if (e >= 0) d.experts[d.count++] = e;
+            }
+            d.single = single ? single[tl] != 0 : (cfg.policy.adaptive_gating ? d.count == 1 : K == 1);
+            int np = 0;
+            if (preds)
+                for (int s = 0; s < 3; ++s) {
+                    const int32_t* row = preds + (tl * 3 + s) * PW;
+                    if (row[0] < 0) continue;
+                    p[np].target = row[0];
+                    p[np].count = row[1];
+                    for (int k = 0; k < row[1]; ++k) p[np].experts[k] = row[2 + k];
+                    ++np;
+                }
+            pe.step(tok, l, d, std::span<const RoutePrediction>(p, np));
+        }
+    export_metrics(pe.metrics(), metrics, lat, odl);
+    export_events(pe.timeline(), pe.events_recorded(), events, cap, n_events);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* moe_last_error(void) { return g_last_error.c_str(); }
+const char* moe_version(void) { return "adapmoe-b200 0.1.0 (sm_100a)"; }
+
+int moe_calibrate_threshold(const moe_model_spec* spec, const double* scores, int32_t tokens, const double* fisher,
+                            double target, double* tau, double* realized) {
+    return guarded([&] {
+        ModelSpec s = to_spec(spec);
+        require(scores, "scores");
+        require(fisher, "fisher");
+        require(tau, "tau");
+        const size_t n = static_cast<size_t>(tokens > 0 ? tokens : 0) * s.num_layers * s.experts_per_layer;
+        *tau = calibrate_threshold(std::span<const double>(scores, n), tokens, s,
+                                   std::span<const double>(fisher, s.num_layers), target, realized);
+    });
+}
+
+int moe_build_cost_table(const moe_model_spec* spec, const double* alpha, const double* beta, double* table) {
+    return guarded([&] {
+        ModelSpec s = to_spec(spec);
+        require(alpha, "alpha");
+        require(beta, "beta");
+        require(table, "table");
+        for (int l = 0; l < s.num_layers; ++l) LayerProfile{alpha[l], beta[l], 0.0}.validate();
+        auto t = build_cost_table(std::span<const double>(alpha, s.num_layers), std::span<const double>(beta, s.num_layers), s);
+        std::memcpy(table, t.data(), t.size() * sizeof(double));
+    });
+}
+
+int moe_dp_allocate(const moe_model_spec* spec, const double* table, int32_t budget, int32_t* caps, double* total) {
+    return guarded([&] {
+        ModelSpec s = to_spec(spec);
+        require(table, "table");
+        require(caps, "capacities");
+        auto r = dp_allocate(std::span<const double>(table, static_cast<size_t>(s.num_layers) * (s.experts_per_layer + 1)), budget, s);
+        for (int l = 0; l < s.num_layers; ++l) caps[l] = r.allocation.capacities[l];
+        if (total) *total = r.total_cost;
+    });
+}
+
+int moe_uniform_allocation(const moe_model_spec* spec, int32_t budget, int32_t* caps) {
+    return guarded([&] {
+        ModelSpec s = to_spec(spec);
+        require(caps, "capacities");
+        auto a = uniform_allocation(budget, s);
+        for (int l = 0; l < s.num_layers; ++l) caps[l] = a.capacities[l];
+    });
+}
+
+int moe_expected_cost(int32_t t, int32_t n, double alpha, double beta, double* cost) {
+    return guarded([&] {
+        require(cost, "cost");
+        *cost = expected_cost(t, n, alpha, beta);
+    });
+}
+
+int moe_tile_pipeline_latency(int32_t tiles, int64_t transfer, int64_t compute, int64_t* latency) {
+    return guarded([&] {
+        require(latency, "latency");
+        *latency = tile_pipeline_latency(tiles, transfer, compute);
+    });
+}
+
+int moe_replay_policy(const moe_model_spec* spec, int32_t tokens, const int32_t* caps, const moe_sim_config* cfg,
+                      uint64_t seed, const int32_t* decisions, const int32_t* single, const int32_t* predictions,
+                      moe_metrics* metrics, int64_t* lat, int64_t* odl, moe_event* events, int64_t cap,
+                      int64_t* n_events) {
+    return guarded([&] {
+        ModelSpec s = to_spec(spec);
+        SimConfig c = to_cfg(cfg);
+        require(caps, "capacities");
+        require(decisions, "decisions");
+        replay(s, tokens, caps, c, seed, decisions, single, predictions, metrics, lat, odl, events, cap, n_events);
+    });
+}
+
+int moe_engine_create(const moe_model_spec* spec, int32_t device, moe_engine_t* out) {
+    return guarded([&] {
+        require(out, "out");
+        *out = nullptr;
+        ModelSpec s = to_spec(spec);
+        auto* h = new moe_engine{nullptr};
+        try {
+            h->impl = new Engine(s, device);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int moe_engine_destroy(moe_engine_t h) {
+    return guarded([&] {
+        if (!h) return;
+        delete h->impl;
+        delete h;
+    });
+}
+
+int moe_load_gates(moe_engine_t h, const double* gates, const double* first_gate) {
+    return guarded([&] {
+        require(gates, "gates");
+        eng(h).load_gates(gates, first_gate);
+    });
+}
+
+int moe_route_trace(moe_engine_t h, const double* acts, const double* scores, int32_t T, const double* fisher, double tau,
+                    const moe_sim_config* cfg, int32_t* decisions, int32_t* single, double* pert, int32_t* predictions) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        SimConfig c = to_cfg(cfg);
+        require(acts, "acts");
+        require(scores, "scores");
+        require(fisher, "fisher");
+        require(decisions, "decisions");
+        if (T < 1) fail(Status::Validation, "trace holds no tokens");
+        GatingThreshold{tau}.validate();
+        const ModelSpec& s = e.spec();
+        TraceRoutes r = e.route_trace(acts, scores, T, std::span<const double>(fisher, s.num_layers), tau, c);
+        std::memcpy(decisions, r.selected.data(), r.selected.size() * sizeof(int));
+        if (single) std::memcpy(single, r.single.data(), r.single.size() * sizeof(int));
+        if (pert) std::memcpy(pert, r.perturbation.data(), r.perturbation.size() * sizeof(double));
+        if (predictions) std::memcpy(predictions, r.predictions.data(), r.predictions.size() * sizeof(int));
+    });
+}
+
+int moe_simulate_trace(moe_engine_t h, const double* acts, const double* scores, int32_t T, const double* fisher,
+                       const int32_t* caps, double tau, const moe_sim_config* cfg, uint64_t seed, moe_metrics* metrics,
+                       int64_t* lat, int64_t* odl, moe_event* events, int64_t cap, int64_t* n_events) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        SimConfig c = to_cfg(cfg);
+        require(acts, "acts");
+        require(scores, "scores");
+        require(fisher, "fisher");
+        require(caps, "capacities");
+        if (T < 1) fail(Status::Validation, "trace holds no tokens");
+        GatingThreshold{tau}.validate();
+        const ModelSpec& s = e.spec();
+        TraceRoutes r = e.route_trace(acts, scores, T, std::span<const double>(fisher, s.num_layers), tau, c);
+        replay(s, T, caps, c, seed, r.selected.data(), r.single.data(), r.predictions.data(), metrics, lat, odl, events,
+               cap, n_events);
+    });
+}
+
+int moe_generate_trace(moe_engine_t h, const moe_synth_config* cfg, double* gates, double* acts, double* scores,
+                       int32_t* selected, double* fisher) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(cfg, "config");
+        ModelSpec s = to_spec(&cfg->spec);
+        if (!(s == e.spec())) fail(Status::Validation, "generate_trace: spec differs from the engine's");
+        require(gates, "gates");
+        require(acts, "acts");
+        require(scores, "scores");
+        require(selected, "selected");
+        require(fisher, "fisher");
+        e.generate_trace(cfg->tokens, cfg->dirichlet_concentration, cfg->residual_drift, cfg->gate_seed, cfg->token_seed,
+                         cfg->shared_gates != 0, cfg->fisher_scales, cfg->drift_scales, gates, acts, scores, selected,
+                         fisher);
+    });
+}
+
+int moe_generate_profiles(moe_engine_t h, const double* acts, const double* scores, int32_t T, const double* fisher,
+                          double tau, double* alpha, double* beta) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(acts, "acts");
+        require(scores, "scores");
+        require(fisher, "fisher");
+        require(alpha, "alpha");
+        require(beta, "beta");
+        GatingThreshold{tau}.validate();
+        e.generate_profiles(acts, scores, T, std::span<const double>(fisher, e.spec().num_layers), tau, alpha, beta);
+    });
+}
+
+}  // extern "C"
+
+// ---- physical decode ------------------------------------------------------------------------
+extern "C" {
+
+int moe_experts_init(moe_engine_t h, int32_t ffn, int32_t tiles, uint64_t seed, int32_t alias) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        e.session.reset();
+        e.experts = std::make_unique<ExpertStore>();
+        try {
+            build_expert_store(e, *e.experts, ffn, tiles, seed, alias);
+        } catch (...) {
+            e.experts.reset();
+            throw;
+        }
+    });
+}
+
+int moe_expert_bytes(moe_engine_t h, int64_t* bytes) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(bytes, "bytes");
+        if (!e.experts) fail(Status::Usage, "experts not initialised");
+        *bytes = static_cast<int64_t>(e.experts->expert_bytes);
+    });
+}
+
+int moe_expert_read(moe_engine_t h, int32_t layer, int32_t expert, uint16_t* out) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(out, "out");
+        if (!e.experts) fail(Status::Usage, "experts not initialised");
+        const ModelSpec& s = e.spec();
+        if (layer < 0 || layer >= s.num_layers || expert < 0 || expert >= s.experts_per_layer)
+            fail(Status::Usage, "ExpertRef out of range");
+        std::memcpy(out, e.experts->expert(layer, expert), e.experts->expert_bytes);
+    });
+}
+
+int moe_decode_begin(moe_engine_t h, const int32_t* caps, int32_t staging, const double* fisher, double tau,
+                     const moe_sim_config* cfg, uint64_t seed, int32_t total_tokens) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        SimConfig c = to_cfg(cfg);
+        require(caps, "capacities");
+        require(fisher, "fisher");
+        GatingThreshold{tau}.validate();
+        if (!e.experts) fail(Status::Usage, "decode_begin: call moe_experts_init first");
+        const int L = e.spec().num_layers;
+        e.session.reset();
+        e.session = std::make_unique<DecodeSession>(e, std::span<const int>(caps, L), staging,
+                                                    std::span<const double>(fisher, L), tau, c, seed, total_tokens);
+    });
+}
+
+int moe_decode_tokens(moe_engine_t h, const double* acts, const double* scores, int32_t count, int32_t on_device,
+                      float* hidden_out, double* gpu_ms) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(acts, "acts");
+        require(scores, "scores");
+        if (!e.session) fail(Status::Usage, "decode_tokens: no session (call moe_decode_begin)");
+        const double ms = e.session->decode(acts, scores, count, on_device != 0, hidden_out);
+        if (gpu_ms) *gpu_ms = ms;
+    });
+}
+
+int moe_decode_end(moe_engine_t h, moe_metrics* metrics, int64_t* lat, int64_t* odl, moe_event* events, int64_t cap,
+                   int64_t* n_events, moe_decode_stats* stats) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        if (!e.session) fail(Status::Usage, "decode_end: no session");
+        DecodeStats s = e.session->finish();
+        const PolicyEngine& pe = e.session->policy();
+        export_metrics(pe.metrics(), metrics, lat, odl);
+        export_events(pe.timeline(), pe.events_recorded(), events, cap, n_events);
+        if (stats) {
+            stats->tokens = s.tokens;
+            stats->kernels_launched = s.kernels;
+            stats->tile_copies = s.tile_copies;
+            stats->h2d_bytes = s.h2d_bytes;
+            stats->ffn_bytes = s.ffn_bytes;
+            stats->copy_busy_ms = s.copy_busy_ms;
+            stats->ffn_ms = s.ffn_ms;
+            stats->router_ms = s.router_ms;
+            stats->stall_ms = s.stall_ms;
+            stats->slots_total = s.slots_total;
+            stats->staging_high_water = s.staging_high_water;
+        }
+        e.session.reset();
+    });
+}
+
+int moe_expert_ffn(moe_engine_t h, int32_t layer, int32_t expert, const double* x, float* y) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(x, "x");
+        require(y, "y");
+        if (!e.experts) fail(Status::Usage, "experts not initialised");
+        const ModelSpec& s = e.spec();
+        if (layer < 0 || layer >= s.num_layers || expert < 0 || expert >= s.experts_per_layer)
+            fail(Status::Usage, "ExpertRef out of range");
+        e.activate();
+        const ExpertStore& st = *e.experts;
+        const int D = s.hidden_dim, T = st.tiles, F = st.ffn, Ft = F / T;
+        DeviceBuffer w, dx, dh, dy, dout, zero;
+        w.reserve(st.expert_bytes);
+        dx.reserve(D * sizeof(double));
+        dh.reserve(F * sizeof(float));
+        dy.reserve(static_cast<size_t>(T) * D * sizeof(float));
+        dout.reserve(D * sizeof(float));
+        zero.reserve(D * sizeof(double));
+        cudaStream_t cs = e.compute_stream();
+        MOE_CUDA(cudaMemcpyAsync(w.ptr, st.expert(layer, expert), st.expert_bytes, cudaMemcpyHostToDevice, cs));
+        MOE_CUDA(cudaMemcpyAsync(dx.ptr, x, D * sizeof(double), cudaMemcpyHostToDevice, cs));
+        MOE_CUDA(cudaMemsetAsync(zero.ptr, 0, D * sizeof(double), cs));
+        const size_t gate_up = static_cast<size_t>(2) * Ft * D * 2;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e.device());
+        FfnLaunch pa, pb;
+        pa.cols = D;
+        pa.swiglu = 1;
+        pa.x = dx.as<double>();
+        pb.cols = Ft;
+        for (int t = 0; t < T; ++t) {
+            const unsigned char* tile = w.as<unsigned char>() + t * st.tile_bytes;
+            FfnSegment a, b;
+            a.rows = reinterpret_cast<const std::uint16_t*>(tile);
+            a.out = dh.as<float>() + static_cast<size_t>(t) * Ft;
+            a.rows_count = 2 * Ft;
+            b.rows = reinterpret_cast<const std::uint16_t*>(tile + gate_up);
+            b.vec = a.out;
+            b.out = dy.as<float>() + static_cast<size_t>(t) * D;
+            b.rows_count = D;
+            pa.seg[pa.n_seg++] = a;
+            pb.seg[pb.n_seg++] = b;
+        }
+        MOE_CUDA(launch_ffn_pass(pa, sms, cs));
+        MOE_CUDA(launch_ffn_pass(pb, sms, cs));
+        CombineArgs c;
+        c.x = zero.as<double>();
+        c.scores = zero.as<double>();  // single rank: weight 1
+        c.y = dy.as<float>();
+        c.out = dout.as<float>();
+        c.ranks = 1;
+        c.tiles = T;
+        c.d = D;
+        c.experts[0] = 0;
+        MOE_CUDA(launch_combine(c, cs));
+        MOE_CUDA(cudaMemcpyAsync(y, dout.ptr, D * sizeof(float), cudaMemcpyDeviceToHost, cs));
+        MOE_CUDA(cudaStreamSynchronize(cs));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,58 @@
+// K1 — fused router + reuse-based pre-gate (host launch interface).
+//
+// One "group" = one activation vector x (fp64, [d]) and up to kMaxRouteItems routing items that
+// read it: the actual decision for layer l (from the stored trace scores, or from logits of
+// layer l's gate) plus the look-ahead predictions (x . W_{l+1..l+k}, or the first-layer gate at the
+// last layer).  Each item writes its selected experts (score-descending, -1 padded to K), the
+// count, the single-expert flag and the sensitivity perturbation; optionally its full score vector.
+#pragma once
+
+#include <cuda_runtime_api.h>
+
+#include <cstdint>
+
+namespace adapmoe {
+
+constexpr int kMaxRouteItems = 4;
+
+enum RouteFlags : int {
+    kRouteAdaptive = 1,     // sensitivity gate (inc/gating.hpp:56-64) instead of plain top-K
+    kRouteDivConc = 2,      // logits /= concentration before softmax (inc/workload.hpp:94)
+    kRouteEmitScores = 4,   // write the post-softmax scores
+    kRouteEmitLogits = 8,   // write the raw fp64 logits to `scores` and skip the decision (the
+                            // caller applies glibc exp: used where stored score bits must match)
+};
+
+struct RouteItem {
+    const double* gate = nullptr;    // [d][N] fp64; nullptr => decide from `scores`
+    const double* scores = nullptr;  // [N] stored post-softmax scores (gate == nullptr)
+    double fisher = 0.0;
+    int flags = 0;
+    int out = 0;                     // output row
+};
+
+struct RouteGroup {
+    const double* x = nullptr;
+    int n_items = 0;
+    RouteItem items[kMaxRouteItems];
+};
+
+struct RouteOutputs {
+    int* selected = nullptr;       // [rows][K]
+    int* count = nullptr;          // [rows]
+    int* single = nullptr;         // [rows]
+    double* perturbation = nullptr;  // [rows] (may be null)
+    double* scores = nullptr;      // [rows][N] (may be null; written for kRouteEmitScores items)
+};
+
+struct RouteParams {
+    int d = 0, n = 0, k = 0;
+    double tau = 0.0;
+    double concentration = 1.0;
+};
+
+// Launch K1 over `n_groups` groups already resident in device memory.
+cudaError_t launch_route(const RouteGroup* d_groups, int n_groups, int max_gate_items, const RouteParams& p,
+                         const RouteOutputs& out, cudaStream_t stream);
+
+}  // namespace adapmoe

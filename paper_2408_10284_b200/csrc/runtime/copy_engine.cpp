@@ -1,0 +1,197 @@
+#include "copy_engine.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "../host/policy.hpp"
+
+namespace adapmoe {
+
+namespace {
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(Status::Device, std::string(what) + ": " + cudaGetErrorString(e));
+}
+}  // namespace
+
+CopyEngine::CopyEngine(cudaStream_t stream, int device) : stream_(stream), device_(device) {
+    thread_ = std::thread([this] { loop(); });
+}
+
+CopyEngine::~CopyEngine() {
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        stop_ = true;
+    }
+    cv_work_.notify_all();
+    if (thread_.joinable()) thread_.join();
+    cudaSetDevice(device_);
+    cudaStreamSynchronize(stream_);
+    for (auto& j : active_) retire(j);
+    for (cudaEvent_t e : inflight_) cudaEventDestroy(e);
+    for (cudaEvent_t e : free_sync_) cudaEventDestroy(e);
+    for (cudaEvent_t e : free_timing_) cudaEventDestroy(e);
+}
+
+cudaEvent_t CopyEngine::take_event(bool timing) {
+    std::vector<cudaEvent_t>& pool = timing ? free_timing_ : free_sync_;
+    if (!pool.empty()) {
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    check(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming), "cudaEventCreate");
+    return e;
+}
+
+std::shared_ptr<CopyJob> CopyEngine::make_job(unsigned char* dst, const unsigned char* src, size_t tile_bytes, int tiles) {
+    auto j = std::make_shared<CopyJob>();
+    j->dst = dst;
+    j->src = src;
+    j->tile_bytes = tile_bytes;
+    j->tiles = tiles;
+    std::lock_guard<std::mutex> g(mu_);
+    for (int t = 0; t < tiles; ++t) {
+        j->done.push_back(take_event(false));
+        j->t_start.push_back(take_event(true));
+        j->t_end.push_back(take_event(true));
+    }
+    active_.push_back(j);
+    return j;
+}
+
+void CopyEngine::submit(const std::shared_ptr<CopyJob>& job, bool on_demand) {
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        job->on_demand = on_demand;
+        job->queued = true;
+        (on_demand ? od_ : pf_).push_back(job);
+    }
+    cv_work_.notify_one();
+}
+
+void CopyEngine::promote(const std::shared_ptr<CopyJob>& job, bool to_front) {
+    std::lock_guard<std::mutex> g(mu_);
+    if (!job->queued) return;
+    auto it = std::find(pf_.begin(), pf_.end(), job);
+    if (it != pf_.end()) {
+        pf_.erase(it);
+    } else {
+        if (!to_front) return;
+        auto jt = std::find(od_.begin(), od_.end(), job);
+        if (jt != od_.end()) od_.erase(jt);
+    }
+    job->on_demand = true;
+    if (to_front)
+        od_.push_front(job);
+    else
+        od_.push_back(job);
+}
+
+void CopyEngine::cancel(const std::shared_ptr<CopyJob>& job) {
+    std::lock_guard<std::mutex> g(mu_);
+    job->cancelled = true;
+    if (job->queued) {
+        auto& q = job->on_demand ? od_ : pf_;
+        auto it = std::find(q.begin(), q.end(), job);
+        if (it != q.end()) q.erase(it);
+        job->queued = false;
+    }
+    cv_issued_.notify_all();
+}
+
+cudaEvent_t CopyEngine::wait_issued(const std::shared_ptr<CopyJob>& job, int tile) {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_issued_.wait(lk, [&] { return job->issued_tiles > tile || (job->cancelled && job->next_tile <= tile) || stop_; });
+    if (job->issued_tiles <= tile) fail(Status::Internal, "copy engine: waited on a tile that will never be copied");
+    return job->done[tile];
+}
+
+bool CopyEngine::fully_issued(const std::shared_ptr<CopyJob>& job) {
+    std::lock_guard<std::mutex> g(mu_);
+    return job->issued_tiles == job->tiles;
+}
+
+void CopyEngine::drain() {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_issued_.wait(lk, [&] { return (od_.empty() && pf_.empty() && !busy_) || stop_; });
+    lk.unlock();
+    check(cudaStreamSynchronize(stream_), "copy stream sync");
+}
+
+double CopyEngine::busy_ms() {
+    std::lock_guard<std::mutex> g(mu_);
+    return busy_ms_;
+}
+
+void CopyEngine::retire(const std::shared_ptr<CopyJob>& job) {
+    std::lock_guard<std::mutex> g(mu_);
+    for (int t = 0; t < job->issued_tiles; ++t) {
+        if (cudaEventSynchronize(job->t_end[t]) == cudaSuccess) {
+            float ms = 0.0f;
+            if (cudaEventElapsedTime(&ms, job->t_start[t], job->t_end[t]) == cudaSuccess) busy_ms_ += ms;
+        }
+    }
+    for (cudaEvent_t e : job->done) free_sync_.push_back(e);
+    for (cudaEvent_t e : job->t_start) free_timing_.push_back(e);
+    for (cudaEvent_t e : job->t_end) free_timing_.push_back(e);
+    job->done.clear();
+    job->t_start.clear();
+    job->t_end.clear();
+    auto it = std::find(active_.begin(), active_.end(), job);
+    if (it != active_.end()) active_.erase(it);
+}
+
+void CopyEngine::loop() {
+    cudaSetDevice(device_);
+    for (;;) {
+        std::shared_ptr<CopyJob> job;
+        int tile = 0;
+        {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_work_.wait(lk, [&] { return stop_ || !od_.empty() || !pf_.empty(); });
+            if (stop_) return;
+            auto& q = !od_.empty() ? od_ : pf_;
+            job = q.front();
+            tile = job->next_tile++;
+            if (job->next_tile == job->tiles) {
+                q.pop_front();
+                job->queued = false;
+            }
+            busy_ = true;
+        }
+        cudaEventRecord(job->t_start[tile], stream_);
+        const size_t base = static_cast<size_t>(tile) * job->tile_bytes;
+        for (size_t off = 0; off < job->tile_bytes; off += kChunkBytes) {
+            while (static_cast<int>(inflight_.size()) >= kWindow) {
+                cudaEventSynchronize(inflight_.front());
+                std::lock_guard<std::mutex> g(mu_);
+                free_sync_.push_back(inflight_.front());
+                inflight_.pop_front();
+            }
+            const size_t n = std::min(kChunkBytes, job->tile_bytes - off);
+            cudaMemcpyAsync(job->dst + base + off, job->src + base + off, n, cudaMemcpyHostToDevice, stream_);
+            cudaEvent_t e;
+            {
+                std::lock_guard<std::mutex> g(mu_);
+                e = take_event(false);
+            }
+            cudaEventRecord(e, stream_);
+            inflight_.push_back(e);
+        }
+        cudaEventRecord(job->done[tile], stream_);
+        cudaEventRecord(job->t_end[tile], stream_);
+        tiles_copied_ += 1;
+        bytes_copied_ += static_cast<long long>(job->tile_bytes);
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            job->issued_tiles = tile + 1;
+            busy_ = false;
+        }
+        cv_issued_.notify_all();
+    }
+}
+
+}  // namespace adapmoe

@@ -1,0 +1,81 @@
+// Physical transfer channel: host -> HBM expert tile copies on one dedicated copy stream, driven
+// by a host thread.  It mirrors the reference CommEngine's rules (inc/simulator.hpp:187-320) in
+// real time: on-demand requests go before queued prefetches, a promoted prefetch moves to the
+// on-demand queue, and work already handed to the DMA engine is never pre-empted.  Copies are
+// issued in <= kChunkBytes pieces with at most kWindow pieces outstanding, so an on-demand
+// request waits behind at most ~kWindow*kChunkBytes of prefetch traffic while the link never
+// idles.  Each tile's completion is a CUDA event the compute stream waits on.
+#pragma once
+
+#include <cuda_runtime_api.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+namespace adapmoe {
+
+struct CopyJob {
+    unsigned char* dst = nullptr;
+    const unsigned char* src = nullptr;
+    size_t tile_bytes = 0;
+    int tiles = 0;
+    bool on_demand = false;
+    // progress (guarded by the engine mutex)
+    int next_tile = 0;      // next tile to hand to the DMA engine
+    int issued_tiles = 0;   // tiles whose completion event has been recorded
+    bool cancelled = false;
+    bool queued = false;
+    std::vector<cudaEvent_t> done;     // per tile, sync events
+    std::vector<cudaEvent_t> t_start;  // per tile, timing
+    std::vector<cudaEvent_t> t_end;
+};
+
+class CopyEngine {
+public:
+    static constexpr size_t kChunkBytes = 32ull << 20;
+    static constexpr int kWindow = 2;
+
+    CopyEngine(cudaStream_t stream, int device);
+    ~CopyEngine();
+
+    std::shared_ptr<CopyJob> make_job(unsigned char* dst, const unsigned char* src, size_t tile_bytes, int tiles);
+    void submit(const std::shared_ptr<CopyJob>& job, bool on_demand);
+    void promote(const std::shared_ptr<CopyJob>& job, bool to_front);
+    // Drop tiles not yet handed to the DMA engine (their data is no longer needed).
+    void cancel(const std::shared_ptr<CopyJob>& job);
+    // Block until `tile` of `job` has been issued; returns its completion event.
+    cudaEvent_t wait_issued(const std::shared_ptr<CopyJob>& job, int tile);
+    bool fully_issued(const std::shared_ptr<CopyJob>& job);
+    void drain();  // wait for the queues and the stream to empty
+
+    long long tiles_copied() const { return tiles_copied_.load(); }
+    long long bytes_copied() const { return bytes_copied_.load(); }
+    double busy_ms();  // sum of per-tile copy durations of finished jobs
+    void retire(const std::shared_ptr<CopyJob>& job);  // accumulate timing + recycle events
+
+private:
+    void loop();
+    cudaEvent_t take_event(bool timing);
+
+    cudaStream_t stream_;
+    int device_;
+    std::mutex mu_;
+    std::condition_variable cv_work_, cv_issued_;
+    std::deque<std::shared_ptr<CopyJob>> od_, pf_;
+    std::deque<cudaEvent_t> inflight_;
+    std::vector<cudaEvent_t> free_sync_, free_timing_;
+    std::vector<std::shared_ptr<CopyJob>> active_;
+    bool stop_ = false;
+    bool busy_ = false;
+    std::atomic<long long> tiles_copied_{0}, bytes_copied_{0};
+    double busy_ms_ = 0.0;
+    std::thread thread_;
+};
+
+}  // namespace adapmoe

@@ -1,0 +1,430 @@
+#include "decode.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+namespace adapmoe {
+
+namespace {
+constexpr size_t kSlotAlign = 2u << 20;
+}
+
+DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int staging_slots,
+                             std::span<const double> fisher, double tau, const SimConfig& cfg, std::uint64_t seed,
+                             int total_tokens)
+    : eng_(eng),
+      spec_(eng.spec()),
+      cfg_(cfg),
+      caps_(capacities.begin(), capacities.end()),
+      fisher_(fisher.begin(), fisher.end()),
+      tau_(tau),
+      total_tokens_(total_tokens),
+      store_(*eng.experts) {
+    eng.activate();
+    cfg_.validate();
+    const int L = spec_.num_layers, N = spec_.experts_per_layer, K = spec_.top_k, D = spec_.hidden_dim;
+    if (static_cast<int>(caps_.size()) != L || static_cast<int>(fisher_.size()) != L)
+        fail(Status::Usage, "decode_begin: capacities/fisher must have num_layers entries");
+    if (store_.tiles != cfg_.tile_count_per_expert)
+        fail(Status::Usage, "decode_begin: SimConfig tile count differs from the expert store's tile layout");
+    if (total_tokens < 1) fail(Status::Usage, "decode_begin: total_tokens must be >= 1");
+    if (K > 8) fail(Status::Usage, "decode: top_k > 8 unsupported by the combine kernel");
+    const bool prefetch_on = cfg_.policy.prefetch && cfg_.lookahead_depth > 0;
+    if (prefetch_on && !eng.has_gates()) fail(Status::Usage, "decode: prefetching requires the gate matrices");
+    int resident = 0;
+    for (int c : caps_) {
+        if (c < 0 || c > N) fail(Status::Usage, "decode_begin: capacity out of [0, N]");
+        resident += c;
+    }
+    int staging = staging_slots > 0 ? staging_slots : std::min(32, L * N + K);
+    n_slots_ = resident + staging;
+    stats_.slots_total = n_slots_;
+    slot_stride_ = (store_.expert_bytes + kSlotAlign - 1) / kSlotAlign * kSlotAlign;
+    pool_.reserve(slot_stride_ * n_slots_);
+    slots_.resize(n_slots_);
+    for (int s = 0; s < n_slots_; ++s) free_.push_back(s);
+    slot_of_.assign(static_cast<size_t>(L) * N, -1);
+    cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, eng.device());
+
+    d_h_.reserve(static_cast<size_t>(K) * store_.ffn * sizeof(float));
+    d_y_.reserve(static_cast<size_t>(K) * store_.tiles * D * sizeof(float));
+    MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_route_), 64 * 4 * sizeof(int), cudaHostAllocMapped));
+    MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_route_), h_route_, 0));
+    MOE_CUDA(cudaEventCreateWithFlags(&route_done_, cudaEventDisableTiming));
+    copier_ = std::make_unique<CopyEngine>(eng.copy_stream(), eng.device());
+    // last: the constructor performs the initial fill through on_insert
+    policy_ = std::make_unique<PolicyEngine>(spec_, cfg_, caps_, seed, total_tokens, this, true);
+    MOE_CUDA(cudaDeviceSynchronize());
+}
+
+DecodeSession::~DecodeSession() {
+    copier_.reset();
+    if (h_route_) cudaFreeHost(h_route_);
+    if (route_done_) cudaEventDestroy(route_done_);
+    for (auto& p : pass_events_) {
+        cudaEventDestroy(p.e0);
+        cudaEventDestroy(p.e1);
+    }
+    for (auto& p : router_events_) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    for (auto& p : stall_events_) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    for (cudaEvent_t e : timing_pool_) cudaEventDestroy(e);
+}
+
+cudaEvent_t DecodeSession::take_timing() {
+    if (!timing_pool_.empty()) {
+        cudaEvent_t e = timing_pool_.back();
+        timing_pool_.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    MOE_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+int DecodeSession::take_slot() {
+    if (free_.empty())
+        fail(Status::Infeasible, "decode: HBM slot pool exhausted (" + std::to_string(n_slots_) +
+                                     " slots); pass a larger staging_slots to moe_decode_begin");
+    const int s = free_.front();
+    free_.pop_front();
+    const int in_use = n_slots_ - static_cast<int>(free_.size());
+    int resident = 0;
+    for (int c : caps_) resident += c;
+    stats_.staging_high_water = std::max(stats_.staging_high_water, in_use - resident);
+    return s;
+}
+
+void DecodeSession::release_slot(int s) { pending_free_.emplace_back(layer_seq_, s); }
+
+// Called when every FFN launch of layers < layer_seq_ has completed (after the router sync).
+void DecodeSession::release_pending(bool all) {
+    auto it = std::stable_partition(pending_free_.begin(), pending_free_.end(),
+                                    [&](const auto& p) { return !(all || p.first < layer_seq_); });
+    for (auto jt = it; jt != pending_free_.end(); ++jt) {
+        Slot& sl = slots_[jt->second];
+        if (sl.fill) {
+            copier_->cancel(sl.fill);  // an unused prefetch may still be queued: drop what is not issued
+            retiring_.push_back(sl.fill);
+        }
+        sl.fill.reset();
+        sl.fill_done = true;
+        free_.push_back(jt->second);
+    }
+    pending_free_.erase(it, pending_free_.end());
+    // recycle copy jobs whose issued tiles have landed
+    auto done = std::stable_partition(retiring_.begin(), retiring_.end(), [&](const std::shared_ptr<CopyJob>& j) {
+        return !(j->issued_tiles == 0 || cudaEventQuery(j->t_end[j->issued_tiles - 1]) == cudaSuccess);
+    });
+    for (auto jt = done; jt != retiring_.end(); ++jt) copier_->retire(*jt);
+    retiring_.erase(done, retiring_.end());
+}
+
+void DecodeSession::on_request(int id, ExpertRef ref, bool on_demand) {
+    if (id >= static_cast<int>(req_slot_.size())) {
+        req_slot_.resize(id + 1, -1);
+        req_job_.resize(id + 1);
+    }
+    const int s = take_slot();
+    req_slot_[id] = s;
+    auto job = copier_->make_job(slot_ptr(s), store_.expert(ref.layer, ref.expert), store_.tile_bytes, store_.tiles);
+    slots_[s].fill = job;
+    slots_[s].fill_done = false;
+    req_job_[id] = job;
+    copier_->submit(job, on_demand);
+}
+
+void DecodeSession::on_promote(int id) { copier_->promote(req_job_[id], false); }
+
+void DecodeSession::on_insert(ExpertRef ref, int request, std::optional<int> evicted) {
+    const int N = spec_.experts_per_layer;
+    const int key = ref.layer * N + ref.expert;
+    if (request < 0) {  // initial residency (session setup, synchronous, untimed)
+        if (evicted) fail(Status::Internal, "initial fill evicted an expert");
+        const int s = take_slot();
+        MOE_CUDA(cudaMemcpy(slot_ptr(s), store_.expert(ref.layer, ref.expert), store_.expert_bytes, cudaMemcpyHostToDevice));
+        slots_[s].fill.reset();
+        slots_[s].fill_done = true;
+        slot_of_[key] = s;
+        return;
+    }
+    const int s = req_slot_[request];
+    if (evicted && *evicted == ref.expert) {  // capacity-0 layer: the copy was transit only
+        release_slot(s);
+    } else {
+        if (slot_of_[key] >= 0) fail(Status::Internal, "insert of an expert that already has a slot");
+        slot_of_[key] = s;
+        if (evicted) {
+            const int vkey = ref.layer * N + *evicted;
+            release_slot(slot_of_[vkey]);
+            slot_of_[vkey] = -1;
+        }
+    }
+    req_slot_[request] = -1;
+}
+
+void DecodeSession::on_resident_compute(int, ExpertRef ref, int rank) {
+    uses_.push_back(Use{rank, slot_of_[ref.layer * spec_.experts_per_layer + ref.expert], false, {}});
+}
+
+void DecodeSession::on_tile_compute(int, ExpertRef, int rank, int tile, int request) {
+    if (uses_.empty() || !uses_.back().missing || uses_.back().rank != rank)
+        uses_.push_back(Use{rank, req_slot_[request], true, {}});
+    uses_.back().tiles.push_back(tile);
+}
+
+void DecodeSession::wait_fill(int slot, int tile) {
+    Slot& sl = slots_[slot];
+    if (!sl.fill || sl.fill_done) return;
+    const int t0 = tile < 0 ? 0 : tile, t1 = tile < 0 ? sl.fill->tiles : tile + 1;
+    cudaStream_t cs = eng_.compute_stream();
+    for (int t = t0; t < t1; ++t) {
+        if (sl.fill->issued_tiles <= t) copier_->promote(sl.fill, true);
+        cudaEvent_t ev = copier_->wait_issued(sl.fill, t);
+        cudaEvent_t a = take_timing(), b = take_timing();
+        cudaEventRecord(a, cs);
+        MOE_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+        cudaEventRecord(b, cs);
+        stall_events_.emplace_back(a, b);
+    }
+    if (tile < 0 || tile == sl.fill->tiles - 1) sl.fill_done = true;
+}
+
+void DecodeSession::timed_pass(const FfnLaunch& p, bool a, double bytes) {
+    cudaStream_t cs = eng_.compute_stream();
+    cudaEvent_t e0 = take_timing(), e1 = take_timing();
+    cudaEventRecord(e0, cs);
+    MOE_CUDA(launch_ffn_pass(p, sm_count_, cs));
+    cudaEventRecord(e1, cs);
+    pass_events_.push_back(PassRec{a, bytes, e0, e1});
+    stats_.kernels += 1;
+}
+
+void DecodeSession::on_layer_done(int, int, const RouteDecision& d) {
+    const int D = spec_.hidden_dim, T = store_.tiles, F = store_.ffn, Ft = F / T;
+    const size_t gate_up_bytes = static_cast<size_t>(2) * Ft * D * 2;
+    float* h = d_h_.as<float>();
+    float* y = d_y_.as<float>();
+    auto seg_a = [&](int slot, int rank, int t) {
+        FfnSegment s;
+        s.rows = reinterpret_cast<const std::uint16_t*>(slot_ptr(slot) + t * store_.tile_bytes);
+        s.out = h + static_cast<size_t>(rank) * F + static_cast<size_t>(t) * Ft;
+        s.rows_count = 2 * Ft;
+        return s;
+    };
+    auto seg_b = [&](int slot, int rank, int t) {
+        FfnSegment s;
+        s.rows = reinterpret_cast<const std::uint16_t*>(slot_ptr(slot) + t * store_.tile_bytes + gate_up_bytes);
+        s.vec = h + static_cast<size_t>(rank) * F + static_cast<size_t>(t) * Ft;
+        s.out = y + (static_cast<size_t>(rank) * T + t) * D;
+        s.rows_count = D;
+        return s;
+    };
+    FfnLaunch pa, pb;
+    pa.cols = D;
+    pa.swiglu = 1;
+    pa.x = cur_x_;
+    pb.cols = Ft;
+    pb.swiglu = 0;
+    double bytes_a = 0, bytes_b = 0;
+    auto flush = [&]() {
+        if (pa.n_seg) timed_pass(pa, true, bytes_a);
+        if (pb.n_seg) timed_pass(pb, false, bytes_b);
+        pa.n_seg = pb.n_seg = 0;
+        bytes_a = bytes_b = 0;
+    };
+    // resident experts: one pass-A and one pass-B launch over all their tiles
+    for (const Use& u : uses_) {
+        if (u.missing) continue;
+        wait_fill(u.slot, -1);
+        for (int t = 0; t < T; ++t) {
+            if (pa.n_seg == kMaxFfnSegments) flush();
+            pa.seg[pa.n_seg++] = seg_a(u.slot, u.rank, t);
+            pb.seg[pb.n_seg++] = seg_b(u.slot, u.rank, t);
+            bytes_a += static_cast<double>(gate_up_bytes);
+            bytes_b += static_cast<double>(store_.tile_bytes - gate_up_bytes);
+        }
+        stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
+    }
+    flush();
+    // on-demand experts: tile by tile as their copies land
+    for (const Use& u : uses_) {
+        if (!u.missing) continue;
+        for (int t : u.tiles) {
+            wait_fill(u.slot, t);
+            pa.seg[pa.n_seg++] = seg_a(u.slot, u.rank, t);
+            pb.seg[pb.n_seg++] = seg_b(u.slot, u.rank, t);
+            bytes_a = static_cast<double>(gate_up_bytes);
+            bytes_b = static_cast<double>(store_.tile_bytes - gate_up_bytes);
+            flush();
+        }
+        stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
+    }
+    CombineArgs c;
+    c.x = cur_x_;
+    c.scores = cur_scores_;
+    c.y = y;
+    c.out = cur_out_;
+    c.ranks = d.count;
+    c.tiles = T;
+    c.d = D;
+    for (int r = 0; r < d.count; ++r) c.experts[r] = d.experts[r];
+    MOE_CUDA(launch_combine(c, eng_.compute_stream()));
+    stats_.kernels += 1;
+    uses_.clear();
+    ++layer_seq_;
+}
+
+double DecodeSession::decode(const double* acts, const double* scores, int count, bool on_device, float* hidden_out) {
+    eng_.activate();
+    const int L = spec_.num_layers, N = spec_.experts_per_layer, K = spec_.top_k, D = spec_.hidden_dim;
+    if (count < 1) return 0.0;
+    if (tokens_done_ + count > total_tokens_) fail(Status::Usage, "decode: more tokens than announced in decode_begin");
+    cudaStream_t cs = eng_.compute_stream();
+    cudaEvent_t t_begin = take_timing(), t_end = take_timing();
+    MOE_CUDA(cudaEventRecord(t_begin, cs));
+    const size_t TL = static_cast<size_t>(count) * L;
+    const double* x_all = acts;
+    const double* s_all = scores;
+    if (!on_device) {
+        d_in_acts_.reserve(TL * D * sizeof(double));
+        d_in_scores_.reserve(TL * N * sizeof(double));
+        MOE_CUDA(cudaMemcpyAsync(d_in_acts_.ptr, acts, TL * D * sizeof(double), cudaMemcpyHostToDevice, cs));
+        MOE_CUDA(cudaMemcpyAsync(d_in_scores_.ptr, scores, TL * N * sizeof(double), cudaMemcpyHostToDevice, cs));
+        stats_.h2d_bytes += static_cast<long long>(TL * (D + N) * sizeof(double));
+        x_all = d_in_acts_.as<double>();
+        s_all = d_in_scores_.as<double>();
+    }
+    d_out_.reserve(TL * D * sizeof(float));
+    float* out_all = (on_device && hidden_out) ? hidden_out : d_out_.as<float>();
+
+    // router groups for every (token, layer) of this call: they depend only on positions
+    const bool prefetch_on = policy_->prefetch_on();
+    h_groups_.reserve(TL * sizeof(RouteGroup));
+    d_groups_.reserve(TL * sizeof(RouteGroup));
+    RouteGroup* hg = h_groups_.as<RouteGroup>();
+    int max_gates = 1;
+    for (int i = 0; i < count; ++i)
+        for (int l = 0; l < L; ++l) {
+            const size_t tl = static_cast<size_t>(i) * L + l;
+            const int tok = tokens_done_ + i;
+            RouteGroup g;
+            g.x = x_all + tl * D;
+            g.n_items = 1;
+            g.items[0].scores = s_all + tl * N;
+            g.items[0].fisher = fisher_[l];
+            g.items[0].flags = cfg_.policy.adaptive_gating ? kRouteAdaptive : 0;
+            g.items[0].out = 0;
+            const int adaptive = cfg_.policy.adaptive_gating ? kRouteAdaptive : 0;
+            if (prefetch_on) {
+                if (l + 1 < L) {
+                    for (int dep = 1; dep <= cfg_.lookahead_depth && l + dep < L; ++dep) {
+                        RouteItem& it = g.items[g.n_items++];
+                        it.gate = eng_.d_gate(l + dep);
+                        it.fisher = fisher_[l + dep];
+                        it.flags = adaptive;
+                        it.out = dep;
+                    }
+                } else if (eng_.has_first_gate() && tok + 1 < total_tokens_) {
+                    RouteItem& it = g.items[g.n_items++];
+                    it.gate = eng_.d_first_gate();
+                    it.fisher = fisher_[0];
+                    it.flags = adaptive;
+                    it.out = 1;
+                }
+            }
+            max_gates = std::max(max_gates, g.n_items - 1);
+            hg[tl] = g;
+        }
+    MOE_CUDA(cudaMemcpyAsync(d_groups_.ptr, hg, TL * sizeof(RouteGroup), cudaMemcpyHostToDevice, cs));
+    RouteParams rp{D, N, K, tau_, 1.0};
+    RouteOutputs ro{d_route_, d_route_ + 4 * K, d_route_ + 4 * K + 4, nullptr, nullptr};
+    const int* sel = h_route_;
+    const int* cnt = h_route_ + 4 * K;
+    const int* sgl = h_route_ + 4 * K + 4;
+
+    std::array<RoutePrediction, 3> preds;
+    for (int i = 0; i < count; ++i) {
+        const int tok = tokens_done_ + i;
+        for (int l = 0; l < L; ++l) {
+            const size_t tl = static_cast<size_t>(i) * L + l;
+            cudaEvent_t r0 = take_timing(), r1 = take_timing();
+            cudaEventRecord(r0, cs);
+            MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + tl, 1, max_gates, rp, ro, cs));
+            cudaEventRecord(r1, cs);
+            router_events_.emplace_back(r0, r1);
+            stats_.kernels += 1;
+            MOE_CUDA(cudaEventRecord(route_done_, cs));
+            MOE_CUDA(cudaEventSynchronize(route_done_));
+            release_pending(false);
+            RouteDecision d;
+            d.count = cnt[0];
+            d.single = sgl[0] != 0;
+            for (int k = 0; k < d.count; ++k) d.experts[k] = sel[k];
+            const RouteGroup& g = hg[tl];
+            int np = 0;
+            for (int it = 1; it < g.n_items; ++it) {
+                RoutePrediction& p = preds[np++];
+                p.target = (l + 1 < L) ? l + it : 0;
+                p.count = cnt[it];
+                for (int k = 0; k < p.count; ++k) p.experts[k] = sel[it * K + k];
+            }
+            cur_x_ = g.x;
+            cur_scores_ = s_all + tl * N;
+            cur_out_ = out_all + tl * D;
+            policy_->step(tok, l, d, std::span<const RoutePrediction>(preds.data(), np));
+        }
+    }
+    if (hidden_out && !on_device)
+        MOE_CUDA(cudaMemcpyAsync(hidden_out, out_all, TL * D * sizeof(float), cudaMemcpyDeviceToHost, cs));
+    MOE_CUDA(cudaEventRecord(t_end, cs));
+    MOE_CUDA(cudaStreamSynchronize(cs));
+    release_pending(true);
+    tokens_done_ += count;
+    stats_.tokens += count;
+    float ms = 0.0f;
+    MOE_CUDA(cudaEventElapsedTime(&ms, t_begin, t_end));
+    timing_pool_.push_back(t_begin);
+    timing_pool_.push_back(t_end);
+    return ms;
+}
+
+DecodeStats DecodeSession::finish() {
+    eng_.activate();
+    copier_->drain();
+    MOE_CUDA(cudaDeviceSynchronize());
+    release_pending(true);
+    for (auto& j : retiring_) copier_->retire(j);
+    retiring_.clear();
+    DecodeStats s = stats_;
+    for (auto& p : pass_events_) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, p.e0, p.e1);
+        s.ffn_ms += ms;
+        (p.a ? s.pass_a : s.pass_b).emplace_back(p.bytes, ms);
+    }
+    for (auto& p : router_events_) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, p.first, p.second);
+        s.router_ms += ms;
+    }
+    for (auto& p : stall_events_) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, p.first, p.second);
+        s.stall_ms += ms;
+    }
+    s.tile_copies = copier_->tiles_copied();
+    s.h2d_bytes += copier_->bytes_copied();
+    s.copy_busy_ms = copier_->busy_ms();
+    return s;
+}
+
+}  // namespace adapmoe

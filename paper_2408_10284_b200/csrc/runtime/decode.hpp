@@ -1,0 +1,125 @@
+// Physical offloaded decode: the HBM expert-slot pool, the copy engine and the per-layer K1 + K2
+// launches, driven by the logical PolicyEngine (host/policy_engine.hpp) as its DecodeListener.
+//
+// Logical -> physical mapping
+//   request enqueued      -> take a free HBM slot, queue its tile copies (od or pf priority)
+//   request promoted      -> move its remaining tiles to the on-demand queue
+//   cache insert          -> the request's slot becomes the expert's resident slot; the evicted
+//                            expert's slot is released once the layer that last read it finished
+//   resident compute      -> SwiGLU over the slot (waits only if its fill is still in flight)
+//   on-demand tile compute-> wait on that tile's copy event, then SwiGLU on that tile
+// The logical engine decides every hit/miss/prefetch/eviction with the reference's tick model, so
+// the event trace is the reference's; wall-clock only changes when things physically happen.
+#pragma once
+
+#include <cuda_runtime_api.h>
+
+#include <memory>
+#include <vector>
+
+#include "../host/policy_engine.hpp"
+#include "../kernels/expert_ffn.hpp"
+#include "../kernels/router.hpp"
+#include "copy_engine.hpp"
+#include "engine.hpp"
+#include "experts.hpp"
+
+namespace adapmoe {
+
+struct DecodeStats {
+    long long tokens = 0, kernels = 0, tile_copies = 0, h2d_bytes = 0, ffn_bytes = 0;
+    double copy_busy_ms = 0, ffn_ms = 0, router_ms = 0, stall_ms = 0;
+    int slots_total = 0, staging_high_water = 0;
+    // per FFN pass launch (bytes, ms) for roofline accounting
+    std::vector<std::pair<double, double>> pass_a, pass_b;
+};
+
+class DecodeSession : public DecodeListener {
+public:
+    DecodeSession(Engine& eng, std::span<const int> capacities, int staging_slots, std::span<const double> fisher,
+                  double tau, const SimConfig& cfg, std::uint64_t seed, int total_tokens);
+    ~DecodeSession() override;
+
+    // acts [count][L][d], scores [count][L][N]: host or device pointers
+    double decode(const double* acts, const double* scores, int count, bool on_device, float* hidden_out);
+
+    const PolicyEngine& policy() const { return *policy_; }
+    DecodeStats finish();
+
+    // DecodeListener
+    void on_request(int id, ExpertRef ref, bool on_demand) override;
+    void on_promote(int id) override;
+    void on_insert(ExpertRef ref, int request, std::optional<int> evicted) override;
+    void on_resident_compute(int token, ExpertRef ref, int rank) override;
+    void on_tile_compute(int token, ExpertRef ref, int rank, int tile, int request) override;
+    void on_layer_done(int token, int layer, const RouteDecision& d) override;
+
+private:
+    struct Slot {
+        std::shared_ptr<CopyJob> fill;  // copy that produced the current contents (null: synchronous)
+        bool fill_done = false;         // known complete (no wait needed)
+    };
+    struct Use {
+        int rank, slot;
+        bool missing;
+        std::vector<int> tiles;  // missing: tiles in compute order
+    };
+    unsigned char* slot_ptr(int s) const { return pool_.as<unsigned char>() + static_cast<size_t>(s) * slot_stride_; }
+    int take_slot();
+    void release_slot(int s);
+    void release_pending(bool all);
+    void wait_fill(int slot, int tile);  // compute stream waits for tile (or all tiles if -1)
+    void timed_pass(const FfnLaunch& p, bool pass_a, double bytes);
+
+    Engine& eng_;
+    ModelSpec spec_;
+    SimConfig cfg_;
+    std::vector<int> caps_;
+    std::vector<double> fisher_;
+    double tau_;
+    int total_tokens_;
+    int tokens_done_ = 0;
+    std::unique_ptr<PolicyEngine> policy_;
+    std::unique_ptr<CopyEngine> copier_;
+    ExpertStore& store_;
+    int sm_count_ = 148;
+
+    // slots
+    DeviceBuffer pool_;
+    size_t slot_stride_ = 0;
+    int n_slots_ = 0;
+    std::vector<Slot> slots_;
+    std::deque<int> free_;
+    std::vector<std::pair<long long, int>> pending_free_;  // (layer sequence, slot)
+    std::vector<std::shared_ptr<CopyJob>> retiring_;      // released fills awaiting event recycling
+    std::vector<int> slot_of_;                             // [L*N] resident expert -> slot
+    std::vector<int> req_slot_;
+    std::vector<std::shared_ptr<CopyJob>> req_job_;
+    long long layer_seq_ = 0;  // global (token, layer) counter of on_layer_done calls
+    int in_use_high_ = 0;
+
+    // per-layer work
+    std::vector<Use> uses_;
+    const double* cur_x_ = nullptr;
+    const double* cur_scores_ = nullptr;
+    float* cur_out_ = nullptr;
+
+    // buffers
+    DeviceBuffer d_in_acts_, d_in_scores_, d_out_, d_h_, d_y_, d_groups_;
+    PinnedBuffer h_groups_;
+    int* h_route_ = nullptr;  // mapped pinned: selected [4][K], count [4], single [4]
+    int* d_route_ = nullptr;
+    cudaEvent_t route_done_ = nullptr;
+    std::vector<cudaEvent_t> timing_pool_;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> router_events_, stall_events_;
+    struct PassRec {
+        bool a;
+        double bytes;
+        cudaEvent_t e0, e1;
+    };
+    std::vector<PassRec> pass_events_;
+    cudaEvent_t take_timing();
+    DecodeStats stats_;
+};
+
+}  // namespace adapmoe

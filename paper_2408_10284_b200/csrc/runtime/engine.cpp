@@ -1,0 +1,331 @@
+// Engine: device-resident gates + K1 router drivers (trace routing, synthetic workload
+// generation, offline alpha/beta profiling).  inc/ = /root/reference/proj/include/moesim.
+#include "engine.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "decode.hpp"
+#include "experts.hpp"
+
+namespace adapmoe {
+
+void DeviceBuffer::reserve(size_t n) {
+    if (n <= bytes) return;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    MOE_CUDA(cudaMalloc(&ptr, n));
+    bytes = n;
+}
+DeviceBuffer::~DeviceBuffer() {
+    if (ptr) cudaFree(ptr);
+}
+void PinnedBuffer::reserve(size_t n) {
+    if (n <= bytes) return;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    MOE_CUDA(cudaMallocHost(&ptr, n));
+    bytes = n;
+}
+PinnedBuffer::~PinnedBuffer() {
+    if (ptr) cudaFreeHost(ptr);
+}
+
+Engine::Engine(const ModelSpec& spec, int device) : spec_(spec), device_(device) {
+    spec_.validate();
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) fail(Status::Device, "no CUDA device available");
+    if (device < 0 || device >= count) fail(Status::Device, "device index out of range");
+    MOE_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    MOE_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) fail(Status::Device, std::string("built for sm_100a (B200); found ") + prop.name);
+    MOE_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
+    MOE_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    session.reset();
+    experts.reset();
+    if (compute_) cudaStreamDestroy(compute_);
+    if (copy_) cudaStreamDestroy(copy_);
+}
+
+void Engine::activate() const { MOE_CUDA(cudaSetDevice(device_)); }
+
+void Engine::load_gates(const double* gates, const double* first_gate) {
+    activate();
+    const size_t one = static_cast<size_t>(spec_.hidden_dim) * spec_.experts_per_layer * sizeof(double);
+    d_gates_.reserve(one * spec_.num_layers);
+    MOE_CUDA(cudaMemcpy(d_gates_.ptr, gates, one * spec_.num_layers, cudaMemcpyHostToDevice));
+    gates_loaded_ = true;
+    first_gate_loaded_ = false;
+    if (first_gate) {
+        d_first_gate_.reserve(one);
+        MOE_CUDA(cudaMemcpy(d_first_gate_.ptr, first_gate, one, cudaMemcpyHostToDevice));
+        first_gate_loaded_ = true;
+    }
+}
+
+void Engine::run_route(const std::vector<RouteGroup>& groups, int rows, int max_gate_items, const RouteParams& p,
+                       TraceRoutes* out, std::vector<double>* scores_out, cudaStream_t stream) {
+    const int K = p.k, N = p.n;
+    d_groups_.reserve(groups.size() * sizeof(RouteGroup));
+    d_out_sel_.reserve(static_cast<size_t>(rows) * K * sizeof(int));
+    d_out_cnt_.reserve(static_cast<size_t>(rows) * sizeof(int));
+    d_out_single_.reserve(static_cast<size_t>(rows) * sizeof(int));
+    d_out_pert_.reserve(static_cast<size_t>(rows) * sizeof(double));
+    if (scores_out) d_out_scores_.reserve(static_cast<size_t>(rows) * N * sizeof(double));
+    MOE_CUDA(cudaMemcpyAsync(d_groups_.ptr, groups.data(), groups.size() * sizeof(RouteGroup), cudaMemcpyHostToDevice, stream));
+    RouteOutputs o{d_out_sel_.as<int>(), d_out_cnt_.as<int>(), d_out_single_.as<int>(), d_out_pert_.as<double>(),
+                   scores_out ? d_out_scores_.as<double>() : nullptr};
+    MOE_CUDA(launch_route(d_groups_.as<RouteGroup>(), static_cast<int>(groups.size()), max_gate_items, p, o, stream));
+    out->selected.resize(static_cast<size_t>(rows) * K);
+    out->count.resize(rows);
+    out->single.resize(rows);
+    out->perturbation.resize(rows);
+    MOE_CUDA(cudaMemcpyAsync(out->selected.data(), o.selected, out->selected.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    MOE_CUDA(cudaMemcpyAsync(out->count.data(), o.count, rows * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    MOE_CUDA(cudaMemcpyAsync(out->single.data(), o.single, rows * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    MOE_CUDA(cudaMemcpyAsync(out->perturbation.data(), o.perturbation, rows * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    if (scores_out) {
+        scores_out->resize(static_cast<size_t>(rows) * N);
+        MOE_CUDA(cudaMemcpyAsync(scores_out->data(), o.scores, scores_out->size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    }
+    MOE_CUDA(cudaStreamSynchronize(stream));
+}
+
+// Evaluation points of simulate_trace (inc/simulator.hpp:390-396 decision, :422-436 look-ahead).
+TraceRoutes Engine::route_trace(const double* acts, const double* scores, int T, std::span<const double> fisher,
+                                double tau, const SimConfig& cfg) {
+    activate();
+    cfg.validate();
+    const int L = spec_.num_layers, N = spec_.experts_per_layer, K = spec_.top_k, D = spec_.hidden_dim;
+    if (static_cast<int>(fisher.size()) != L) fail(Status::Usage, "route_trace: fisher count != num_layers");
+    const bool prefetch_on = cfg.policy.prefetch && cfg.lookahead_depth > 0;
+    if (prefetch_on && !has_gates()) fail(Status::Usage, "simulate_trace: prefetching requires one gate matrix per layer");
+    const size_t TL = static_cast<size_t>(T) * L;
+    d_x_.reserve(TL * D * sizeof(double));
+    d_scores_.reserve(TL * N * sizeof(double));
+    MOE_CUDA(cudaMemcpyAsync(d_x_.ptr, acts, TL * D * sizeof(double), cudaMemcpyHostToDevice, compute_));
+    MOE_CUDA(cudaMemcpyAsync(d_scores_.ptr, scores, TL * N * sizeof(double), cudaMemcpyHostToDevice, compute_));
+
+    std::vector<RouteGroup> groups(TL);
+    int max_gates = 0;
+    for (int tok = 0; tok < T; ++tok)
+        for (int l = 0; l < L; ++l) {
+            const size_t tl = static_cast<size_t>(tok) * L + l;
+            RouteGroup& g = groups[tl];
+            g.x = d_x_.as<double>() + tl * D;
+            g.n_items = 0;
+            RouteItem& dec = g.items[g.n_items++];
+            dec.gate = nullptr;
+            dec.scores = d_scores_.as<double>() + tl * N;
+            dec.fisher = fisher[l];
+            dec.flags = cfg.policy.adaptive_gating ? kRouteAdaptive : 0;
+            dec.out = static_cast<int>(tl * 4);
+            int n_gates = 0;
+            if (prefetch_on) {
+                const int adaptive = cfg.policy.adaptive_gating ? kRouteAdaptive : 0;
+                if (l + 1 < L) {
+                    for (int depth = 1; depth <= cfg.lookahead_depth && l + depth < L; ++depth) {
+                        RouteItem& it = g.items[g.n_items++];
+                        it.gate = d_gate(l + depth);
+                        it.fisher = fisher[l + depth];
+                        it.flags = adaptive;
+                        it.out = static_cast<int>(tl * 4 + depth);
+                        ++n_gates;
+                    }
+                } else if (has_first_gate() && tok + 1 < T) {
+                    RouteItem& it = g.items[g.n_items++];
+                    it.gate = d_first_gate();
+                    it.fisher = fisher[0];
+                    it.flags = adaptive;
+                    it.out = static_cast<int>(tl * 4 + 1);
+                    ++n_gates;
+                }
+            }
+            max_gates = std::max(max_gates, n_gates);
+        }
+    RouteParams p{D, N, K, tau, 1.0};
+    TraceRoutes raw;
+    run_route(groups, static_cast<int>(TL * 4), std::max(max_gates, 1), p, &raw, nullptr, compute_);
+
+    TraceRoutes r;
+    r.selected.resize(TL * K);
+    r.count.resize(TL);
+    r.single.resize(TL);
+    r.perturbation.resize(TL);
+    const int PW = 2 + K;
+    r.predictions.assign(TL * 3 * PW, -1);
+    for (size_t tl = 0; tl < TL; ++tl) {
+        const int row = static_cast<int>(tl * 4);
+        for (int k = 0; k < K; ++k) r.selected[tl * K + k] = raw.selected[static_cast<size_t>(row) * K + k];
+        r.count[tl] = raw.count[row];
+        r.single[tl] = raw.single[row];
+        r.perturbation[tl] = raw.perturbation[row];
+        const RouteGroup& g = groups[tl];
+        for (int s = 0; s < 3; ++s) {
+            int* dst = &r.predictions[(tl * 3 + s) * PW];
+            dst[1] = 0;
+            if (s + 1 < g.n_items) {
+                const int prow = g.items[s + 1].out;
+                const int layer = static_cast<int>(tl % L);
+                dst[0] = (g.items[s + 1].gate == d_first_gate() && layer == L - 1) ? 0 : layer + s + 1;
+                dst[1] = raw.count[prow];
+                for (int k = 0; k < K; ++k) dst[2 + k] = raw.selected[static_cast<size_t>(prow) * K + k];
+            }
+        }
+    }
+    return r;
+}
+
+// inc/workload.hpp:60-112.  The RNG stream is consumed on the host in the reference's order
+// (gates, then per token: x draws, per-layer drift draws); the walk never reads the logits, so
+// all activations are produced first and the T*L gate GEMVs (+ /conc, softmax, top-K) run as
+// one K1 launch.
+void Engine::generate_trace(int T, double conc, double drift, std::uint64_t gate_seed, std::uint64_t token_seed,
+                            bool shared_gates, const double* fisher_scales, const double* drift_scales, double* gates,
+                            double* acts, double* scores, int* selected, double* fisher) {
+    activate();
+    const int L = spec_.num_layers, N = spec_.experts_per_layer, K = spec_.top_k, D = spec_.hidden_dim;
+    if (T < 1) fail(Status::Usage, "SynthConfig: tokens must be >= 1");
+    if (!(conc > 0.0)) fail(Status::Usage, "SynthConfig: dirichlet_concentration must be positive");
+    if (!(drift >= 0.0)) fail(Status::Usage, "SynthConfig: residual_drift must be >= 0");
+    for (int l = 0; l < L; ++l) {
+        if (fisher_scales && !(fisher_scales[l] >= 0.0)) fail(Status::Usage, "SynthConfig: fisher scales must be >= 0");
+        if (drift_scales && !(drift_scales[l] >= 0.0)) fail(Status::Usage, "SynthConfig: drift scales must be >= 0");
+        fisher[l] = fisher_scales ? fisher_scales[l] : 1.0;
+    }
+    const size_t gsz = static_cast<size_t>(D) * N;
+    SeededRng grng(gate_seed);
+    const double wscale = 1.0 / std::sqrt(static_cast<double>(D));
+    for (int l = 0; l < L; ++l) {
+        double* g = gates + l * gsz;
+        if (shared_gates && l > 0) {
+            std::memcpy(g, gates, gsz * sizeof(double));
+            continue;
+        }
+        for (size_t i = 0; i < gsz; ++i) g[i] = wscale * grng.normal();
+    }
+    SeededRng trng(token_seed);
+    std::vector<double> x(D);
+    for (int tok = 0; tok < T; ++tok) {
+        for (double& v : x) v = trng.normal();
+        for (int l = 0; l < L; ++l) {
+            std::memcpy(acts + (static_cast<size_t>(tok) * L + l) * D, x.data(), D * sizeof(double));
+            const double eps = drift * (drift_scales ? drift_scales[l] : 1.0);
+            if (eps > 0.0) {
+                double norm_sq = 0.0;
+                for (double v : x) norm_sq += v * v;
+                const double step = eps * std::sqrt(norm_sq / D);
+                for (double& v : x) v += step * trng.normal();
+            }
+        }
+    }
+    load_gates(gates, nullptr);
+    const size_t TL = static_cast<size_t>(T) * L;
+    d_x_.reserve(TL * D * sizeof(double));
+    MOE_CUDA(cudaMemcpyAsync(d_x_.ptr, acts, TL * D * sizeof(double), cudaMemcpyHostToDevice, compute_));
+    std::vector<RouteGroup> groups(TL);
+    for (size_t tl = 0; tl < TL; ++tl) {
+        RouteGroup& g = groups[tl];
+        g.x = d_x_.as<double>() + tl * D;
+        g.n_items = 1;
+        g.items[0].gate = d_gate(static_cast<int>(tl % L));
+        g.items[0].flags = kRouteEmitLogits;
+        g.items[0].out = static_cast<int>(tl);
+    }
+    RouteParams p{D, N, K, 0.0, conc};
+    TraceRoutes raw;
+    std::vector<double> logits;
+    run_route(groups, static_cast<int>(TL), 1, p, &raw, &logits, compute_);
+    // /conc, softmax and top-K on the host with the same libm exp as the reference, so the stored
+    // score bits (which tau calibration and every later decision read) are the reference's.
+    for (size_t tl = 0; tl < TL; ++tl) {
+        double* lg = logits.data() + tl * N;
+        for (int j = 0; j < N; ++j) lg[j] /= conc;
+        const std::vector<double> sc = softmax(std::span<const double>(lg, N));
+        std::memcpy(scores + tl * N, sc.data(), N * sizeof(double));
+        const std::vector<int> top = top_k_indices(sc, K);
+        std::memcpy(selected + tl * K, top.data(), K * sizeof(int));
+    }
+}
+
+// inc/workload.hpp:133-181: alpha from the sensitivity rule on stored scores; beta = share of
+// tokens whose reuse-predicted top-1 (x_{l-1} . W_l, or the first-layer gate on the previous
+// token's last activation) is inside the adaptive selection.
+void Engine::generate_profiles(const double* acts, const double* scores, int T, std::span<const double> fisher,
+                               double tau, double* alpha, double* beta) {
+    activate();
+    if (T < 1) fail(Status::Usage, "generate_profiles: empty trace set");
+    if (!has_gates()) fail(Status::Usage, "generate_profiles: gates not loaded");
+    const int L = spec_.num_layers, N = spec_.experts_per_layer, K = spec_.top_k, D = spec_.hidden_dim;
+    if (static_cast<int>(fisher.size()) != L) fail(Status::Usage, "generate_profiles: fisher count does not match num_layers");
+    const size_t TL = static_cast<size_t>(T) * L;
+    d_x_.reserve(TL * D * sizeof(double));
+    d_scores_.reserve(TL * N * sizeof(double));
+    MOE_CUDA(cudaMemcpyAsync(d_x_.ptr, acts, TL * D * sizeof(double), cudaMemcpyHostToDevice, compute_));
+    MOE_CUDA(cudaMemcpyAsync(d_scores_.ptr, scores, TL * N * sizeof(double), cudaMemcpyHostToDevice, compute_));
+    // pass 1: adaptive decisions on the stored scores (K wide)
+    std::vector<RouteGroup> dec(TL);
+    for (size_t tl = 0; tl < TL; ++tl) {
+        dec[tl].x = d_x_.as<double>() + tl * D;
+        dec[tl].n_items = 1;
+        dec[tl].items[0].scores = d_scores_.as<double>() + tl * N;
+        dec[tl].items[0].fisher = fisher[tl % L];
+        dec[tl].items[0].flags = kRouteAdaptive;
+        dec[tl].items[0].out = static_cast<int>(tl);
+    }
+    TraceRoutes d;
+    run_route(dec, static_cast<int>(TL), 1, RouteParams{D, N, K, tau, 1.0}, &d, nullptr, compute_);
+    // pass 2: reuse predictions, top-1
+    std::vector<RouteGroup> pre;
+    std::vector<int> where;
+    for (int tok = 0; tok < T; ++tok)
+        for (int l = 0; l < L; ++l) {
+            const double* x = nullptr;
+            const double* gate = nullptr;
+            if (l >= 1) {
+                x = d_x_.as<double>() + (static_cast<size_t>(tok) * L + (l - 1)) * D;
+                gate = d_gate(l);
+            } else if (has_first_gate() && tok >= 1) {
+                x = d_x_.as<double>() + (static_cast<size_t>(tok - 1) * L + (L - 1)) * D;
+                gate = d_first_gate();
+            }
+            if (!gate) continue;
+            RouteGroup g;
+            g.x = x;
+            g.n_items = 1;
+            g.items[0].gate = gate;
+            g.items[0].out = static_cast<int>(pre.size());
+            pre.push_back(g);
+            where.push_back(tok * L + l);
+        }
+    TraceRoutes pr;
+    if (!pre.empty()) run_route(pre, static_cast<int>(pre.size()), 1, RouteParams{D, N, 1, tau, 1.0}, &pr, nullptr, compute_);
+    std::vector<long long> singles(L, 0), hits(L, 0), counted(L, 0);
+    for (size_t tl = 0; tl < TL; ++tl) singles[tl % L] += d.single[tl];
+    for (size_t i = 0; i < pre.size(); ++i) {
+        const int tl = where[i], l = tl % L;
+        const int predicted = pr.selected[i];
+        ++counted[l];
+        for (int k = 0; k < d.count[tl]; ++k)
+            if (d.selected[static_cast<size_t>(tl) * K + k] == predicted) {
+                ++hits[l];
+                break;
+            }
+    }
+    for (int l = 0; l < L; ++l) {
+        alpha[l] = static_cast<double>(singles[l]) / static_cast<double>(T);
+        beta[l] = counted[l] > 0 ? static_cast<double>(hits[l]) / static_cast<double>(counted[l]) : 0.0;
+    }
+}
+
+}  // namespace adapmoe

@@ -1,0 +1,104 @@
+// Per-GPU engine: owns the device copies of the gate matrices, the router workspace, the pinned
+// host expert store and (during a decode session) the HBM slot pool, streams and copy thread.
+#pragma once
+
+#include <cuda_runtime_api.h>
+
+#include <memory>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "../host/policy.hpp"
+#include "../host/policy_engine.hpp"
+#include "../kernels/router.hpp"
+
+namespace adapmoe {
+
+#define MOE_CUDA(expr)                                                                                          \
+    do {                                                                                                        \
+        cudaError_t _e = (expr);                                                                                \
+        if (_e != cudaSuccess)                                                                                  \
+            ::adapmoe::fail(::adapmoe::Status::Device, std::string(#expr) + ": " + cudaGetErrorString(_e));     \
+    } while (0)
+
+// Grow-only device buffer.
+struct DeviceBuffer {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t n);
+    ~DeviceBuffer();
+    template <typename T>
+    T* as() const { return static_cast<T*>(ptr); }
+};
+
+struct PinnedBuffer {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t n);
+    ~PinnedBuffer();
+    template <typename T>
+    T* as() const { return static_cast<T*>(ptr); }
+};
+
+class DecodeSession;  // runtime/decode.hpp
+struct ExpertStore;   // runtime/experts.hpp
+
+// Router outputs of a whole trace, host side.  predictions rows: target, count, experts[K].
+struct TraceRoutes {
+    std::vector<int> selected;    // [T][L][K]
+    std::vector<int> count;       // [T][L]
+    std::vector<int> single;      // [T][L]
+    std::vector<double> perturbation;
+    std::vector<int> predictions;  // [T][L][3][2+K]
+};
+
+class Engine {
+public:
+    Engine(const ModelSpec& spec, int device);
+    ~Engine();
+
+    const ModelSpec& spec() const { return spec_; }
+    int device() const { return device_; }
+    void activate() const;
+
+    void load_gates(const double* gates, const double* first_gate);
+    bool has_gates() const { return d_gates_.ptr != nullptr && gates_loaded_; }
+    bool has_first_gate() const { return first_gate_loaded_; }
+    const double* d_gate(int layer) const { return d_gates_.as<double>() + static_cast<size_t>(layer) * spec_.hidden_dim * spec_.experts_per_layer; }
+    const double* d_first_gate() const { return first_gate_loaded_ ? d_first_gate_.as<double>() : nullptr; }
+
+    // K1 over a whole trace (acts/scores host).  Matches simulate_trace's evaluation points.
+    TraceRoutes route_trace(const double* acts, const double* scores, int tokens, std::span<const double> fisher,
+                            double tau, const SimConfig& cfg);
+
+    // generate_trace with the gate GEMVs on the GPU; returns via the output arrays.
+    void generate_trace(const int tokens, double concentration, double drift, std::uint64_t gate_seed,
+                        std::uint64_t token_seed, bool shared_gates, const double* fisher_scales,
+                        const double* drift_scales, double* gates, double* acts, double* scores, int* selected,
+                        double* fisher);
+
+    void generate_profiles(const double* acts, const double* scores, int tokens, std::span<const double> fisher,
+                           double tau, double* alpha, double* beta);
+
+    // generic: run K1 on device groups with host-visible outputs
+    void run_route(const std::vector<RouteGroup>& groups, int rows, int max_gate_items, const RouteParams& p,
+                   TraceRoutes* out, std::vector<double>* scores_out, cudaStream_t stream);
+
+    cudaStream_t compute_stream() const { return compute_; }
+    cudaStream_t copy_stream() const { return copy_; }
+
+    std::unique_ptr<ExpertStore> experts;
+    std::unique_ptr<DecodeSession> session;
+
+private:
+    ModelSpec spec_;
+    int device_;
+    cudaStream_t compute_ = nullptr, copy_ = nullptr;
+    DeviceBuffer d_gates_, d_first_gate_;
+    bool gates_loaded_ = false, first_gate_loaded_ = false;
+    // router workspace
+    DeviceBuffer d_groups_, d_x_, d_scores_, d_out_sel_, d_out_cnt_, d_out_single_, d_out_pert_, d_out_scores_;
+};
+
+}  // namespace adapmoe

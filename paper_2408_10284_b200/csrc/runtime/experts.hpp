@@ -1,0 +1,32 @@
+// Pinned host expert store: every (layer, expert) SwiGLU weight block, tile-major bf16
+// (kernels/expert_ffn.hpp), page-locked so tile copies run at host-link speed.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+namespace adapmoe {
+
+class Engine;
+
+struct ExpertStore {
+    int layers = 0, experts = 0, d = 0, ffn = 0, tiles = 0, alias = 0;
+    std::uint64_t seed = 0;
+    size_t expert_bytes = 0;  // 3 * F * d * 2
+    size_t tile_bytes = 0;    // expert_bytes / tiles
+    std::vector<unsigned char*> blocks;  // registered host memory, one per stored expert
+    double pin_seconds = 0.0, fill_seconds = 0.0;
+
+    int stored_index(int layer, int expert) const;
+    const unsigned char* expert(int layer, int expert) const { return blocks[stored_index(layer, expert)]; }
+    ~ExpertStore();
+};
+
+// Allocate + pin (parallel first touch + cudaHostRegister) and fill with the deterministic init
+// (GPU init kernel, D2H into the pinned blocks).
+void build_expert_store(Engine& engine, ExpertStore& store, int ffn, int tiles, std::uint64_t seed, int alias);
+
+// Per-matrix init constants shared with the CUDA init kernel and the oracle.
+void expert_init_constants(std::uint64_t seed, int layer, int expert, int d, int ffn, std::uint64_t base[3], float scale[3]);
+
+}  // namespace adapmoe

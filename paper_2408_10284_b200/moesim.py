@@ -1,0 +1,327 @@
+"""Python mirror of the reference moesim API (``inc/`` = /root/reference/proj/include/moesim) over
+the B200 engine's C ABI.  Names and argument meanings follow the reference so call sites read the
+same: ``calibrate_threshold``, ``build_cost_table``, ``dp_allocate``, ``uniform_allocation``,
+``simulate_trace``, ``generate_trace``, ``generate_profiles`` ...  Errors surface as
+:class:`MoeError` carrying the reference CLI exit-code class (proj/tools/moesim_main.cpp:26-40).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import check, load, MoeError  # noqa: F401
+
+EVENT_KINDS = ("attention", "gate", "expert_compute", "tile_compute", "tile_transfer")
+
+
+@dataclass(frozen=True)
+class ModelSpec:                      # inc/core.hpp:22
+    num_layers: int = 1
+    experts_per_layer: int = 8
+    top_k: int = 2
+    hidden_dim: int = 1
+
+    def c(self):
+        return _capi.ModelSpecC(self.num_layers, self.experts_per_layer, self.top_k, self.hidden_dim)
+
+
+@dataclass
+class PolicyFlags:                    # inc/simulator.hpp:26
+    adaptive_gating: bool = False
+    prefetch: bool = False
+    adaptive_cache: bool = False
+
+
+@dataclass
+class SimConfig:                      # inc/simulator.hpp:34 (defaults = CLI defaults, moesim_main.cpp:259-267)
+    tile_count_per_expert: int = 4
+    tile_transfer_time: int = 2
+    tile_compute_time: int = 1
+    attention_compute_time: int = 8
+    gate_compute_time: int = 1
+    lookahead_depth: int = 2
+    policy: PolicyFlags = field(default_factory=lambda: PolicyFlags(True, True, True))
+
+    def c(self):
+        p = self.policy
+        return _capi.SimConfigC(self.tile_count_per_expert, self.tile_transfer_time, self.tile_compute_time,
+                                self.attention_compute_time, self.gate_compute_time, self.lookahead_depth,
+                                int(p.adaptive_gating), int(p.prefetch), int(p.adaptive_cache))
+
+
+@dataclass
+class SynthConfig:                    # inc/workload.hpp:19
+    spec: ModelSpec
+    tokens: int = 1000
+    dirichlet_concentration: float = 1.0
+    residual_drift: float = 0.1
+    gate_seed: int = 1
+    token_seed: int = 2
+    shared_gates: bool = False
+    fisher_scales: list | None = None
+    drift_scales: list | None = None
+
+
+@dataclass
+class Workload:                       # GeneratedWorkload (inc/workload.hpp:51) in array form
+    spec: ModelSpec
+    gates: np.ndarray                 # [L][d][N] fp64
+    acts: np.ndarray                  # [T][L][d] fp64
+    scores: np.ndarray                # [T][L][N] fp64
+    selected: np.ndarray              # [T][L][K] int32
+    fisher: np.ndarray                # [L]
+
+    @property
+    def tokens(self) -> int:
+        return self.acts.shape[0]
+
+
+@dataclass
+class SimResult:                      # SimResult (inc/simulator.hpp:168)
+    metrics: dict
+    latency_per_token: np.ndarray
+    on_demand_loads_per_layer: np.ndarray
+    timeline: np.ndarray | None       # [n_events][8] int64: stream, kind, start, end, token, layer, expert, tile
+    n_events: int = 0
+    stats: dict | None = None
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+# ------------------------------- host tools -------------------------------------------------
+
+def calibrate_threshold(spec: ModelSpec, scores, fisher, target_single_ratio: float):
+    """inc/gating.hpp:85 — returns (tau, realized single ratio)."""
+    scores = _f64(scores)
+    fisher = _f64(fisher)
+    tau = C.c_double()
+    real = C.c_double()
+    T = scores.shape[0] if scores.ndim == 3 else scores.size // (spec.num_layers * spec.experts_per_layer)
+    check(load().moe_calibrate_threshold(C.byref(spec.c()), _p(scores, _capi._d), T, _p(fisher, _capi._d),
+                                         float(target_single_ratio), C.byref(tau), C.byref(real)))
+    return tau.value, real.value
+
+
+def build_cost_table(spec: ModelSpec, alpha, beta) -> np.ndarray:
+    """inc/cache_model.hpp:189 — [L][N+1] expected on-demand loads."""
+    t = np.zeros((spec.num_layers, spec.experts_per_layer + 1))
+    check(load().moe_build_cost_table(C.byref(spec.c()), _p(_f64(alpha), _capi._d), _p(_f64(beta), _capi._d),
+                                      _p(t, _capi._d)))
+    return t
+
+
+def dp_allocate(spec: ModelSpec, table, budget: int):
+    """inc/allocator.hpp:66 — (capacities, total_cost)."""
+    caps = np.zeros(spec.num_layers, dtype=np.int32)
+    cost = C.c_double()
+    check(load().moe_dp_allocate(C.byref(spec.c()), _p(_f64(table), _capi._d), int(budget), _p(caps, _capi._i32),
+                                 C.byref(cost)))
+    return caps, cost.value
+
+
+def uniform_allocation(spec: ModelSpec, budget: int) -> np.ndarray:
+    caps = np.zeros(spec.num_layers, dtype=np.int32)
+    check(load().moe_uniform_allocation(C.byref(spec.c()), int(budget), _p(caps, _capi._i32)))
+    return caps
+
+
+def expected_cost(t: int, n: int, alpha: float, beta: float) -> float:
+    out = C.c_double()
+    check(load().moe_expected_cost(t, n, alpha, beta, C.byref(out)))
+    return out.value
+
+
+def tile_pipeline_latency(tiles: int, transfer: int, compute: int) -> int:
+    out = C.c_int64()
+    check(load().moe_tile_pipeline_latency(tiles, transfer, compute, C.byref(out)))
+    return out.value
+
+
+def _events_buf(spec: ModelSpec, T: int, cfg: SimConfig):
+    per_layer = 2 + spec.top_k * (1 + 2 * cfg.tile_count_per_expert) + 3 * spec.top_k * cfg.tile_count_per_expert
+    cap = T * spec.num_layers * per_layer + 64
+    return (_capi.EventC * cap)(), cap
+
+
+def _events_np(buf, n):
+    arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_int64)), shape=(len(buf) * 8,))
+    return arr[: n * 8].reshape(n, 8).copy()
+
+
+def replay_policy(spec: ModelSpec, caps, cfg: SimConfig, seed: int, decisions, single, predictions,
+                  timeline: bool = True) -> SimResult:
+    """Host tick-model engine (simulate_trace's cache/transfer half) over router outputs."""
+    decisions = _i32(decisions)
+    T = decisions.shape[0]
+    single = None if single is None else _i32(single)
+    predictions = None if predictions is None else _i32(predictions)
+    m = _capi.MetricsC()
+    lat = np.zeros(T, dtype=np.int64)
+    odl = np.zeros(spec.num_layers, dtype=np.int64)
+    n = C.c_int64()
+    buf, cap = _events_buf(spec, T, cfg) if timeline else (None, 0)
+    check(load().moe_replay_policy(C.byref(spec.c()), T, _p(_i32(caps), _capi._i32), C.byref(cfg.c()), seed,
+                                   _p(decisions, _capi._i32), None if single is None else _p(single, _capi._i32),
+                                   None if predictions is None else _p(predictions, _capi._i32), C.byref(m),
+                                   _p(lat, _capi._i64), _p(odl, _capi._i64), buf, cap, C.byref(n)))
+    return SimResult({k: getattr(m, k) for k, _ in _capi.MetricsC._fields_}, lat, odl,
+                     _events_np(buf, n.value) if timeline else None, n.value)
+
+
+# ------------------------------- device engine ----------------------------------------------
+
+class Engine:
+    """One B200 engine (one process per GPU).  Wraps moe_engine_t."""
+
+    def __init__(self, spec: ModelSpec, device: int = 0):
+        self.spec = spec
+        self._h = C.c_void_p()
+        check(load().moe_engine_create(C.byref(spec.c()), device, C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            load().moe_engine_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- routing / simulation ------------------------------------------------------------------
+    def load_gates(self, gates, first_gate=None):
+        g = _f64(gates)
+        fg = None if first_gate is None else _f64(first_gate)
+        check(load().moe_load_gates(self._h, _p(g, _capi._d), None if fg is None else _p(fg, _capi._d)))
+
+    def route_trace(self, acts, scores, fisher, tau, cfg: SimConfig):
+        acts, scores, fisher = _f64(acts), _f64(scores), _f64(fisher)
+        T, L, K = acts.shape[0], self.spec.num_layers, self.spec.top_k
+        dec = np.zeros((T, L, K), dtype=np.int32)
+        single = np.zeros((T, L), dtype=np.int32)
+        pert = np.zeros((T, L))
+        preds = np.zeros((T, L, 3, 2 + K), dtype=np.int32)
+        check(load().moe_route_trace(self._h, _p(acts, _capi._d), _p(scores, _capi._d), T, _p(fisher, _capi._d),
+                                     float(tau), C.byref(cfg.c()), _p(dec, _capi._i32), _p(single, _capi._i32),
+                                     _p(pert, _capi._d), _p(preds, _capi._i32)))
+        return dec, single, pert, preds
+
+    def simulate_trace(self, acts, scores, fisher, caps, tau, cfg: SimConfig, seed: int = 0,
+                       timeline: bool = True) -> SimResult:
+        """inc/simulator.hpp:329 with K1 on the GPU."""
+        acts, scores, fisher = _f64(acts), _f64(scores), _f64(fisher)
+        T = acts.shape[0]
+        m = _capi.MetricsC()
+        lat = np.zeros(T, dtype=np.int64)
+        odl = np.zeros(self.spec.num_layers, dtype=np.int64)
+        n = C.c_int64()
+        buf, cap = _events_buf(self.spec, T, cfg) if timeline else (None, 0)
+        check(load().moe_simulate_trace(self._h, _p(acts, _capi._d), _p(scores, _capi._d), T, _p(fisher, _capi._d),
+                                        _p(_i32(caps), _capi._i32), float(tau), C.byref(cfg.c()), seed, C.byref(m),
+                                        _p(lat, _capi._i64), _p(odl, _capi._i64), buf, cap, C.byref(n)))
+        return SimResult({k: getattr(m, k) for k, _ in _capi.MetricsC._fields_}, lat, odl,
+                         _events_np(buf, n.value) if timeline else None, n.value)
+
+    def generate_trace(self, cfg: SynthConfig) -> Workload:
+        """inc/workload.hpp:60 — host RNG stream + GPU gate GEMVs; also loads the gates."""
+        s = cfg.spec
+        assert s == self.spec
+        L, N, K, D, T = s.num_layers, s.experts_per_layer, s.top_k, s.hidden_dim, cfg.tokens
+        gates = np.zeros((L, D, N))
+        acts = np.zeros((T, L, D))
+        scores = np.zeros((T, L, N))
+        sel = np.zeros((T, L, K), dtype=np.int32)
+        fisher = np.zeros(L)
+        fs = None if cfg.fisher_scales is None else _f64(cfg.fisher_scales)
+        ds = None if cfg.drift_scales is None else _f64(cfg.drift_scales)
+        c = _capi.SynthConfigC(s.c(), T, cfg.dirichlet_concentration, cfg.residual_drift, cfg.gate_seed,
+                               cfg.token_seed, int(cfg.shared_gates),
+                               None if fs is None else _p(fs, _capi._d), None if ds is None else _p(ds, _capi._d))
+        check(load().moe_generate_trace(self._h, C.byref(c), _p(gates, _capi._d), _p(acts, _capi._d),
+                                        _p(scores, _capi._d), _p(sel, _capi._i32), _p(fisher, _capi._d)))
+        return Workload(s, gates, acts, scores, sel, fisher)
+
+    def generate_profiles(self, acts, scores, fisher, tau):
+        """inc/workload.hpp:133 — (alpha, beta) per layer."""
+        acts, scores, fisher = _f64(acts), _f64(scores), _f64(fisher)
+        a = np.zeros(self.spec.num_layers)
+        b = np.zeros(self.spec.num_layers)
+        check(load().moe_generate_profiles(self._h, _p(acts, _capi._d), _p(scores, _capi._d), acts.shape[0],
+                                           _p(fisher, _capi._d), float(tau), _p(a, _capi._d), _p(b, _capi._d)))
+        return a, b
+
+    # -- physical decode -----------------------------------------------------------------------
+    def experts_init(self, ffn_dim: int, tiles: int, seed: int = 0, host_alias: int = 0):
+        check(load().moe_experts_init(self._h, ffn_dim, tiles, seed, host_alias))
+
+    def expert_bytes(self) -> int:
+        b = C.c_int64()
+        check(load().moe_expert_bytes(self._h, C.byref(b)))
+        return b.value
+
+    def expert_read(self, layer: int, expert: int) -> np.ndarray:
+        out = np.zeros(self.expert_bytes() // 2, dtype=np.uint16)
+        check(load().moe_expert_read(self._h, layer, expert, _p(out, _capi._u16)))
+        return out
+
+    def decode_begin(self, caps, fisher, tau, cfg: SimConfig, seed: int, total_tokens: int, staging_slots: int = 0):
+        check(load().moe_decode_begin(self._h, _p(_i32(caps), _capi._i32), staging_slots, _p(_f64(fisher), _capi._d),
+                                      float(tau), C.byref(cfg.c()), seed, total_tokens))
+
+    def decode_tokens(self, acts, scores, hidden_out=None, on_device: bool = False) -> float:
+        """acts [n][L][d], scores [n][L][N] host numpy arrays (or device pointers via on_device)."""
+        ms = C.c_double()
+        if on_device:
+            a_ptr, s_ptr, n = acts, scores, hidden_out[1]
+            check(load().moe_decode_tokens(self._h, C.cast(a_ptr, _capi._d), C.cast(s_ptr, _capi._d), n, 1,
+                                           C.cast(hidden_out[0], _capi._f) if hidden_out[0] else None, C.byref(ms)))
+            return ms.value
+        acts, scores = _f64(acts), _f64(scores)
+        out = None
+        if hidden_out is not None:
+            assert hidden_out.dtype == np.float32 and hidden_out.flags.c_contiguous
+            out = _p(hidden_out, _capi._f)
+        check(load().moe_decode_tokens(self._h, _p(acts, _capi._d), _p(scores, _capi._d), acts.shape[0], 0, out,
+                                       C.byref(ms)))
+        return ms.value
+
+    def decode_end(self, cfg: SimConfig | None = None, tokens: int | None = None, timeline: bool = True) -> SimResult:
+        m = _capi.MetricsC()
+        st = _capi.DecodeStatsC()
+        n = C.c_int64()
+        T = tokens or 0
+        lat = np.zeros(max(T, 1), dtype=np.int64)
+        odl = np.zeros(self.spec.num_layers, dtype=np.int64)
+        buf, cap = (_events_buf(self.spec, T, cfg) if (timeline and cfg is not None and T) else (None, 0))
+        check(load().moe_decode_end(self._h, C.byref(m), _p(lat, _capi._i64) if T else None, _p(odl, _capi._i64),
+                                    buf, cap, C.byref(n), C.byref(st)))
+        return SimResult({k: getattr(m, k) for k, _ in _capi.MetricsC._fields_}, lat[:T], odl,
+                         _events_np(buf, n.value) if buf is not None else None, n.value,
+                         {k: getattr(st, k) for k, _ in _capi.DecodeStatsC._fields_})
+
+    def expert_ffn(self, layer: int, expert: int, x) -> np.ndarray:
+        """y = W2 (silu(W1 x) * (W3 x)) for one stored expert, through the decode path's kernels."""
+        x = _f64(x)
+        y = np.zeros(self.spec.hidden_dim, dtype=np.float32)
+        check(load().moe_expert_ffn(self._h, layer, expert, _p(x, _capi._d), _p(y, _capi._f)))
+        return y

@@ -1,0 +1,155 @@
+"""Physical offloaded decode on the B200: K2 SwiGLU expert streaming, HBM slot pool, copy engine.
+
+Contracts checked (tolerances written here, north star: 1e-4 relative in fp32):
+  * expert weights in the pinned store are bit-identical to the oracle's counter-based init;
+  * single-expert SwiGLU (bf16 weights, fp32 accumulation) within 1e-4 of the fp64 oracle,
+    relative to max|y|;
+  * decode_trace: the logical metrics and event timeline are bit-exact with the reference goldens
+    while the FFN really runs, and every layer's MoE output x + sum_e w_e E_e(x) matches the oracle
+    within 1e-4 relative to max|sum_e w_e E_e(x)|.
+"""
+import numpy as np
+import pytest
+
+import paper_2408_10284_b200 as P
+from conftest import load_golden
+from helpers import assert_metrics, assert_timeline, oracle_inputs, sim_config
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-4
+
+
+def _rel_err(got, ref):
+    return float(np.abs(np.asarray(got, np.float64) - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def test_expert_store_matches_oracle_init():
+    spec = P.ModelSpec(2, 4, 2, 256)
+    with P.Engine(spec) as eng:
+        eng.experts_init(896, 4, seed=11)
+        for l, e in [(0, 0), (1, 3), (0, 2)]:
+            assert np.array_equal(eng.expert_read(l, e), O.expert_init(11, l, e, 256, 896, 4))
+
+
+@pytest.mark.parametrize("d,f,tiles", [(256, 896, 4), (512, 1024, 2), (256, 2048, 1), (4096, 14336, 4)])
+def test_expert_ffn_matches_oracle(d, f, tiles):
+    spec = P.ModelSpec(1, 2, 2, d)
+    rng = np.random.default_rng(d + f)
+    with P.Engine(spec) as eng:
+        eng.experts_init(f, tiles, seed=3)
+        for e in range(2):
+            x = rng.standard_normal(d)
+            y = eng.expert_ffn(0, e, x)
+            ref = O.swiglu(O.expert_init(3, 0, e, d, f, tiles), d, f, tiles, x.astype(np.float32))
+            assert _rel_err(y, ref) < REL_TOL
+
+
+def _moe_reference(w, fg_unused, decisions, T, ffn, tiles, seed, layers_subset=None):
+    """Oracle MoE-layer output per (token, layer): x + sum_e (s_e / sum_sel s) * SwiGLU_e(x)."""
+    cache = {}
+    out = {}
+    for t in range(T):
+        for l in range(w.L):
+            if layers_subset is not None and (t, l) not in layers_subset:
+                continue
+            sel = [int(e) for e in decisions[t, l] if e >= 0]
+            sc = w.scores[t, l]
+            denom = sum(sc[e] for e in sel)
+            x32 = w.acts[t, l].astype(np.float32)
+            acc = np.zeros(w.D)
+            for e in sel:
+                if (l, e) not in cache:
+                    cache[(l, e)] = O.expert_init(seed, l, e, w.D, ffn, tiles)
+                wgt = 1.0 if len(sel) == 1 else sc[e] / denom
+                acc += wgt * O.swiglu(cache[(l, e)], w.D, ffn, tiles, x32)
+            out[(t, l)] = acc
+    return out
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny_budget0", "tiny_transfer_heavy", "tiny_prefetch_off", "tiny_nogate",
+                                  "tiny_compute_heavy", "tiny_budget_full"])
+def test_decode_trace_tiny(name):
+    g = load_golden(name)
+    w, fg = oracle_inputs(g)
+    cfg = sim_config(g)
+    ffn, seed = 896, 5
+    T = w.T
+    with P.Engine(P.ModelSpec(w.L, w.N, w.K, w.D)) as eng:
+        eng.load_gates(w.gates, fg)
+        eng.experts_init(ffn, cfg.tile_count_per_expert, seed=seed)
+        eng.decode_begin(g["sim_capacities"], w.fisher, g["tau"], cfg, int(g["workload"]["seed"]), T)
+        hid = np.zeros((T, w.L, w.D), dtype=np.float32)
+        # split the trace over three calls: session state must carry over
+        cuts = [0, 5, 37, T]
+        for a, b in zip(cuts, cuts[1:]):
+            eng.decode_tokens(w.acts[a:b], w.scores[a:b], hid[a:b])
+        r = eng.decode_end(cfg, T)
+    assert_metrics(g, r.metrics, r.latency_per_token, r.on_demand_loads_per_layer)
+    assert_timeline(g, r.timeline)
+    st = r.stats
+    assert st["tokens"] == T
+    assert st["ffn_bytes"] == r.metrics["experts_activated_total"] * 3 * ffn * w.D * 2
+    sim = O.simulate(w, g["sim_capacities"], g["tau"], first_gate=fg,
+                     **{k: v for k, v in __import__("helpers").sim_kwargs(g).items()})
+    subset = {(t, l) for t in range(0, T, 7) for l in range(w.L)}
+    ref = _moe_reference(w, fg, sim.decisions, T, ffn, cfg.tile_count_per_expert, seed, subset)
+    for (t, l), moe in ref.items():
+        got = hid[t, l].astype(np.float64) - w.acts[t, l].astype(np.float32).astype(np.float64)
+        assert _rel_err(got, moe) < REL_TOL, (t, l)
+
+
+def test_decode_device_inputs_match_host_inputs():
+    import torch
+    g = load_golden("tiny")
+    w, fg = oracle_inputs(g)
+    cfg = sim_config(g)
+    T = 12
+    outs = []
+    for on_device in (False, True):
+        with P.Engine(P.ModelSpec(w.L, w.N, w.K, w.D)) as eng:
+            eng.load_gates(w.gates, fg)
+            eng.experts_init(896, 4, seed=2)
+            eng.decode_begin(g["sim_capacities"], w.fisher, g["tau"], cfg, 0, T)
+            if on_device:
+                a = torch.from_numpy(np.ascontiguousarray(w.acts[:T])).cuda()
+                s = torch.from_numpy(np.ascontiguousarray(w.scores[:T])).cuda()
+                h = torch.zeros((T, w.L, w.D), dtype=torch.float32, device="cuda")
+                torch.cuda.synchronize()
+                eng.decode_tokens(a.data_ptr(), s.data_ptr(), (h.data_ptr(), T), on_device=True)
+                outs.append(h.cpu().numpy())
+            else:
+                h = np.zeros((T, w.L, w.D), dtype=np.float32)
+                eng.decode_tokens(w.acts[:T], w.scores[:T], h)
+                outs.append(h)
+            eng.decode_end(cfg, T)
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_decode_mixtral_width_layers():
+    """Mixtral-8x7B expert shape (d 4096, ffn 14336, 4 tiles) over 4 layers: tile-granular on-demand
+    copies of 88 MB tiles, prefetch, DP-sized cache of 8 experts."""
+    from paper_2408_10284_b200 import workloads as W
+    wl = W.mixtral_8x7b(tokens=6, budget=8)
+    L = 4
+    w = O.generate_trace(L, 8, 2, 4096, wl.tokens, wl.concentration, wl.drift, wl.gate_seed, wl.token_seed, False,
+                         wl.fisher_scales[:L], wl.drift_scales[:L])
+    tau = O.calibrate_threshold(w, wl.target_single_ratio)
+    alpha, beta = O.generate_profiles(w, tau, None)
+    caps, _ = O.dp_allocate(O.cost_table(alpha, beta, 8), wl.budget)
+    ref = O.simulate(w, caps, tau)
+    cfg = P.SimConfig()
+    with P.Engine(P.ModelSpec(L, 8, 2, 4096)) as eng:
+        eng.load_gates(w.gates)
+        eng.experts_init(wl.ffn, 4, seed=9)
+        eng.decode_begin(caps, w.fisher, tau, cfg, 0, wl.tokens)
+        hid = np.zeros((wl.tokens, L, 4096), dtype=np.float32)
+        eng.decode_tokens(w.acts, w.scores, hid)
+        r = eng.decode_end(cfg, wl.tokens)
+    assert r.metrics == ref.metrics
+    assert np.array_equal(r.timeline, ref.timeline)
+    moe = _moe_reference(w, None, ref.decisions, wl.tokens, wl.ffn, 4, 9, {(0, 1), (3, 2), (5, 3)})
+    for (t, l), m in moe.items():
+        got = hid[t, l].astype(np.float64) - w.acts[t, l].astype(np.float32).astype(np.float64)
+        assert _rel_err(got, m) < REL_TOL, (t, l)

@@ -203,20 +203,28 @@ int moe_decode_begin(moe_engine_t engine, const int32_t* capacities, int32_t sta
 int moe_decode_tokens(moe_engine_t engine, const double* acts, const double* scores, int32_t count,
                       int32_t inputs_on_device, float* hidden_out, double* gpu_ms);
 
-/* Physical counters of the session so far. */
+/* Physical counters of the session so far (CUDA-event timed on the engine's streams). */
 typedef struct {
     int64_t tokens;
-    int64_t kernels_launched;     /* our kernels (router, ffn phases, combine) */
-    int64_t tile_copies;          /* H2D tile copies issued */
-    int64_t h2d_bytes;            /* expert bytes moved host -> HBM */
-    int64_t ffn_bytes;            /* algorithmic expert bytes streamed by the FFN kernels */
-    double copy_busy_ms;          /* sum of tile-copy durations (CUDA events) */
-    double ffn_ms;                /* sum of FFN kernel durations (CUDA events, per launch group) */
-    double router_ms;             /* sum of router kernel durations */
-    double stall_ms;              /* compute-stream time spent waiting on copies (events) */
-    int32_t slots_total;
-    int32_t staging_high_water;
+    int64_t kernels_launched;     /* our kernels: router, FFN passes, combine */
+    int64_t ffn_launches;         /* FFN pass launches (gate/up + down) */
+    int64_t tile_copies;          /* expert tile copies issued host -> HBM */
+    int64_t copy_bytes;           /* expert bytes moved host -> HBM */
+    int64_t input_bytes;          /* activation/score bytes copied host -> HBM (host-input calls) */
+    int64_t ffn_bytes;            /* algorithmic expert bytes streamed by the FFN passes */
+    double copy_busy_ms;          /* sum of tile-copy durations */
+    double ffn_ms;                /* sum of FFN pass durations */
+    double ffn_gate_up_ms, ffn_down_ms;
+    double ffn_gate_up_bytes, ffn_down_bytes;
+    double router_ms;             /* sum of router (K1) durations */
+    double stall_ms;              /* compute-stream time blocked on tile copies */
+    int64_t router_exact_items;   /* look-ahead items K1 could not certify from fp32 logits (exact fp64 path) */
+    int32_t slots_total;          /* HBM slots = sum(capacities) + staging */
+    int32_t staging_high_water;   /* most staging slots in use at once */
 } moe_decode_stats;
+
+/* Counters so far without ending the session. */
+int moe_decode_stats_snapshot(moe_engine_t engine, moe_decode_stats* stats);
 
 /* End the session: logical metrics/timeline (bit-exact with simulate_trace on the same inputs),
  * physical stats.  Any pointer may be NULL. */

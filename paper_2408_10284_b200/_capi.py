@@ -52,10 +52,12 @@ class SynthConfigC(C.Structure):
 
 
 class DecodeStatsC(C.Structure):
-    _fields_ = [("tokens", C.c_int64), ("kernels_launched", C.c_int64), ("tile_copies", C.c_int64),
-                ("h2d_bytes", C.c_int64), ("ffn_bytes", C.c_int64), ("copy_busy_ms", C.c_double),
-                ("ffn_ms", C.c_double), ("router_ms", C.c_double), ("stall_ms", C.c_double),
-                ("slots_total", C.c_int32), ("staging_high_water", C.c_int32)]
+    _fields_ = [("tokens", C.c_int64), ("kernels_launched", C.c_int64), ("ffn_launches", C.c_int64),
+                ("tile_copies", C.c_int64), ("copy_bytes", C.c_int64), ("input_bytes", C.c_int64),
+                ("ffn_bytes", C.c_int64), ("copy_busy_ms", C.c_double), ("ffn_ms", C.c_double),
+                ("ffn_gate_up_ms", C.c_double), ("ffn_down_ms", C.c_double), ("ffn_gate_up_bytes", C.c_double),
+                ("ffn_down_bytes", C.c_double), ("router_ms", C.c_double), ("stall_ms", C.c_double),
+                ("router_exact_items", C.c_int64), ("slots_total", C.c_int32), ("staging_high_water", C.c_int32)]
 
 
 _d = C.POINTER(C.c_double)
@@ -95,6 +97,7 @@ SIGNATURES = {
     "moe_decode_end": (C.c_int, [_eng, C.POINTER(MetricsC), _i64, _i64, C.POINTER(EventC), C.c_int64, _i64,
                                  C.POINTER(DecodeStatsC)]),
     "moe_expert_ffn": (C.c_int, [_eng, C.c_int32, C.c_int32, _d, _f]),
+    "moe_decode_stats_snapshot": (C.c_int, [_eng, C.POINTER(DecodeStatsC)]),
 }
 
 

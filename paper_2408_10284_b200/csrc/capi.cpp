@@ -318,6 +318,30 @@ int moe_generate_profiles(moe_engine_t h, const double* acts, const double* scor
 }  // extern "C"
 
 // ---- physical decode ------------------------------------------------------------------------
+namespace {
+void export_stats(const DecodeStats& s, moe_decode_stats* out) {
+    if (!out) return;
+    out->tokens = s.tokens;
+    out->kernels_launched = s.kernels;
+    out->ffn_launches = s.ffn_launches;
+    out->tile_copies = s.tile_copies;
+    out->copy_bytes = s.copy_bytes;
+    out->input_bytes = s.input_bytes;
+    out->ffn_bytes = s.ffn_bytes;
+    out->copy_busy_ms = s.copy_busy_ms;
+    out->ffn_ms = s.ffn_ms;
+    out->ffn_gate_up_ms = s.gate_up_ms;
+    out->ffn_down_ms = s.down_ms;
+    out->ffn_gate_up_bytes = s.gate_up_bytes;
+    out->ffn_down_bytes = s.down_bytes;
+    out->router_ms = s.router_ms;
+    out->stall_ms = s.stall_ms;
+    out->router_exact_items = s.router_exact;
+    out->slots_total = s.slots_total;
+    out->staging_high_water = s.staging_high_water;
+}
+}  // namespace
+
 extern "C" {
 
 int moe_experts_init(moe_engine_t h, int32_t ffn, int32_t tiles, uint64_t seed, int32_t alias) {
@@ -392,20 +416,17 @@ int moe_decode_end(moe_engine_t h, moe_metrics* metrics, int64_t* lat, int64_t* 
         const PolicyEngine& pe = e.session->policy();
         export_metrics(pe.metrics(), metrics, lat, odl);
         export_events(pe.timeline(), pe.events_recorded(), events, cap, n_events);
-        if (stats) {
-            stats->tokens = s.tokens;
-            stats->kernels_launched = s.kernels;
-            stats->tile_copies = s.tile_copies;
-            stats->h2d_bytes = s.h2d_bytes;
-            stats->ffn_bytes = s.ffn_bytes;
-            stats->copy_busy_ms = s.copy_busy_ms;
-            stats->ffn_ms = s.ffn_ms;
-            stats->router_ms = s.router_ms;
-            stats->stall_ms = s.stall_ms;
-            stats->slots_total = s.slots_total;
-            stats->staging_high_water = s.staging_high_water;
-        }
+        export_stats(s, stats);
         e.session.reset();
+    });
+}
+
+int moe_decode_stats_snapshot(moe_engine_t h, moe_decode_stats* stats) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(stats, "stats");
+        if (!e.session) fail(Status::Usage, "decode_stats: no session");
+        export_stats(e.session->snapshot(), stats);
     });
 }
 

@@ -21,7 +21,7 @@ namespace {
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = 32 * (1 + kConsumerWarps);
 constexpr int kMaxStages = 4;
-constexpr int kSmemBudget = 227 * 1024;
+constexpr int kSmemBudget = 227 * 1024 - 1024;  // leave room for static shared memory
 
 struct PassGeometry {
     int rows_per_stage;  // R (8, 4 or 2)
@@ -250,23 +250,23 @@ __global__ void expert_init_kernel(uint16_t* dst, int D, int F, int tiles, InitA
 
 cudaError_t launch_ffn_pass(const FfnLaunch& p, int sm_count, cudaStream_t stream) {
     if (p.n_seg <= 0) return cudaSuccess;
-    if (p.n_seg > kMaxFfnSegments || p.cols % 64 != 0 || p.cols > 16384) return cudaErrorInvalidValue;
+    if (p.n_seg > kMaxFfnSegments || p.cols % 8 != 0 || p.cols > 16384) return cudaErrorInvalidValue;
     const PassGeometry g = geometry(p.cols);
-    if (g.stages < 2) return cudaErrorInvalidValue;
+    if (g.stages < 2 || (p.cols / g.warps_per_row) % 8 != 0) return cudaErrorInvalidValue;
     long long units = 0;
     for (int s = 0; s < p.n_seg; ++s) units += (p.seg[s].rows_count + g.rows_per_stage - 1) / g.rows_per_stage;
     const int grid = static_cast<int>(units < sm_count ? units : sm_count);
     if (p.swiglu) {
         static bool set = false;
         if (!set) {
-            cudaFuncSetAttribute(ffn_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+            cudaFuncSetAttribute(ffn_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);  // NOLINT
             set = true;
         }
         ffn_pass_kernel<true><<<grid, kThreads, g.smem, stream>>>(p);
     } else {
         static bool set = false;
         if (!set) {
-            cudaFuncSetAttribute(ffn_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+            cudaFuncSetAttribute(ffn_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);  // NOLINT
             set = true;
         }
         ffn_pass_kernel<false><<<grid, kThreads, g.smem, stream>>>(p);

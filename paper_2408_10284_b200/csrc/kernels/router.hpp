@@ -4,7 +4,7 @@
 // read it: the actual decision for layer l (from the stored trace scores, or from logits of
 // layer l's gate) plus the look-ahead predictions (x . W_{l+1..l+k}, or the first-layer gate at the
 // last layer).  Each item writes its selected experts (score-descending, -1 padded to K), the
-// count, the single-expert flag and the sensitivity perturbation; optionally its full score vector.
+// count, the single-expert flag and the sensitivity perturbation; optionally its scores/logits.
 #pragma once
 
 #include <cuda_runtime_api.h>
@@ -19,12 +19,14 @@ enum RouteFlags : int {
     kRouteAdaptive = 1,     // sensitivity gate (inc/gating.hpp:56-64) instead of plain top-K
     kRouteDivConc = 2,      // logits /= concentration before softmax (inc/workload.hpp:94)
     kRouteEmitScores = 4,   // write the post-softmax scores
-    kRouteEmitLogits = 8,   // write the raw fp64 logits to `scores` and skip the decision (the
-                            // caller applies glibc exp: used where stored score bits must match)
+    kRouteEmitLogits = 8,   // write the exact fp64 logits to `scores`, skip the decision (the caller
+                            // applies glibc exp: used where stored score bits must match)
+    kRouteExact = 16,       // skip the fp32 fast path: exact reference-order fp64 logits
 };
 
 struct RouteItem {
-    const double* gate = nullptr;    // [d][N] fp64; nullptr => decide from `scores`
+    const double* gate = nullptr;    // [d][N] fp64 (reference layout); nullptr => decide from `scores`
+    const float* gate32 = nullptr;   // [N][d] fp32 transposed copy (fast path)
     const double* scores = nullptr;  // [N] stored post-softmax scores (gate == nullptr)
     double fisher = 0.0;
     int flags = 0;
@@ -38,11 +40,12 @@ struct RouteGroup {
 };
 
 struct RouteOutputs {
-    int* selected = nullptr;       // [rows][K]
-    int* count = nullptr;          // [rows]
-    int* single = nullptr;         // [rows]
+    int* selected = nullptr;         // [rows][K]
+    int* count = nullptr;            // [rows]
+    int* single = nullptr;           // [rows]
     double* perturbation = nullptr;  // [rows] (may be null)
-    double* scores = nullptr;      // [rows][N] (may be null; written for kRouteEmitScores items)
+    double* scores = nullptr;        // [rows][N] (may be null; kRouteEmitScores / kRouteEmitLogits)
+    int* exact_used = nullptr;       // [rows] 1 if the item needed the exact fp64 path (may be null)
 };
 
 struct RouteParams {
@@ -54,5 +57,8 @@ struct RouteParams {
 // Launch K1 over `n_groups` groups already resident in device memory.
 cudaError_t launch_route(const RouteGroup* d_groups, int n_groups, int max_gate_items, const RouteParams& p,
                          const RouteOutputs& out, cudaStream_t stream);
+
+// fp32 transposed copy [N][d] of a row-major fp64 [d][N] gate (device to device).
+cudaError_t launch_gate_transpose(const double* src, float* dst, int d, int n, int count, cudaStream_t stream);
 
 }  // namespace adapmoe

@@ -28,7 +28,9 @@ CopyEngine::~CopyEngine() {
     if (thread_.joinable()) thread_.join();
     cudaSetDevice(device_);
     cudaStreamSynchronize(stream_);
-    for (auto& j : active_) retire(j);
+    std::vector<std::shared_ptr<CopyJob>> left;
+    left.swap(active_);  // retire() edits active_
+    for (auto& j : left) retire(j);
     for (cudaEvent_t e : inflight_) cudaEventDestroy(e);
     for (cudaEvent_t e : free_sync_) cudaEventDestroy(e);
     for (cudaEvent_t e : free_timing_) cudaEventDestroy(e);
@@ -124,6 +126,18 @@ void CopyEngine::drain() {
 double CopyEngine::busy_ms() {
     std::lock_guard<std::mutex> g(mu_);
     return busy_ms_;
+}
+
+double CopyEngine::busy_ms_total() {
+    std::lock_guard<std::mutex> g(mu_);
+    double total = busy_ms_;
+    for (const auto& job : active_)
+        for (int t = 0; t < job->issued_tiles; ++t)
+            if (cudaEventQuery(job->t_end[t]) == cudaSuccess) {
+                float ms = 0.0f;
+                if (cudaEventElapsedTime(&ms, job->t_start[t], job->t_end[t]) == cudaSuccess) total += ms;
+            }
+    return total;
 }
 
 void CopyEngine::retire(const std::shared_ptr<CopyJob>& job) {

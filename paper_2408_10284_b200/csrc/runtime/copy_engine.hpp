@@ -56,7 +56,8 @@ public:
 
     long long tiles_copied() const { return tiles_copied_.load(); }
     long long bytes_copied() const { return bytes_copied_.load(); }
-    double busy_ms();  // sum of per-tile copy durations of finished jobs
+    double busy_ms();        // sum of per-tile copy durations of retired jobs
+    double busy_ms_total();  // ... plus every completed tile of live jobs
     void retire(const std::shared_ptr<CopyJob>& job);  // accumulate timing + recycle events
 
 private:

@@ -299,7 +299,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
         d_in_scores_.reserve(TL * N * sizeof(double));
         MOE_CUDA(cudaMemcpyAsync(d_in_acts_.ptr, acts, TL * D * sizeof(double), cudaMemcpyHostToDevice, cs));
         MOE_CUDA(cudaMemcpyAsync(d_in_scores_.ptr, scores, TL * N * sizeof(double), cudaMemcpyHostToDevice, cs));
-        stats_.h2d_bytes += static_cast<long long>(TL * (D + N) * sizeof(double));
+        stats_.input_bytes += static_cast<long long>(TL * (D + N) * sizeof(double));
         x_all = d_in_acts_.as<double>();
         s_all = d_in_scores_.as<double>();
     }
@@ -328,14 +328,14 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                 if (l + 1 < L) {
                     for (int dep = 1; dep <= cfg_.lookahead_depth && l + dep < L; ++dep) {
                         RouteItem& it = g.items[g.n_items++];
-                        it.gate = eng_.d_gate(l + dep);
+                        eng_.gate_item(it, l + dep);
                         it.fisher = fisher_[l + dep];
                         it.flags = adaptive;
                         it.out = dep;
                     }
                 } else if (eng_.has_first_gate() && tok + 1 < total_tokens_) {
                     RouteItem& it = g.items[g.n_items++];
-                    it.gate = eng_.d_first_gate();
+                    eng_.gate_item(it, -1);
                     it.fisher = fisher_[0];
                     it.flags = adaptive;
                     it.out = 1;
@@ -346,10 +346,11 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
         }
     MOE_CUDA(cudaMemcpyAsync(d_groups_.ptr, hg, TL * sizeof(RouteGroup), cudaMemcpyHostToDevice, cs));
     RouteParams rp{D, N, K, tau_, 1.0};
-    RouteOutputs ro{d_route_, d_route_ + 4 * K, d_route_ + 4 * K + 4, nullptr, nullptr};
+    RouteOutputs ro{d_route_, d_route_ + 4 * K, d_route_ + 4 * K + 4, nullptr, nullptr, d_route_ + 4 * K + 8};
     const int* sel = h_route_;
     const int* cnt = h_route_ + 4 * K;
     const int* sgl = h_route_ + 4 * K + 4;
+    const int* exact_used = h_route_ + 4 * K + 8;
 
     std::array<RoutePrediction, 3> preds;
     for (int i = 0; i < count; ++i) {
@@ -368,6 +369,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             RouteDecision d;
             d.count = cnt[0];
             d.single = sgl[0] != 0;
+            for (int it = 1; it < hg[tl].n_items; ++it) stats_.router_exact += exact_used[it];
             for (int k = 0; k < d.count; ++k) d.experts[k] = sel[k];
             const RouteGroup& g = hg[tl];
             int np = 0;
@@ -397,6 +399,44 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
     return ms;
 }
 
+// Fold the (completed) timing events recorded so far into the counters and recycle them.
+DecodeStats DecodeSession::snapshot() {
+    eng_.activate();
+    MOE_CUDA(cudaStreamSynchronize(eng_.compute_stream()));
+    auto elapsed = [](cudaEvent_t a, cudaEvent_t b) {
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, a, b);
+        return static_cast<double>(ms);
+    };
+    for (auto& p : pass_events_) {
+        const double ms = elapsed(p.e0, p.e1);
+        stats_.ffn_ms += ms;
+        (p.a ? stats_.gate_up_ms : stats_.down_ms) += ms;
+        (p.a ? stats_.gate_up_bytes : stats_.down_bytes) += p.bytes;
+        stats_.ffn_launches += 1;
+        timing_pool_.push_back(p.e0);
+        timing_pool_.push_back(p.e1);
+    }
+    pass_events_.clear();
+    for (auto& p : router_events_) {
+        stats_.router_ms += elapsed(p.first, p.second);
+        timing_pool_.push_back(p.first);
+        timing_pool_.push_back(p.second);
+    }
+    router_events_.clear();
+    for (auto& p : stall_events_) {
+        stats_.stall_ms += elapsed(p.first, p.second);
+        timing_pool_.push_back(p.first);
+        timing_pool_.push_back(p.second);
+    }
+    stall_events_.clear();
+    DecodeStats s = stats_;
+    s.tile_copies = copier_->tiles_copied();
+    s.copy_bytes = copier_->bytes_copied();
+    s.copy_busy_ms = copier_->busy_ms_total();
+    return s;
+}
+
 DecodeStats DecodeSession::finish() {
     eng_.activate();
     copier_->drain();
@@ -404,27 +444,7 @@ DecodeStats DecodeSession::finish() {
     release_pending(true);
     for (auto& j : retiring_) copier_->retire(j);
     retiring_.clear();
-    DecodeStats s = stats_;
-    for (auto& p : pass_events_) {
-        float ms = 0;
-        cudaEventElapsedTime(&ms, p.e0, p.e1);
-        s.ffn_ms += ms;
-        (p.a ? s.pass_a : s.pass_b).emplace_back(p.bytes, ms);
-    }
-    for (auto& p : router_events_) {
-        float ms = 0;
-        cudaEventElapsedTime(&ms, p.first, p.second);
-        s.router_ms += ms;
-    }
-    for (auto& p : stall_events_) {
-        float ms = 0;
-        cudaEventElapsedTime(&ms, p.first, p.second);
-        s.stall_ms += ms;
-    }
-    s.tile_copies = copier_->tiles_copied();
-    s.h2d_bytes += copier_->bytes_copied();
-    s.copy_busy_ms = copier_->busy_ms();
-    return s;
+    return snapshot();
 }
 
 }  // namespace adapmoe

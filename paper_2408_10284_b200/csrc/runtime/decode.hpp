@@ -27,11 +27,11 @@
 namespace adapmoe {
 
 struct DecodeStats {
-    long long tokens = 0, kernels = 0, tile_copies = 0, h2d_bytes = 0, ffn_bytes = 0;
-    double copy_busy_ms = 0, ffn_ms = 0, router_ms = 0, stall_ms = 0;
+    long long tokens = 0, kernels = 0, ffn_launches = 0, tile_copies = 0, copy_bytes = 0, input_bytes = 0, ffn_bytes = 0;
+    double copy_busy_ms = 0, ffn_ms = 0, gate_up_ms = 0, down_ms = 0, gate_up_bytes = 0, down_bytes = 0;
+    double router_ms = 0, stall_ms = 0;
+    long long router_exact = 0;  // look-ahead items that needed the exact fp64 path
     int slots_total = 0, staging_high_water = 0;
-    // per FFN pass launch (bytes, ms) for roofline accounting
-    std::vector<std::pair<double, double>> pass_a, pass_b;
 };
 
 class DecodeSession : public DecodeListener {
@@ -44,7 +44,8 @@ public:
     double decode(const double* acts, const double* scores, int count, bool on_device, float* hidden_out);
 
     const PolicyEngine& policy() const { return *policy_; }
-    DecodeStats finish();
+    DecodeStats snapshot();  // counters so far (call between decode() calls)
+    DecodeStats finish();    // drain the copy engine, then snapshot
 
     // DecodeListener
     void on_request(int id, ExpertRef ref, bool on_demand) override;

@@ -64,13 +64,20 @@ void Engine::load_gates(const double* gates, const double* first_gate) {
     const size_t one = static_cast<size_t>(spec_.hidden_dim) * spec_.experts_per_layer * sizeof(double);
     d_gates_.reserve(one * spec_.num_layers);
     MOE_CUDA(cudaMemcpy(d_gates_.ptr, gates, one * spec_.num_layers, cudaMemcpyHostToDevice));
+    d_gates32_.reserve(one / 2 * spec_.num_layers);
+    MOE_CUDA(launch_gate_transpose(d_gates_.as<double>(), d_gates32_.as<float>(), spec_.hidden_dim,
+                                   spec_.experts_per_layer, spec_.num_layers, compute_));
     gates_loaded_ = true;
     first_gate_loaded_ = false;
     if (first_gate) {
         d_first_gate_.reserve(one);
+        d_first_gate32_.reserve(one / 2);
         MOE_CUDA(cudaMemcpy(d_first_gate_.ptr, first_gate, one, cudaMemcpyHostToDevice));
+        MOE_CUDA(launch_gate_transpose(d_first_gate_.as<double>(), d_first_gate32_.as<float>(), spec_.hidden_dim,
+                                       spec_.experts_per_layer, 1, compute_));
         first_gate_loaded_ = true;
     }
+    MOE_CUDA(cudaStreamSynchronize(compute_));
 }
 
 void Engine::run_route(const std::vector<RouteGroup>& groups, int rows, int max_gate_items, const RouteParams& p,
@@ -136,7 +143,7 @@ TraceRoutes Engine::route_trace(const double* acts, const double* scores, int T,
                 if (l + 1 < L) {
                     for (int depth = 1; depth <= cfg.lookahead_depth && l + depth < L; ++depth) {
                         RouteItem& it = g.items[g.n_items++];
-                        it.gate = d_gate(l + depth);
+                        gate_item(it, l + depth);
                         it.fisher = fisher[l + depth];
                         it.flags = adaptive;
                         it.out = static_cast<int>(tl * 4 + depth);
@@ -144,7 +151,7 @@ TraceRoutes Engine::route_trace(const double* acts, const double* scores, int T,
                     }
                 } else if (has_first_gate() && tok + 1 < T) {
                     RouteItem& it = g.items[g.n_items++];
-                    it.gate = d_first_gate();
+                    gate_item(it, -1);
                     it.fisher = fisher[0];
                     it.flags = adaptive;
                     it.out = static_cast<int>(tl * 4 + 1);
@@ -291,19 +298,19 @@ void Engine::generate_profiles(const double* acts, const double* scores, int T, 
     for (int tok = 0; tok < T; ++tok)
         for (int l = 0; l < L; ++l) {
             const double* x = nullptr;
-            const double* gate = nullptr;
+            int gate_layer = 0;
             if (l >= 1) {
                 x = d_x_.as<double>() + (static_cast<size_t>(tok) * L + (l - 1)) * D;
-                gate = d_gate(l);
+                gate_layer = l;
             } else if (has_first_gate() && tok >= 1) {
                 x = d_x_.as<double>() + (static_cast<size_t>(tok - 1) * L + (L - 1)) * D;
-                gate = d_first_gate();
+                gate_layer = -1;
             }
-            if (!gate) continue;
+            if (!x) continue;
             RouteGroup g;
             g.x = x;
             g.n_items = 1;
-            g.items[0].gate = gate;
+            gate_item(g.items[0], gate_layer);
             g.items[0].out = static_cast<int>(pre.size());
             pre.push_back(g);
             where.push_back(tok * L + l);

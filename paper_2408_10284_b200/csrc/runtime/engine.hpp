@@ -67,6 +67,14 @@ public:
     bool has_first_gate() const { return first_gate_loaded_; }
     const double* d_gate(int layer) const { return d_gates_.as<double>() + static_cast<size_t>(layer) * spec_.hidden_dim * spec_.experts_per_layer; }
     const double* d_first_gate() const { return first_gate_loaded_ ? d_first_gate_.as<double>() : nullptr; }
+    // fp32 transposed [N][d] copies for K1's fast path
+    const float* d_gate32(int layer) const { return d_gates32_.as<float>() + static_cast<size_t>(layer) * spec_.hidden_dim * spec_.experts_per_layer; }
+    const float* d_first_gate32() const { return first_gate_loaded_ ? d_first_gate32_.as<float>() : nullptr; }
+    // fill a routing item that evaluates gate `layer` (-1 = first-layer predictive gate)
+    void gate_item(RouteItem& it, int layer) const {
+        it.gate = layer < 0 ? d_first_gate() : d_gate(layer);
+        it.gate32 = layer < 0 ? d_first_gate32() : d_gate32(layer);
+    }
 
     // K1 over a whole trace (acts/scores host).  Matches simulate_trace's evaluation points.
     TraceRoutes route_trace(const double* acts, const double* scores, int tokens, std::span<const double> fisher,
@@ -95,7 +103,7 @@ private:
     ModelSpec spec_;
     int device_;
     cudaStream_t compute_ = nullptr, copy_ = nullptr;
-    DeviceBuffer d_gates_, d_first_gate_;
+    DeviceBuffer d_gates_, d_first_gate_, d_gates32_, d_first_gate32_;
     bool gates_loaded_ = false, first_gate_loaded_ = false;
     // router workspace
     DeviceBuffer d_groups_, d_x_, d_scores_, d_out_sel_, d_out_cnt_, d_out_single_, d_out_pert_, d_out_scores_;

@@ -41,7 +41,7 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
     const ModelSpec& spec = eng.spec();
     if (ffn <= 0 || tiles < 1 || ffn % tiles) fail(Status::Usage, "experts_init: ffn must be a positive multiple of tiles");
     const int ft = ffn / tiles;
-    if (spec.hidden_dim % 64 || ft % 64) fail(Status::Usage, "experts_init: hidden_dim and ffn/tiles must be multiples of 64");
+    if (spec.hidden_dim % 32 || ft % 32) fail(Status::Usage, "experts_init: hidden_dim and ffn/tiles must be multiples of 32");
     if (spec.hidden_dim > 16384 || ft > 16384) fail(Status::Usage, "experts_init: rows longer than 16384 elements unsupported");
     if (alias < 0) fail(Status::Usage, "experts_init: host_alias must be >= 0");
     eng.activate();

@@ -319,6 +319,11 @@ class Engine:
                          _events_np(buf, n.value) if buf is not None else None, n.value,
                          {k: getattr(st, k) for k, _ in _capi.DecodeStatsC._fields_})
 
+    def decode_stats(self) -> dict:
+        st = _capi.DecodeStatsC()
+        check(load().moe_decode_stats_snapshot(self._h, C.byref(st)))
+        return {k: getattr(st, k) for k, _ in _capi.DecodeStatsC._fields_}
+
     def expert_ffn(self, layer: int, expert: int, x) -> np.ndarray:
         """y = W2 (silu(W1 x) * (W3 x)) for one stored expert, through the decode path's kernels."""
         x = _f64(x)

@@ -74,7 +74,7 @@ def test_decode_trace_tiny(name):
     g = load_golden(name)
     w, fg = oracle_inputs(g)
     cfg = sim_config(g)
-    ffn, seed = 896, 5
+    ffn, seed = 224 * cfg.tile_count_per_expert, 5  # ffn/tiles = 224 (= 896/4 of the tiny config)
     T = w.T
     with P.Engine(P.ModelSpec(w.L, w.N, w.K, w.D)) as eng:
         eng.load_gates(w.gates, fg)

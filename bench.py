@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--trace-tokens", type=int, default=64)
     ap.add_argument("--staging", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--host-alias", type=int, default=None,
+                    help="store only this many distinct experts in host memory (profiling runs; same bytes moved)")
     return ap.parse_args()
 
 
@@ -207,6 +209,8 @@ def ours(args):
             alias = max(1, per_rank // expert_bytes)
     except Exception:  # noqa: BLE001
         pass
+    if args.host_alias is not None:
+        alias = args.host_alias
     t0 = time.time()
     eng.experts_init(wl.ffn, wl.tiles, seed=1234, host_alias=alias)
     t_store = time.time() - t0
@@ -261,7 +265,7 @@ def ours(args):
     act_timed = int((((tl[:, 1] == 2) | ((tl[:, 1] == 3) & (tl[:, 7] == 0))) & (tokens_col >= W) & (tokens_col < W + K)).sum())
 
     d = {k: s1[k] - s0[k] for k in s0 if isinstance(s0[k], (int, float))}
-    ffn_ms = d["ffn_gate_up_ms"] + d["ffn_down_ms"]
+    ffn_ms = d["ffn_ms"]
     ffn_bytes = d["ffn_gate_up_bytes"] + d["ffn_down_bytes"]
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
@@ -286,12 +290,11 @@ def ours(args):
         "on_demand_loads_per_token": od_timed / K,
         "experts_activated_per_token": act_timed / K,
         "on_demand_loads_per_token_trace": res.metrics["on_demand_loads"] / wl.tokens if wl.tokens else None,
-        "roofline": {"bound": "hbm", "kernel": "K2 SwiGLU passes (gate/up + down)", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": "K2 fused SwiGLU expert streaming (ffn_kernel)", "achieved": achieved,
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
                      "launches": d["ffn_launches"], "bytes_per_launch": ffn_bytes / max(1, d["ffn_launches"]),
                      "ms_per_launch": ffn_ms / max(1, d["ffn_launches"]),
-                     "gate_up_gbs": d["ffn_gate_up_bytes"] / max(1e-9, d["ffn_gate_up_ms"] * 1e-3) / 1e9,
-                     "down_gbs": d["ffn_down_bytes"] / max(1e-9, d["ffn_down_ms"] * 1e-3) / 1e9,
+                     "algorithmic_bytes": "3*d*ffn/tiles*2 B per (expert, tile) segment: every bf16 weight once",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"},
         "host_link": {"copy_bytes": d["copy_bytes"], "copy_busy_ms": d["copy_busy_ms"], "achieved_gbs": copy_gbs,
                       "tile_copies": d["tile_copies"], "stall_ms": d["stall_ms"],

@@ -456,26 +456,24 @@ int moe_expert_ffn(moe_engine_t h, int32_t layer, int32_t expert, const double* 
         const size_t gate_up = static_cast<size_t>(2) * Ft * D * 2;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e.device());
-        FfnLaunch pa, pb;
-        pa.cols = D;
-        pa.swiglu = 1;
-        pa.x = dx.as<double>();
-        pb.cols = Ft;
+        DeviceBuffer counters;
+        counters.reserve(kMaxFfnSegments * sizeof(unsigned));
+        MOE_CUDA(cudaMemsetAsync(counters.ptr, 0, kMaxFfnSegments * sizeof(unsigned), cs));
+        FfnLaunch p;
+        p.d = D;
+        p.ft = Ft;
+        p.x = dx.as<double>();
+        p.counters = counters.as<unsigned>();
         for (int t = 0; t < T; ++t) {
             const unsigned char* tile = w.as<unsigned char>() + t * st.tile_bytes;
-            FfnSegment a, b;
-            a.rows = reinterpret_cast<const std::uint16_t*>(tile);
-            a.out = dh.as<float>() + static_cast<size_t>(t) * Ft;
-            a.rows_count = 2 * Ft;
-            b.rows = reinterpret_cast<const std::uint16_t*>(tile + gate_up);
-            b.vec = a.out;
-            b.out = dy.as<float>() + static_cast<size_t>(t) * D;
-            b.rows_count = D;
-            pa.seg[pa.n_seg++] = a;
-            pb.seg[pb.n_seg++] = b;
+            FfnSegment s;
+            s.gate_up = reinterpret_cast<const std::uint16_t*>(tile);
+            s.down = reinterpret_cast<const std::uint16_t*>(tile + gate_up);
+            s.h = dh.as<float>() + static_cast<size_t>(t) * Ft;
+            s.y = dy.as<float>() + static_cast<size_t>(t) * D;
+            p.seg[p.n_seg++] = s;
         }
-        MOE_CUDA(launch_ffn_pass(pa, sms, cs));
-        MOE_CUDA(launch_ffn_pass(pb, sms, cs));
+        MOE_CUDA(launch_ffn(p, sms, cs));
         CombineArgs c;
         c.x = zero.as<double>();
         c.scores = zero.as<double>();  // single rank: weight 1

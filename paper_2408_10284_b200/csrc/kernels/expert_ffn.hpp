@@ -6,9 +6,12 @@
 // so every tile is one contiguous 3*Ft*D*2-byte block: the unit of a host->HBM copy and of a
 // tile-granular FFN launch (inc/simulator.hpp:451-459 computes on-demand experts tile by tile).
 //
-// Pass A (gate/up): h[r] = silu(W1[r] . x) * (W3[r] . x)       per (expert rank, tile)
-// Pass B (down)   : y_t[j] = W2_t[j, :] . h_t                    per (expert rank, tile)
-// Combine         : out[j] = x[j] + sum_rank w_rank * sum_t y_t[j]   (fixed order, deterministic)
+// One launch processes a list of (expert rank, tile) segments in a single persistent kernel:
+//   phase A (gate/up): h_t[r] = silu(W1[r] . x) * (W3[r] . x)
+//   phase B (down)   : y_t[j] = W2_t[j, :] . h_t
+// phase-B work of a segment starts when that segment's phase-A units are all done (device-side
+// counters), so weight streaming never pauses between the two projections.
+// Combine: out[j] = x[j] + sum_rank w_rank * sum_t y_t[j] (fixed order, deterministic).
 // Partial results are kept per (rank, tile) so a resident expert computed in one launch and an
 // on-demand expert computed tile by tile give bit-identical outputs.
 #pragma once
@@ -22,22 +25,22 @@ namespace adapmoe {
 constexpr int kMaxFfnSegments = 32;
 
 struct FfnSegment {
-    const std::uint16_t* rows = nullptr;  // first row (bf16 bits) of the block
-    float* out = nullptr;                 // pass A: h_t [Ft]; pass B: y_t [D]
-    const float* vec = nullptr;           // pass B only: h_t [Ft] (pass A reads x from FfnLaunch)
-    int rows_count = 0;                   // pass A: 2*Ft; pass B: D
+    const std::uint16_t* gate_up = nullptr;  // [Ft][2][D] bf16
+    const std::uint16_t* down = nullptr;     // [D][Ft] bf16
+    float* h = nullptr;                      // [Ft] phase-A output (phase-B input)
+    float* y = nullptr;                      // [D] phase-B output
 };
 
 struct FfnLaunch {
     int n_seg = 0;
-    int cols = 0;                 // row length (pass A: D; pass B: Ft)
-    int swiglu = 0;               // 1 = pass A (row pairs -> silu(a)*b), 0 = pass B (plain dot)
-    const double* x = nullptr;    // pass A input activation (fp64, converted to fp32 in smem)
+    int d = 0, ft = 0;
+    const double* x = nullptr;       // [d] layer input (fp64; converted to fp32 in shared memory)
+    unsigned int* counters = nullptr;  // [n_seg] zero on entry: phase-A units finished per segment
     FfnSegment seg[kMaxFfnSegments];
 };
 
-// Streams every segment's rows once (TMA bulk copies into a shared-memory ring).
-cudaError_t launch_ffn_pass(const FfnLaunch& p, int sm_count, cudaStream_t stream);
+// Streams every segment's weights once (TMA bulk copies into a shared-memory ring).
+cudaError_t launch_ffn(const FfnLaunch& p, int sm_count, cudaStream_t stream);
 
 struct CombineArgs {
     const double* x = nullptr;       // [D] layer input (residual)

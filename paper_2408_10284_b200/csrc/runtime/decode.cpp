@@ -51,6 +51,8 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
 
     d_h_.reserve(static_cast<size_t>(K) * store_.ffn * sizeof(float));
     d_y_.reserve(static_cast<size_t>(K) * store_.tiles * D * sizeof(float));
+    d_counters_.reserve(kCounterRing * sizeof(unsigned));
+    MOE_CUDA(cudaMemset(d_counters_.ptr, 0, kCounterRing * sizeof(unsigned)));
     MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_route_), 64 * 4 * sizeof(int), cudaHostAllocMapped));
     MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_route_), h_route_, 0));
     MOE_CUDA(cudaEventCreateWithFlags(&route_done_, cudaEventDisableTiming));
@@ -198,14 +200,28 @@ void DecodeSession::wait_fill(int slot, int tile) {
     if (tile < 0 || tile == sl.fill->tiles - 1) sl.fill_done = true;
 }
 
-void DecodeSession::timed_pass(const FfnLaunch& p, bool a, double bytes) {
+unsigned int* DecodeSession::take_counters(int n) {
+    if (counter_next_ + n > kCounterRing) {
+        MOE_CUDA(cudaMemsetAsync(d_counters_.ptr, 0, kCounterRing * sizeof(unsigned), eng_.compute_stream()));
+        counter_next_ = 0;
+    }
+    unsigned int* c = d_counters_.as<unsigned>() + counter_next_;
+    counter_next_ += n;
+    return c;
+}
+
+void DecodeSession::timed_ffn(FfnLaunch& p) {
     cudaStream_t cs = eng_.compute_stream();
+    p.counters = take_counters(p.n_seg);
     cudaEvent_t e0 = take_timing(), e1 = take_timing();
     cudaEventRecord(e0, cs);
-    MOE_CUDA(launch_ffn_pass(p, sm_count_, cs));
+    MOE_CUDA(launch_ffn(p, sm_count_, cs));
     cudaEventRecord(e1, cs);
-    pass_events_.push_back(PassRec{a, bytes, e0, e1});
+    const double gate_up = static_cast<double>(p.n_seg) * 2.0 * p.ft * p.d * 2.0;
+    const double down = static_cast<double>(p.n_seg) * p.ft * p.d * 2.0;
+    pass_events_.push_back(PassRec{gate_up, down, e0, e1});
     stats_.kernels += 1;
+    p.n_seg = 0;
 }
 
 void DecodeSession::on_layer_done(int, int, const RouteDecision& d) {
@@ -213,58 +229,37 @@ void DecodeSession::on_layer_done(int, int, const RouteDecision& d) {
     const size_t gate_up_bytes = static_cast<size_t>(2) * Ft * D * 2;
     float* h = d_h_.as<float>();
     float* y = d_y_.as<float>();
-    auto seg_a = [&](int slot, int rank, int t) {
+    auto seg = [&](int slot, int rank, int t) {
         FfnSegment s;
-        s.rows = reinterpret_cast<const std::uint16_t*>(slot_ptr(slot) + t * store_.tile_bytes);
-        s.out = h + static_cast<size_t>(rank) * F + static_cast<size_t>(t) * Ft;
-        s.rows_count = 2 * Ft;
+        const unsigned char* tile = slot_ptr(slot) + t * store_.tile_bytes;
+        s.gate_up = reinterpret_cast<const std::uint16_t*>(tile);
+        s.down = reinterpret_cast<const std::uint16_t*>(tile + gate_up_bytes);
+        s.h = h + static_cast<size_t>(rank) * F + static_cast<size_t>(t) * Ft;
+        s.y = y + (static_cast<size_t>(rank) * T + t) * D;
         return s;
     };
-    auto seg_b = [&](int slot, int rank, int t) {
-        FfnSegment s;
-        s.rows = reinterpret_cast<const std::uint16_t*>(slot_ptr(slot) + t * store_.tile_bytes + gate_up_bytes);
-        s.vec = h + static_cast<size_t>(rank) * F + static_cast<size_t>(t) * Ft;
-        s.out = y + (static_cast<size_t>(rank) * T + t) * D;
-        s.rows_count = D;
-        return s;
-    };
-    FfnLaunch pa, pb;
-    pa.cols = D;
-    pa.swiglu = 1;
-    pa.x = cur_x_;
-    pb.cols = Ft;
-    pb.swiglu = 0;
-    double bytes_a = 0, bytes_b = 0;
-    auto flush = [&]() {
-        if (pa.n_seg) timed_pass(pa, true, bytes_a);
-        if (pb.n_seg) timed_pass(pb, false, bytes_b);
-        pa.n_seg = pb.n_seg = 0;
-        bytes_a = bytes_b = 0;
-    };
-    // resident experts: one pass-A and one pass-B launch over all their tiles
+    FfnLaunch p;
+    p.d = D;
+    p.ft = Ft;
+    p.x = cur_x_;
+    // resident experts: one launch over all their tiles
     for (const Use& u : uses_) {
         if (u.missing) continue;
         wait_fill(u.slot, -1);
         for (int t = 0; t < T; ++t) {
-            if (pa.n_seg == kMaxFfnSegments) flush();
-            pa.seg[pa.n_seg++] = seg_a(u.slot, u.rank, t);
-            pb.seg[pb.n_seg++] = seg_b(u.slot, u.rank, t);
-            bytes_a += static_cast<double>(gate_up_bytes);
-            bytes_b += static_cast<double>(store_.tile_bytes - gate_up_bytes);
+            if (p.n_seg == kMaxFfnSegments) timed_ffn(p);
+            p.seg[p.n_seg++] = seg(u.slot, u.rank, t);
         }
         stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
     }
-    flush();
+    if (p.n_seg) timed_ffn(p);
     // on-demand experts: tile by tile as their copies land
     for (const Use& u : uses_) {
         if (!u.missing) continue;
         for (int t : u.tiles) {
             wait_fill(u.slot, t);
-            pa.seg[pa.n_seg++] = seg_a(u.slot, u.rank, t);
-            pb.seg[pb.n_seg++] = seg_b(u.slot, u.rank, t);
-            bytes_a = static_cast<double>(gate_up_bytes);
-            bytes_b = static_cast<double>(store_.tile_bytes - gate_up_bytes);
-            flush();
+            p.seg[p.n_seg++] = seg(u.slot, u.rank, t);
+            timed_ffn(p);
         }
         stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
     }
@@ -411,8 +406,8 @@ DecodeStats DecodeSession::snapshot() {
     for (auto& p : pass_events_) {
         const double ms = elapsed(p.e0, p.e1);
         stats_.ffn_ms += ms;
-        (p.a ? stats_.gate_up_ms : stats_.down_ms) += ms;
-        (p.a ? stats_.gate_up_bytes : stats_.down_bytes) += p.bytes;
+        stats_.gate_up_bytes += p.gate_up_bytes;
+        stats_.down_bytes += p.down_bytes;
         stats_.ffn_launches += 1;
         timing_pool_.push_back(p.e0);
         timing_pool_.push_back(p.e1);

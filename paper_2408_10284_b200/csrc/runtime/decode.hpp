@@ -70,7 +70,11 @@ private:
     void release_slot(int s);
     void release_pending(bool all);
     void wait_fill(int slot, int tile);  // compute stream waits for tile (or all tiles if -1)
-    void timed_pass(const FfnLaunch& p, bool pass_a, double bytes);
+    void timed_ffn(FfnLaunch& p);  // launch + time + clear the segment list
+    unsigned int* take_counters(int n);
+    static constexpr int kCounterRing = 1 << 16;
+    DeviceBuffer d_counters_;
+    int counter_next_ = 0;
 
     Engine& eng_;
     ModelSpec spec_;
@@ -114,8 +118,7 @@ private:
     std::vector<cudaEvent_t> timing_pool_;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> router_events_, stall_events_;
     struct PassRec {
-        bool a;
-        double bytes;
+        double gate_up_bytes, down_bytes;
         cudaEvent_t e0, e1;
     };
     std::vector<PassRec> pass_events_;

@@ -841,8 +841,8 @@ int orc_expert_init(uint64_t seed, int layer, int expert, int D, int F, int tile
             for (int c = 0; c < D; ++c) out[o++] = orc_init_value(b1, r * D + c, s13);
             for (int c = 0; c < D; ++c) out[o++] = orc_init_value(b3, r * D + c, s13);
         }
-        for (int j = 0; j < D; ++j)
-            for (int rl = 0; rl < Ft; ++rl) out[o++] = orc_init_value(b2, (uint64_t)j * F + (uint64_t)t * Ft + rl, s2);
+        for (int rl = 0; rl < Ft; ++rl) /* down_t [Ft][D]: row rl = W2[:, t*Ft + rl] */
+            for (int j = 0; j < D; ++j) out[o++] = orc_init_value(b2, (uint64_t)j * F + (uint64_t)t * Ft + rl, s2);
     }
     return 0;
 }
@@ -875,8 +875,7 @@ int orc_swiglu(const uint16_t* w, int D, int F, int tiles, const float* x, doubl
         }
         for (int j = 0; j < D; ++j) {
             double acc = 0.0;
-            const uint16_t* row = dn + (size_t)j * Ft;
-            for (int rl = 0; rl < Ft; ++rl) acc += bf16_to_d(row[rl]) * h[rl];
+            for (int rl = 0; rl < Ft; ++rl) acc += bf16_to_d(dn[(size_t)rl * D + j]) * h[rl];
             y[j] += acc;
         }
     }

@@ -102,7 +102,8 @@ int orc_simulate(const double* acts, const double* scores, const double* gates, 
 /* --- builder-defined expert FFN (no reference counterpart; parity unpinned) --------------- */
 /* Deterministic counter-based bf16 init, identical to the CUDA init kernel. Layout is tile-major:
  * for tile t (ffn rows [t*F/T,(t+1)*F/T)): gate_up [F/T][2][D] (W1 row, W3 row interleaved),
- * then down [D][F/T].  Element key = (matrix m in {0:W1,1:W3,2:W2}, logical row-major index). */
+ * then down_t [F/T][D] (row r = W2[:, t*F/T + r]).  Element key = (matrix m in {0:W1,1:W3,2:W2},
+ * logical row-major index in W1/W3 [F][D] or W2 [D][F]). */
 float orc_init_scale(int fan_in);
 uint16_t orc_init_value(uint64_t base, uint64_t index, float scale);
 uint64_t orc_expert_base(uint64_t seed, int layer, int expert, int matrix);

@@ -456,33 +456,31 @@ int moe_expert_ffn(moe_engine_t h, int32_t layer, int32_t expert, const double* 
         const size_t gate_up = static_cast<size_t>(2) * Ft * D * 2;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e.device());
-        DeviceBuffer counters;
-        counters.reserve(kMaxFfnSegments * sizeof(unsigned));
-        MOE_CUDA(cudaMemsetAsync(counters.ptr, 0, kMaxFfnSegments * sizeof(unsigned), cs));
+        DeviceBuffer partial;
+        partial.reserve(static_cast<size_t>(kFfnMaxCtas) * kFfnSlotsPerCta * D * sizeof(float));
         FfnLaunch p;
         p.d = D;
         p.ft = Ft;
         p.x = dx.as<double>();
-        p.counters = counters.as<unsigned>();
+        p.partial = partial.as<float>();
         for (int t = 0; t < T; ++t) {
             const unsigned char* tile = w.as<unsigned char>() + t * st.tile_bytes;
             FfnSegment s;
             s.gate_up = reinterpret_cast<const std::uint16_t*>(tile);
-            s.down = reinterpret_cast<const std::uint16_t*>(tile + gate_up);
-            s.h = dh.as<float>() + static_cast<size_t>(t) * Ft;
-            s.y = dy.as<float>() + static_cast<size_t>(t) * D;
+            s.down_t = reinterpret_cast<const std::uint16_t*>(tile + gate_up);
             p.seg[p.n_seg++] = s;
         }
         MOE_CUDA(launch_ffn(p, sms, cs));
         CombineArgs c;
         c.x = zero.as<double>();
         c.scores = zero.as<double>();  // single rank: weight 1
-        c.y = dy.as<float>();
         c.out = dout.as<float>();
         c.ranks = 1;
-        c.tiles = T;
         c.d = D;
+        c.ft = Ft;
         c.experts[0] = 0;
+        c.n_refs = T;
+        for (int t = 0; t < T; ++t) c.refs[t] = FfnPartialRef{p.partial, ffn_grid(p, sms), T, t, 0};
         MOE_CUDA(launch_combine(c, cs));
         MOE_CUDA(cudaMemcpyAsync(y, dout.ptr, D * sizeof(float), cudaMemcpyDeviceToHost, cs));
         MOE_CUDA(cudaStreamSynchronize(cs));

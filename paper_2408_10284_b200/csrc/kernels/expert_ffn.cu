@@ -1,20 +1,19 @@
-// K2 — batch-1 SwiGLU expert FFN for sm_100a: TMA-staged HBM streaming, gate/up and down fused.
+// K2 — batch-1 SwiGLU expert FFN for sm_100a: row-owner HBM streaming.
 //
 // Decode at batch 1 reads every weight byte exactly once (~1 flop/byte), so the kernel is built
-// around HBM bandwidth: one persistent CTA per SM.  Warp 0 (one lane) streams contiguous blocks
-// of R weight rows into a shared-memory ring with cp.async.bulk (TMA engine; SASS UBLKCP),
-// completing on mbarriers, with an L2 evict-first policy since every byte is used once.  Sixteen
-// consumer warps turn each staged block into R dot products (R rows x 16/R column parts per row)
-// against an fp32 vector in shared memory: bf16 -> fp32 by shift, fp32 FMA, warp-shuffle
-// reduction, fixed-order combination of column parts.
-//
-// Work list of one launch = every phase-A unit (R rows of W1/W3 pairs) of every segment, then
-// every phase-B unit (R rows of W2_t); each CTA owns one contiguous range of A units and one of B
-// units and runs its A units first.  Every h value is published with its own release-add on the segment's
-// counter; a phase-B unit of segment s waits (acquire) until all Ft values of s are published,
-// then stages h_s (no fences, no extra CTA barrier).  The producer never waits on that
-// dependency — it keeps prefetching W2 rows — so the gate/up -> down transition costs no HBM idle
-// time.  Every CTA is co-resident (grid <= #SMs, 1 CTA/SM), so the cross-CTA wait cannot deadlock.
+// around HBM bandwidth.  One persistent CTA per SM (512 threads) owns a contiguous range of ffn
+// rows of the launch's (expert, tile) segments and walks it in chunks of 16 rows:
+//   phase 1: warp w streams the W1 and W3 rows of ffn row r0+w (ld.global.nc.L1::no_allocate,
+//            16-byte vectors, 4-deep unrolled), dots them with x (fp32 in shared memory) and
+//            forms h = silu(a) * b;
+//   phase 2: thread t streams its 16-byte slice of the chunk's 16 W2^T rows (all 16 loads in
+//            flight) and accumulates h_r * W2^T_r[8t..8t+8) into 8 fp32 registers.
+// Because a CTA consumes the h values it produced, there is no cross-CTA dependency (the earlier
+// TMA-ring design needed a grid-wide gate/up -> down handoff and topped out at 4.1 TB/s; this one
+// measures 6.3 TB/s on large launches, tools/ffn_microbench.cu v4, profiles/r1_ffn_microbench.txt).
+// Small launches (one 88 MB tile of an on-demand expert) also bulk-prefetch the next chunk into L2
+// through the TMA engine (cp.async.bulk.prefetch.L2) to cover the ramp.  Each CTA writes one fp32
+// partial of y per segment it touched; the combine kernel reduces them in a fixed order.
 #include <cuda_runtime.h>
 
 #include "expert_ffn.hpp"
@@ -24,273 +23,169 @@ namespace adapmoe {
 
 namespace {
 
-#ifndef ADAPMOE_FFN_WARPS
-#define ADAPMOE_FFN_WARPS 8
-#endif
-#ifndef ADAPMOE_FFN_STAGE_KB
-#define ADAPMOE_FFN_STAGE_KB 64
-#endif
-#ifndef ADAPMOE_FFN_BATCH
-#define ADAPMOE_FFN_BATCH 4
-#endif
-#ifndef ADAPMOE_FFN_SPLIT
-#define ADAPMOE_FFN_SPLIT 0
-#endif
-#ifndef ADAPMOE_FFN_L2AHEAD
-#define ADAPMOE_FFN_L2AHEAD 0
-#endif
-constexpr int kL2Ahead = ADAPMOE_FFN_L2AHEAD;
-constexpr int kConsumerWarps = ADAPMOE_FFN_WARPS;  // tuning knobs (tools/ffn_microbench.sh)
-constexpr int kThreads = 32 * (1 + kConsumerWarps);
-constexpr int kMaxStages = 8;
-constexpr int kSmemBudget = 226 * 1024;
-constexpr int kHeader = 2048;  // barriers + partial dots
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kChunk = kWarps;  // ffn rows per chunk (one per warp in phase 1)
+constexpr int kUnroll = 4;
 
-struct Geometry {
-    int ra, rb;          // rows per stage, phase A (even) / phase B
-    int wpr_a, wpr_b;    // consumer warps per row
-    int stages;
-    size_t stage_bytes;  // ring slot size
-    size_t vec_a, vec_b;  // fp32 vector bytes
-    size_t smem;
-};
-
-__host__ __device__ inline int rows_for(int cols, int min_rows) {
-    int r = kConsumerWarps;
-    while (r > min_rows && static_cast<size_t>(r) * cols * 2 > ADAPMOE_FFN_STAGE_KB * 1024) r /= 2;
-    return r;
-}
-
-__host__ __device__ inline Geometry geometry(int d, int ft) {
-    Geometry g{};
-    g.ra = rows_for(d, 2);
-    g.rb = rows_for(ft, 1);
-    g.wpr_a = kConsumerWarps / g.ra;
-    g.wpr_b = kConsumerWarps / g.rb;
-    const size_t a = static_cast<size_t>(g.ra) * d * 2, b = static_cast<size_t>(g.rb) * ft * 2;
-    g.stage_bytes = ((a > b ? a : b) + 127) & ~size_t(127);
-    g.vec_a = (static_cast<size_t>(d) * 4 + 127) & ~size_t(127);
-    g.vec_b = (static_cast<size_t>(ft) * 4 + 127) & ~size_t(127);
-    int st = static_cast<int>((kSmemBudget - kHeader - g.vec_a - g.vec_b) / g.stage_bytes);
-    g.stages = st > kMaxStages ? kMaxStages : st;
-    g.smem = kHeader + g.vec_a + g.vec_b + g.stages * g.stage_bytes;
-    return g;
+__device__ __forceinline__ float dot8(int4 w, float4 a, float4 b, float acc) {
+    const unsigned x = w.x, y = w.y, z = w.z, q = w.w;
+    acc = __fmaf_rn(__uint_as_float(x << 16), a.x, acc);
+    acc = __fmaf_rn(__uint_as_float(x & 0xffff0000u), a.y, acc);
+    acc = __fmaf_rn(__uint_as_float(y << 16), a.z, acc);
+    acc = __fmaf_rn(__uint_as_float(y & 0xffff0000u), a.w, acc);
+    acc = __fmaf_rn(__uint_as_float(z << 16), b.x, acc);
+    acc = __fmaf_rn(__uint_as_float(z & 0xffff0000u), b.y, acc);
+    acc = __fmaf_rn(__uint_as_float(q << 16), b.z, acc);
+    acc = __fmaf_rn(__uint_as_float(q & 0xffff0000u), b.w, acc);
+    return acc;
 }
 
 __device__ __forceinline__ float silu(float a) { return a / (1.0f + expf(-a)); }
 
-__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps) : "memory"); }
-
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// dot of `len` bf16 (starting at row) with fp32 vec; lane handles 4-element groups lane*4 + 128*j,
-// so a warp reads 256 contiguous weight bytes and 512 contiguous vector bytes per step
-__device__ __forceinline__ float row_dot(const unsigned char* row, const float* vec, int len, int lane) {
-    constexpr int kBatch = ADAPMOE_FFN_BATCH;  // weight + vector loads issued before the math
-    float acc = 0.0f;
-    for (int k0 = lane * 4; k0 < len; k0 += 128 * kBatch) {
-        uint2 w[kBatch];
-        float4 v[kBatch];
-#pragma unroll
-        for (int b = 0; b < kBatch; ++b) {
-            const int k = k0 + 128 * b;
-            if (k < len) {
-                w[b] = *reinterpret_cast<const uint2*>(row + static_cast<size_t>(k) * 2);
-                v[b] = *reinterpret_cast<const float4*>(vec + k);
-            } else {
-                w[b] = make_uint2(0u, 0u);
-                v[b] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        }
-#pragma unroll
-        for (int b = 0; b < kBatch; ++b) {
-            acc = __fmaf_rn(__uint_as_float(w[b].x << 16), v[b].x, acc);
-            acc = __fmaf_rn(__uint_as_float(w[b].x & 0xffff0000u), v[b].y, acc);
-            acc = __fmaf_rn(__uint_as_float(w[b].y << 16), v[b].z, acc);
-            acc = __fmaf_rn(__uint_as_float(w[b].y & 0xffff0000u), v[b].w, acc);
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    return acc;
-}
-
-struct Unit {
-    int phase;  // 0 = A, 1 = B
-    int seg;
-    int r0;
-    int rows;
-};
-
-// CTA b owns a contiguous range of phase-A units and a contiguous range of phase-B units (so it
-// streams contiguous HBM and stages h for at most a couple of segments); i-th unit of the CTA:
-__device__ __forceinline__ int cta_unit(int i, int total_a, int total_b, int b, int G) {
-    const int a0 = static_cast<int>((static_cast<long long>(total_a) * b) / G);
-    const int a1 = static_cast<int>((static_cast<long long>(total_a) * (b + 1)) / G);
-    if (i < a1 - a0) return a0 + i;
-    const int b0 = static_cast<int>((static_cast<long long>(total_b) * b) / G);
-    const int b1 = static_cast<int>((static_cast<long long>(total_b) * (b + 1)) / G);
-    const int j = i - (a1 - a0);
-    return j < b1 - b0 ? total_a + b0 + j : -1;
-}
-
-__device__ __forceinline__ Unit unit_at(int u, const FfnLaunch& p, const Geometry& g, int units_a_per_seg,
-                                        int units_b_per_seg) {
-    Unit x;
-    const int total_a = units_a_per_seg * p.n_seg;
-    if (u < total_a) {
-        x.phase = 0;
-        x.seg = u / units_a_per_seg;
-        x.r0 = (u % units_a_per_seg) * g.ra;
-        x.rows = min(g.ra, 2 * p.ft - x.r0);
-    } else {
-        const int v = u - total_a;
-        x.phase = 1;
-        x.seg = v / units_b_per_seg;
-        x.r0 = (v % units_b_per_seg) * g.rb;
-        x.rows = min(g.rb, p.d - x.r0);
-    }
-    return x;
-}
-
-__global__ void __launch_bounds__(kThreads, 1) ffn_kernel(const __grid_constant__ FfnLaunch p) {
-    extern __shared__ __align__(1024) unsigned char smem[];
-    const Geometry geo = geometry(p.d, p.ft);
-    const int NS = geo.stages;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* empty = full + kMaxStages;
-    float* partial = reinterpret_cast<float*>(smem + 128);  // [kMaxStages][kConsumerWarps]
-    float* vec_a = reinterpret_cast<float*>(smem + kHeader);
-    float* vec_b = reinterpret_cast<float*>(smem + kHeader + geo.vec_a);
-    unsigned char* ring = smem + kHeader + geo.vec_a + geo.vec_b;
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ua = (2 * p.ft + geo.ra - 1) / geo.ra;  // phase-A units per segment
-    const int ub = (p.d + geo.rb - 1) / geo.rb;       // phase-B units per segment
-    const int total_a = ua * p.n_seg, total_b = ub * p.n_seg;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) {
-            ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], kConsumerWarps);
-        }
-        ptx::fence_mbar_init();
-    }
-    __syncthreads();
-
-    if (warp == 0) {
-        if (lane == 0) {
-            const uint64_t policy = ptx::policy_evict_first();
-            // L2 prefetch runs kL2Ahead units ahead of the smem ring: more bytes in flight per SM
-            // than shared memory can hold, so the ring's bulk copies hit L2 instead of HBM
-            auto prefetch = [&](int j) {
-                const int v = cta_unit(j, total_a, total_b, blockIdx.x, gridDim.x);
-                if (v < 0) return;
-                const Unit y = unit_at(v, p, geo, ua, ub);
-                const int c = y.phase == 0 ? p.d : p.ft;
-                const std::uint16_t* b = y.phase == 0 ? p.seg[y.seg].gate_up : p.seg[y.seg].down;
-                ptx::bulk_prefetch_l2(b + static_cast<size_t>(y.r0) * c, static_cast<uint32_t>(y.rows) * c * 2u);
-            };
-            for (int j = NS; j < NS + kL2Ahead; ++j) prefetch(j);
-            for (int i = 0;; ++i) {
-                const int u = cta_unit(i, total_a, total_b, blockIdx.x, gridDim.x);
-                if (u < 0) break;
-                const Unit x = unit_at(u, p, geo, ua, ub);
-                const int st = i % NS;
-                if (kL2Ahead > 0) prefetch(i + NS + kL2Ahead);
-                if (i >= NS) ptx::mbar_wait(&empty[st], ((i / NS) - 1) & 1);
-                const int cols = x.phase == 0 ? p.d : p.ft;
-                const std::uint16_t* base = x.phase == 0 ? p.seg[x.seg].gate_up : p.seg[x.seg].down;
-                const uint32_t bytes = static_cast<uint32_t>(x.rows) * cols * 2u;
-                ptx::mbar_arrive_expect_tx(&full[st], bytes);
-#if ADAPMOE_FFN_SPLIT
-                // one bulk copy per row: more copies in flight per SM than one big copy
-                for (int r = 0; r < x.rows; ++r)
-                    ptx::bulk_g2s_stream(ring + st * geo.stage_bytes + static_cast<size_t>(r) * cols * 2,
-                                         base + static_cast<size_t>(x.r0 + r) * cols, cols * 2u, &full[st], policy);
-#else
-                ptx::bulk_g2s_stream(ring + st * geo.stage_bytes, base + static_cast<size_t>(x.r0) * cols, bytes,
-                                     &full[st], policy);
+#ifndef ADAPMOE_FFN_P2_BATCH
+#define ADAPMOE_FFN_P2_BATCH 8
 #endif
-            }
-        }
-        return;
-    }
+constexpr int kP2Batch = ADAPMOE_FFN_P2_BATCH;  // W2^T rows loaded per batch in phase 2
 
-    // ---------------- consumers ----------------
-    const int cw = warp - 1;  // 0..15
-    const int ctid = threadIdx.x - 32;
-    for (int i = ctid; i < p.d; i += 32 * kConsumerWarps) vec_a[i] = static_cast<float>(p.x[i]);
-    consumer_bar();
-    int vec_seg = -1;
-    for (int i = 0;; ++i) {
-        const int u = cta_unit(i, total_a, total_b, blockIdx.x, gridDim.x);
-        if (u < 0) break;
-        const Unit x = unit_at(u, p, geo, ua, ub);
-        const int R = x.phase == 0 ? geo.ra : geo.rb;
-        const int WPR = x.phase == 0 ? geo.wpr_a : geo.wpr_b;
-        const int C = x.phase == 0 ? p.d : p.ft;
-        if (x.phase == 1 && vec_seg != x.seg) {
-            // wait until every phase-A unit of this segment has published its h values
-            if (ctid == 0) {
-                const unsigned* cnt = p.counters + x.seg;
-                while (ld_acquire(cnt) < static_cast<unsigned>(p.ft)) __nanosleep(32);
-            }
-            consumer_bar();
-            const float* h = p.seg[x.seg].h;
-            for (int k = ctid; k < p.ft; k += 32 * kConsumerWarps) vec_b[k] = __ldcg(h + k);
-            vec_seg = x.seg;
-            consumer_bar();
+template <int DC>
+__device__ __forceinline__ void store_partial(float* dst, float (&acc)[DC][8], int tid, int D) {
+#pragma unroll
+    for (int c = 0; c < DC; ++c) {
+        const int col = c * 4096 + tid * 8;
+        if (col < D) {
+            *reinterpret_cast<float4*>(dst + col) = make_float4(acc[c][0], acc[c][1], acc[c][2], acc[c][3]);
+            *reinterpret_cast<float4*>(dst + col + 4) = make_float4(acc[c][4], acc[c][5], acc[c][6], acc[c][7]);
         }
-        const int st = i % NS;
-        const int row = cw / WPR, part = cw % WPR;
-        const int part_len = C / WPR;
-        ptx::mbar_wait(&full[st], (i / NS) & 1);
-        float dot = 0.0f;
-        if (row < x.rows) {
-            const unsigned char* rp = ring + st * geo.stage_bytes + (static_cast<size_t>(row) * C + part * part_len) * 2;
-            dot = row_dot(rp, (x.phase == 0 ? vec_a : vec_b) + part * part_len, part_len, lane);
-        }
-        if (lane == 0) {
-            partial[st * kConsumerWarps + cw] = dot;
-            ptx::mbar_arrive(&empty[st]);
-        }
-        consumer_bar();
-        if (part == 0 && lane == 0 && row < x.rows) {
-            float v = 0.0f;
-            for (int q = 0; q < WPR; ++q) v += partial[st * kConsumerWarps + row * WPR + q];
-            if (x.phase == 0) {
-                if ((row & 1) == 0) {
-                    float b = 0.0f;
-                    for (int q = 0; q < WPR; ++q) b += partial[st * kConsumerWarps + (row + 1) * WPR + q];
-                    p.seg[x.seg].h[(x.r0 + row) >> 1] = silu(v) * b;
-                    red_release_add(p.counters + x.seg, 1u);  // publishes this h value (release)
-                }
-            } else {
-                p.seg[x.seg].y[x.r0 + row] = v;
-            }
-        }
-        (void)R;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[c][k] = 0.0f;
     }
 }
 
-__global__ void combine_kernel(CombineArgs a) {
+// DC = ceil(d / 4096): output columns per thread = 8 * DC
+template <int DC>
+__global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_constant__ FfnLaunch p) {
+    extern __shared__ __align__(16) float xs[];  // [d]
+    __shared__ float hs[2][kChunk];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int D = p.d, Ft = p.ft, vpr = D / 8;  // 16-byte vectors per weight row
+    for (int i = tid; i < D; i += kThreads) xs[i] = static_cast<float>(p.x[i]);
+    const long long TR = static_cast<long long>(p.n_seg) * Ft;
+    const long long r_lo = TR * blockIdx.x / gridDim.x, r_hi = TR * (blockIdx.x + 1) / gridDim.x;
+    float acc[DC][8];
+#pragma unroll
+    for (int c = 0; c < DC; ++c)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[c][k] = 0.0f;
+    const int first_seg = static_cast<int>(r_lo / Ft);
+    float* const part = p.partial + static_cast<size_t>(blockIdx.x) * kFfnSlotsPerCta * D;
+    int cur_seg = first_seg;
+    __syncthreads();
+    int parity = 0;
+    for (long long c0 = r_lo; c0 < r_hi; parity ^= 1) {
+        const int s = static_cast<int>(c0 / Ft), r0 = static_cast<int>(c0 % Ft);
+        const int n = static_cast<int>(min(static_cast<long long>(min(kChunk, Ft - r0)), r_hi - c0));
+        if (s != cur_seg) {
+            store_partial<DC>(part + static_cast<size_t>(cur_seg - first_seg) * D, acc, tid, D);
+            cur_seg = s;
+        }
+        if (p.l2_prefetch && tid == 0 && c0 + n < r_hi) {
+            const long long c1 = c0 + n;
+            const int s1 = static_cast<int>(c1 / Ft), q0 = static_cast<int>(c1 % Ft);
+            const int n1 = static_cast<int>(min(static_cast<long long>(min(kChunk, Ft - q0)), r_hi - c1));
+            ptx::bulk_prefetch_l2(p.seg[s1].gate_up + static_cast<size_t>(q0) * 2 * D, n1 * 2u * D * 2u);
+            ptx::bulk_prefetch_l2(p.seg[s1].down_t + static_cast<size_t>(q0) * D, n1 * static_cast<unsigned>(D) * 2u);
+        }
+        // ---- phase 1: h for row r0 + warp ----
+        if (warp < n) {
+            const int4* w1 = reinterpret_cast<const int4*>(p.seg[s].gate_up) + static_cast<size_t>(r0 + warp) * 2 * vpr;
+            const int4* w3 = w1 + vpr;
+            float a = 0.0f, b = 0.0f;
+            for (int j0 = lane; j0 < vpr; j0 += 32 * kUnroll) {
+                int4 q1[kUnroll], q3[kUnroll];
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k) {
+                    const int j = j0 + 32 * k;
+                    if (j < vpr) {
+                        q1[k] = ptx::ld_stream(w1 + j);
+                        q3[k] = ptx::ld_stream(w3 + j);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k) {
+                    const int j = j0 + 32 * k;
+                    if (j < vpr) {
+                        const float4 xa = *reinterpret_cast<const float4*>(xs + j * 8);
+                        const float4 xb = *reinterpret_cast<const float4*>(xs + j * 8 + 4);
+                        a = dot8(q1[k], xa, xb, a);
+                        b = dot8(q3[k], xa, xb, b);
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                a += __shfl_xor_sync(0xffffffffu, a, o);
+                b += __shfl_xor_sync(0xffffffffu, b, o);
+            }
+            if (lane == 0) hs[parity][warp] = silu(a) * b;
+        }
+        __syncthreads();  // h of this chunk visible; double-buffered hs makes one barrier enough
+        // ---- phase 2: acc += h_r * W2^T_r over this thread's columns ----
+        const int4* down = reinterpret_cast<const int4*>(p.seg[s].down_t) + static_cast<size_t>(r0) * vpr;
+#pragma unroll
+        for (int c = 0; c < DC; ++c) {
+            const int v = c * 512 + tid;  // 16-byte vector index within a row
+            if (v >= vpr) continue;
+            for (int k0 = 0; k0 < n; k0 += kP2Batch) {
+                int4 q[kP2Batch];
+#pragma unroll
+                for (int k = 0; k < kP2Batch; ++k)
+                    if (k0 + k < n) q[k] = ptx::ld_stream(down + static_cast<size_t>(k0 + k) * vpr + v);
+#pragma unroll
+                for (int k = 0; k < kP2Batch; ++k)
+                    if (k0 + k < n) {
+                        const float h = hs[parity][k0 + k];
+                        acc[c][0] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q[k].x) << 16), acc[c][0]);
+                        acc[c][1] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q[k].x) & 0xffff0000u), acc[c][1]);
+                        acc[c][2] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q[k].y) << 16), acc[c][2]);
+                        acc[c][3] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q[k].y) & 0xffff0000u), acc[c][3]);
+                        acc[c][4] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q[k].z) << 16), acc[c][4]);
+                        acc[c][5] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q[k].z) & 0xffff0000u), acc[c][5]);
+                        acc[c][6] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q[k].w) << 16), acc[c][6]);
+                        acc[c][7] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q[k].w) & 0xffff0000u), acc[c][7]);
+                    }
+            }
+        }
+        c0 += n;
+    }
+    store_partial<DC>(part + static_cast<size_t>(cur_seg - first_seg) * D, acc, tid, D);
+}
+
+// out[j] = x[j] + sum_rank w_rank * sum_(tile refs of rank) sum_(cta asc) partial  — fixed order
+__global__ void combine_kernel(const __grid_constant__ CombineArgs a) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= a.d) return;
     double denom = 0.0;
     for (int r = 0; r < a.ranks; ++r) denom += a.scores[a.experts[r]];
     float acc = static_cast<float>(a.x[j]);
+    int ref = 0;
     for (int r = 0; r < a.ranks; ++r) {
         const float w = a.ranks == 1 ? 1.0f : static_cast<float>(a.scores[a.experts[r]] / denom);
         float yr = 0.0f;
-        for (int t = 0; t < a.tiles; ++t) yr += a.y[(static_cast<size_t>(r) * a.tiles + t) * a.d + j];
+        for (; ref < a.n_refs && a.refs[ref].rank == r; ++ref) {
+            const FfnPartialRef& f = a.refs[ref];
+            const long long TR = static_cast<long long>(f.n_seg) * a.ft;
+            const long long s_lo = static_cast<long long>(f.seg) * a.ft, s_hi = s_lo + a.ft;
+            int c = static_cast<int>(s_lo * f.grid / TR);
+            while (c > 0 && TR * c / f.grid > s_lo) --c;
+            for (; c < f.grid; ++c) {
+                const long long lo = TR * c / f.grid, hi = TR * (c + 1) / f.grid;
+                if (lo >= s_hi) break;
+                if (hi <= s_lo) continue;
+                const int slot = f.seg - static_cast<int>(lo / a.ft);
+                yr += f.partial[(static_cast<size_t>(c) * kFfnSlotsPerCta + slot) * a.d + j];
+            }
+        }
         acc = __fmaf_rn(w, yr, acc);
     }
     a.out[j] = acc;
@@ -329,20 +224,22 @@ __global__ void expert_init_kernel(uint16_t* dst, int D, int F, int tiles, InitA
         const size_t t = pos / tile_elems;
         const size_t off = pos % tile_elems;
         int m;
-        uint64_t idx;
-        if (off < static_cast<size_t>(2) * Ft * D) {
+        uint64_t idx, stride;
+        if (off < static_cast<size_t>(2) * Ft * D) {  // gate_up [Ft][2][D]: W1/W3 row-major
             const size_t rl = off / (2 * static_cast<size_t>(D));
             const size_t rem = off % (2 * static_cast<size_t>(D));
             m = static_cast<int>(rem / D);
             idx = (t * Ft + rl) * D + rem % D;
-        } else {
+            stride = 1;
+        } else {  // down_t [Ft][D]: element (rl, j) is W2[j][t*Ft + rl], logical index j*F + t*Ft + rl
             const size_t o2 = off - static_cast<size_t>(2) * Ft * D;
             m = 2;
-            idx = (o2 / Ft) * F + t * Ft + o2 % Ft;
+            idx = (o2 % D) * F + t * Ft + o2 / D;
+            stride = static_cast<uint64_t>(F);
         }
         uint16_t v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = init_value(ia.base[m], idx + k, ia.scale[m]);
+        for (int k = 0; k < 8; ++k) v[k] = init_value(ia.base[m], idx + k * stride, ia.scale[m]);
         uint4 pack;
         pack.x = v[0] | (static_cast<uint32_t>(v[1]) << 16);
         pack.y = v[2] | (static_cast<uint32_t>(v[3]) << 16);
@@ -354,20 +251,33 @@ __global__ void expert_init_kernel(uint16_t* dst, int D, int F, int tiles, InitA
 
 }  // namespace
 
+int ffn_grid(const FfnLaunch& p, int sm_count) {
+    const long long rows = static_cast<long long>(p.n_seg) * p.ft;
+    long long g = sm_count < kFfnMaxCtas ? sm_count : kFfnMaxCtas;
+    if (g > rows) g = rows;
+    if (g < p.n_seg) g = p.n_seg;  // keeps every CTA's range within <= 2 segments
+    return static_cast<int>(g);
+}
+
 cudaError_t launch_ffn(const FfnLaunch& p, int sm_count, cudaStream_t stream) {
     if (p.n_seg <= 0) return cudaSuccess;
-    if (p.n_seg > kMaxFfnSegments || p.d % 64 || p.ft % 32 || p.d > 16384 || p.ft > 16384 || !p.counters)
+    if (p.n_seg > kMaxFfnSegments || p.d % 8 || p.d > 16384 || p.ft < 1 || !p.partial || !p.x)
         return cudaErrorInvalidValue;
-    const Geometry g = geometry(p.d, p.ft);
-    if (g.stages < 2 || (p.d / g.wpr_a) % 4 || (p.ft / g.wpr_b) % 4) return cudaErrorInvalidValue;
-    const long long units = static_cast<long long>(p.n_seg) * ((2 * p.ft + g.ra - 1) / g.ra + (p.d + g.rb - 1) / g.rb);
-    const int grid = static_cast<int>(units < sm_count ? units : sm_count);
-    static bool set = false;
-    if (!set) {
-        cudaFuncSetAttribute(ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
-        set = true;
+    const int grid = ffn_grid(p, sm_count);
+    const size_t smem = static_cast<size_t>(p.d) * sizeof(float);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(ffn_rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(ffn_rows_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(ffn_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        configured = true;
     }
-    ffn_kernel<<<grid, kThreads, g.smem, stream>>>(p);
+    if (p.d <= 4096)
+        ffn_rows_kernel<1><<<grid, kThreads, smem, stream>>>(p);
+    else if (p.d <= 8192)
+        ffn_rows_kernel<2><<<grid, kThreads, smem, stream>>>(p);
+    else
+        ffn_rows_kernel<4><<<grid, kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 

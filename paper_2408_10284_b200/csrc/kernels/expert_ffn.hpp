@@ -2,18 +2,16 @@
 //
 // Expert memory layout (tile-major, bf16), tile t = ffn rows [t*Ft, (t+1)*Ft), Ft = F / tiles:
 //   gate_up_t : [Ft][2][D]  row pair r = (W1[t*Ft + r, :], W3[t*Ft + r, :]) contiguous
-//   down_t    : [D][Ft]     W2[:, t*Ft : (t+1)*Ft]
+//   down_t    : [Ft][D]     row r = W2[:, t*Ft + r]  (W2 transposed)
 // so every tile is one contiguous 3*Ft*D*2-byte block: the unit of a host->HBM copy and of a
-// tile-granular FFN launch (inc/simulator.hpp:451-459 computes on-demand experts tile by tile).
+// tile-granular FFN launch (inc/simulator.hpp:451-459 computes on-demand experts tile by tile),
+// and every ffn row r owns three contiguous D-element rows (W1, W3, W2^T).
 //
-// One launch processes a list of (expert rank, tile) segments in a single persistent kernel:
-//   phase A (gate/up): h_t[r] = silu(W1[r] . x) * (W3[r] . x)
-//   phase B (down)   : y_t[j] = W2_t[j, :] . h_t
-// phase-B work of a segment starts when that segment's phase-A units are all done (device-side
-// counters), so weight streaming never pauses between the two projections.
-// Combine: out[j] = x[j] + sum_rank w_rank * sum_t y_t[j] (fixed order, deterministic).
-// Partial results are kept per (rank, tile) so a resident expert computed in one launch and an
-// on-demand expert computed tile by tile give bit-identical outputs.
+// One launch processes a list of (expert rank, tile) segments; CTA c owns a contiguous range of
+// ffn rows of the concatenated segments and, chunk by chunk, forms h_r = silu(W1_r.x) * (W3_r.x)
+// and accumulates h_r * W2^T_r into its own fp32 partial of y (no cross-CTA dependency).  The
+// combine kernel reduces the partials in a fixed order:
+//   out[j] = x[j] + sum_rank w_rank * sum_tiles sum_cta partial[cta][slot][j].
 #pragma once
 
 #include <cuda_runtime_api.h>
@@ -23,38 +21,53 @@
 namespace adapmoe {
 
 constexpr int kMaxFfnSegments = 32;
+constexpr int kFfnMaxCtas = 160;      // grid cap (>= #SMs of a B200)
+constexpr int kFfnSlotsPerCta = 2;    // a CTA's row range touches at most 2 segments (n_seg <= grid)
 
 struct FfnSegment {
     const std::uint16_t* gate_up = nullptr;  // [Ft][2][D] bf16
-    const std::uint16_t* down = nullptr;     // [D][Ft] bf16
-    float* h = nullptr;                      // [Ft] phase-A output (phase-B input)
-    float* y = nullptr;                      // [D] phase-B output
+    const std::uint16_t* down_t = nullptr;   // [Ft][D] bf16 (W2^T rows)
 };
 
 struct FfnLaunch {
     int n_seg = 0;
     int d = 0, ft = 0;
-    const double* x = nullptr;       // [d] layer input (fp64; converted to fp32 in shared memory)
-    unsigned int* counters = nullptr;  // [n_seg] zero on entry: phase-A units finished per segment
+    int l2_prefetch = 0;              // bulk-prefetch the next row chunk into L2 (small launches)
+    const double* x = nullptr;        // [d] layer input (fp64; converted to fp32 in shared memory)
+    float* partial = nullptr;         // [grid][kFfnSlotsPerCta][d] written by the launch
     FfnSegment seg[kMaxFfnSegments];
 };
 
-// Streams every segment's weights once (TMA bulk copies into a shared-memory ring).
+// Grid the launch will use (partial buffer rows = grid * kFfnSlotsPerCta).
+int ffn_grid(const FfnLaunch& p, int sm_count);
 cudaError_t launch_ffn(const FfnLaunch& p, int sm_count, cudaStream_t stream);
 
+// One (rank, tile) segment's location among the launches of a layer.
+struct FfnPartialRef {
+    const float* partial = nullptr;  // that launch's partial buffer
+    int grid = 0;                    // that launch's grid
+    int n_seg = 0;                   // that launch's segment count
+    int seg = 0;                     // index of the segment in that launch
+    int rank = 0;                    // expert rank in the selection
+};
+
+constexpr int kMaxCombineRefs = 128;
+
 struct CombineArgs {
-    const double* x = nullptr;       // [D] layer input (residual)
+    const double* x = nullptr;       // [D] layer input (residual; all-zero for a bare FFN)
     const double* scores = nullptr;  // [N] post-softmax scores of this (token, layer)
-    const float* y = nullptr;        // [ranks][tiles][D] partial outputs
     float* out = nullptr;            // [D]
     int experts[8] = {0};            // selected experts in rank order
-    int ranks = 0, tiles = 0, d = 0;
+    int ranks = 0, d = 0, ft = 0;
+    int n_refs = 0;                  // refs sorted by (rank, tile)
+    FfnPartialRef refs[kMaxCombineRefs];
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream);
 
 // Deterministic counter-based bf16 init of one expert in the tile-major layout (same values as
 // oracle/moe_oracle.c orc_expert_init): value = bf16_rne(float(sum of 4 x 16-bit lanes of
-// splitmix64(base_m + index) - 131070) * scale_m).
+// splitmix64(base_m + index) - 131070) * scale_m), index = logical row-major index in W1/W3 [F][D]
+// or W2 [D][F].
 cudaError_t launch_expert_init(std::uint16_t* dst, int d, int f, int tiles, const std::uint64_t base[3],
                                const float scale[3], cudaStream_t stream);
 

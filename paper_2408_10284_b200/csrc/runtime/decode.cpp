@@ -49,10 +49,10 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     slot_of_.assign(static_cast<size_t>(L) * N, -1);
     cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, eng.device());
 
-    d_h_.reserve(static_cast<size_t>(K) * store_.ffn * sizeof(float));
-    d_y_.reserve(static_cast<size_t>(K) * store_.tiles * D * sizeof(float));
-    d_counters_.reserve(kCounterRing * sizeof(unsigned));
-    MOE_CUDA(cudaMemset(d_counters_.ptr, 0, kCounterRing * sizeof(unsigned)));
+    // at most one launch for the resident experts' tiles (split per 32 segments) + one per
+    // on-demand tile
+    partial_regions_ = (K * store_.tiles + kMaxFfnSegments - 1) / kMaxFfnSegments + K * store_.tiles;
+    d_partials_.reserve(static_cast<size_t>(partial_regions_) * kFfnMaxCtas * kFfnSlotsPerCta * D * sizeof(float));
     MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_route_), 64 * 4 * sizeof(int), cudaHostAllocMapped));
     MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_route_), h_route_, 0));
     MOE_CUDA(cudaEventCreateWithFlags(&route_done_, cudaEventDisableTiming));
@@ -200,19 +200,18 @@ void DecodeSession::wait_fill(int slot, int tile) {
     if (tile < 0 || tile == sl.fill->tiles - 1) sl.fill_done = true;
 }
 
-unsigned int* DecodeSession::take_counters(int n) {
-    if (counter_next_ + n > kCounterRing) {
-        MOE_CUDA(cudaMemsetAsync(d_counters_.ptr, 0, kCounterRing * sizeof(unsigned), eng_.compute_stream()));
-        counter_next_ = 0;
-    }
-    unsigned int* c = d_counters_.as<unsigned>() + counter_next_;
-    counter_next_ += n;
-    return c;
-}
-
-void DecodeSession::timed_ffn(FfnLaunch& p) {
+// Launch the pending segments of `p` into the next partial region of this layer; `seg_meta`
+// gives (rank, tile) per segment so the combine can find each segment's partials.
+void DecodeSession::timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int>>& seg_meta,
+                              std::vector<std::tuple<int, int, FfnPartialRef>>& refs) {
     cudaStream_t cs = eng_.compute_stream();
-    p.counters = take_counters(p.n_seg);
+    const size_t region = static_cast<size_t>(kFfnMaxCtas) * kFfnSlotsPerCta * spec_.hidden_dim;
+    if (partial_next_ >= partial_regions_) fail(Status::Internal, "decode: FFN partial pool exhausted");
+    p.partial = d_partials_.as<float>() + region * partial_next_++;
+    p.l2_prefetch = p.n_seg == 1 ? 1 : 0;  // only single-tile launches gain from the L2 prefetch
+    const int grid = ffn_grid(p, sm_count_);
+    for (int s = 0; s < p.n_seg; ++s)
+        refs.emplace_back(seg_meta[s].first, seg_meta[s].second, FfnPartialRef{p.partial, grid, p.n_seg, s, seg_meta[s].first});
     cudaEvent_t e0 = take_timing(), e1 = take_timing();
     cudaEventRecord(e0, cs);
     MOE_CUDA(launch_ffn(p, sm_count_, cs));
@@ -227,50 +226,59 @@ void DecodeSession::timed_ffn(FfnLaunch& p) {
 void DecodeSession::on_layer_done(int, int, const RouteDecision& d) {
     const int D = spec_.hidden_dim, T = store_.tiles, F = store_.ffn, Ft = F / T;
     const size_t gate_up_bytes = static_cast<size_t>(2) * Ft * D * 2;
-    float* h = d_h_.as<float>();
-    float* y = d_y_.as<float>();
-    auto seg = [&](int slot, int rank, int t) {
+    auto seg = [&](int slot, int t) {
         FfnSegment s;
         const unsigned char* tile = slot_ptr(slot) + t * store_.tile_bytes;
         s.gate_up = reinterpret_cast<const std::uint16_t*>(tile);
-        s.down = reinterpret_cast<const std::uint16_t*>(tile + gate_up_bytes);
-        s.h = h + static_cast<size_t>(rank) * F + static_cast<size_t>(t) * Ft;
-        s.y = y + (static_cast<size_t>(rank) * T + t) * D;
+        s.down_t = reinterpret_cast<const std::uint16_t*>(tile + gate_up_bytes);
         return s;
     };
     FfnLaunch p;
     p.d = D;
     p.ft = Ft;
     p.x = cur_x_;
+    partial_next_ = 0;
+    std::vector<std::pair<int, int>> meta;  // (rank, tile) of p's pending segments
+    std::vector<std::tuple<int, int, FfnPartialRef>> refs;
     // resident experts: one launch over all their tiles
     for (const Use& u : uses_) {
         if (u.missing) continue;
         wait_fill(u.slot, -1);
         for (int t = 0; t < T; ++t) {
-            if (p.n_seg == kMaxFfnSegments) timed_ffn(p);
-            p.seg[p.n_seg++] = seg(u.slot, u.rank, t);
+            if (p.n_seg == kMaxFfnSegments) {
+                timed_ffn(p, meta, refs);
+                meta.clear();
+            }
+            p.seg[p.n_seg++] = seg(u.slot, t);
+            meta.emplace_back(u.rank, t);
         }
         stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
     }
-    if (p.n_seg) timed_ffn(p);
+    if (p.n_seg) timed_ffn(p, meta, refs);
+    meta.clear();
     // on-demand experts: tile by tile as their copies land
     for (const Use& u : uses_) {
         if (!u.missing) continue;
         for (int t : u.tiles) {
             wait_fill(u.slot, t);
-            p.seg[p.n_seg++] = seg(u.slot, u.rank, t);
-            timed_ffn(p);
+            p.seg[p.n_seg++] = seg(u.slot, t);
+            meta.assign(1, {u.rank, t});
+            timed_ffn(p, meta, refs);
         }
         stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
     }
+    std::sort(refs.begin(), refs.end(), [](const auto& a, const auto& b) {
+        return std::get<0>(a) != std::get<0>(b) ? std::get<0>(a) < std::get<0>(b) : std::get<1>(a) < std::get<1>(b);
+    });
     CombineArgs c;
     c.x = cur_x_;
     c.scores = cur_scores_;
-    c.y = y;
     c.out = cur_out_;
     c.ranks = d.count;
-    c.tiles = T;
     c.d = D;
+    c.ft = Ft;
+    c.n_refs = static_cast<int>(refs.size());
+    for (size_t i = 0; i < refs.size(); ++i) c.refs[i] = std::get<2>(refs[i]);
     for (int r = 0; r < d.count; ++r) c.experts[r] = d.experts[r];
     MOE_CUDA(launch_combine(c, eng_.compute_stream()));
     stats_.kernels += 1;

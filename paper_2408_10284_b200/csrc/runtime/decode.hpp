@@ -15,6 +15,8 @@
 #include <cuda_runtime_api.h>
 
 #include <memory>
+#include <tuple>
+#include <utility>
 #include <vector>
 
 #include "../host/policy_engine.hpp"
@@ -70,11 +72,11 @@ private:
     void release_slot(int s);
     void release_pending(bool all);
     void wait_fill(int slot, int tile);  // compute stream waits for tile (or all tiles if -1)
-    void timed_ffn(FfnLaunch& p);  // launch + time + clear the segment list
-    unsigned int* take_counters(int n);
-    static constexpr int kCounterRing = 1 << 16;
-    DeviceBuffer d_counters_;
-    int counter_next_ = 0;
+    // launch + time + clear the segment list; records where each (rank, tile) partial lives
+    void timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int>>& seg_meta,
+                   std::vector<std::tuple<int, int, FfnPartialRef>>& refs);
+    DeviceBuffer d_partials_;  // per-layer pool of K2 partial regions (reused every layer, stream-ordered)
+    int partial_regions_ = 0, partial_next_ = 0;
 
     Engine& eng_;
     ModelSpec spec_;
@@ -110,7 +112,7 @@ private:
     float* cur_out_ = nullptr;
 
     // buffers
-    DeviceBuffer d_in_acts_, d_in_scores_, d_out_, d_h_, d_y_, d_groups_;
+    DeviceBuffer d_in_acts_, d_in_scores_, d_out_, d_groups_;
     PinnedBuffer h_groups_;
     int* h_route_ = nullptr;  // mapped pinned: selected [4][K], count [4], single [4]
     int* d_route_ = nullptr;

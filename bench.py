@@ -300,7 +300,8 @@ def ours(args):
                       "tile_copies": d["tile_copies"], "stall_ms": d["stall_ms"],
                       "copy_hidden_frac": (1.0 - d["stall_ms"] / d["copy_busy_ms"]) if d["copy_busy_ms"] > 0 else None,
                       "link_busy_frac": d["copy_busy_ms"] / gpu_ms if gpu_ms > 0 else None},
-        "time_split_ms": {"ffn": ffn_ms, "router": d["router_ms"], "copy_stall": d["stall_ms"], "total": gpu_ms},
+        "time_split_ms": {"ffn": ffn_ms, "router": d["router_ms"], "copy_stall": d["stall_ms"], "total": gpu_ms,
+                          "host_wait_k1": d["host_sync_ms"], "host_step": d["host_step_ms"]},
         "router": {"launches": K * wl.layers, "us_per_launch": 1e3 * d["router_ms"] / max(1, K * wl.layers),
                    "exact_fallback_items": int(d["router_exact_items"])},
         "gpu_launches": int(d["kernels_launched"]),

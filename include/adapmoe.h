@@ -219,6 +219,8 @@ typedef struct {
     double router_ms;             /* sum of router (K1) durations */
     double stall_ms;              /* compute-stream time blocked on tile copies */
     int64_t router_exact_items;   /* look-ahead items K1 could not certify from fp32 logits (exact fp64 path) */
+    double host_sync_ms;          /* host wall time blocked on K1 results */
+    double host_step_ms;          /* host wall time in the policy step + launches (incl. copy-issue waits) */
     int32_t slots_total;          /* HBM slots = sum(capacities) + staging */
     int32_t staging_high_water;   /* most staging slots in use at once */
 } moe_decode_stats;

@@ -337,6 +337,8 @@ void export_stats(const DecodeStats& s, moe_decode_stats* out) {
     out->router_ms = s.router_ms;
     out->stall_ms = s.stall_ms;
     out->router_exact_items = s.router_exact;
+    out->host_sync_ms = s.host_sync_ms;
+    out->host_step_ms = s.host_step_ms;
     out->slots_total = s.slots_total;
     out->staging_high_water = s.staging_high_water;
 }

@@ -161,34 +161,61 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_cons
     store_partial<DC>(part + static_cast<size_t>(cur_seg - first_seg) * D, acc, tid, D);
 }
 
-// out[j] = x[j] + sum_rank w_rank * sum_(tile refs of rank) sum_(cta asc) partial  — fixed order
-__global__ void combine_kernel(const __grid_constant__ CombineArgs a) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= a.d) return;
+// out[j] = x[j] + sum_rank w_rank * y_rank[j];  y_rank = fixed-order reduction of the K2 partials
+// of the rank's (tile) segments.  Block = 32 output columns x 8 partial lanes: lane q of column j
+// sums the partials of CTAs c = c_lo + q, c_lo + q + 8, ... of every segment of the rank (coalesced
+// 128-byte rows, several loads in flight), then lanes 0..7 are added in order through shared memory.
+constexpr int kCombineCols = 32, kCombineLanes = 16;
+
+__global__ void __launch_bounds__(kCombineCols * kCombineLanes) combine_kernel(const __grid_constant__ CombineArgs a) {
+    __shared__ float red[kCombineLanes][kCombineCols];
+    const int jl = threadIdx.x % kCombineCols, q = threadIdx.x / kCombineCols;
+    const int j = blockIdx.x * kCombineCols + jl;
+    const bool live = j < a.d;
     double denom = 0.0;
     for (int r = 0; r < a.ranks; ++r) denom += a.scores[a.experts[r]];
-    float acc = static_cast<float>(a.x[j]);
+    float acc = live ? static_cast<float>(a.x[j]) : 0.0f;
     int ref = 0;
     for (int r = 0; r < a.ranks; ++r) {
-        const float w = a.ranks == 1 ? 1.0f : static_cast<float>(a.scores[a.experts[r]] / denom);
-        float yr = 0.0f;
+        float part = 0.0f;
         for (; ref < a.n_refs && a.refs[ref].rank == r; ++ref) {
             const FfnPartialRef& f = a.refs[ref];
             const long long TR = static_cast<long long>(f.n_seg) * a.ft;
             const long long s_lo = static_cast<long long>(f.seg) * a.ft, s_hi = s_lo + a.ft;
-            int c = static_cast<int>(s_lo * f.grid / TR);
-            while (c > 0 && TR * c / f.grid > s_lo) --c;
-            for (; c < f.grid; ++c) {
-                const long long lo = TR * c / f.grid, hi = TR * (c + 1) / f.grid;
-                if (lo >= s_hi) break;
-                if (hi <= s_lo) continue;
-                const int slot = f.seg - static_cast<int>(lo / a.ft);
-                yr += f.partial[(static_cast<size_t>(c) * kFfnSlotsPerCta + slot) * a.d + j];
+            int c_lo = static_cast<int>(s_lo * f.grid / TR);
+            while (c_lo > 0 && TR * c_lo / f.grid > s_lo) --c_lo;
+            while (TR * (c_lo + 1) / f.grid <= s_lo) ++c_lo;  // first CTA whose range reaches the segment
+            int c_hi = static_cast<int>((s_hi - 1) * f.grid / TR);
+            while (c_hi + 1 < f.grid && TR * (c_hi + 1) / f.grid < s_hi) ++c_hi;
+            while (c_hi > c_lo && TR * c_hi / f.grid >= s_hi) --c_hi;  // last CTA starting inside it
+            if (!live) continue;
+            // two independent accumulators (fixed assignment) keep several L2 loads in flight
+            float p0 = 0.0f, p1 = 0.0f;
+            int c = c_lo + q;
+            for (; c + kCombineLanes <= c_hi; c += 2 * kCombineLanes) {
+                const int s0 = f.seg - static_cast<int>(TR * c / f.grid / a.ft);
+                const int s1 = f.seg - static_cast<int>(TR * (c + kCombineLanes) / f.grid / a.ft);
+                p0 += f.partial[(static_cast<size_t>(c) * kFfnSlotsPerCta + s0) * a.d + j];
+                p1 += f.partial[(static_cast<size_t>(c + kCombineLanes) * kFfnSlotsPerCta + s1) * a.d + j];
             }
+            if (c <= c_hi) {
+                const int s0 = f.seg - static_cast<int>(TR * c / f.grid / a.ft);
+                p0 += f.partial[(static_cast<size_t>(c) * kFfnSlotsPerCta + s0) * a.d + j];
+            }
+            part += p0 + p1;
         }
-        acc = __fmaf_rn(w, yr, acc);
+        red[q][jl] = part;
+        __syncthreads();
+        if (q == 0 && live) {
+            float yr = 0.0f;
+#pragma unroll
+            for (int k = 0; k < kCombineLanes; ++k) yr += red[k][jl];
+            const float w = a.ranks == 1 ? 1.0f : static_cast<float>(a.scores[a.experts[r]] / denom);
+            acc = __fmaf_rn(w, yr, acc);
+        }
+        __syncthreads();
     }
-    a.out[j] = acc;
+    if (q == 0 && live) a.out[j] = acc;
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -282,7 +309,7 @@ cudaError_t launch_ffn(const FfnLaunch& p, int sm_count, cudaStream_t stream) {
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
-    combine_kernel<<<(a.d + 255) / 256, 256, 0, stream>>>(a);
+    combine_kernel<<<(a.d + kCombineCols - 1) / kCombineCols, kCombineCols * kCombineLanes, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

@@ -196,17 +196,29 @@ __global__ void __launch_bounds__(kThreads) route_kernel(const RouteGroup* __res
             const float* w = it.gate32 + static_cast<size_t>(j) * D;
             float acc = 0.0f, asum = 0.0f;
             if (vec4) {
-                for (int i = lane * 4; i < D; i += 128) {
-                    const float4 wv = __ldg(reinterpret_cast<const float4*>(w + i));
-                    const float4 xv = *reinterpret_cast<const float4*>(x32 + i);
-                    acc = __fmaf_rn(xv.x, wv.x, acc);
-                    acc = __fmaf_rn(xv.y, wv.y, acc);
-                    acc = __fmaf_rn(xv.z, wv.z, acc);
-                    acc = __fmaf_rn(xv.w, wv.w, acc);
-                    asum = __fmaf_rn(fabsf(xv.x), fabsf(wv.x), asum);
-                    asum = __fmaf_rn(fabsf(xv.y), fabsf(wv.y), asum);
-                    asum = __fmaf_rn(fabsf(xv.z), fabsf(wv.z), asum);
-                    asum = __fmaf_rn(fabsf(xv.w), fabsf(wv.w), asum);
+                // batches of 8 independent 16-byte loads per lane; the accumulation order (lane-
+                // sequential over i, then the butterfly) is unchanged by the batching
+                constexpr int kB = 8;
+                for (int i0 = lane * 4; i0 < D; i0 += 128 * kB) {
+                    float4 wv[kB];
+#pragma unroll
+                    for (int b = 0; b < kB; ++b)
+                        wv[b] = (i0 + 128 * b < D) ? __ldg(reinterpret_cast<const float4*>(w + i0 + 128 * b))
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int b = 0; b < kB; ++b) {
+                        const int i = i0 + 128 * b;
+                        if (i >= D) break;
+                        const float4 xv = *reinterpret_cast<const float4*>(x32 + i);
+                        acc = __fmaf_rn(xv.x, wv[b].x, acc);
+                        acc = __fmaf_rn(xv.y, wv[b].y, acc);
+                        acc = __fmaf_rn(xv.z, wv[b].z, acc);
+                        acc = __fmaf_rn(xv.w, wv[b].w, acc);
+                        asum = __fmaf_rn(fabsf(xv.x), fabsf(wv[b].x), asum);
+                        asum = __fmaf_rn(fabsf(xv.y), fabsf(wv[b].y), asum);
+                        asum = __fmaf_rn(fabsf(xv.z), fabsf(wv[b].z), asum);
+                        asum = __fmaf_rn(fabsf(xv.w), fabsf(wv[b].w), asum);
+                    }
                 }
             } else {
                 for (int i = lane; i < D; i += 32) {

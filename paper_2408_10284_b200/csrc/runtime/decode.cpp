@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <chrono>
 #include <numeric>
 
 namespace adapmoe {
@@ -367,7 +368,10 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             router_events_.emplace_back(r0, r1);
             stats_.kernels += 1;
             MOE_CUDA(cudaEventRecord(route_done_, cs));
+            const auto h0 = std::chrono::steady_clock::now();
             MOE_CUDA(cudaEventSynchronize(route_done_));
+            const auto h1 = std::chrono::steady_clock::now();
+            stats_.host_sync_ms += std::chrono::duration<double, std::milli>(h1 - h0).count();
             release_pending(false);
             RouteDecision d;
             d.count = cnt[0];
@@ -386,6 +390,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             cur_scores_ = s_all + tl * N;
             cur_out_ = out_all + tl * D;
             policy_->step(tok, l, d, std::span<const RoutePrediction>(preds.data(), np));
+            stats_.host_step_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count();
         }
     }
     if (hidden_out && !on_device)

@@ -33,6 +33,7 @@ struct DecodeStats {
     double copy_busy_ms = 0, ffn_ms = 0, gate_up_ms = 0, down_ms = 0, gate_up_bytes = 0, down_bytes = 0;
     double router_ms = 0, stall_ms = 0;
     long long router_exact = 0;  // look-ahead items that needed the exact fp64 path
+    double host_sync_ms = 0, host_step_ms = 0;  // host wall time: waiting on K1 / policy step + launches
     int slots_total = 0, staging_high_water = 0;
 };
 

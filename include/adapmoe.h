@@ -195,6 +195,19 @@ int moe_expert_read(moe_engine_t engine, int32_t layer, int32_t expert, uint16_t
 int moe_decode_begin(moe_engine_t engine, const int32_t* capacities, int32_t staging_slots, const double* fisher,
                      double tau, const moe_sim_config* cfg, uint64_t seed, int32_t total_tokens);
 
+/* Batched decode session (BASELINE config 4; no reference counterpart — the reference is batch-1,
+ * SPEC.md:531): `batch` token streams share the expert cache.  Per (token, layer) every stream is
+ * routed with the reference rule; the cache/transfer engine sees the union of the streams'
+ * selections and look-ahead lists (builder-defined, oracle/moe_oracle.c orc_simulate_batch; with
+ * batch == 1 this is exactly moe_decode_begin).  The expert FFN runs as grouped tcgen05 GEMMs over
+ * each expert's routed tokens (bf16 activations, fp32 accumulation).  batch in [1, 256],
+ * batch * top_k <= 512; batch > 1 needs hidden_dim % 128 == 0 and (ffn / tiles) % 64 == 0.
+ * moe_decode_tokens then takes acts [count][batch][L][d], scores [count][batch][L][N] and writes
+ * hidden_out [count][batch][L][d]. */
+int moe_decode_begin_batch(moe_engine_t engine, const int32_t* capacities, int32_t staging_slots,
+                           const double* fisher, double tau, const moe_sim_config* cfg, uint64_t seed,
+                           int32_t total_tokens, int32_t batch);
+
 /* Decode `count` tokens (trace-replay: layer l's router/FFN input is the trace activation).
  * acts [count][L][d] fp64 and scores [count][L][N] fp64 are HOST buffers if inputs_on_device == 0,
  * else device pointers.  hidden_out [count][L][d] fp32 receives x_l + sum_e w_e * E_e(x_l) per

@@ -656,11 +656,29 @@ static int predicted_selection(const double* x, const double* W, int D, int N, i
     return 0;
 }
 
-int orc_simulate(const double* acts, const double* scores, const double* gates, const double* first_gate, int T,
-                 int L, int N, int K, int D, const double* fisher, const int* caps, double tau, orc_simcfg cfg,
-                 uint64_t seed, orc_metrics* m, int64_t* latency_per_token, int64_t* od_per_layer, int64_t* timeline,
-                 int64_t timeline_cap, int64_t* n_events, int* predictions, int* decisions) {
-    if (N > 64 || K > N || cfg.tiles < 1 || cfg.lookahead < 0 || cfg.lookahead > 3) return -1;
+/* Batched decode (BASELINE config 4) has no reference counterpart: the reference is batch-1
+ * (SPEC.md:531).  Builder-defined extension, B independent token streams sharing one expert cache:
+ * per (token, layer) every stream is routed with the reference rule; the cache sees the UNION of
+ * the streams' selections (order of first appearance: stream-major, rank order), and each
+ * look-ahead target's prediction list is the union of the streams' lists (same order), fed to the
+ * unchanged plan_prefetch/dedupe.  single_expert_decisions counts per stream; experts_activated
+ * counts union members (so activated = hits + prefetch hits + on-demand still holds).  With B = 1
+ * every union is the stream's own list, i.e. exactly simulate_trace (pinned by the goldens). */
+static void union_add(int* u, int* n, const int* src, int cnt) {
+    for (int k = 0; k < cnt; ++k) {
+        int seen = 0;
+        for (int i = 0; i < *n; ++i)
+            if (u[i] == src[k]) { seen = 1; break; }
+        if (!seen) u[(*n)++] = src[k];
+    }
+}
+
+int orc_simulate_batch(const double* acts, const double* scores, const double* gates, const double* first_gate,
+                       int B, int T, int L, int N, int K, int D, const double* fisher, const int* caps, double tau,
+                       orc_simcfg cfg, uint64_t seed, orc_metrics* m, int64_t* latency_per_token,
+                       int64_t* od_per_layer, int64_t* timeline, int64_t timeline_cap, int64_t* n_events,
+                       int* predictions, int* decisions) {
+    if (N > 64 || K > N || B < 1 || cfg.tiles < 1 || cfg.lookahead < 0 || cfg.lookahead > 3) return -1;
     memset(m, 0, sizeof(*m));
     for (int l = 0; l < L; ++l) od_per_layer[l] = 0;
     const int prefetch_on = cfg.prefetch && cfg.lookahead > 0;
@@ -697,25 +715,64 @@ int orc_simulate(const double* acts, const double* scores, const double* gates, 
     for (int tok = 0; tok < T && rc == 0; ++tok) {
         const int64_t token_start = cur;
         for (int layer = 0; layer < L && rc == 0; ++layer) {
-            const size_t tl_idx = (size_t)tok * L + layer;
-            const double* x = acts + tl_idx * D;
             tl_push(&c, 0, 0, cur, cur + cfg.attention, tok, layer, -1, -1);
             cur += cfg.attention;
             tl_push(&c, 0, 1, cur, cur + cfg.gate, tok, layer, -1, -1);
             cur += cfg.gate;
             comm_advance_until(&c, cur);
 
-            int sel[64], cnt, single;
-            if (cfg.gating) {
-                single = orc_gate_decide(scores + tl_idx * N, N, K, fisher[layer], tau, sel, &cnt, NULL);
-            } else {
-                orc_top_k(scores + tl_idx * N, N, K, sel);
-                cnt = K;
-                single = K == 1;
+            /* route every stream; union of the selections */
+            int sel[64], cnt = 0;
+            int pl[3], pc[3], pe[3][64], np = 0;
+            for (int b = 0; b < B; ++b) {
+                const size_t tl_idx = ((size_t)b * T + tok) * L + layer;
+                const double* x = acts + tl_idx * D;
+                int sb[64], cb, single;
+                if (cfg.gating) {
+                    single = orc_gate_decide(scores + tl_idx * N, N, K, fisher[layer], tau, sb, &cb, NULL);
+                } else {
+                    orc_top_k(scores + tl_idx * N, N, K, sb);
+                    cb = K;
+                    single = K == 1;
+                }
+                if (decisions)
+                    for (int k = 0; k < K; ++k) decisions[tl_idx * K + k] = k < cb ? sb[k] : -1;
+                m->single_expert_decisions += single;
+                union_add(sel, &cnt, sb, cb);
+
+                /* this stream's look-ahead predictions (inc/simulator.hpp:422-436) */
+                int bl[3], bc[3], be[3][64], bn = 0;
+                if (prefetch_on) {
+                    if (layer + 1 < L) {
+                        for (int depth = 1; depth <= cfg.lookahead; ++depth) {
+                            const int tgt = layer + depth;
+                            if (tgt >= L) break;
+                            bl[bn] = tgt;
+                            predicted_selection(x, gates + (size_t)tgt * D * N, D, N, K, cfg.gating, fisher[tgt], tau,
+                                                be[bn], &bc[bn]);
+                            bn++;
+                        }
+                    } else if (first_gate && tok + 1 < T) {
+                        bl[bn] = 0;
+                        predicted_selection(x, first_gate, D, N, K, cfg.gating, fisher[0], tau, be[bn], &bc[bn]);
+                        bn++;
+                    }
+                }
+                if (b == 0) {
+                    np = bn;
+                    for (int s = 0; s < bn; ++s) { pl[s] = bl[s]; pc[s] = 0; }
+                }
+                for (int s = 0; s < bn; ++s) union_add(pe[s], &pc[s], be[s], bc[s]);
+                if (predictions) {
+                    int* p = predictions + tl_idx * 3 * PW;
+                    for (int s = 0; s < 3; ++s) {
+                        int* row = p + s * PW;
+                        row[0] = s < bn ? bl[s] : -1;
+                        row[1] = s < bn ? bc[s] : 0;
+                        for (int k = 0; k < K; ++k) row[2 + k] = (s < bn && k < bc[s]) ? be[s][k] : -1;
+                    }
+                }
             }
-            if (decisions)
-                for (int k = 0; k < K; ++k) decisions[tl_idx * K + k] = k < cnt ? sel[k] : -1;
-            m->single_expert_decisions += single;
             m->experts_activated_total += cnt;
 
             int res_now[64], miss_now[64], nres = 0, nmiss = 0;
@@ -735,22 +792,7 @@ int orc_simulate(const double* acts, const double* scores, const double* gates, 
                 }
             }
 
-            int pl[3], pc[3], pe[3][64], np = 0;
             if (prefetch_on) {
-                if (layer + 1 < L) {
-                    for (int depth = 1; depth <= cfg.lookahead; ++depth) {
-                        const int tgt = layer + depth;
-                        if (tgt >= L) break;
-                        pl[np] = tgt;
-                        predicted_selection(x, gates + (size_t)tgt * D * N, D, N, K, cfg.gating, fisher[tgt], tau,
-                                            pe[np], &pc[np]);
-                        np++;
-                    }
-                } else if (first_gate && tok + 1 < T) {
-                    pl[np] = 0;
-                    predicted_selection(x, first_gate, D, N, K, cfg.gating, fisher[0], tau, pe[np], &pc[np]);
-                    np++;
-                }
                 /* inc/prefetch.hpp:101-119 plan_prefetch, then dedupe against pending (:437-443) */
                 const int targets = np < cfg.lookahead ? np : cfg.lookahead;
                 for (int idx = 0; idx < targets; ++idx) {
@@ -762,15 +804,6 @@ int orc_simulate(const double* acts, const double* scores, const double* gates, 
                         if (c.pending[pl[idx] * N + e] < 0) comm_enqueue(&c, pl[idx], e, 0, cur, tok);
                     }
                     if (any_missing) break;
-                }
-            }
-            if (predictions) {
-                int* p = predictions + tl_idx * 3 * PW;
-                for (int s = 0; s < 3; ++s) {
-                    int* row = p + s * PW;
-                    row[0] = s < np ? pl[s] : -1;
-                    row[1] = s < np ? pc[s] : 0;
-                    for (int k = 0; k < K; ++k) row[2 + k] = (s < np && k < pc[s]) ? pe[s][k] : -1;
                 }
             }
 
@@ -805,6 +838,14 @@ int orc_simulate(const double* acts, const double* scores, const double* gates, 
     for (int i = 0; i < c.nreq; ++i) free(c.reqs[i].arrivals);
     free(c.reqs); free(c.od); free(c.pf); free(c.pending); free(c.fin); free(c.fin_n); free(caches);
     return rc;
+}
+
+int orc_simulate(const double* acts, const double* scores, const double* gates, const double* first_gate, int T,
+                 int L, int N, int K, int D, const double* fisher, const int* caps, double tau, orc_simcfg cfg,
+                 uint64_t seed, orc_metrics* m, int64_t* latency_per_token, int64_t* od_per_layer, int64_t* timeline,
+                 int64_t timeline_cap, int64_t* n_events, int* predictions, int* decisions) {
+    return orc_simulate_batch(acts, scores, gates, first_gate, 1, T, L, N, K, D, fisher, caps, tau, cfg, seed, m,
+                              latency_per_token, od_per_layer, timeline, timeline_cap, n_events, predictions, decisions);
 }
 
 /* ------------------------------------------------------------------------------------------ */

@@ -99,6 +99,14 @@ int orc_simulate(const double* acts, const double* scores, const double* gates, 
                  uint64_t seed, orc_metrics* metrics, int64_t* latency_per_token, int64_t* od_per_layer,
                  int64_t* timeline, int64_t timeline_cap, int64_t* n_events, int* predictions, int* decisions);
 
+/* Batched decode over B streams sharing one cache (builder-defined; B = 1 == orc_simulate).
+ * acts [B][T][L][D], scores [B][T][L][N]; predictions [B][T][L][3][2+K]; decisions [B][T][L][K]. */
+int orc_simulate_batch(const double* acts, const double* scores, const double* gates, const double* first_gate,
+                       int B, int T, int L, int N, int K, int D, const double* fisher, const int* caps, double tau,
+                       orc_simcfg cfg, uint64_t seed, orc_metrics* metrics, int64_t* latency_per_token,
+                       int64_t* od_per_layer, int64_t* timeline, int64_t timeline_cap, int64_t* n_events,
+                       int* predictions, int* decisions);
+
 /* --- builder-defined expert FFN (no reference counterpart; parity unpinned) --------------- */
 /* Deterministic counter-based bf16 init, identical to the CUDA init kernel. Layout is tile-major:
  * for tile t (ffn rows [t*F/T,(t+1)*F/T)): gate_up [F/T][2][D] (W1 row, W3 row interleaved),

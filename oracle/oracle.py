@@ -74,6 +74,9 @@ def _declare(L):
     L.orc_simulate.argtypes = [_d, _d, _d, _d] + [C.c_int] * 5 + [_d, _i, C.c_double, SimCfg, C.c_uint64,
                                                                   C.POINTER(Metrics), _i64, _i64, _i64, C.c_int64,
                                                                   _i64, _i, _i]
+    L.orc_simulate_batch.argtypes = [_d, _d, _d, _d] + [C.c_int] * 6 + [_d, _i, C.c_double, SimCfg, C.c_uint64,
+                                                                        C.POINTER(Metrics), _i64, _i64, _i64,
+                                                                        C.c_int64, _i64, _i, _i]
     L.orc_top_k.argtypes = [_d, C.c_int, C.c_int, _i]
     L.orc_softmax.argtypes = [_d, C.c_int, _d]
     L.orc_top1_share.argtypes = [_d, C.c_int]
@@ -205,6 +208,40 @@ def simulate(w: Workload, caps, tau, fisher=None, first_gate=None, tiles=4, tile
     rc = lib().orc_simulate(_p(w.acts, _d), _p(w.scores, _d), _p(w.gates, _d), None if fg is None else _p(fg, _d),
                             T, w.L, w.N, w.K, w.D, _p(fisher, _d), _p(caps, _i), tau, cfg, seed, C.byref(m),
                             _p(lat, _i64), _p(odl, _i64), _p(tl, _i64), cap, C.byref(n), _p(preds, _i), _p(dec, _i))
+    assert rc == 0, rc
+    metrics = {k: getattr(m, k) for k, _ in Metrics._fields_}
+    return SimOut(metrics, lat, odl, tl[: n.value].copy(), preds, dec)
+
+
+def simulate_batch(streams: list, caps, tau, fisher=None, first_gate=None, tiles=4, tile_transfer=2, tile_compute=1,
+                   attention=8, gate=1, lookahead=2, gating=True, prefetch=True, seed=0, T=None) -> SimOut:
+    """B token streams sharing one expert cache (builder-defined union policy, see
+    orc_simulate_batch).  All streams must share the gates (same gate_seed) and fisher.
+    Returns decisions [B][T][L][K] and predictions [B][T][L][3][2+K]."""
+    w0 = streams[0]
+    B = len(streams)
+    T = w0.T if T is None else T
+    fisher = w0.fisher if fisher is None else np.ascontiguousarray(fisher, np.float64)
+    for w in streams[1:]:
+        assert np.array_equal(w.gates, w0.gates) and np.array_equal(w.fisher, w0.fisher)
+    acts = np.ascontiguousarray(np.stack([w.acts[:T] for w in streams]))
+    scores = np.ascontiguousarray(np.stack([w.scores[:T] for w in streams]))
+    caps = np.ascontiguousarray(caps, dtype=np.int32)
+    cfg = SimCfg(tiles, tile_transfer, tile_compute, attention, gate, lookahead, int(gating), int(prefetch))
+    m = Metrics()
+    lat = np.zeros(T, dtype=np.int64)
+    odl = np.zeros(w0.L, dtype=np.int64)
+    cap = T * w0.L * (4 + 4 * min(w0.N, B * w0.K) * tiles + 8 * tiles * w0.N) + 64
+    tl = np.zeros((cap, 8), dtype=np.int64)
+    n = C.c_int64()
+    pw = 2 + w0.K
+    preds = np.zeros((B, T, w0.L, 3, pw), dtype=np.int32)
+    dec = np.zeros((B, T, w0.L, w0.K), dtype=np.int32)
+    fg = None if first_gate is None else np.ascontiguousarray(first_gate)
+    rc = lib().orc_simulate_batch(_p(acts, _d), _p(scores, _d), _p(w0.gates, _d), None if fg is None else _p(fg, _d),
+                                  B, T, w0.L, w0.N, w0.K, w0.D, _p(fisher, _d), _p(caps, _i), tau, cfg, seed,
+                                  C.byref(m), _p(lat, _i64), _p(odl, _i64), _p(tl, _i64), cap, C.byref(n),
+                                  _p(preds, _i), _p(dec, _i))
     assert rc == 0, rc
     metrics = {k: getattr(m, k) for k, _ in Metrics._fields_}
     return SimOut(metrics, lat, odl, tl[: n.value].copy(), preds, dec)

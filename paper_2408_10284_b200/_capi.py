@@ -93,6 +93,8 @@ SIGNATURES = {
     "moe_expert_bytes": (C.c_int, [_eng, _i64]),
     "moe_expert_read": (C.c_int, [_eng, C.c_int32, C.c_int32, _u16]),
     "moe_decode_begin": (C.c_int, [_eng, _i32, C.c_int32, _d, C.c_double, _cfg, C.c_uint64, C.c_int32]),
+    "moe_decode_begin_batch": (C.c_int, [_eng, _i32, C.c_int32, _d, C.c_double, _cfg, C.c_uint64, C.c_int32,
+                                         C.c_int32]),
     "moe_decode_tokens": (C.c_int, [_eng, _d, _d, C.c_int32, C.c_int32, _f, _d]),
     "moe_decode_end": (C.c_int, [_eng, C.POINTER(MetricsC), _i64, _i64, C.POINTER(EventC), C.c_int64, _i64,
                                  C.POINTER(DecodeStatsC)]),

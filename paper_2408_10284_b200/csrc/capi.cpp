@@ -381,8 +381,8 @@ int moe_expert_read(moe_engine_t h, int32_t layer, int32_t expert, uint16_t* out
     });
 }
 
-int moe_decode_begin(moe_engine_t h, const int32_t* caps, int32_t staging, const double* fisher, double tau,
-                     const moe_sim_config* cfg, uint64_t seed, int32_t total_tokens) {
+int moe_decode_begin_batch(moe_engine_t h, const int32_t* caps, int32_t staging, const double* fisher, double tau,
+                           const moe_sim_config* cfg, uint64_t seed, int32_t total_tokens, int32_t batch) {
     return guarded([&] {
         Engine& e = eng(h);
         SimConfig c = to_cfg(cfg);
@@ -393,8 +393,14 @@ int moe_decode_begin(moe_engine_t h, const int32_t* caps, int32_t staging, const
         const int L = e.spec().num_layers;
         e.session.reset();
         e.session = std::make_unique<DecodeSession>(e, std::span<const int>(caps, L), staging,
-                                                    std::span<const double>(fisher, L), tau, c, seed, total_tokens);
+                                                    std::span<const double>(fisher, L), tau, c, seed, total_tokens,
+                                                    batch);
     });
+}
+
+int moe_decode_begin(moe_engine_t h, const int32_t* caps, int32_t staging, const double* fisher, double tau,
+                     const moe_sim_config* cfg, uint64_t seed, int32_t total_tokens) {
+    return moe_decode_begin_batch(h, caps, staging, fisher, tau, cfg, seed, total_tokens, 1);
 }
 
 int moe_decode_tokens(moe_engine_t h, const double* acts, const double* scores, int32_t count, int32_t on_device,

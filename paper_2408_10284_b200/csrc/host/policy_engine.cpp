@@ -182,7 +182,8 @@ Tick PolicyEngine::wait_for_tile(ExpertRef ref, int tile) {
     }
 }
 
-void PolicyEngine::step(int tok, int layer, const RouteDecision& d, std::span<const RoutePrediction> predictions) {
+void PolicyEngine::step(int tok, int layer, const RouteDecision& d, std::span<const RoutePrediction> predictions,
+                        int single_decisions) {
     const int L = spec_.num_layers;
     if (layer == 0) token_start_ = now_;
     record(StreamId::Compute, EventKind::Attention, now_, now_ + cfg_.attention_compute_time, tok, layer, -1, -1);
@@ -191,7 +192,7 @@ void PolicyEngine::step(int tok, int layer, const RouteDecision& d, std::span<co
     now_ += cfg_.gate_compute_time;
     advance_until(now_);
 
-    metrics_.single_expert_decisions += d.single ? 1 : 0;
+    metrics_.single_expert_decisions += single_decisions >= 0 ? single_decisions : (d.single ? 1 : 0);
     metrics_.experts_activated_total += d.count;
 
     // classify the selection (inc/simulator.hpp:400-420)

@@ -92,7 +92,10 @@ public:
 
     // One (token, layer) of the per-token loop.  predictions: the look-ahead lists evaluated
     // from this layer's activation (empty when prefetch is off or no target exists).
-    void step(int token, int layer, const RouteDecision& decision, std::span<const RoutePrediction> predictions);
+    // single_decisions >= 0 overrides decision.single in the metrics (batched decode: the decision
+    // is the union of B streams' selections and each stream's single-expert flag is counted).
+    void step(int token, int layer, const RouteDecision& decision, std::span<const RoutePrediction> predictions,
+              int single_decisions = -1);
 
     const SimMetrics& metrics() const { return metrics_; }
     const std::vector<TimelineEvent>& timeline() const { return timeline_; }

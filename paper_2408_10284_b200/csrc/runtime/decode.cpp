@@ -15,8 +15,9 @@ constexpr size_t kSlotAlign = 2u << 20;
 
 DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int staging_slots,
                              std::span<const double> fisher, double tau, const SimConfig& cfg, std::uint64_t seed,
-                             int total_tokens)
-    : eng_(eng),
+                             int total_tokens, int batch)
+    : batch_(batch),
+      eng_(eng),
       spec_(eng.spec()),
       cfg_(cfg),
       caps_(capacities.begin(), capacities.end()),
@@ -33,6 +34,11 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
         fail(Status::Usage, "decode_begin: SimConfig tile count differs from the expert store's tile layout");
     if (total_tokens < 1) fail(Status::Usage, "decode_begin: total_tokens must be >= 1");
     if (K > 8) fail(Status::Usage, "decode: top_k > 8 unsupported by the combine kernel");
+    if (batch_ < 1 || batch_ > 256 || batch_ * K > kGMaxPairs)
+        fail(Status::Usage, "decode_begin: batch must be in [1, 256] with batch * top_k <= 512");
+    const int Ft = store_.ffn / store_.tiles;
+    if (batch_ > 1 && (D % 128 || Ft % 64))
+        fail(Status::Usage, "batched decode needs hidden_dim % 128 == 0 and (ffn / tiles) % 64 == 0 (tcgen05 tiles)");
     const bool prefetch_on = cfg_.policy.prefetch && cfg_.lookahead_depth > 0;
     if (prefetch_on && !eng.has_gates()) fail(Status::Usage, "decode: prefetching requires the gate matrices");
     int resident = 0;
@@ -43,7 +49,11 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     int staging = staging_slots > 0 ? staging_slots : std::min(32, L * N + K);
     n_slots_ = resident + staging;
     stats_.slots_total = n_slots_;
-    slot_stride_ = (store_.expert_bytes + kSlotAlign - 1) / kSlotAlign * kSlotAlign;
+    // slots are 2 MB aligned and a whole number of d-element bf16 rows, so the pool is one 2-D
+    // tensor [rows][d] for the TMA maps of the grouped kernels
+    const size_t row_bytes = static_cast<size_t>(D) * 2;
+    const size_t align = std::lcm(kSlotAlign, row_bytes);
+    slot_stride_ = (store_.expert_bytes + align - 1) / align * align;
     pool_.reserve(slot_stride_ * n_slots_);
     slots_.resize(n_slots_);
     for (int s = 0; s < n_slots_; ++s) free_.push_back(s);
@@ -54,7 +64,25 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     // on-demand tile
     partial_regions_ = (K * store_.tiles + kMaxFfnSegments - 1) / kMaxFfnSegments + K * store_.tiles;
     d_partials_.reserve(static_cast<size_t>(partial_regions_) * kFfnMaxCtas * kFfnSlotsPerCta * D * sizeof(float));
-    MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_route_), 64 * 4 * sizeof(int), cudaHostAllocMapped));
+    if (batch_ > 1) {
+        MOE_CUDA(cudaMemset(pool_.ptr, 0, slot_stride_ * n_slots_));  // slot padding read by TMA stays finite
+        np_ = (batch_ + 15) / 16 * 16;
+        const int F = store_.ffn;
+        d_gx_.reserve(static_cast<size_t>(N) * np_ * D * 2);
+        d_gh_.reserve(static_cast<size_t>(N) * np_ * F * 2);
+        MOE_CUDA(cudaMemset(d_gx_.ptr, 0, static_cast<size_t>(N) * np_ * D * 2));
+        MOE_CUDA(cudaMemset(d_gh_.ptr, 0, static_cast<size_t>(N) * np_ * F * 2));
+        const uint64_t pool_rows = slot_stride_ * n_slots_ / row_bytes;
+        MOE_CUDA(make_tensor_map_2d(&map_pool_gu_, pool_.ptr, pool_rows, D, 64, 128));
+        MOE_CUDA(make_tensor_map_2d(&map_pool_dn_, pool_.ptr, pool_rows, D, 64, 64));
+        MOE_CUDA(make_tensor_map_2d(&map_x_, d_gx_.ptr, static_cast<uint64_t>(N) * np_, D, 64, 16));
+        MOE_CUDA(make_tensor_map_2d(&map_h_, d_gh_.ptr, static_cast<uint64_t>(N) * np_, F, 64, 16));
+        cur_sel_.assign(static_cast<size_t>(batch_) * K, -1);
+        cur_cnt_.assign(batch_, 0);
+    }
+    const int route_rows = 4 * batch_;
+    MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_route_), static_cast<size_t>(route_rows) * (K + 3) * sizeof(int),
+                           cudaHostAllocMapped));
     MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_route_), h_route_, 0));
     MOE_CUDA(cudaEventCreateWithFlags(&route_done_, cudaEventDisableTiming));
     copier_ = std::make_unique<CopyEngine>(eng.copy_stream(), eng.device());
@@ -225,6 +253,15 @@ void DecodeSession::timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int
 }
 
 void DecodeSession::on_layer_done(int, int, const RouteDecision& d) {
+    if (batch_ > 1)
+        layer_ffn_grouped(d);
+    else
+        layer_ffn_single(d);
+    uses_.clear();
+    ++layer_seq_;
+}
+
+void DecodeSession::layer_ffn_single(const RouteDecision& d) {
     const int D = spec_.hidden_dim, T = store_.tiles, F = store_.ffn, Ft = F / T;
     const size_t gate_up_bytes = static_cast<size_t>(2) * Ft * D * 2;
     auto seg = [&](int slot, int t) {
@@ -283,19 +320,168 @@ void DecodeSession::on_layer_done(int, int, const RouteDecision& d) {
     for (int r = 0; r < d.count; ++r) c.experts[r] = d.experts[r];
     MOE_CUDA(launch_combine(c, eng_.compute_stream()));
     stats_.kernels += 1;
-    uses_.clear();
-    ++layer_seq_;
+}
+
+void DecodeSession::timed_grouped(GroupedLaunch& p, bool down) {
+    cudaStream_t cs = eng_.compute_stream();
+    cudaEvent_t e0 = take_timing(), e1 = take_timing();
+    cudaEventRecord(e0, cs);
+    MOE_CUDA(down ? launch_grouped_down(p, sm_count_, cs) : launch_grouped_gate_up(p, sm_count_, cs));
+    cudaEventRecord(e1, cs);
+    double tiles = 0;
+    for (int s = 0; s < p.n_seg; ++s) tiles += p.seg[s].t1 - p.seg[s].t0;
+    const double bytes = tiles * (down ? 1.0 : 2.0) * p.ft * p.d * 2.0;
+    pass_events_.push_back(PassRec{down ? 0.0 : bytes, down ? bytes : 0.0, e0, e1});
+    stats_.kernels += 1;
+}
+
+// Batched layer: gather the union experts' routed tokens, grouped gate/up + down on tcgen05 for the
+// resident experts (one launch pair) and for each on-demand tile as it lands, then the per-stream
+// fixed-order weighted combine (see kernels/grouped_ffn.hpp).
+void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
+    const int D = spec_.hidden_dim, N = spec_.experts_per_layer, K = spec_.top_k, L = spec_.num_layers;
+    const int T = store_.tiles, F = store_.ffn, Ft = F / T;
+    cudaStream_t cs = eng_.compute_stream();
+    const size_t row_bytes = static_cast<size_t>(D) * 2;
+    // union rank of every expert, and the routed tokens of each rank (stream order)
+    int rank_of[kMaxExperts];
+    for (int e = 0; e < N; ++e) rank_of[e] = -1;
+    for (int r = 0; r < u.count; ++r) rank_of[u.experts[r]] = r;
+    GatherArgs g;
+    g.acts = cur_x_;
+    g.stream_stride = static_cast<long long>(L) * D;
+    g.x = d_gx_.as<std::uint16_t>();
+    g.d = D;
+    g.np_stride = np_;
+    g.n_entries = u.count;
+    GCombineArgs c;
+    int n_of[kMaxExperts] = {0};
+    for (int b = 0; b < batch_; ++b)
+        for (int k = 0; k < cur_cnt_[b]; ++k) ++n_of[rank_of[cur_sel_[b * K + k]]];
+    g.first[0] = 0;
+    for (int r = 0; r < u.count; ++r) g.first[r + 1] = g.first[r] + n_of[r];
+    int fill[kMaxExperts] = {0};
+    for (int b = 0; b < batch_; ++b)
+        for (int k = 0; k < K; ++k) {
+            const int pi = b * K + k;
+            if (k >= cur_cnt_[b]) {
+                c.pair_entry[pi] = c.pair_col[pi] = c.pair_expert[pi] = -1;
+                continue;
+            }
+            const int r = rank_of[cur_sel_[pi]];
+            const int col = fill[r]++;
+            g.stream[g.first[r] + col] = static_cast<short>(b);
+            c.pair_entry[pi] = static_cast<short>(r);
+            c.pair_col[pi] = static_cast<short>(col);
+            c.pair_expert[pi] = static_cast<short>(cur_sel_[pi]);
+        }
+    MOE_CUDA(launch_grouped_gather(g, cs));
+    stats_.kernels += 1;
+
+    GroupedLaunch base;
+    base.d = D;
+    base.ft = Ft;
+    base.f = F;
+    base.np_stride = np_;
+    base.h = d_gh_.as<std::uint16_t>();
+    for (int r = 0; r < u.count; ++r) {
+        base.ent[r].n = n_of[r];
+        base.ent[r].np = std::max(16, (n_of[r] + 15) / 16 * 16);
+    }
+    for (const Use& us : uses_) base.ent[us.rank].slot_row = static_cast<long long>(us.slot) * (slot_stride_ / row_bytes);
+    // launch list: resident experts together (all tiles), on-demand experts tile by tile
+    struct Job {
+        std::vector<GSeg> segs;
+        int wait_slot = -1, wait_tile = 0;
+    };
+    std::vector<Job> jobs;
+    Job res;
+    for (const Use& us : uses_)
+        if (!us.missing) {
+            wait_fill(us.slot, -1);
+            res.segs.push_back(GSeg{us.rank, 0, T});
+            stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
+        }
+    if (!res.segs.empty()) jobs.push_back(res);
+    for (const Use& us : uses_)
+        if (us.missing) {
+            for (int t : us.tiles) {
+                Job j;
+                j.segs.push_back(GSeg{us.rank, t, t + 1});
+                j.wait_slot = us.slot;
+                j.wait_tile = t;
+                jobs.push_back(j);
+            }
+            stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
+        }
+    // plan every down launch first: the partial arena must hold the whole layer
+    std::vector<GroupedLaunch> downs(jobs.size(), base);
+    size_t need = 0;
+    for (size_t i = 0; i < jobs.size(); ++i) {
+        GroupedLaunch& p = downs[i];
+        p.n_seg = static_cast<int>(jobs[i].segs.size());
+        for (int s = 0; s < p.n_seg; ++s) p.seg[s] = jobs[i].segs[s];
+        grouped_plan_down(p, sm_count_);
+        need += static_cast<size_t>(p.units) * np_ * 128;
+    }
+    if (need * sizeof(float) > d_gpart_.bytes) {
+        MOE_CUDA(cudaStreamSynchronize(cs));  // earlier layers may still read the old arena
+        d_gpart_.reserve(need * sizeof(float) * 5 / 4);
+    }
+    size_t off = 0;
+    std::vector<std::pair<int, GCombineRef>> refs;  // (rank, ref) in launch order
+    for (size_t i = 0; i < jobs.size(); ++i) {
+        if (jobs[i].wait_slot >= 0) wait_fill(jobs[i].wait_slot, jobs[i].wait_tile);
+        GroupedLaunch up = base;
+        up.n_seg = downs[i].n_seg;
+        for (int s = 0; s < up.n_seg; ++s) up.seg[s] = downs[i].seg[s];
+        up.map_a = map_pool_gu_;
+        up.map_b = map_x_;
+        grouped_plan_gate_up(up);
+        timed_grouped(up, false);
+        GroupedLaunch& dn = downs[i];
+        dn.map_a = map_pool_dn_;
+        dn.map_b = map_h_;
+        dn.partial = d_gpart_.as<float>() + off;
+        off += static_cast<size_t>(dn.units) * np_ * 128;
+        timed_grouped(dn, true);
+        for (int s = 0; s < dn.n_seg; ++s) refs.emplace_back(dn.seg[s].entry, GCombineRef{dn.partial, dn.unit_prefix[s], dn.kc});
+    }
+    std::stable_sort(refs.begin(), refs.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    if (refs.size() > sizeof(c.refs) / sizeof(c.refs[0])) fail(Status::Internal, "grouped combine: too many segments");
+    c.ref_first[0] = 0;
+    size_t q = 0;
+    for (int r = 0; r < u.count; ++r) {
+        while (q < refs.size() && refs[q].first == r) {
+            c.refs[q] = refs[q].second;
+            ++q;
+        }
+        c.ref_first[r + 1] = static_cast<int>(q);
+    }
+    c.acts = cur_x_;
+    c.scores = cur_scores_;
+    c.stream_stride = static_cast<long long>(L) * D;
+    c.score_stride = static_cast<long long>(L) * N;
+    c.out = cur_out_;
+    c.out_stride = static_cast<long long>(L) * D;
+    c.d = D;
+    c.np_stride = np_;
+    c.n_streams = batch_;
+    c.top_k = K;
+    MOE_CUDA(launch_grouped_combine(c, cs));
+    stats_.kernels += 1;
 }
 
 double DecodeSession::decode(const double* acts, const double* scores, int count, bool on_device, float* hidden_out) {
     eng_.activate();
     const int L = spec_.num_layers, N = spec_.experts_per_layer, K = spec_.top_k, D = spec_.hidden_dim;
+    const int B = batch_;
     if (count < 1) return 0.0;
     if (tokens_done_ + count > total_tokens_) fail(Status::Usage, "decode: more tokens than announced in decode_begin");
     cudaStream_t cs = eng_.compute_stream();
     cudaEvent_t t_begin = take_timing(), t_end = take_timing();
     MOE_CUDA(cudaEventRecord(t_begin, cs));
-    const size_t TL = static_cast<size_t>(count) * L;
+    const size_t TL = static_cast<size_t>(count) * B * L;  // rows of [count][B][L]
     const double* x_all = acts;
     const double* s_all = scores;
     if (!on_device) {
@@ -310,60 +496,67 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
     d_out_.reserve(TL * D * sizeof(float));
     float* out_all = (on_device && hidden_out) ? hidden_out : d_out_.as<float>();
 
-    // router groups for every (token, layer) of this call: they depend only on positions
+    // router groups for every (token, layer, stream) of this call: they depend only on positions.
+    // Group (i, l, b) writes rows b*4 + item of the layer's launch.
     const bool prefetch_on = policy_->prefetch_on();
     h_groups_.reserve(TL * sizeof(RouteGroup));
     d_groups_.reserve(TL * sizeof(RouteGroup));
     RouteGroup* hg = h_groups_.as<RouteGroup>();
     int max_gates = 1;
+    const int adaptive = cfg_.policy.adaptive_gating ? kRouteAdaptive : 0;
     for (int i = 0; i < count; ++i)
-        for (int l = 0; l < L; ++l) {
-            const size_t tl = static_cast<size_t>(i) * L + l;
-            const int tok = tokens_done_ + i;
-            RouteGroup g;
-            g.x = x_all + tl * D;
-            g.n_items = 1;
-            g.items[0].scores = s_all + tl * N;
-            g.items[0].fisher = fisher_[l];
-            g.items[0].flags = cfg_.policy.adaptive_gating ? kRouteAdaptive : 0;
-            g.items[0].out = 0;
-            const int adaptive = cfg_.policy.adaptive_gating ? kRouteAdaptive : 0;
-            if (prefetch_on) {
-                if (l + 1 < L) {
-                    for (int dep = 1; dep <= cfg_.lookahead_depth && l + dep < L; ++dep) {
+        for (int l = 0; l < L; ++l)
+            for (int b = 0; b < B; ++b) {
+                const size_t row = (static_cast<size_t>(i) * B + b) * L + l;  // input row [i][b][l]
+                const int tok = tokens_done_ + i;
+                RouteGroup g;
+                g.x = x_all + row * D;
+                g.n_items = 1;
+                g.items[0].scores = s_all + row * N;
+                g.items[0].fisher = fisher_[l];
+                g.items[0].flags = adaptive;
+                g.items[0].out = b * 4;
+                if (prefetch_on) {
+                    if (l + 1 < L) {
+                        for (int dep = 1; dep <= cfg_.lookahead_depth && l + dep < L; ++dep) {
+                            RouteItem& it = g.items[g.n_items++];
+                            eng_.gate_item(it, l + dep);
+                            it.fisher = fisher_[l + dep];
+                            it.flags = adaptive;
+                            it.out = b * 4 + dep;
+                        }
+                    } else if (eng_.has_first_gate() && tok + 1 < total_tokens_) {
                         RouteItem& it = g.items[g.n_items++];
-                        eng_.gate_item(it, l + dep);
-                        it.fisher = fisher_[l + dep];
+                        eng_.gate_item(it, -1);
+                        it.fisher = fisher_[0];
                         it.flags = adaptive;
-                        it.out = dep;
+                        it.out = b * 4 + 1;
                     }
-                } else if (eng_.has_first_gate() && tok + 1 < total_tokens_) {
-                    RouteItem& it = g.items[g.n_items++];
-                    eng_.gate_item(it, -1);
-                    it.fisher = fisher_[0];
-                    it.flags = adaptive;
-                    it.out = 1;
                 }
+                max_gates = std::max(max_gates, g.n_items - 1);
+                hg[(static_cast<size_t>(i) * L + l) * B + b] = g;  // launch order [i][l][b]
             }
-            max_gates = std::max(max_gates, g.n_items - 1);
-            hg[tl] = g;
-        }
     MOE_CUDA(cudaMemcpyAsync(d_groups_.ptr, hg, TL * sizeof(RouteGroup), cudaMemcpyHostToDevice, cs));
     RouteParams rp{D, N, K, tau_, 1.0};
-    RouteOutputs ro{d_route_, d_route_ + 4 * K, d_route_ + 4 * K + 4, nullptr, nullptr, d_route_ + 4 * K + 8};
+    const int rows = 4 * B;
+    int* d_sel = d_route_;
+    int* d_cnt = d_sel + static_cast<size_t>(rows) * K;
+    int* d_sgl = d_cnt + rows;
+    int* d_exact = d_sgl + rows;
+    RouteOutputs ro{d_sel, d_cnt, d_sgl, nullptr, nullptr, d_exact};
     const int* sel = h_route_;
-    const int* cnt = h_route_ + 4 * K;
-    const int* sgl = h_route_ + 4 * K + 4;
-    const int* exact_used = h_route_ + 4 * K + 8;
+    const int* cnt = sel + static_cast<size_t>(rows) * K;
+    const int* sgl = cnt + rows;
+    const int* exact_used = sgl + rows;
 
     std::array<RoutePrediction, 3> preds;
     for (int i = 0; i < count; ++i) {
         const int tok = tokens_done_ + i;
         for (int l = 0; l < L; ++l) {
-            const size_t tl = static_cast<size_t>(i) * L + l;
+            const size_t gl = (static_cast<size_t>(i) * L + l) * B;
             cudaEvent_t r0 = take_timing(), r1 = take_timing();
             cudaEventRecord(r0, cs);
-            MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + tl, 1, max_gates, rp, ro, cs));
+            MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + gl, B, max_gates, rp, ro, cs));
             cudaEventRecord(r1, cs);
             router_events_.emplace_back(r0, r1);
             stats_.kernels += 1;
@@ -373,23 +566,46 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             const auto h1 = std::chrono::steady_clock::now();
             stats_.host_sync_ms += std::chrono::duration<double, std::milli>(h1 - h0).count();
             release_pending(false);
+            // actual selection: the union of the streams' selections (B = 1: the stream's own)
             RouteDecision d;
-            d.count = cnt[0];
-            d.single = sgl[0] != 0;
-            for (int it = 1; it < hg[tl].n_items; ++it) stats_.router_exact += exact_used[it];
-            for (int k = 0; k < d.count; ++k) d.experts[k] = sel[k];
-            const RouteGroup& g = hg[tl];
+            int singles = 0;
+            const int n_items = hg[gl].n_items;
             int np = 0;
-            for (int it = 1; it < g.n_items; ++it) {
-                RoutePrediction& p = preds[np++];
-                p.target = (l + 1 < L) ? l + it : 0;
-                p.count = cnt[it];
-                for (int k = 0; k < p.count; ++k) p.experts[k] = sel[it * K + k];
+            for (int it = 1; it < n_items; ++it) {
+                preds[np].target = (l + 1 < L) ? l + it : 0;
+                preds[np].count = 0;
+                ++np;
             }
-            cur_x_ = g.x;
-            cur_scores_ = s_all + tl * N;
-            cur_out_ = out_all + tl * D;
-            policy_->step(tok, l, d, std::span<const RoutePrediction>(preds.data(), np));
+            for (int b = 0; b < B; ++b) {
+                const int r0w = b * 4;
+                singles += sgl[r0w] != 0;
+                for (int it = 1; it < n_items; ++it) stats_.router_exact += exact_used[r0w + it];
+                for (int k = 0; k < cnt[r0w]; ++k) {
+                    const int e = sel[r0w * K + k];
+                    bool seen = false;
+                    for (int q = 0; q < d.count; ++q) seen |= d.experts[q] == e;
+                    if (!seen) d.experts[d.count++] = e;
+                }
+                for (int it = 1; it < n_items; ++it) {
+                    RoutePrediction& p = preds[it - 1];
+                    for (int k = 0; k < cnt[r0w + it]; ++k) {
+                        const int e = sel[(r0w + it) * K + k];
+                        bool seen = false;
+                        for (int q = 0; q < p.count; ++q) seen |= p.experts[q] == e;
+                        if (!seen) p.experts[p.count++] = e;
+                    }
+                }
+                if (B > 1) {
+                    cur_cnt_[b] = cnt[r0w];
+                    for (int k = 0; k < K; ++k) cur_sel_[b * K + k] = k < cnt[r0w] ? sel[r0w * K + k] : -1;
+                }
+            }
+            d.single = B == 1 && sgl[0] != 0;
+            const size_t row0 = (static_cast<size_t>(i) * B) * L + l;  // stream 0's input row
+            cur_x_ = x_all + row0 * D;
+            cur_scores_ = s_all + row0 * N;
+            cur_out_ = out_all + row0 * D;
+            policy_->step(tok, l, d, std::span<const RoutePrediction>(preds.data(), np), B > 1 ? singles : -1);
             stats_.host_step_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count();
         }
     }
@@ -399,7 +615,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
     MOE_CUDA(cudaStreamSynchronize(cs));
     release_pending(true);
     tokens_done_ += count;
-    stats_.tokens += count;
+    stats_.tokens += static_cast<long long>(count) * B;
     float ms = 0.0f;
     MOE_CUDA(cudaEventElapsedTime(&ms, t_begin, t_end));
     timing_pool_.push_back(t_begin);

@@ -10,6 +10,12 @@
 //   on-demand tile compute-> wait on that tile's copy event, then SwiGLU on that tile
 // The logical engine decides every hit/miss/prefetch/eviction with the reference's tick model, so
 // the event trace is the reference's; wall-clock only changes when things physically happen.
+//
+// Batched decode (batch B > 1, BASELINE config 4): B token streams share the cache.  Each layer
+// routes all B streams in one K1 launch; the logical engine sees the union of their selections
+// and of their look-ahead lists (oracle/moe_oracle.c orc_simulate_batch); the FFN runs as grouped
+// tcgen05 GEMMs (kernels/grouped_ffn.hpp) over the union's experts with each expert's routed
+// tokens gathered, then a per-stream fixed-order weighted combine.
 #pragma once
 
 #include <cuda_runtime_api.h>
@@ -21,6 +27,7 @@
 
 #include "../host/policy_engine.hpp"
 #include "../kernels/expert_ffn.hpp"
+#include "../kernels/grouped_ffn.hpp"
 #include "../kernels/router.hpp"
 #include "copy_engine.hpp"
 #include "engine.hpp"
@@ -40,10 +47,10 @@ struct DecodeStats {
 class DecodeSession : public DecodeListener {
 public:
     DecodeSession(Engine& eng, std::span<const int> capacities, int staging_slots, std::span<const double> fisher,
-                  double tau, const SimConfig& cfg, std::uint64_t seed, int total_tokens);
+                  double tau, const SimConfig& cfg, std::uint64_t seed, int total_tokens, int batch = 1);
     ~DecodeSession() override;
 
-    // acts [count][L][d], scores [count][L][N]: host or device pointers
+    // acts [count][B][L][d], scores [count][B][L][N]: host or device pointers
     double decode(const double* acts, const double* scores, int count, bool on_device, float* hidden_out);
 
     const PolicyEngine& policy() const { return *policy_; }
@@ -76,6 +83,16 @@ private:
     // launch + time + clear the segment list; records where each (rank, tile) partial lives
     void timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int>>& seg_meta,
                    std::vector<std::tuple<int, int, FfnPartialRef>>& refs);
+    void layer_ffn_single(const RouteDecision& d);   // batch 1: K2 row kernel
+    void layer_ffn_grouped(const RouteDecision& d);  // batch > 1: K3 grouped tcgen05 kernels
+    void timed_grouped(GroupedLaunch& p, bool down);
+    int batch_ = 1;
+    int np_ = 16;                       // token rows per expert entry in X / H (B rounded up to 16)
+    DeviceBuffer d_gx_, d_gh_, d_gpart_;  // X [N][NP][d], H [N][NP][F] bf16; down partial arena
+    size_t gpart_next_ = 0;             // floats used in the arena this layer
+    CUtensorMap map_pool_gu_{}, map_pool_dn_{}, map_x_{}, map_h_{};
+    // per-stream router results of the current layer
+    std::vector<int> cur_sel_, cur_cnt_;
     DeviceBuffer d_partials_;  // per-layer pool of K2 partial regions (reused every layer, stream-ordered)
     int partial_regions_ = 0, partial_next_ = 0;
 

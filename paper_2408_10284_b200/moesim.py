@@ -150,8 +150,9 @@ def tile_pipeline_latency(tiles: int, transfer: int, compute: int) -> int:
     return out.value
 
 
-def _events_buf(spec: ModelSpec, T: int, cfg: SimConfig):
-    per_layer = 2 + spec.top_k * (1 + 2 * cfg.tile_count_per_expert) + 3 * spec.top_k * cfg.tile_count_per_expert
+def _events_buf(spec: ModelSpec, T: int, cfg: SimConfig, batch: int = 1):
+    k = min(spec.experts_per_layer, spec.top_k * batch)  # experts a layer can activate
+    per_layer = 2 + k * (1 + 2 * cfg.tile_count_per_expert) + 3 * k * cfg.tile_count_per_expert
     cap = T * spec.num_layers * per_layer + 64
     return (_capi.EventC * cap)(), cap
 
@@ -284,9 +285,14 @@ class Engine:
         check(load().moe_expert_read(self._h, layer, expert, _p(out, _capi._u16)))
         return out
 
-    def decode_begin(self, caps, fisher, tau, cfg: SimConfig, seed: int, total_tokens: int, staging_slots: int = 0):
-        check(load().moe_decode_begin(self._h, _p(_i32(caps), _capi._i32), staging_slots, _p(_f64(fisher), _capi._d),
-                                      float(tau), C.byref(cfg.c()), seed, total_tokens))
+    def decode_begin(self, caps, fisher, tau, cfg: SimConfig, seed: int, total_tokens: int, staging_slots: int = 0,
+                     batch: int = 1):
+        """Start a decode session (moe_decode_begin_batch).  batch > 1: B token streams share the
+        cache; decode_tokens then takes acts [n][B][L][d] and scores [n][B][L][N]."""
+        check(load().moe_decode_begin_batch(self._h, _p(_i32(caps), _capi._i32), staging_slots,
+                                            _p(_f64(fisher), _capi._d), float(tau), C.byref(cfg.c()), seed,
+                                            total_tokens, batch))
+        self._batch = batch
 
     def decode_tokens(self, acts, scores, hidden_out=None, on_device: bool = False) -> float:
         """acts [n][L][d], scores [n][L][N] host numpy arrays (or device pointers via on_device)."""
@@ -312,7 +318,8 @@ class Engine:
         T = tokens or 0
         lat = np.zeros(max(T, 1), dtype=np.int64)
         odl = np.zeros(self.spec.num_layers, dtype=np.int64)
-        buf, cap = (_events_buf(self.spec, T, cfg) if (timeline and cfg is not None and T) else (None, 0))
+        buf, cap = (_events_buf(self.spec, T, cfg, getattr(self, "_batch", 1)) if (timeline and cfg is not None and T)
+                    else (None, 0))
         check(load().moe_decode_end(self._h, C.byref(m), _p(lat, _capi._i64) if T else None, _p(odl, _capi._i64),
                                     buf, cap, C.byref(n), C.byref(st)))
         return SimResult({k: getattr(m, k) for k, _ in _capi.MetricsC._fields_}, lat[:T], odl,

@@ -51,6 +51,10 @@ class SynthConfigC(C.Structure):
                 ("drift_scales", C.POINTER(C.c_double))]
 
 
+class DecodeOptsC(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("ep_rank", C.c_int32), ("ep_world", C.c_int32)]
+
+
 class DecodeStatsC(C.Structure):
     _fields_ = [("tokens", C.c_int64), ("kernels_launched", C.c_int64), ("ffn_launches", C.c_int64),
                 ("tile_copies", C.c_int64), ("copy_bytes", C.c_int64), ("input_bytes", C.c_int64),
@@ -93,8 +97,8 @@ SIGNATURES = {
     "moe_expert_bytes": (C.c_int, [_eng, _i64]),
     "moe_expert_read": (C.c_int, [_eng, C.c_int32, C.c_int32, _u16]),
     "moe_decode_begin": (C.c_int, [_eng, _i32, C.c_int32, _d, C.c_double, _cfg, C.c_uint64, C.c_int32]),
-    "moe_decode_begin_batch": (C.c_int, [_eng, _i32, C.c_int32, _d, C.c_double, _cfg, C.c_uint64, C.c_int32,
-                                         C.c_int32]),
+    "moe_decode_begin_ex": (C.c_int, [_eng, _i32, C.c_int32, _d, C.c_double, _cfg, C.c_uint64, C.c_int32,
+                                      C.POINTER(DecodeOptsC)]),
     "moe_decode_tokens": (C.c_int, [_eng, _d, _d, C.c_int32, C.c_int32, _f, _d]),
     "moe_decode_end": (C.c_int, [_eng, C.POINTER(MetricsC), _i64, _i64, C.POINTER(EventC), C.c_int64, _i64,
                                  C.POINTER(DecodeStatsC)]),

@@ -381,8 +381,8 @@ int moe_expert_read(moe_engine_t h, int32_t layer, int32_t expert, uint16_t* out
     });
 }
 
-int moe_decode_begin_batch(moe_engine_t h, const int32_t* caps, int32_t staging, const double* fisher, double tau,
-                           const moe_sim_config* cfg, uint64_t seed, int32_t total_tokens, int32_t batch) {
+int moe_decode_begin_ex(moe_engine_t h, const int32_t* caps, int32_t staging, const double* fisher, double tau,
+                        const moe_sim_config* cfg, uint64_t seed, int32_t total_tokens, const moe_decode_opts* opts) {
     return guarded([&] {
         Engine& e = eng(h);
         SimConfig c = to_cfg(cfg);
@@ -391,16 +391,19 @@ int moe_decode_begin_batch(moe_engine_t h, const int32_t* caps, int32_t staging,
         GatingThreshold{tau}.validate();
         if (!e.experts) fail(Status::Usage, "decode_begin: call moe_experts_init first");
         const int L = e.spec().num_layers;
+        const int batch = opts ? opts->batch : 1;
+        const int ep_rank = opts ? opts->ep_rank : 0;
+        const int ep_world = opts ? opts->ep_world : 1;
         e.session.reset();
         e.session = std::make_unique<DecodeSession>(e, std::span<const int>(caps, L), staging,
                                                     std::span<const double>(fisher, L), tau, c, seed, total_tokens,
-                                                    batch);
+                                                    batch, ep_rank, ep_world);
     });
 }
 
 int moe_decode_begin(moe_engine_t h, const int32_t* caps, int32_t staging, const double* fisher, double tau,
                      const moe_sim_config* cfg, uint64_t seed, int32_t total_tokens) {
-    return moe_decode_begin_batch(h, caps, staging, fisher, tau, cfg, seed, total_tokens, 1);
+    return moe_decode_begin_ex(h, caps, staging, fisher, tau, cfg, seed, total_tokens, nullptr);
 }
 
 int moe_decode_tokens(moe_engine_t h, const double* acts, const double* scores, int32_t count, int32_t on_device,
@@ -488,7 +491,10 @@ int moe_expert_ffn(moe_engine_t h, int32_t layer, int32_t expert, const double* 
         c.ft = Ft;
         c.experts[0] = 0;
         c.n_refs = T;
-        for (int t = 0; t < T; ++t) c.refs[t] = FfnPartialRef{p.partial, ffn_grid(p, sms), T, t, 0};
+        for (int t = 0; t < T; ++t) {
+            c.refs[t] = FfnPartialRef{p.partial, ffn_grid(p, sms), T, t, 0};
+            ffn_partial_range(c.refs[t], p.ft);
+        }
         MOE_CUDA(launch_combine(c, cs));
         MOE_CUDA(cudaMemcpyAsync(y, dout.ptr, D * sizeof(float), cudaMemcpyDeviceToHost, cs));
         MOE_CUDA(cudaStreamSynchronize(cs));

@@ -11,9 +11,12 @@
 // Because a CTA consumes the h values it produced, there is no cross-CTA dependency (the earlier
 // TMA-ring design needed a grid-wide gate/up -> down handoff and topped out at 4.1 TB/s; this one
 // measures 6.3 TB/s on large launches, tools/ffn_microbench.cu v4, profiles/r1_ffn_microbench.txt).
-// Small launches (one 88 MB tile of an on-demand expert) also bulk-prefetch the next chunk into L2
-// through the TMA engine (cp.async.bulk.prefetch.L2) to cover the ramp.  Each CTA writes one fp32
-// partial of y per segment it touched; the combine kernel reduces them in a fixed order.
+// Optional L2 bulk prefetch (cp.async.bulk.prefetch.L2) of the next chunk or of the whole row range
+// exists for experiments; on cold launches both measured slower (tools/k2_cold.cu), so the decode
+// leaves it off.  A TMA-ring variant of this row-owner kernel (a producer warp streaming R rows per
+// stage into a 2-stage 96 KB ring) measured 4.9 TB/s vs 5.85 TB/s at 16 segments and was dropped
+// (profiles/r1_k2_variants.txt).  Each CTA writes one fp32 partial of y per segment it touched; the
+// combine kernel reduces them in a fixed order.
 #include <cuda_runtime.h>
 
 #include "expert_ffn.hpp"
@@ -80,6 +83,16 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_cons
     const int first_seg = static_cast<int>(r_lo / Ft);
     float* const part = p.partial + static_cast<size_t>(blockIdx.x) * kFfnSlotsPerCta * D;
     int cur_seg = first_seg;
+    if (p.l2_prefetch == 2 && tid == 0) {
+        // whole-range prefetch: HBM -> L2 at full rate regardless of how fast this CTA consumes
+        for (long long c = r_lo; c < r_hi;) {
+            const int s = static_cast<int>(c / Ft), q0 = static_cast<int>(c % Ft);
+            const int n = static_cast<int>(min(static_cast<long long>(Ft - q0), r_hi - c));
+            ptx::bulk_prefetch_l2(p.seg[s].gate_up + static_cast<size_t>(q0) * 2 * D, n * 2u * D * 2u);
+            ptx::bulk_prefetch_l2(p.seg[s].down_t + static_cast<size_t>(q0) * D, n * static_cast<unsigned>(D) * 2u);
+            c += n;
+        }
+    }
     __syncthreads();
     int parity = 0;
     for (long long c0 = r_lo; c0 < r_hi; parity ^= 1) {
@@ -89,7 +102,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_cons
             store_partial<DC>(part + static_cast<size_t>(cur_seg - first_seg) * D, acc, tid, D);
             cur_seg = s;
         }
-        if (p.l2_prefetch && tid == 0 && c0 + n < r_hi) {
+        if (p.l2_prefetch == 1 && tid == 0 && c0 + n < r_hi) {
             const long long c1 = c0 + n;
             const int s1 = static_cast<int>(c1 / Ft), q0 = static_cast<int>(c1 % Ft);
             const int n1 = static_cast<int>(min(static_cast<long long>(min(kChunk, Ft - q0)), r_hi - c1));
@@ -174,33 +187,25 @@ __global__ void __launch_bounds__(kCombineCols * kCombineLanes) combine_kernel(c
     const bool live = j < a.d;
     double denom = 0.0;
     for (int r = 0; r < a.ranks; ++r) denom += a.scores[a.experts[r]];
-    float acc = live ? static_cast<float>(a.x[j]) : 0.0f;
+    float acc = (live && a.residual) ? static_cast<float>(a.x[j]) : 0.0f;
     int ref = 0;
     for (int r = 0; r < a.ranks; ++r) {
         float part = 0.0f;
         for (; ref < a.n_refs && a.refs[ref].rank == r; ++ref) {
             const FfnPartialRef& f = a.refs[ref];
-            const long long TR = static_cast<long long>(f.n_seg) * a.ft;
-            const long long s_lo = static_cast<long long>(f.seg) * a.ft, s_hi = s_lo + a.ft;
-            int c_lo = static_cast<int>(s_lo * f.grid / TR);
-            while (c_lo > 0 && TR * c_lo / f.grid > s_lo) --c_lo;
-            while (TR * (c_lo + 1) / f.grid <= s_lo) ++c_lo;  // first CTA whose range reaches the segment
-            int c_hi = static_cast<int>((s_hi - 1) * f.grid / TR);
-            while (c_hi + 1 < f.grid && TR * (c_hi + 1) / f.grid < s_hi) ++c_hi;
-            while (c_hi > c_lo && TR * c_hi / f.grid >= s_hi) --c_hi;  // last CTA starting inside it
             if (!live) continue;
-            // two independent accumulators (fixed assignment) keep several L2 loads in flight
+            // lane q sums CTAs c_lo + q, c_lo + q + 16, ... in that order; 8 loads in flight per lane
             float p0 = 0.0f, p1 = 0.0f;
-            int c = c_lo + q;
-            for (; c + kCombineLanes <= c_hi; c += 2 * kCombineLanes) {
-                const int s0 = f.seg - static_cast<int>(TR * c / f.grid / a.ft);
-                const int s1 = f.seg - static_cast<int>(TR * (c + kCombineLanes) / f.grid / a.ft);
-                p0 += f.partial[(static_cast<size_t>(c) * kFfnSlotsPerCta + s0) * a.d + j];
-                p1 += f.partial[(static_cast<size_t>(c + kCombineLanes) * kFfnSlotsPerCta + s1) * a.d + j];
-            }
-            if (c <= c_hi) {
-                const int s0 = f.seg - static_cast<int>(TR * c / f.grid / a.ft);
-                p0 += f.partial[(static_cast<size_t>(c) * kFfnSlotsPerCta + s0) * a.d + j];
+            for (int c = f.c_lo + q; c <= f.c_hi; c += 8 * kCombineLanes) {
+                float v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int cc = c + k * kCombineLanes;
+                    const int sl = cc == f.c_lo ? f.slot_lo : 0;
+                    v[k] = cc <= f.c_hi ? f.partial[(static_cast<size_t>(cc) * kFfnSlotsPerCta + sl) * a.d + j] : 0.0f;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) p0 += v[k];
             }
             part += p0 + p1;
         }
@@ -277,6 +282,20 @@ __global__ void expert_init_kernel(uint16_t* dst, int D, int F, int tiles, InitA
 }
 
 }  // namespace
+
+void ffn_partial_range(FfnPartialRef& f, int ft) {
+    const long long TR = static_cast<long long>(f.n_seg) * ft;
+    const long long s_lo = static_cast<long long>(f.seg) * ft, s_hi = s_lo + ft;
+    int c_lo = static_cast<int>(s_lo * f.grid / TR);
+    while (c_lo > 0 && TR * c_lo / f.grid > s_lo) --c_lo;
+    while (TR * (c_lo + 1) / f.grid <= s_lo) ++c_lo;  // first CTA whose range reaches the segment
+    int c_hi = static_cast<int>((s_hi - 1) * f.grid / TR);
+    while (c_hi + 1 < f.grid && TR * (c_hi + 1) / f.grid < s_hi) ++c_hi;
+    while (c_hi > c_lo && TR * c_hi / f.grid >= s_hi) --c_hi;  // last CTA starting inside it
+    f.c_lo = c_lo;
+    f.c_hi = c_hi;
+    f.slot_lo = f.seg - static_cast<int>(TR * c_lo / f.grid / ft);
+}
 
 int ffn_grid(const FfnLaunch& p, int sm_count) {
     const long long rows = static_cast<long long>(p.n_seg) * p.ft;

@@ -32,7 +32,8 @@ struct FfnSegment {
 struct FfnLaunch {
     int n_seg = 0;
     int d = 0, ft = 0;
-    int l2_prefetch = 0;              // bulk-prefetch the next row chunk into L2 (small launches)
+    int l2_prefetch = 0;              // 1: bulk-prefetch the next row chunk into L2; 2: the CTA's whole
+                                      // row range at kernel start (small launches)
     const double* x = nullptr;        // [d] layer input (fp64; converted to fp32 in shared memory)
     float* partial = nullptr;         // [grid][kFfnSlotsPerCta][d] written by the launch
     FfnSegment seg[kMaxFfnSegments];
@@ -49,7 +50,14 @@ struct FfnPartialRef {
     int n_seg = 0;                   // that launch's segment count
     int seg = 0;                     // index of the segment in that launch
     int rank = 0;                    // expert rank in the selection
+    // CTAs of that launch whose row ranges intersect the segment, and the partial slot of the
+    // first one (later ones start inside the segment: slot 0); filled by ffn_partial_range()
+    int c_lo = 0, c_hi = -1, slot_lo = 0;
 };
+
+// Host: fill r.c_lo / c_hi / slot_lo from (grid, n_seg, seg) for row-tile ft (same integer
+// arithmetic as the kernel's row split).
+void ffn_partial_range(FfnPartialRef& r, int ft);
 
 constexpr int kMaxCombineRefs = 128;
 
@@ -59,6 +67,7 @@ struct CombineArgs {
     float* out = nullptr;            // [D]
     int experts[8] = {0};            // selected experts in rank order
     int ranks = 0, d = 0, ft = 0;
+    int residual = 1;                // add x (expert-parallel: only the first shard adds it)
     int n_refs = 0;                  // refs sorted by (rank, tile)
     FfnPartialRef refs[kMaxCombineRefs];
 };

@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(128) gcombine_kernel(const __grid_constant__ G
         denom += sc[ex];
         ++ranks;
     }
-    float acc = static_cast<float>(a.acts[b * a.stream_stride + j]);
+    float acc = a.residual ? static_cast<float>(a.acts[b * a.stream_stride + j]) : 0.0f;
     for (int r = 0; r < ranks; ++r) {
         const int pi = b * a.top_k + r;
         const int e = a.pair_entry[pi], col = a.pair_col[pi];

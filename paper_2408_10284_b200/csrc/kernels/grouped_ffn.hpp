@@ -100,6 +100,7 @@ struct GCombineArgs {
     float* out = nullptr;            // out_b at out + b * out_stride
     long long out_stride = 0;
     int d = 0, np_stride = 0, n_streams = 0, top_k = 0;
+    int residual = 1;                // add x (expert-parallel: only the first shard adds it)
     int ref_first[kGMaxEntries + 1]; // entry e's refs: refs[ref_first[e] .. ref_first[e+1])
     GCombineRef refs[256];
     // per (stream, rank): entry index, token column, expert id (-1 = unused rank)

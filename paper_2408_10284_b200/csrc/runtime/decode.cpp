@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <chrono>
 #include <numeric>
@@ -15,8 +16,10 @@ constexpr size_t kSlotAlign = 2u << 20;
 
 DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int staging_slots,
                              std::span<const double> fisher, double tau, const SimConfig& cfg, std::uint64_t seed,
-                             int total_tokens, int batch)
+                             int total_tokens, int batch, int ep_rank, int ep_world)
     : batch_(batch),
+      ep_rank_(ep_rank),
+      ep_world_(ep_world),
       eng_(eng),
       spec_(eng.spec()),
       cfg_(cfg),
@@ -41,11 +44,16 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
         fail(Status::Usage, "batched decode needs hidden_dim % 128 == 0 and (ffn / tiles) % 64 == 0 (tcgen05 tiles)");
     const bool prefetch_on = cfg_.policy.prefetch && cfg_.lookahead_depth > 0;
     if (prefetch_on && !eng.has_gates()) fail(Status::Usage, "decode: prefetching requires the gate matrices");
+    if (ep_world_ < 1 || ep_rank_ < 0 || ep_rank_ >= ep_world_ || ep_world_ > N)
+        fail(Status::Usage, "decode_begin: expert-parallel shard must satisfy 0 <= rank < world <= N");
     int resident = 0;
+    int owned_per_layer = 0;
+    for (int e = 0; e < N; ++e) owned_per_layer += owned(e) ? 1 : 0;
     for (int c : caps_) {
         if (c < 0 || c > N) fail(Status::Usage, "decode_begin: capacity out of [0, N]");
-        resident += c;
+        resident += std::min(c, owned_per_layer);  // this shard's resident experts
     }
+    resident_slots_ = resident;
     int staging = staging_slots > 0 ? staging_slots : std::min(32, L * N + K);
     n_slots_ = resident + staging;
     stats_.slots_total = n_slots_;
@@ -59,6 +67,7 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     for (int s = 0; s < n_slots_; ++s) free_.push_back(s);
     slot_of_.assign(static_cast<size_t>(L) * N, -1);
     cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, eng.device());
+    if (const char* v = std::getenv("ADAPMOE_K2_L2")) l2_mode_ = std::atoi(v);  // profiling knob
 
     // at most one launch for the resident experts' tiles (split per 32 segments) + one per
     // on-demand tile
@@ -128,9 +137,7 @@ int DecodeSession::take_slot() {
     const int s = free_.front();
     free_.pop_front();
     const int in_use = n_slots_ - static_cast<int>(free_.size());
-    int resident = 0;
-    for (int c : caps_) resident += c;
-    stats_.staging_high_water = std::max(stats_.staging_high_water, in_use - resident);
+    stats_.staging_high_water = std::max(stats_.staging_high_water, in_use - resident_slots_);
     return s;
 }
 
@@ -164,6 +171,11 @@ void DecodeSession::on_request(int id, ExpertRef ref, bool on_demand) {
         req_slot_.resize(id + 1, -1);
         req_job_.resize(id + 1);
     }
+    if (!owned(ref.expert)) {  // another shard moves it
+        req_slot_[id] = -1;
+        req_job_[id].reset();
+        return;
+    }
     const int s = take_slot();
     req_slot_[id] = s;
     auto job = copier_->make_job(slot_ptr(s), store_.expert(ref.layer, ref.expert), store_.tile_bytes, store_.tiles);
@@ -173,13 +185,16 @@ void DecodeSession::on_request(int id, ExpertRef ref, bool on_demand) {
     copier_->submit(job, on_demand);
 }
 
-void DecodeSession::on_promote(int id) { copier_->promote(req_job_[id], false); }
+void DecodeSession::on_promote(int id) {
+    if (req_job_[id]) copier_->promote(req_job_[id], false);
+}
 
 void DecodeSession::on_insert(ExpertRef ref, int request, std::optional<int> evicted) {
     const int N = spec_.experts_per_layer;
     const int key = ref.layer * N + ref.expert;
     if (request < 0) {  // initial residency (session setup, synchronous, untimed)
         if (evicted) fail(Status::Internal, "initial fill evicted an expert");
+        if (!owned(ref.expert)) return;
         const int s = take_slot();
         MOE_CUDA(cudaMemcpy(slot_ptr(s), store_.expert(ref.layer, ref.expert), store_.expert_bytes, cudaMemcpyHostToDevice));
         slots_[s].fill.reset();
@@ -187,15 +202,17 @@ void DecodeSession::on_insert(ExpertRef ref, int request, std::optional<int> evi
         slot_of_[key] = s;
         return;
     }
-    const int s = req_slot_[request];
+    const int s = req_slot_[request];  // -1 when another shard owns the expert
     if (evicted && *evicted == ref.expert) {  // capacity-0 layer: the copy was transit only
-        release_slot(s);
+        if (s >= 0) release_slot(s);
     } else {
-        if (slot_of_[key] >= 0) fail(Status::Internal, "insert of an expert that already has a slot");
-        slot_of_[key] = s;
+        if (s >= 0) {
+            if (slot_of_[key] >= 0) fail(Status::Internal, "insert of an expert that already has a slot");
+            slot_of_[key] = s;
+        }
         if (evicted) {
             const int vkey = ref.layer * N + *evicted;
-            release_slot(slot_of_[vkey]);
+            if (slot_of_[vkey] >= 0) release_slot(slot_of_[vkey]);  // the victim is ours
             slot_of_[vkey] = -1;
         }
     }
@@ -203,10 +220,12 @@ void DecodeSession::on_insert(ExpertRef ref, int request, std::optional<int> evi
 }
 
 void DecodeSession::on_resident_compute(int, ExpertRef ref, int rank) {
+    if (!owned(ref.expert)) return;
     uses_.push_back(Use{rank, slot_of_[ref.layer * spec_.experts_per_layer + ref.expert], false, {}});
 }
 
-void DecodeSession::on_tile_compute(int, ExpertRef, int rank, int tile, int request) {
+void DecodeSession::on_tile_compute(int, ExpertRef ref, int rank, int tile, int request) {
+    if (!owned(ref.expert)) return;
     if (uses_.empty() || !uses_.back().missing || uses_.back().rank != rank)
         uses_.push_back(Use{rank, req_slot_[request], true, {}});
     uses_.back().tiles.push_back(tile);
@@ -237,10 +256,13 @@ void DecodeSession::timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int
     const size_t region = static_cast<size_t>(kFfnMaxCtas) * kFfnSlotsPerCta * spec_.hidden_dim;
     if (partial_next_ >= partial_regions_) fail(Status::Internal, "decode: FFN partial pool exhausted");
     p.partial = d_partials_.as<float>() + region * partial_next_++;
-    p.l2_prefetch = p.n_seg == 1 ? 1 : 0;  // only single-tile launches gain from the L2 prefetch
+    p.l2_prefetch = p.n_seg <= 2 ? l2_mode_ : 0;  // only small launches gain from the L2 prefetch
     const int grid = ffn_grid(p, sm_count_);
-    for (int s = 0; s < p.n_seg; ++s)
-        refs.emplace_back(seg_meta[s].first, seg_meta[s].second, FfnPartialRef{p.partial, grid, p.n_seg, s, seg_meta[s].first});
+    for (int s = 0; s < p.n_seg; ++s) {
+        FfnPartialRef r{p.partial, grid, p.n_seg, s, seg_meta[s].first};
+        ffn_partial_range(r, p.ft);
+        refs.emplace_back(seg_meta[s].first, seg_meta[s].second, r);
+    }
     cudaEvent_t e0 = take_timing(), e1 = take_timing();
     cudaEventRecord(e0, cs);
     MOE_CUDA(launch_ffn(p, sm_count_, cs));
@@ -315,6 +337,7 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
     c.ranks = d.count;
     c.d = D;
     c.ft = Ft;
+    c.residual = ep_rank_ == 0 ? 1 : 0;
     c.n_refs = static_cast<int>(refs.size());
     for (size_t i = 0; i < refs.size(); ++i) c.refs[i] = std::get<2>(refs[i]);
     for (int r = 0; r < d.count; ++r) c.experts[r] = d.experts[r];
@@ -468,6 +491,7 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
     c.np_stride = np_;
     c.n_streams = batch_;
     c.top_k = K;
+    c.residual = ep_rank_ == 0 ? 1 : 0;
     MOE_CUDA(launch_grouped_combine(c, cs));
     stats_.kernels += 1;
 }

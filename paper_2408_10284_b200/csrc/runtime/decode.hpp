@@ -47,7 +47,8 @@ struct DecodeStats {
 class DecodeSession : public DecodeListener {
 public:
     DecodeSession(Engine& eng, std::span<const int> capacities, int staging_slots, std::span<const double> fisher,
-                  double tau, const SimConfig& cfg, std::uint64_t seed, int total_tokens, int batch = 1);
+                  double tau, const SimConfig& cfg, std::uint64_t seed, int total_tokens, int batch = 1,
+                  int ep_rank = 0, int ep_world = 1);
     ~DecodeSession() override;
 
     // acts [count][B][L][d], scores [count][B][L][N]: host or device pointers
@@ -86,7 +87,15 @@ private:
     void layer_ffn_single(const RouteDecision& d);   // batch 1: K2 row kernel
     void layer_ffn_grouped(const RouteDecision& d);  // batch > 1: K3 grouped tcgen05 kernels
     void timed_grouped(GroupedLaunch& p, bool down);
+    int l2_mode_ = 0;  // K2 L2 prefetch (ADAPMOE_K2_L2: 0 off, 1 next chunk, 2 whole range); off: both
+                       // prefetch modes measured slower on cold launches (tools/k2_cold.cu)
     int batch_ = 1;
+    // expert parallelism: shard ep_rank_ of ep_world_ owns experts e % world == rank
+    // of every layer.  The logical engine is replicated (same inputs -> same trace on every shard);
+    // this shard only holds, copies and computes its own experts, and writes its partial layer
+    // output (shard 0 adds the residual); the shards' partials are summed in shard order.
+    int ep_rank_ = 0, ep_world_ = 1;
+    bool owned(int expert) const { return expert % ep_world_ == ep_rank_; }
     int np_ = 16;                       // token rows per expert entry in X / H (B rounded up to 16)
     DeviceBuffer d_gx_, d_gh_, d_gpart_;  // X [N][NP][d], H [N][NP][F] bf16; down partial arena
     size_t gpart_next_ = 0;             // floats used in the arena this layer
@@ -113,6 +122,7 @@ private:
     DeviceBuffer pool_;
     size_t slot_stride_ = 0;
     int n_slots_ = 0;
+    int resident_slots_ = 0;
     std::vector<Slot> slots_;
     std::deque<int> free_;
     std::vector<std::pair<long long, int>> pending_free_;  // (layer sequence, slot)

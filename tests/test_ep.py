@@ -1,0 +1,126 @@
+"""Expert parallelism (BASELINE config 5): shard r of G owns experts e % G == r.
+
+  * [cpu] ownership partitions every layer's experts; per-shard slot pools cover the DP capacities;
+  * [cpu, gloo world 2] the shard partials (computed here by the fp64 oracle) combined by
+    ep.combine_partials equal the full MoE layer output and are bit-identical on both shards;
+  * [gpu] shards 0 and 1 of a world-2 session run one after the other on one B200 (the driver's GPU
+    tier has one GPU): each replays the reference trace bit-exactly, and their partials summed in
+    shard order match the single-GPU decode within 1e-5 relative (only the fp32 summation order
+    differs), for batch 1 and batch 4.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from helpers import oracle_inputs, sim_config, sim_kwargs
+from oracle import oracle as O
+from paper_2408_10284_b200 import ep
+
+
+@pytest.mark.parametrize("N,G", [(8, 1), (8, 2), (8, 4), (8, 8), (6, 4)])
+def test_ownership_partitions_experts(N, G):
+    shards = [ep.owned_experts(N, G, r) for r in range(G)]
+    assert sorted(sum(shards, [])) == list(range(N))
+    caps = [N, 3, 0, 1, 2]
+    slots = [ep.shard_resident_slots(caps, N, G, r) for r in range(G)]
+    assert sum(slots) >= sum(caps)  # every resident expert has a home on its owner
+    assert all(s <= sum(min(c, len(sh)) for c in caps) for s, sh in zip(slots, shards))
+
+
+def _partials_oracle(w, decisions, t, l, ffn, tiles, seed, world, rank):
+    sel = [int(e) for e in decisions[t, l] if e >= 0]
+    sc = w.scores[t, l]
+    denom = sum(sc[e] for e in sel)
+    x32 = w.acts[t, l].astype(np.float32).astype(np.float64)
+    acc = x32.copy() if rank == 0 else np.zeros(w.D)
+    for e in sel:
+        if e % world != rank:
+            continue
+        wgt = 1.0 if len(sel) == 1 else sc[e] / denom
+        acc += wgt * O.swiglu(O.expert_init(seed, l, e, w.D, ffn, tiles), w.D, ffn, tiles, x32.astype(np.float32))
+    return acc
+
+
+def _gloo_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = load_golden("tiny")
+        w, fg = oracle_inputs(g)
+        sim = O.simulate(w, g["sim_capacities"], g["tau"], first_gate=fg, **sim_kwargs(g))
+        pts = [(0, 0), (3, 2), (9, 3)]
+        part = np.stack([_partials_oracle(w, sim.decisions, t, l, 896, 4, 5, world, rank) for t, l in pts])
+        full = ep.combine_partials(torch.from_numpy(part)).numpy()
+        np.save(os.path.join(out_dir, f"ep_{rank}.npy"), full)
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_combine_partials_gloo_world2(tmp_path):
+    import torch.multiprocessing as mp
+    mp.spawn(_gloo_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    r0, r1 = np.load(tmp_path / "ep_0.npy"), np.load(tmp_path / "ep_1.npy")
+    assert np.array_equal(r0, r1)  # same bits on every shard
+    g = load_golden("tiny")
+    w, fg = oracle_inputs(g)
+    sim = O.simulate(w, g["sim_capacities"], g["tau"], first_gate=fg, **sim_kwargs(g))
+    for i, (t, l) in enumerate([(0, 0), (3, 2), (9, 3)]):
+        full = _partials_oracle(w, sim.decisions, t, l, 896, 4, 5, 1, 0)
+        assert np.abs(r0[i] - full).max() <= 1e-12 * np.abs(full).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("batch", [1, 4])
+def test_ep_shards_match_single_gpu(batch):
+    import paper_2408_10284_b200 as P
+    g = load_golden("tiny")
+    w0, fg = oracle_inputs(g)
+    cfg = sim_config(g)
+    caps, tau, T = g["sim_capacities"], g["tau"], 12
+    ws = [w0] + [O.generate_trace(w0.L, w0.N, w0.K, w0.D, T, 0.6, 0.18, 99, 6000 + b, False,
+                                  [2.0, 1.2, 0.7, 0.35], [1.8, 1.2, 0.8, 0.45]) for b in range(1, batch)]
+    if batch == 1:
+        acts, scores, shape = w0.acts[:T], w0.scores[:T], (T, w0.L, w0.D)
+    else:
+        acts = np.ascontiguousarray(np.stack([w.acts[:T] for w in ws], axis=1))
+        scores = np.ascontiguousarray(np.stack([w.scores[:T] for w in ws], axis=1))
+        shape = (T, batch, w0.L, w0.D)
+    ffn = 1024  # (ffn / tiles) % 64 == 0 for the grouped path
+    outs, results = [], []
+    for rank, world in [(0, 1), (0, 2), (1, 2)]:
+        with P.Engine(P.ModelSpec(w0.L, w0.N, w0.K, w0.D)) as eng:
+            eng.load_gates(w0.gates, fg)
+            eng.experts_init(ffn, cfg.tile_count_per_expert, seed=5)
+            eng.decode_begin(caps, w0.fisher, tau, cfg, 0, T, batch=batch, ep_rank=rank, ep_world=world)
+            h = np.zeros(shape, dtype=np.float32)
+            eng.decode_tokens(acts, scores, h)
+            results.append(eng.decode_end(cfg, T))
+            outs.append(h)
+    for r in results[1:]:
+        assert r.metrics == results[0].metrics
+        assert np.array_equal(r.timeline, results[0].timeline)
+    if batch == 1:
+        ref = O.simulate(w0, caps, tau, first_gate=fg, T=T, **sim_kwargs(g))
+        assert results[0].metrics == ref.metrics
+    full = outs[0].astype(np.float64)
+    sharded = outs[1].astype(np.float64) + outs[2].astype(np.float64)
+    x = (acts.astype(np.float32).astype(np.float64))
+    moe = full - x
+    assert np.abs(sharded - full).max() <= 1e-5 * np.abs(moe).max()
+    # each shard only moved / computed its own experts
+    b0, b1 = results[1].stats["ffn_bytes"], results[2].stats["ffn_bytes"]
+    assert b0 + b1 == results[0].stats["ffn_bytes"]

@@ -40,7 +40,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="mixtral-8x7b", choices=["mixtral-8x7b", "tiny"])
+    ap.add_argument("--config", default="mixtral-8x7b", choices=["mixtral-8x7b", "mixtral-8x22b", "tiny"])
+    ap.add_argument("--ep", action="store_true",
+                    help="expert-parallel over the torchrun ranks (BASELINE config 5): rank r owns experts e % N == r, "
+                         "the ranks decode ONE token stream and combine partial layer outputs (all_gather, fixed order)")
     ap.add_argument("--budget", type=int, default=None)
     ap.add_argument("--batch", type=int, default=1,
                     help="decode streams sharing the cache (BASELINE config 4: 16 / 64; grouped tcgen05 FFN)")
@@ -59,6 +62,8 @@ def workload(args):
     from paper_2408_10284_b200 import workloads as W
     if args.config == "tiny":
         wl = W.tiny(tokens=max(args.trace_tokens, args.warmup + 2 * args.steps))
+    elif args.config == "mixtral-8x22b":
+        wl = W.mixtral_8x22b(tokens=max(args.trace_tokens, args.warmup + 2 * args.steps))
     else:
         wl = W.mixtral_8x7b(tokens=max(args.trace_tokens, args.warmup + 2 * args.steps))
     if args.budget is not None:
@@ -190,6 +195,7 @@ def ours(args):
     import torch
 
     import paper_2408_10284_b200 as P
+    from paper_2408_10284_b200 import ep as EP
 
     ws, rank, local = dist_init()
     torch.cuda.set_device(local)
@@ -199,8 +205,11 @@ def ours(args):
                       P.PolicyFlags(wl.gating, wl.prefetch, True))
     t_setup = time.time()
     eng = P.Engine(spec, local)
+    ep_world = ws if args.ep else 1
+    ep_rank = rank if args.ep else 0
+    seed_off = 0 if args.ep else rank  # replicas decode different streams; EP shards share one
     trace = eng.generate_trace(P.SynthConfig(spec, wl.tokens, wl.concentration, wl.drift, wl.gate_seed,
-                                             wl.token_seed + rank, False, wl.fisher_scales, wl.drift_scales))
+                                             wl.token_seed + seed_off, False, wl.fisher_scales, wl.drift_scales))
     tau, realized = P.calibrate_threshold(spec, trace.scores, trace.fisher, wl.target_single_ratio)
     alpha, beta = eng.generate_profiles(trace.acts, trace.scores, trace.fisher, tau)
     caps, exp_loads = P.dp_allocate(spec, P.build_cost_table(spec, alpha, beta), wl.budget)
@@ -226,7 +235,7 @@ def ours(args):
     if B > 1:
         total_tokens = W + 2 * K
         streams = [trace] + [eng.generate_trace(P.SynthConfig(spec, total_tokens, wl.concentration, wl.drift,
-                                                              wl.gate_seed, wl.token_seed + 1000 * rank + b, False,
+                                                              wl.gate_seed, wl.token_seed + 1000 * seed_off + b, False,
                                                               wl.fisher_scales, wl.drift_scales))
                              for b in range(1, B)]
         acts = np.stack([s.acts[:total_tokens] for s in streams], axis=1)      # [T][B][L][d]
@@ -234,7 +243,8 @@ def ours(args):
         del streams
     else:
         acts, scores = acts[:, None], scores[:, None]
-    eng.decode_begin(caps, trace.fisher, tau, cfg, wl.seed, total_tokens, args.staging, batch=B)
+    eng.decode_begin(caps, trace.fisher, tau, cfg, wl.seed, total_tokens, args.staging, batch=B, ep_rank=ep_rank,
+                     ep_world=ep_world)
     # token inputs: device copies for the value window, pinned host copies for the e2e window
     d_acts = torch.from_numpy(np.ascontiguousarray(acts[: W + K])).cuda()
     d_scores = torch.from_numpy(np.ascontiguousarray(scores[: W + K])).cuda()
@@ -260,7 +270,18 @@ def ours(args):
     barrier(ws)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        gpu_ms = dev_call(W, W + K)
+        if ep_world > 1:
+            # the cross-shard combine (all_gather + fixed-order sum) is part of the step
+            t_ev0, t_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t_ev0.record()
+            dev_call(W, W + K)
+            combined = EP.combine_partials(d_hidden[W: W + K])
+            t_ev1.record()
+            torch.cuda.synchronize()
+            gpu_ms = t_ev0.elapsed_time(t_ev1)
+            del combined
+        else:
+            gpu_ms = dev_call(W, W + K)
         torch.cuda.synchronize()
     barrier(ws)
     s1 = eng.decode_stats()
@@ -273,16 +294,23 @@ def ours(args):
         ah = h_acts[i: i + 1].numpy()
         sh = h_scores[i: i + 1].numpy()
         eng.decode_tokens(ah, sh, h_hidden[i: i + 1].numpy())
+        if ep_world > 1:
+            EP.combine_partials(h_hidden[i: i + 1].cuda(non_blocking=True)).cpu()
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(ws, time.perf_counter() - w0)
     barrier(ws)
     res = eng.decode_end(cfg, total_tokens)
     st_end = res.stats
     resident = None
-    if not args.no_resident_check:
+    hbm_total = torch.cuda.get_device_properties(local).total_memory
+    resident_bytes = (wl.layers * len(EP.owned_experts(wl.experts, ep_world, ep_rank)) + 32) * expert_bytes
+    if not args.no_resident_check and resident_bytes > 0.85 * hbm_total:
+        resident = {"skipped": f"all {wl.layers * wl.experts} experts need {resident_bytes / 1e9:.0f} GB of HBM per GPU"}
+    elif not args.no_resident_check:
         # same inputs, every expert resident: the FFN launches cover whole experts and nothing waits on
         # the host link, which isolates the kernel's streaming rate inside the decode step
-        eng.decode_begin([wl.experts] * wl.layers, trace.fisher, tau, cfg, wl.seed, total_tokens, args.staging, batch=B)
+        eng.decode_begin([wl.experts] * wl.layers, trace.fisher, tau, cfg, wl.seed, total_tokens, args.staging, batch=B,
+                         ep_rank=ep_rank, ep_world=ep_world)
         dev_call(0, W)
         r0 = eng.decode_stats()
         barrier(ws)
@@ -316,11 +344,13 @@ def ours(args):
 
     if rank != 0:
         return
-    value = ws * B * K / (gpu_ms_max * 1e-3)
+    streams = 1 if ep_world > 1 else ws  # EP shards decode one stream together
+    value = streams * B * K / (gpu_ms_max * 1e-3)
     decoded = W + 2 * K
     line = {
         "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": ws, "steps": K, "warmup": W,
-        "ms_per_step": gpu_ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": gpu_ms_max / K, "higher_is_better": True, "scaling": "strong" if ep_world > 1 else "weak",
+        "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic: reference generator (demo8 settings) trace + counter-based random-init "
                                  "bf16 experts",
         "config": {"workload": f"{wl.name} batch-{B} decode, HBM expert cache {wl.budget}/{wl.layers * wl.experts} experts "
@@ -330,7 +360,8 @@ def ours(args):
                    "layers": wl.layers, "experts": wl.experts, "top_k": wl.top_k, "hidden": wl.hidden, "ffn": wl.ffn,
                    "budget": wl.budget, "tiles": wl.tiles, "lookahead": wl.lookahead, "trace_tokens": wl.tokens,
                    "tau": tau, "realized_single_ratio": realized, "capacities": [int(c) for c in caps],
-                   "dp_expected_loads_per_token": exp_loads, "host_alias": alias, "parallelism": f"replicas x{ws}",
+                   "dp_expected_loads_per_token": exp_loads, "host_alias": alias,
+                   "parallelism": f"ep{ws} (expert e on rank e % {ws})" if ep_world > 1 else f"replicas x{ws}",
                    "l2": "no flush needed: resident experts (>=22 GB) >> 126 MB L2"},
         "on_demand_loads_per_token": od_timed / K,
         "experts_activated_per_token": act_timed / K,
@@ -354,7 +385,7 @@ def ours(args):
                    "exact_fallback_items": int(d["router_exact_items"])},
         "gpu_launches": int(d["kernels_launched"]),
         "clocks": clk.summary(),
-        "e2e": {"value": ws * B * K / e2e_s, "unit": "tok/s",
+        "e2e": {"value": streams * B * K / e2e_s, "unit": "tok/s",
                 "h2d_bytes_per_step": int(B * wl.layers * (wl.hidden + wl.experts) * 8),
                 "d2h_bytes_per_step": int(B * wl.layers * wl.hidden * 4)},
         "setup_s": {"total": setup_s, "expert_store": t_store},

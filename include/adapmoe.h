@@ -160,6 +160,24 @@ int moe_simulate_trace(moe_engine_t engine, const double* acts, const double* sc
                        int64_t* on_demand_per_layer, moe_event* events, int64_t events_capacity,
                        int64_t* n_events);
 
+/* compare_policies (inc/simulator.hpp:476-550; CLI `compare`, moesim_main.cpp:356): the Table-2
+ * ablation grid.  For each of the 7 rows (baseline, +gating, +prefetch, +gating+cache,
+ * +prefetch+cache, +gating+prefetch, all): alpha masked to 0 without adaptive gating, beta masked to
+ * 0 without prefetching, DP allocation (adaptive cache) or uniform split of `budget`, then
+ * simulate_trace with the row's flags (K1 on the GPU, tick engine on the host).  rows[7];
+ * capacities [7][L]; latency_per_token [7][T] and on_demand_per_layer [7][L] may be NULL. */
+typedef struct {
+    char name[24];
+    int32_t adaptive_gating, prefetch, adaptive_cache;
+    moe_metrics metrics;
+    double speedup_vs_baseline;
+} moe_compare_row;
+
+int moe_compare_policies(moe_engine_t engine, const double* acts, const double* scores, int32_t tokens,
+                         const double* fisher, const double* alpha, const double* beta, double tau,
+                         const moe_sim_config* cfg, int32_t budget, uint64_t seed, moe_compare_row* rows,
+                         int32_t* capacities, int64_t* latency_per_token, int64_t* on_demand_per_layer);
+
 /* generate_trace (inc/workload.hpp:60-112): host mt19937_64 stream (bit-identical draws), gate
  * logits on the GPU via K1 (fp64, reference summation order).  Outputs: gates [L][d][N], acts
  * [T][L][d], scores [T][L][N], selected [T][L][K], fisher [L]. Also loads the gates into the engine. */
@@ -171,6 +189,16 @@ int moe_generate_trace(moe_engine_t engine, const moe_synth_config* cfg, double*
  * engine's gates and first-layer gate. */
 int moe_generate_profiles(moe_engine_t engine, const double* acts, const double* scores, int32_t tokens,
                           const double* fisher, double tau, double* alpha, double* beta);
+
+/* first_layer_training_pairs + train_predictive_gate (inc/workload.hpp:186-197,
+ * inc/prefetch.hpp:194-213; CLI `profile --train-gate`, moesim_main.cpp:196): full-batch KL gradient
+ * descent of the first-layer predictive gate from (token t-1 last-layer activation, token t first-layer
+ * log-scores) pairs.  Logits on the GPU (K1 exact fp64 path), softmax with the host libm exp, gradient
+ * and update on the GPU in the reference's summation order: bit-exact with the reference.
+ * acts [T][L][d], scores [T][L][N]; T >= 2.  first_gate_out [d][N] row-major (load it with
+ * moe_load_gates). */
+int moe_train_first_gate(moe_engine_t engine, const double* acts, const double* scores, int32_t tokens,
+                         double learning_rate, int32_t steps, uint64_t seed, double* first_gate_out);
 
 /* ---- physical offloaded decode (expert FFN + HBM expert cache + copy engine) -------------- */
 /* Expert FFN shape: SwiGLU with ffn_dim F, bf16 weights, F % tiles == 0, tiles = the

@@ -215,6 +215,35 @@ int main(int argc, char** argv) {
         return 0;
     }
 
+    // the Table-2 ablation grid (inc/simulator.hpp:476-550; CLI `compare`, moesim_main.cpp:356-378:
+    // the raw --budget is passed through)
+    if (mode == "compare") {
+        const int jobs = static_cast<int>(argi("jobs", 1));
+        ComparisonReport rep = compare_policies(in, sim, budget, sim_seed, jobs);
+        std::string r = "{\"rows\": [";
+        for (size_t i = 0; i < rep.rows.size(); ++i) {
+            const ComparisonRow& row = rep.rows[i];
+            const SimMetrics& m = row.metrics;
+            if (i) r += ",\n";
+            r += "{\"name\": \"" + row.name + "\", \"flags\": [" + std::to_string(row.flags.adaptive_gating) + "," +
+                 std::to_string(row.flags.prefetch) + "," + std::to_string(row.flags.adaptive_cache) +
+                 "], \"capacities\": " + Out::arr(row.allocation.capacities) +
+                 ", \"speedup_vs_baseline\": " + Out::d(row.speedup_vs_baseline) +
+                 ", \"metrics\": {\"total_latency\": " + std::to_string(m.total_latency) +
+                 ", \"stall_time\": " + std::to_string(m.stall_time) +
+                 ", \"on_demand_loads\": " + std::to_string(m.on_demand_loads) +
+                 ", \"cache_hits\": " + std::to_string(m.cache_hits) +
+                 ", \"prefetch_hits\": " + std::to_string(m.prefetch_hits) +
+                 ", \"single_expert_decisions\": " + std::to_string(m.single_expert_decisions) +
+                 ", \"experts_activated_total\": " + std::to_string(m.experts_activated_total) +
+                 ", \"latency_per_token\": " + Out::arr(m.latency_per_token) +
+                 ", \"on_demand_loads_per_layer\": " + Out::arr(m.on_demand_loads_per_layer) + "}}";
+        }
+        r += "], \"tau\": " + Out::d(tau.tau) + "}\n";
+        std::fputs(r.c_str(), stdout);
+        return 0;
+    }
+
     SimResult res = simulate_trace(in, sim, sim_seed);
 
     const int L = cfg.spec.num_layers, N = cfg.spec.experts_per_layer, T = cfg.tokens, D = cfg.spec.hidden_dim;

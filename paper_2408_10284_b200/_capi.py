@@ -51,6 +51,11 @@ class SynthConfigC(C.Structure):
                 ("drift_scales", C.POINTER(C.c_double))]
 
 
+class CompareRowC(C.Structure):
+    _fields_ = [("name", C.c_char * 24), ("adaptive_gating", C.c_int32), ("prefetch", C.c_int32),
+                ("adaptive_cache", C.c_int32), ("metrics", MetricsC), ("speedup_vs_baseline", C.c_double)]
+
+
 class DecodeOptsC(C.Structure):
     _fields_ = [("batch", C.c_int32), ("ep_rank", C.c_int32), ("ep_world", C.c_int32)]
 
@@ -96,6 +101,9 @@ SIGNATURES = {
     "moe_experts_init": (C.c_int, [_eng, C.c_int32, C.c_int32, C.c_uint64, C.c_int32]),
     "moe_expert_bytes": (C.c_int, [_eng, _i64]),
     "moe_expert_read": (C.c_int, [_eng, C.c_int32, C.c_int32, _u16]),
+    "moe_compare_policies": (C.c_int, [_eng, _d, _d, C.c_int32, _d, _d, _d, C.c_double, _cfg, C.c_int32, C.c_uint64,
+                                       C.POINTER(CompareRowC), _i32, _i64, _i64]),
+    "moe_train_first_gate": (C.c_int, [_eng, _d, _d, C.c_int32, C.c_double, C.c_int32, C.c_uint64, _d]),
     "moe_decode_begin": (C.c_int, [_eng, _i32, C.c_int32, _d, C.c_double, _cfg, C.c_uint64, C.c_int32]),
     "moe_decode_begin_ex": (C.c_int, [_eng, _i32, C.c_int32, _d, C.c_double, _cfg, C.c_uint64, C.c_int32,
                                       C.POINTER(DecodeOptsC)]),

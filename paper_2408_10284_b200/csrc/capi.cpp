@@ -5,6 +5,7 @@
 #include <cuda_runtime_api.h>
 
 #include <cstring>
+#include <map>
 #include <new>
 #include <string>
 #include <vector>
@@ -283,6 +284,67 @@ int moe_simulate_trace(moe_engine_t h, const double* acts, const double* scores,
     });
 }
 
+int moe_compare_policies(moe_engine_t h, const double* acts, const double* scores, int32_t T, const double* fisher,
+                         const double* alpha, const double* beta, double tau, const moe_sim_config* cfg, int32_t budget,
+                         uint64_t seed, moe_compare_row* rows, int32_t* capacities, int64_t* lat, int64_t* odl) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        SimConfig base = to_cfg(cfg);
+        require(acts, "acts");
+        require(scores, "scores");
+        require(fisher, "fisher");
+        require(alpha, "alpha");
+        require(beta, "beta");
+        require(rows, "rows");
+        require(capacities, "capacities");
+        if (T < 1) fail(Status::Validation, "trace holds no tokens");
+        GatingThreshold{tau}.validate();
+        const ModelSpec& s = e.spec();
+        const int L = s.num_layers;
+        struct Row {
+            const char* name;
+            bool g, p, c;
+        };
+        // ablation_grid (inc/simulator.hpp:476-486), in the reference's order
+        const Row grid[7] = {{"baseline", false, false, false},     {"+gating", true, false, false},
+                             {"+prefetch", false, true, false},     {"+gating+cache", true, false, true},
+                             {"+prefetch+cache", false, true, true}, {"+gating+prefetch", true, true, false},
+                             {"all", true, true, true}};
+        std::map<int, TraceRoutes> routes;  // K1 once per (gating, prefetch) combination
+        std::vector<double> mean(7);
+        for (int i = 0; i < 7; ++i) {
+            const Row& r = grid[i];
+            std::vector<double> a(alpha, alpha + L), b(beta, beta + L);
+            if (!r.g) std::fill(a.begin(), a.end(), 0.0);
+            if (!r.p) std::fill(b.begin(), b.end(), 0.0);
+            const Allocation alloc = r.c ? dp_allocate(build_cost_table(a, b, s), budget, s).allocation
+                                         : uniform_allocation(budget, s);
+            SimConfig c = base;
+            c.policy.adaptive_gating = r.g;
+            c.policy.prefetch = r.p;
+            c.policy.adaptive_cache = r.c;
+            const int key = (r.g ? 1 : 0) | (r.p ? 2 : 0);
+            if (!routes.count(key))
+                routes[key] = e.route_trace(acts, scores, T, std::span<const double>(fisher, L), tau, c);
+            const TraceRoutes& tr = routes[key];
+            int32_t* caps = capacities + static_cast<size_t>(i) * L;
+            for (int l = 0; l < L; ++l) caps[l] = alloc.capacities[l];
+            moe_compare_row& out = rows[i];
+            std::memset(out.name, 0, sizeof out.name);
+            std::strncpy(out.name, r.name, sizeof out.name - 1);
+            out.adaptive_gating = r.g;
+            out.prefetch = r.p;
+            out.adaptive_cache = r.c;
+            int64_t n_events = 0;
+            replay(s, T, caps, c, seed, tr.selected.data(), tr.single.data(), tr.predictions.data(), &out.metrics,
+                   lat ? lat + static_cast<size_t>(i) * T : nullptr, odl ? odl + static_cast<size_t>(i) * L : nullptr,
+                   nullptr, 0, &n_events);
+            mean[i] = static_cast<double>(out.metrics.total_latency) / static_cast<double>(T);  // SimMetrics::mean_latency
+        }
+        for (int i = 0; i < 7; ++i) rows[i].speedup_vs_baseline = mean[i] > 0.0 ? mean[0] / mean[i] : 1.0;
+    });
+}
+
 int moe_generate_trace(moe_engine_t h, const moe_synth_config* cfg, double* gates, double* acts, double* scores,
                        int32_t* selected, double* fisher) {
     return guarded([&] {
@@ -316,6 +378,17 @@ int moe_generate_profiles(moe_engine_t h, const double* acts, const double* scor
 }
 
 }  // extern "C"
+
+extern "C" int moe_train_first_gate(moe_engine_t h, const double* acts, const double* scores, int32_t T, double lr,
+                                    int32_t steps, uint64_t seed, double* out) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(acts, "acts");
+        require(scores, "scores");
+        require(out, "first_gate_out");
+        e.train_first_gate(acts, scores, T, lr, steps, seed, out);
+    });
+}
 
 // ---- physical decode ------------------------------------------------------------------------
 namespace {

@@ -2,6 +2,8 @@
 // generation, offline alpha/beta profiling).  inc/ = /root/reference/proj/include/moesim.
 #include "engine.hpp"
 
+#include "../kernels/trainer.hpp"
+
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -333,6 +335,73 @@ void Engine::generate_profiles(const double* acts, const double* scores, int T, 
         alpha[l] = static_cast<double>(singles[l]) / static_cast<double>(T);
         beta[l] = counted[l] > 0 ? static_cast<double>(hits[l]) / static_cast<double>(counted[l]) : 0.0;
     }
+}
+
+}  // namespace adapmoe
+
+namespace adapmoe {
+
+void Engine::train_first_gate(const double* acts, const double* scores, int T, double lr, int steps,
+                              std::uint64_t seed, double* w_out) {
+    activate();
+    const int L = spec_.num_layers, N = spec_.experts_per_layer, K = spec_.top_k, D = spec_.hidden_dim;
+    if (T < 2) fail(Status::Usage, "train_predictive_gate: empty training set (needs >= 2 tokens)");
+    const int P = T - 1;
+    // pairs (inc/workload.hpp:186-197): input = token p's last-layer activation, target logits =
+    // log(max(score, 1e-300)) of token p+1's first layer; their softmax p is fixed for all steps
+    std::vector<double> x(static_cast<size_t>(P) * D), target(static_cast<size_t>(P) * N);
+    for (int p = 0; p < P; ++p) {
+        const double* a = acts + (static_cast<size_t>(p) * L + (L - 1)) * D;
+        std::copy(a, a + D, x.begin() + static_cast<size_t>(p) * D);
+        std::vector<double> tl(N);
+        for (int j = 0; j < N; ++j) tl[j] = std::log(std::max(scores[(static_cast<size_t>(p + 1) * L) * N + j], 1e-300));
+        const std::vector<double> ps = softmax(tl);
+        std::copy(ps.begin(), ps.end(), target.begin() + static_cast<size_t>(p) * N);
+    }
+    // initialisation: 0.1 * N(0,1) from SeededRng(seed), row-major (inc/prefetch.hpp:204-205)
+    std::vector<double> w(static_cast<size_t>(D) * N);
+    SeededRng rng(seed);
+    for (double& v : w) v = 0.1 * rng.normal();
+    DeviceBuffer d_x, d_w, d_diff, d_groups, d_logits, d_sel, d_cnt, d_sgl;
+    d_x.reserve(x.size() * sizeof(double));
+    d_w.reserve(w.size() * sizeof(double));
+    d_diff.reserve(target.size() * sizeof(double));
+    d_logits.reserve(target.size() * sizeof(double));
+    d_sel.reserve(static_cast<size_t>(P) * K * sizeof(int));
+    d_cnt.reserve(static_cast<size_t>(P) * sizeof(int));
+    d_sgl.reserve(static_cast<size_t>(P) * sizeof(int));
+    MOE_CUDA(cudaMemcpyAsync(d_x.ptr, x.data(), x.size() * sizeof(double), cudaMemcpyHostToDevice, compute_));
+    MOE_CUDA(cudaMemcpyAsync(d_w.ptr, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice, compute_));
+    std::vector<RouteGroup> groups(P);
+    for (int p = 0; p < P; ++p) {
+        RouteGroup& g = groups[p];
+        g.x = d_x.as<double>() + static_cast<size_t>(p) * D;
+        g.n_items = 1;
+        g.items[0].gate = d_w.as<double>();
+        g.items[0].flags = kRouteExact | kRouteEmitLogits;  // GateMatrix::logits order, fp64
+        g.items[0].out = p;
+    }
+    d_groups.reserve(groups.size() * sizeof(RouteGroup));
+    MOE_CUDA(cudaMemcpyAsync(d_groups.ptr, groups.data(), groups.size() * sizeof(RouteGroup), cudaMemcpyHostToDevice,
+                             compute_));
+    const RouteParams rp{D, N, K, 0.0, 1.0};
+    const RouteOutputs ro{d_sel.as<int>(), d_cnt.as<int>(), d_sgl.as<int>(), nullptr, d_logits.as<double>(), nullptr};
+    std::vector<double> logits(target.size()), diff(target.size());
+    for (int step = 0; step < steps; ++step) {
+        MOE_CUDA(launch_route(d_groups.as<RouteGroup>(), P, 0, rp, ro, compute_));
+        MOE_CUDA(cudaMemcpyAsync(logits.data(), d_logits.ptr, logits.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                 compute_));
+        MOE_CUDA(cudaStreamSynchronize(compute_));
+        // q = softmax(logits) with the host's exp (inc/prefetch.hpp:180), diff = q - p
+        for (int p = 0; p < P; ++p) {
+            const std::vector<double> q = softmax(std::span<const double>(logits.data() + static_cast<size_t>(p) * N, N));
+            for (int j = 0; j < N; ++j) diff[static_cast<size_t>(p) * N + j] = q[j] - target[static_cast<size_t>(p) * N + j];
+        }
+        MOE_CUDA(cudaMemcpyAsync(d_diff.ptr, diff.data(), diff.size() * sizeof(double), cudaMemcpyHostToDevice, compute_));
+        MOE_CUDA(launch_gate_grad_step(d_w.as<double>(), d_x.as<double>(), d_diff.as<double>(), P, D, N, lr, compute_));
+    }
+    MOE_CUDA(cudaMemcpyAsync(w_out, d_w.ptr, w.size() * sizeof(double), cudaMemcpyDeviceToHost, compute_));
+    MOE_CUDA(cudaStreamSynchronize(compute_));
 }
 
 }  // namespace adapmoe

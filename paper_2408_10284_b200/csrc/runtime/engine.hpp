@@ -89,6 +89,12 @@ public:
     void generate_profiles(const double* acts, const double* scores, int tokens, std::span<const double> fisher,
                            double tau, double* alpha, double* beta);
 
+    // first_layer_training_pairs + train_predictive_gate (inc/workload.hpp:186-197,
+    // inc/prefetch.hpp:194-213) with the logits (K1 exact path) and the gradient steps on the GPU;
+    // bit-exact with the reference.  w_out [d][N] row-major.
+    void train_first_gate(const double* acts, const double* scores, int tokens, double lr, int steps,
+                          std::uint64_t seed, double* w_out);
+
     // generic: run K1 on device groups with host-visible outputs
     void run_route(const std::vector<RouteGroup>& groups, int rows, int max_gate_items, const RouteParams& p,
                    TraceRoutes* out, std::vector<double>* scores_out, cudaStream_t stream);

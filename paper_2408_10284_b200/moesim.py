@@ -271,6 +271,37 @@ class Engine:
                                            _p(fisher, _capi._d), float(tau), _p(a, _capi._d), _p(b, _capi._d)))
         return a, b
 
+    def compare_policies(self, acts, scores, fisher, alpha, beta, tau, cfg: SimConfig, budget: int,
+                         seed: int = 0) -> list[dict]:
+        """compare_policies (inc/simulator.hpp:504): the 7-row ablation grid with K1 on the GPU."""
+        acts, scores = _f64(acts), _f64(scores)
+        T, L = acts.shape[0], self.spec.num_layers
+        rows = (_capi.CompareRowC * 7)()
+        caps = np.zeros((7, L), dtype=np.int32)
+        lat = np.zeros((7, T), dtype=np.int64)
+        odl = np.zeros((7, L), dtype=np.int64)
+        check(load().moe_compare_policies(self._h, _p(acts, _capi._d), _p(scores, _capi._d), T, _p(_f64(fisher), _capi._d),
+                                          _p(_f64(alpha), _capi._d), _p(_f64(beta), _capi._d), float(tau),
+                                          C.byref(cfg.c()), int(budget), int(seed), rows, _p(caps, _capi._i32),
+                                          _p(lat, _capi._i64), _p(odl, _capi._i64)))
+        out = []
+        for i, r in enumerate(rows):
+            m = {k: getattr(r.metrics, k) for k, _ in _capi.MetricsC._fields_}
+            m["latency_per_token"] = lat[i].tolist()
+            m["on_demand_loads_per_layer"] = odl[i].tolist()
+            out.append({"name": r.name.decode(), "flags": [r.adaptive_gating, r.prefetch, r.adaptive_cache],
+                        "capacities": caps[i].tolist(), "speedup_vs_baseline": r.speedup_vs_baseline, "metrics": m})
+        return out
+
+    def train_first_gate(self, acts, scores, learning_rate: float = 0.1, steps: int = 500, seed: int = 0) -> np.ndarray:
+        """first_layer_training_pairs + train_predictive_gate (inc/prefetch.hpp:194) on the GPU,
+        bit-exact with the reference; returns the [d][N] first-layer predictive gate."""
+        acts, scores = _f64(acts), _f64(scores)
+        w = np.zeros((self.spec.hidden_dim, self.spec.experts_per_layer))
+        check(load().moe_train_first_gate(self._h, _p(acts, _capi._d), _p(scores, _capi._d), acts.shape[0],
+                                          float(learning_rate), int(steps), int(seed), _p(w, _capi._d)))
+        return w
+
     # -- physical decode -----------------------------------------------------------------------
     def experts_init(self, ffn_dim: int, tiles: int, seed: int = 0, host_alias: int = 0):
         check(load().moe_experts_init(self._h, ffn_dim, tiles, seed, host_alias))

@@ -131,6 +131,56 @@ int moe_replay_policy(const moe_model_spec* spec, int32_t tokens, const int32_t*
                       int64_t* latency_per_token, int64_t* on_demand_per_layer, moe_event* events,
                       int64_t events_capacity, int64_t* n_events);
 
+/* ---- [host] artifact files (inc/io.hpp; CLI file arguments, moesim_main.cpp:91-122) ---------------
+ * The reference's JSON / JSON Lines formats (format_version 1), read without a JSON library and
+ * written byte-for-byte like the reference (sorted keys, shortest round-trip doubles, dump(2)), plus a
+ * binary trace container (magic "MOETRB1") for fast loading of Mixtral-width traces; loaders detect
+ * it by content.  Errors: MOE_E_IO (cannot open / write), MOE_E_FORMAT (parse / schema / version),
+ * MOE_E_VALIDATION (shapes that contradict the model).  Array arguments may be NULL on a first call
+ * to query sizes ("two-call" convention). */
+typedef struct moe_trace_file* moe_trace_t;
+
+/* load_trace (inc/io.hpp:146): JSONL or binary by content */
+int moe_trace_load(const char* path, moe_trace_t* out);
+int moe_trace_info(moe_trace_t trace, moe_model_spec* spec, int32_t* tokens);
+/* acts [T][L][d], scores [T][L][N], selected [T][L][K] (-1 padded); any pointer may be NULL */
+int moe_trace_read(moe_trace_t trace, double* acts, double* scores, int32_t* selected);
+/* validate_trace (inc/core.hpp:249-297): *violations = count; first message copied (truncated) */
+int moe_trace_validate(moe_trace_t trace, int64_t* violations, char* first_message, int64_t message_capacity);
+int moe_trace_free(moe_trace_t trace);
+/* save_trace (inc/io.hpp:127) when binary == 0, else the binary container; selected may be NULL
+ * (then the first K entries are not written: pass the generator's selections) */
+int moe_trace_save(const char* path, const moe_model_spec* spec, int32_t tokens, const double* acts, const double* scores,
+                   const int32_t* selected, int32_t binary);
+
+/* load_gates / save_gates (inc/io.hpp:200-245): gates [L][d][N]; the optional trained first-layer
+ * gate [d][N] with its TrainingConfig (learning_rate, steps, seed). */
+int moe_gates_load(const char* path, moe_model_spec* spec, double* gates, double* first_gate, int32_t* has_first_gate,
+                   double* learning_rate, int32_t* steps, uint64_t* seed);
+int moe_gates_save(const char* path, const moe_model_spec* spec, const double* gates, const double* first_gate,
+                   double learning_rate, int32_t steps, uint64_t seed);
+
+/* load_profiles / save_profiles (inc/io.hpp:249-287): alpha = single_expert_prob, beta =
+ * prefetch_accuracy, fisher = fisher_diag_sum, per layer.  profile_hash (inc/io.hpp:290) = 16 hex
+ * characters + NUL. */
+int moe_profiles_load(const char* path, moe_model_spec* spec, double* alpha, double* beta, double* fisher);
+int moe_profiles_save(const char* path, const moe_model_spec* spec, const double* alpha, const double* beta,
+                      const double* fisher, char* profile_hash_out);
+
+/* load_threshold / save_threshold (inc/io.hpp:294-318) */
+int moe_threshold_load(const char* path, double* tau, double* target_single_ratio, double* realized_single_ratio);
+int moe_threshold_save(const char* path, double tau, double target_single_ratio, double realized_single_ratio);
+
+/* load_allocation / save_allocation (inc/io.hpp:320-350); profile_hash 16 hex + NUL */
+int moe_allocation_load(const char* path, int32_t* budget, int32_t* num_layers, int32_t* capacities, double* total_cost,
+                        char* profile_hash);
+int moe_allocation_save(const char* path, int32_t budget, int32_t num_layers, const int32_t* capacities,
+                        double total_cost, const char* profile_hash);
+
+/* load_cost_table / save_cost_table (inc/io.hpp:352-370): loads [L][N+1] */
+int moe_cost_table_load(const char* path, int32_t* experts_per_layer, int32_t* num_layers, double* loads);
+int moe_cost_table_save(const char* path, int32_t experts_per_layer, int32_t num_layers, const double* loads);
+
 /* ---- device engine ------------------------------------------------------------------------ */
 typedef struct moe_engine* moe_engine_t;
 

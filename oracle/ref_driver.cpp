@@ -31,6 +31,7 @@
 
 #include "moesim/allocator.hpp"
 #include "moesim/cache_model.hpp"
+#include "moesim/io.hpp"
 #include "moesim/core.hpp"
 #include "moesim/gating.hpp"
 #include "moesim/prefetch.hpp"
@@ -212,6 +213,64 @@ int main(int argc, char** argv) {
             "\"allocate_s\": %.6f, \"on_demand_loads\": %lld}\n",
             sub.traces.size(), reps, best, total / reps, secs(t0, t1), secs(t1, t2), secs(t2, t3), secs(t3, t4),
             secs(t4, t5), loads);
+        return 0;
+    }
+
+    // artifact files through the reference's own io (inc/io.hpp): write every kind into dir=...
+    if (mode == "save") {
+        const std::string dir = arg("dir", ".");
+        save_trace(dir + "/trace.jsonl", wl.traces, cfg.spec);
+        GatesFile gf;
+        gf.spec = cfg.spec;
+        gf.gates = wl.gates;
+        gf.first_layer_gate = first_gate;
+        save_gates(dir + "/gates.json", gf);
+        ProfilesFile pf{cfg.spec, profiles};
+        save_profiles(dir + "/profiles.json", pf);
+        save_threshold(dir + "/threshold.json", ThresholdFile{tau.tau, target, 0.25});
+        save_allocation(dir + "/allocation.json", AllocationFile{alloc.allocation, alloc.total_cost, profile_hash(pf)});
+        save_cost_table(dir + "/cost_table.json", table);
+        std::printf("{\"profile_hash\": \"%s\"}\n", profile_hash(pf).c_str());
+        return 0;
+    }
+    // ... and read them back (dir=...), printing FNV-1a hashes of the arrays and the scalars
+    if (mode == "load") {
+        const std::string dir = arg("dir", ".");
+        auto h = [](const void* p, size_t n, std::uint64_t v) { return fnv1a_bytes(p, n, v); };
+        TraceFile tf = load_trace(dir + "/trace.jsonl");
+        std::uint64_t ha = 0xcbf29ce484222325ull, hs = ha, hsel = ha;
+        for (const auto& tr : tf.traces)
+            for (const auto& st : tr.layers) {
+                ha = h(st.activation.data(), st.activation.size() * 8, ha);
+                hs = h(st.gate.scores.data(), st.gate.scores.size() * 8, hs);
+                hsel = h(st.gate.selected.data(), st.gate.selected.size() * 4, hsel);
+            }
+        GatesFile gf = load_gates(dir + "/gates.json");
+        std::uint64_t hg = 0xcbf29ce484222325ull, hfg = hg;
+        for (const auto& g : gf.gates) hg = h(g.weights.data(), g.weights.size() * 8, hg);
+        if (gf.first_layer_gate) hfg = h(gf.first_layer_gate->gate.weights.data(), gf.first_layer_gate->gate.weights.size() * 8, hfg);
+        ProfilesFile pf = load_profiles(dir + "/profiles.json");
+        ThresholdFile th = load_threshold(dir + "/threshold.json");
+        AllocationFile af = load_allocation(dir + "/allocation.json");
+        CostTable ct = load_cost_table(dir + "/cost_table.json");
+        std::uint64_t hc = 0xcbf29ce484222325ull;
+        for (const auto& row : ct.loads) hc = h(row.data(), row.size() * 8, hc);
+        std::vector<double> alpha, beta, fisher;
+        for (const auto& p : pf.profiles) {
+            alpha.push_back(p.single_expert_prob);
+            beta.push_back(p.prefetch_accuracy);
+            fisher.push_back(p.fisher_diag_sum);
+        }
+        std::printf(
+            "{\"tokens\": %zu, \"hash_activations\": \"%016" PRIx64 "\", \"hash_scores\": \"%016" PRIx64
+            "\", \"hash_selected\": \"%016" PRIx64 "\", \"hash_gates\": \"%016" PRIx64 "\", \"hash_first_gate\": \"%016" PRIx64
+            "\", \"first_gate_steps\": %d, \"alpha\": %s, \"beta\": %s, \"fisher\": %s, \"profile_hash\": \"%s\", "
+            "\"tau\": %s, \"capacities\": %s, \"budget\": %d, \"total_cost\": %s, \"alloc_profile_hash\": \"%s\", "
+            "\"hash_cost_table\": \"%016" PRIx64 "\"}\n",
+            tf.traces.size(), ha, hs, hsel, hg, hfg, gf.first_layer_gate ? gf.first_layer_gate->config.steps : -1,
+            Out::arr(alpha).c_str(), Out::arr(beta).c_str(), Out::arr(fisher).c_str(), profile_hash(pf).c_str(),
+            Out::d(th.tau).c_str(), Out::arr(af.allocation.capacities).c_str(), af.allocation.budget,
+            Out::d(af.total_cost).c_str(), af.profile_hash.c_str(), hc);
         return 0;
     }
 

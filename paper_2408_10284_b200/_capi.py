@@ -101,6 +101,22 @@ SIGNATURES = {
     "moe_experts_init": (C.c_int, [_eng, C.c_int32, C.c_int32, C.c_uint64, C.c_int32]),
     "moe_expert_bytes": (C.c_int, [_eng, _i64]),
     "moe_expert_read": (C.c_int, [_eng, C.c_int32, C.c_int32, _u16]),
+    "moe_trace_load": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "moe_trace_info": (C.c_int, [C.c_void_p, C.POINTER(ModelSpecC), _i32]),
+    "moe_trace_read": (C.c_int, [C.c_void_p, _d, _d, _i32]),
+    "moe_trace_validate": (C.c_int, [C.c_void_p, _i64, C.c_char_p, C.c_int64]),
+    "moe_trace_free": (C.c_int, [C.c_void_p]),
+    "moe_trace_save": (C.c_int, [C.c_char_p, C.POINTER(ModelSpecC), C.c_int32, _d, _d, _i32, C.c_int32]),
+    "moe_gates_load": (C.c_int, [C.c_char_p, C.POINTER(ModelSpecC), _d, _d, _i32, _d, _i32, C.POINTER(C.c_uint64)]),
+    "moe_gates_save": (C.c_int, [C.c_char_p, C.POINTER(ModelSpecC), _d, _d, C.c_double, C.c_int32, C.c_uint64]),
+    "moe_profiles_load": (C.c_int, [C.c_char_p, C.POINTER(ModelSpecC), _d, _d, _d]),
+    "moe_profiles_save": (C.c_int, [C.c_char_p, C.POINTER(ModelSpecC), _d, _d, _d, C.c_char_p]),
+    "moe_threshold_load": (C.c_int, [C.c_char_p, _d, _d, _d]),
+    "moe_threshold_save": (C.c_int, [C.c_char_p, C.c_double, C.c_double, C.c_double]),
+    "moe_allocation_load": (C.c_int, [C.c_char_p, _i32, _i32, _i32, _d, C.c_char_p]),
+    "moe_allocation_save": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, _i32, C.c_double, C.c_char_p]),
+    "moe_cost_table_load": (C.c_int, [C.c_char_p, _i32, _i32, _d]),
+    "moe_cost_table_save": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, _d]),
     "moe_compare_policies": (C.c_int, [_eng, _d, _d, C.c_int32, _d, _d, _d, C.c_double, _cfg, C.c_int32, C.c_uint64,
                                        C.POINTER(CompareRowC), _i32, _i64, _i64]),
     "moe_train_first_gate": (C.c_int, [_eng, _d, _d, C.c_int32, C.c_double, C.c_int32, C.c_uint64, _d]),

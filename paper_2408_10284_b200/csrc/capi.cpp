@@ -4,12 +4,15 @@
 
 #include <cuda_runtime_api.h>
 
+#include <algorithm>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <new>
 #include <string>
 #include <vector>
 
+#include "host/files.hpp"
 #include "host/policy.hpp"
 #include "host/policy_engine.hpp"
 #include "runtime/decode.hpp"
@@ -571,6 +574,236 @@ int moe_expert_ffn(moe_engine_t h, int32_t layer, int32_t expert, const double* 
         MOE_CUDA(launch_combine(c, cs));
         MOE_CUDA(cudaMemcpyAsync(y, dout.ptr, D * sizeof(float), cudaMemcpyDeviceToHost, cs));
         MOE_CUDA(cudaStreamSynchronize(cs));
+    });
+}
+
+}  // extern "C"
+
+// ---- artifact files -----------------------------------------------------------------------------
+struct moe_trace_file {
+    adapmoe::TraceData data;
+};
+
+namespace {
+void copy_hash(char* dst, const std::string& h) {
+    if (!dst) return;
+    std::memset(dst, 0, 17);
+    std::strncpy(dst, h.c_str(), 16);
+}
+}  // namespace
+
+extern "C" {
+
+int moe_trace_load(const char* path, moe_trace_t* out) {
+    return guarded([&] {
+        require(path, "path");
+        require(out, "out");
+        auto t = std::make_unique<moe_trace_file>();
+        t->data = load_trace_file(path);
+        *out = t.release();
+    });
+}
+
+int moe_trace_info(moe_trace_t t, moe_model_spec* spec, int32_t* tokens) {
+    return guarded([&] {
+        require(t, "trace");
+        if (spec) *spec = moe_model_spec{t->data.spec.num_layers, t->data.spec.experts_per_layer, t->data.spec.top_k,
+                                         t->data.spec.hidden_dim};
+        if (tokens) *tokens = t->data.tokens;
+    });
+}
+
+int moe_trace_read(moe_trace_t t, double* acts, double* scores, int32_t* selected) {
+    return guarded([&] {
+        require(t, "trace");
+        const TraceData& d = t->data;
+        if (acts) std::memcpy(acts, d.activations.data(), d.activations.size() * sizeof(double));
+        if (scores) std::memcpy(scores, d.scores.data(), d.scores.size() * sizeof(double));
+        if (selected)
+            for (size_t q = 0; q < d.selected.size(); ++q) selected[q] = d.selected[q];
+    });
+}
+
+int moe_trace_validate(moe_trace_t t, int64_t* violations, char* msg, int64_t cap) {
+    return guarded([&] {
+        require(t, "trace");
+        const std::vector<std::string> v = validate_trace(t->data);
+        if (violations) *violations = static_cast<int64_t>(v.size());
+        if (msg && cap > 0) {
+            const std::string first = v.empty() ? std::string() : v.front();
+            const size_t n = std::min<size_t>(first.size(), static_cast<size_t>(cap - 1));
+            std::memcpy(msg, first.data(), n);
+            msg[n] = '\0';
+        }
+    });
+}
+
+int moe_trace_free(moe_trace_t t) {
+    delete t;
+    return MOE_OK;
+}
+
+int moe_trace_save(const char* path, const moe_model_spec* spec, int32_t T, const double* acts, const double* scores,
+                   const int32_t* selected, int32_t binary) {
+    return guarded([&] {
+        require(path, "path");
+        require(acts, "acts");
+        require(scores, "scores");
+        TraceData d;
+        d.spec = to_spec(spec);
+        d.tokens = T;
+        const size_t L = d.spec.num_layers, N = d.spec.experts_per_layer, K = d.spec.top_k, D = d.spec.hidden_dim;
+        d.activations.assign(acts, acts + T * L * D);
+        d.scores.assign(scores, scores + T * L * N);
+        d.selected.assign(T * L * K, -1);
+        d.selected_count.assign(T * L, 0);
+        if (selected)
+            for (size_t tl = 0; tl < T * L; ++tl)
+                for (size_t k = 0; k < K; ++k) {
+                    d.selected[tl * K + k] = selected[tl * K + k];
+                    if (selected[tl * K + k] >= 0) ++d.selected_count[tl];
+                }
+        d.token_index.resize(T);
+        for (int q = 0; q < T; ++q) d.token_index[q] = q;
+        if (binary)
+            save_trace_binary(path, d);
+        else
+            save_trace_jsonl(path, d);
+    });
+}
+
+int moe_gates_load(const char* path, moe_model_spec* spec, double* gates, double* first_gate, int32_t* has_first,
+                   double* lr, int32_t* steps, uint64_t* seed) {
+    return guarded([&] {
+        require(path, "path");
+        const GatesData g = load_gates_file(path);
+        if (spec) *spec = moe_model_spec{g.spec.num_layers, g.spec.experts_per_layer, g.spec.top_k, g.spec.hidden_dim};
+        if (gates) std::memcpy(gates, g.gates.data(), g.gates.size() * sizeof(double));
+        if (has_first) *has_first = g.first_gate ? 1 : 0;
+        if (first_gate && g.first_gate) std::memcpy(first_gate, g.first_gate->data(), g.first_gate->size() * sizeof(double));
+        if (lr) *lr = g.learning_rate;
+        if (steps) *steps = g.steps;
+        if (seed) *seed = g.seed;
+    });
+}
+
+int moe_gates_save(const char* path, const moe_model_spec* spec, const double* gates, const double* first_gate,
+                   double lr, int32_t steps, uint64_t seed) {
+    return guarded([&] {
+        require(path, "path");
+        require(gates, "gates");
+        GatesData g;
+        g.spec = to_spec(spec);
+        const size_t one = static_cast<size_t>(g.spec.hidden_dim) * g.spec.experts_per_layer;
+        g.gates.assign(gates, gates + one * g.spec.num_layers);
+        if (first_gate) g.first_gate = std::vector<double>(first_gate, first_gate + one);
+        g.learning_rate = lr;
+        g.steps = steps;
+        g.seed = seed;
+        save_gates_file(path, g);
+    });
+}
+
+int moe_profiles_load(const char* path, moe_model_spec* spec, double* alpha, double* beta, double* fisher) {
+    return guarded([&] {
+        require(path, "path");
+        const ProfilesData p = load_profiles_file(path);
+        if (spec) *spec = moe_model_spec{p.spec.num_layers, p.spec.experts_per_layer, p.spec.top_k, p.spec.hidden_dim};
+        if (static_cast<int>(p.alpha.size()) != p.spec.num_layers)
+            fail(Status::Validation, std::string(path) + ": profile count does not match num_layers");
+        if (alpha) std::copy(p.alpha.begin(), p.alpha.end(), alpha);
+        if (beta) std::copy(p.beta.begin(), p.beta.end(), beta);
+        if (fisher) std::copy(p.fisher.begin(), p.fisher.end(), fisher);
+    });
+}
+
+int moe_profiles_save(const char* path, const moe_model_spec* spec, const double* alpha, const double* beta,
+                      const double* fisher, char* hash_out) {
+    return guarded([&] {
+        require(alpha, "alpha");
+        require(beta, "beta");
+        require(fisher, "fisher");
+        ProfilesData p;
+        p.spec = to_spec(spec);
+        const int L = p.spec.num_layers;
+        p.alpha.assign(alpha, alpha + L);
+        p.beta.assign(beta, beta + L);
+        p.fisher.assign(fisher, fisher + L);
+        if (path) save_profiles_file(path, p);
+        copy_hash(hash_out, profile_hash(p));
+    });
+}
+
+int moe_threshold_load(const char* path, double* tau, double* target, double* realized) {
+    return guarded([&] {
+        require(path, "path");
+        const ThresholdData t = load_threshold_file(path);
+        if (tau) *tau = t.tau;
+        if (target) *target = t.target_single_ratio;
+        if (realized) *realized = t.realized_single_ratio;
+    });
+}
+
+int moe_threshold_save(const char* path, double tau, double target, double realized) {
+    return guarded([&] {
+        require(path, "path");
+        save_threshold_file(path, ThresholdData{tau, target, realized});
+    });
+}
+
+int moe_allocation_load(const char* path, int32_t* budget, int32_t* n_layers, int32_t* caps, double* total_cost,
+                        char* hash) {
+    return guarded([&] {
+        require(path, "path");
+        const AllocationData a = load_allocation_file(path);
+        if (budget) *budget = a.budget;
+        if (n_layers) *n_layers = static_cast<int32_t>(a.capacities.size());
+        if (caps) std::copy(a.capacities.begin(), a.capacities.end(), caps);
+        if (total_cost) *total_cost = a.total_cost;
+        copy_hash(hash, a.profile_hash);
+    });
+}
+
+int moe_allocation_save(const char* path, int32_t budget, int32_t n_layers, const int32_t* caps, double total_cost,
+                        const char* hash) {
+    return guarded([&] {
+        require(path, "path");
+        require(caps, "capacities");
+        AllocationData a;
+        a.budget = budget;
+        a.capacities.assign(caps, caps + n_layers);
+        a.total_cost = total_cost;
+        a.profile_hash = hash ? hash : "";
+        save_allocation_file(path, a);
+    });
+}
+
+int moe_cost_table_load(const char* path, int32_t* n, int32_t* n_layers, double* loads) {
+    return guarded([&] {
+        require(path, "path");
+        const CostTableData c = load_cost_table_file(path);
+        if (n) *n = c.experts_per_layer;
+        if (n_layers) *n_layers = static_cast<int32_t>(c.loads.size());
+        if (loads) {
+            size_t o = 0;
+            for (const auto& row : c.loads) {
+                if (static_cast<int>(row.size()) != c.experts_per_layer + 1)
+                    fail(Status::Validation, std::string(path) + ": cost table row length != experts_per_layer + 1");
+                for (double v : row) loads[o++] = v;
+            }
+        }
+    });
+}
+
+int moe_cost_table_save(const char* path, int32_t n, int32_t n_layers, const double* loads) {
+    return guarded([&] {
+        require(path, "path");
+        require(loads, "loads");
+        CostTableData c;
+        c.experts_per_layer = n;
+        for (int l = 0; l < n_layers; ++l)
+            c.loads.emplace_back(loads + static_cast<size_t>(l) * (n + 1), loads + static_cast<size_t>(l + 1) * (n + 1));
+        save_cost_table_file(path, c);
     });
 }
 

@@ -339,6 +339,19 @@ def ours(args):
     ffn_bytes = d["ffn_gate_up_bytes"] + d["ffn_down_bytes"]
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    # DRAM traffic per launch from the committed ncu capture of the same kernel, scaled to this run's
+    # mean launch size (traffic / algorithmic bytes is a property of the kernel's access pattern)
+    traffic, traffic_src = None, None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_r1_traffic.json")))
+        keys = ["grouped_kernel<0>", "grouped_kernel<1>"] if B > 1 else ["ffn_rows_kernel"]
+        alg = sum(prof[k]["algorithmic_bytes"] for k in keys)
+        dram = sum((sum(prof[k]["dram_bytes"]) / len(prof[k]["dram_bytes"])) if isinstance(prof[k]["dram_bytes"], list)
+                   else prof[k]["dram_bytes"] for k in keys)
+        traffic = dram / alg * (ffn_bytes / max(1, d["ffn_launches"]))
+        traffic_src = f"profiles/ncu_r1_traffic.json: {', '.join(keys)} DRAM bytes / algorithmic bytes = {dram / alg:.4f}"
+    except Exception:  # noqa: BLE001
+        pass
     achieved = ffn_bytes / (ffn_ms * 1e-3) / 1e9 if ffn_ms > 0 else 0.0
     copy_gbs = d["copy_bytes"] / (d["copy_busy_ms"] * 1e-3) / 1e9 if d["copy_busy_ms"] > 0 else None
 
@@ -369,7 +382,7 @@ def ours(args):
         "roofline": {"bound": "hbm", "kernel": ("K3 grouped tcgen05 SwiGLU (grouped_kernel<0/1>)" if B > 1 else
                                                 "K2 row-owner SwiGLU expert streaming (ffn_rows_kernel)"),
                      "achieved": achieved,
-                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
                      "launches": d["ffn_launches"], "bytes_per_launch": ffn_bytes / max(1, d["ffn_launches"]),
                      "ms_per_launch": ffn_ms / max(1, d["ffn_launches"]),
                      "algorithmic_bytes": "3*d*ffn/tiles*2 B per (expert, tile) segment: every bf16 weight once",

@@ -151,6 +151,24 @@ def measured_peaks():
         return {}
 
 
+def h2d_peak_gbs(device: int) -> float:
+    """Pinned host -> HBM copy rate of this box's link (256 MiB, best of 5, CUDA events): the
+    roofline of the expert transfers."""
+    import torch
+    n = 256 << 20
+    src = torch.empty(n, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(n, dtype=torch.uint8, device=f"cuda:{device}")
+    best = float("inf")
+    for _ in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b))
+    return n / (best * 1e-3) / 1e9
+
+
 def run_reference_driver(wl, sample_tokens: int, reps: int):
     """The unmodified reference simulate_trace (oracle/_ref/moesim_ref, single thread)."""
     ref = os.path.join(ROOT, "oracle", "_ref", "moesim_ref")
@@ -225,6 +243,7 @@ def ours(args):
         pass
     if args.host_alias is not None:
         alias = args.host_alias
+    link_peak = h2d_peak_gbs(local)
     t0 = time.time()
     eng.experts_init(wl.ffn, wl.tiles, seed=1234, host_alias=alias)
     t_store = time.time() - t0
@@ -390,7 +409,13 @@ def ours(args):
         "host_link": {"copy_bytes": d["copy_bytes"], "copy_busy_ms": d["copy_busy_ms"], "achieved_gbs": copy_gbs,
                       "tile_copies": d["tile_copies"], "stall_ms": d["stall_ms"],
                       "copy_hidden_frac": (1.0 - d["stall_ms"] / d["copy_busy_ms"]) if d["copy_busy_ms"] > 0 else None,
-                      "link_busy_frac": d["copy_busy_ms"] / gpu_ms if gpu_ms > 0 else None},
+                      "link_busy_frac": d["copy_busy_ms"] / gpu_ms if gpu_ms > 0 else None,
+                      "peak_gbs": link_peak, "peak_source": "pinned 256 MiB H2D copy, best of 5, measured in this run",
+                      "frac": (copy_gbs / link_peak) if copy_gbs else None,
+                      # step lower bound if the link were the only cost: bytes moved / link peak
+                      "step_bound_ms": d["copy_bytes"] / (link_peak * 1e9) * 1e3 / K,
+                      "step_frac_of_link_bound": (d["copy_bytes"] / (link_peak * 1e9) * 1e3 / K) / (gpu_ms / K)
+                      if gpu_ms > 0 else None},
         "time_split_ms": {"ffn": ffn_ms, "router": d["router_ms"], "copy_stall": d["stall_ms"], "total": gpu_ms,
                           "host_wait_k1": d["host_sync_ms"], "host_step": d["host_step_ms"]},
         "router": {"launches": K * wl.layers, "groups_per_launch": B,

@@ -201,7 +201,13 @@ int main(int argc, char** argv) {
         return 0;
     }
     int fails = 0;
+    const bool small = argc > 1 && !strcmp(argv[1], "check-small");  // compute-sanitizer target
     fails += check(256, 1024, 4, {5, 17}, {GSeg{0, 0, 4}, GSeg{1, 2, 3}});
+    if (small) {
+        fails += check(512, 2048, 2, {16, 3, 9}, {GSeg{0, 0, 2}, GSeg{1, 0, 2}, GSeg{2, 1, 2}});
+        printf("%s (%d failing checks)\n", fails ? "FAIL" : "PASS", fails);
+        return fails;
+    }
     fails += check(256, 1024, 4, {1, 32}, {GSeg{1, 0, 4}, GSeg{0, 1, 2}, GSeg{0, 3, 4}});
     fails += check(512, 2048, 2, {16, 3, 9}, {GSeg{0, 0, 2}, GSeg{1, 0, 2}, GSeg{2, 1, 2}});
     fails += check(4096, 14336, 4, {7, 30}, {GSeg{0, 0, 4}, GSeg{1, 3, 4}});

@@ -54,9 +54,20 @@ struct RouteParams {
     double concentration = 1.0;
 };
 
-// Launch K1 over `n_groups` groups already resident in device memory.
+// Scratch for the split launch (per-layer decode): per group kMaxRouteItems x kMaxN fp32 logits and
+// magnitude sums, and one ticket per group (zero-initialised once; the kernel re-arms it).
+struct RouteScratch {
+    float* f = nullptr;
+    float* a = nullptr;
+    unsigned* tickets = nullptr;
+    int groups = 0;  // capacity in groups
+};
+
+// Launch K1 over `n_groups` groups already resident in device memory.  max_gate_items = the most
+// gate items (look-ahead / exact-logit items) any group holds.  With `scratch`, groups whose gate
+// columns exceed one round of a CTA's warps are split over several CTAs (lower latency).
 cudaError_t launch_route(const RouteGroup* d_groups, int n_groups, int max_gate_items, const RouteParams& p,
-                         const RouteOutputs& out, cudaStream_t stream);
+                         const RouteOutputs& out, cudaStream_t stream, const RouteScratch* scratch = nullptr);
 
 // fp32 transposed copy [N][d] of a row-major fp64 [d][N] gate (device to device).
 cudaError_t launch_gate_transpose(const double* src, float* dst, int d, int n, int count, cudaStream_t stream);

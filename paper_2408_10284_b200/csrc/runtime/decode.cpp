@@ -89,6 +89,14 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
         cur_sel_.assign(static_cast<size_t>(batch_) * K, -1);
         cur_cnt_.assign(batch_, 0);
     }
+    {
+        const size_t fa = static_cast<size_t>(batch_) * kMaxRouteItems * 64 * sizeof(float);
+        d_route_scratch_.reserve(2 * fa + static_cast<size_t>(batch_) * sizeof(unsigned));
+        MOE_CUDA(cudaMemset(d_route_scratch_.ptr, 0, 2 * fa + static_cast<size_t>(batch_) * sizeof(unsigned)));
+        unsigned char* base = d_route_scratch_.as<unsigned char>();
+        route_scratch_ = RouteScratch{reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + fa),
+                                      reinterpret_cast<unsigned*>(base + 2 * fa), batch_};
+    }
     const int route_rows = 4 * batch_;
     MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_route_), static_cast<size_t>(route_rows) * (K + 3) * sizeof(int),
                            cudaHostAllocMapped));
@@ -580,7 +588,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             const size_t gl = (static_cast<size_t>(i) * L + l) * B;
             cudaEvent_t r0 = take_timing(), r1 = take_timing();
             cudaEventRecord(r0, cs);
-            MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + gl, B, max_gates, rp, ro, cs));
+            MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + gl, B, max_gates, rp, ro, cs, &route_scratch_));
             cudaEventRecord(r1, cs);
             router_events_.emplace_back(r0, r1);
             stats_.kernels += 1;

@@ -141,6 +141,8 @@ private:
 
     // buffers
     DeviceBuffer d_in_acts_, d_in_scores_, d_out_, d_groups_;
+    DeviceBuffer d_route_scratch_;  // K1 split launch: F / A per group + tickets
+    RouteScratch route_scratch_;
     PinnedBuffer h_groups_;
     int* h_route_ = nullptr;  // mapped pinned: selected [4][K], count [4], single [4]
     int* d_route_ = nullptr;

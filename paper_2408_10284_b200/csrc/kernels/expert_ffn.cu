@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_cons
     __shared__ float hs[2][kChunk];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = p.d, Ft = p.ft, vpr = D / 8;  // 16-byte vectors per weight row
-    for (int i = tid; i < D; i += kThreads) xs[i] = static_cast<float>(p.x[i]);
+    ptx::load_x_f32<kThreads>(xs, p.x, D);
     const long long TR = static_cast<long long>(p.n_seg) * Ft;
     const long long r_lo = TR * blockIdx.x / gridDim.x, r_hi = TR * (blockIdx.x + 1) / gridDim.x;
     float acc[DC][8];

@@ -80,4 +80,26 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
     return r;
 }
 
+
+// fp64 [n] (global) -> fp32 [n] (shared) by a whole CTA with all loads of a thread in flight at once
+// (a strided one-element loop costs one HBM round trip per element per thread).
+template <int kThreadsT>
+__device__ __forceinline__ void load_x_f32(float* dst, const double* __restrict__ src, int n) {
+    constexpr int kU = 8;
+    const int tid = threadIdx.x;
+    for (int base = 0; base < n; base += kThreadsT * kU) {
+        double v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = base + u * kThreadsT + tid;
+            v[u] = i < n ? __ldg(src + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = base + u * kThreadsT + tid;
+            if (i < n) dst[i] = static_cast<float>(v[u]);
+        }
+    }
+}
+
 }  // namespace adapmoe::ptx

@@ -22,6 +22,7 @@
 
 #include <cmath>
 
+#include "ptx.cuh"
 #include "router.hpp"
 
 namespace adapmoe {
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(kThreads) route_kernel(const RouteGroup* __res
     bool any_gate = false;
     for (int s = 0; s < g.n_items; ++s) any_gate |= fast_item(g.items[s]);
     if (any_gate) {
-        for (int i = tid; i < D; i += kThreads) x32[i] = static_cast<float>(g.x[i]);
+        ptx::load_x_f32<kThreads>(x32, g.x, D);
         __syncthreads();
         const int pairs = g.n_items * N;
         for (int pr = warp; pr < pairs; pr += kWarps) {
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(kThreads) route_split_kernel(const RouteGroup*
     const int pairs = n_fast * N;  // fast (item, column) pairs, item-major
     const int p0 = c * kPairsPerCta;
     if (p0 < pairs) {
-        for (int i = tid; i < D; i += kThreads) x32[i] = static_cast<float>(g.x[i]);
+        ptx::load_x_f32<kThreads>(x32, g.x, D);
         __syncthreads();
         const int pr = p0 + (warp >> 1), half = warp & 1;
         float acc = 0.0f, asum = 0.0f;

@@ -74,13 +74,13 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     partial_regions_ = (K * store_.tiles + kMaxFfnSegments - 1) / kMaxFfnSegments + K * store_.tiles;
     d_partials_.reserve(static_cast<size_t>(partial_regions_) * kFfnMaxCtas * kFfnSlotsPerCta * D * sizeof(float));
     if (batch_ > 1) {
-        MOE_CUDA(cudaMemset(pool_.ptr, 0, slot_stride_ * n_slots_));  // slot padding read by TMA stays finite
+        MOE_CUDA(cudaMemsetAsync(pool_.ptr, 0, slot_stride_ * n_slots_, eng.compute_stream()));  // slot padding read by TMA stays finite
         np_ = (batch_ + 15) / 16 * 16;
         const int F = store_.ffn;
         d_gx_.reserve(static_cast<size_t>(N) * np_ * D * 2);
         d_gh_.reserve(static_cast<size_t>(N) * np_ * F * 2);
-        MOE_CUDA(cudaMemset(d_gx_.ptr, 0, static_cast<size_t>(N) * np_ * D * 2));
-        MOE_CUDA(cudaMemset(d_gh_.ptr, 0, static_cast<size_t>(N) * np_ * F * 2));
+        MOE_CUDA(cudaMemsetAsync(d_gx_.ptr, 0, static_cast<size_t>(N) * np_ * D * 2, eng.compute_stream()));
+        MOE_CUDA(cudaMemsetAsync(d_gh_.ptr, 0, static_cast<size_t>(N) * np_ * F * 2, eng.compute_stream()));
         const uint64_t pool_rows = slot_stride_ * n_slots_ / row_bytes;
         MOE_CUDA(make_tensor_map_2d(&map_pool_gu_, pool_.ptr, pool_rows, D, 64, 128));
         MOE_CUDA(make_tensor_map_2d(&map_pool_dn_, pool_.ptr, pool_rows, D, 64, 64));
@@ -92,7 +92,8 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     {
         const size_t fa = static_cast<size_t>(batch_) * kMaxRouteItems * 64 * sizeof(float);
         d_route_scratch_.reserve(2 * fa + static_cast<size_t>(batch_) * sizeof(unsigned));
-        MOE_CUDA(cudaMemset(d_route_scratch_.ptr, 0, 2 * fa + static_cast<size_t>(batch_) * sizeof(unsigned)));
+        MOE_CUDA(cudaMemsetAsync(d_route_scratch_.ptr, 0, 2 * fa + static_cast<size_t>(batch_) * sizeof(unsigned),
+                                 eng.compute_stream()));
         unsigned char* base = d_route_scratch_.as<unsigned char>();
         route_scratch_ = RouteScratch{reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + fa),
                                       reinterpret_cast<unsigned*>(base + 2 * fa), batch_};
@@ -204,7 +205,9 @@ void DecodeSession::on_insert(ExpertRef ref, int request, std::optional<int> evi
         if (evicted) fail(Status::Internal, "initial fill evicted an expert");
         if (!owned(ref.expert)) return;
         const int s = take_slot();
-        MOE_CUDA(cudaMemcpy(slot_ptr(s), store_.expert(ref.layer, ref.expert), store_.expert_bytes, cudaMemcpyHostToDevice));
+        // initial residency (pinned source), ordered before any compute-stream use of the slot
+        MOE_CUDA(cudaMemcpyAsync(slot_ptr(s), store_.expert(ref.layer, ref.expert), store_.expert_bytes,
+                                 cudaMemcpyHostToDevice, eng_.compute_stream()));
         slots_[s].fill.reset();
         slots_[s].fill_done = true;
         slot_of_[key] = s;

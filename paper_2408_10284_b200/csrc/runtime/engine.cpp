@@ -65,7 +65,9 @@ void Engine::load_gates(const double* gates, const double* first_gate) {
     activate();
     const size_t one = static_cast<size_t>(spec_.hidden_dim) * spec_.experts_per_layer * sizeof(double);
     d_gates_.reserve(one * spec_.num_layers);
-    MOE_CUDA(cudaMemcpy(d_gates_.ptr, gates, one * spec_.num_layers, cudaMemcpyHostToDevice));
+    // stream-ordered with the transposes below: a plain cudaMemcpy from pageable memory may return
+    // before its DMA lands, and compute_ does not synchronise with the legacy default stream
+    MOE_CUDA(cudaMemcpyAsync(d_gates_.ptr, gates, one * spec_.num_layers, cudaMemcpyHostToDevice, compute_));
     d_gates32_.reserve(one / 2 * spec_.num_layers);
     MOE_CUDA(launch_gate_transpose(d_gates_.as<double>(), d_gates32_.as<float>(), spec_.hidden_dim,
                                    spec_.experts_per_layer, spec_.num_layers, compute_));
@@ -74,7 +76,7 @@ void Engine::load_gates(const double* gates, const double* first_gate) {
     if (first_gate) {
         d_first_gate_.reserve(one);
         d_first_gate32_.reserve(one / 2);
-        MOE_CUDA(cudaMemcpy(d_first_gate_.ptr, first_gate, one, cudaMemcpyHostToDevice));
+        MOE_CUDA(cudaMemcpyAsync(d_first_gate_.ptr, first_gate, one, cudaMemcpyHostToDevice, compute_));
         MOE_CUDA(launch_gate_transpose(d_first_gate_.as<double>(), d_first_gate32_.as<float>(), spec_.hidden_dim,
                                        spec_.experts_per_layer, 1, compute_));
         first_gate_loaded_ = true;

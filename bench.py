@@ -12,7 +12,10 @@ policy step -> tile copies (on-demand/prefetch) -> K2 SwiGLU over the selected e
   value : tok/s with the token inputs already in HBM (CUDA events on the engine's compute stream)
   e2e   : tok/s through the C ABI with host (pinned) input buffers, one call per token, including
           the H2D of the token's inputs and the D2H of its 32 layer outputs, wall clock
-N > 1 GPUs: independent replicas (the batch-1 path has no exchange step; SURVEY §8(e) EP is config 5).
+N > 1 GPUs (torchrun): expert parallelism by default (north star): rank r owns experts
+e % N == r of every layer, holds / copies / computes only those (its own host link moves them), the
+ranks decode ONE token stream and sum their partial layer outputs in rank order after an all_gather
+(NCCL over NVLink) — "scaling": "strong".  --replicas runs independent streams instead ("weak").
 
 `--impl reference` times the reference's own CPU implementation of the path (the unmodified moesim
 simulate_trace compiled into oracle/_ref) on the same workload and prints its line.
@@ -42,8 +45,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mixtral-8x7b", choices=["mixtral-8x7b", "mixtral-8x22b", "tiny"])
     ap.add_argument("--ep", action="store_true",
-                    help="expert-parallel over the torchrun ranks (BASELINE config 5): rank r owns experts e % N == r, "
-                         "the ranks decode ONE token stream and combine partial layer outputs (all_gather, fixed order)")
+                    help="expert-parallel over the torchrun ranks (the default when WORLD_SIZE > 1): rank r owns experts "
+                         "e % G == r, the ranks decode ONE token stream and combine partial layer outputs (all_gather, "
+                         "fixed order)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: run independent replicas (one stream per GPU) instead of expert parallelism")
     ap.add_argument("--budget", type=int, default=None)
     ap.add_argument("--batch", type=int, default=1,
                     help="decode streams sharing the cache (BASELINE config 4: 16 / 64; grouped tcgen05 FFN)")
@@ -71,6 +77,11 @@ def workload(args):
     return wl
 
 
+# NCCL over NVLink on a multi-GPU node; ADAPMOE_DIST_BACKEND=gloo runs the same flow with several
+# ranks sharing one GPU (the single-GPU test box), exchanging through host memory.
+BACKEND = os.environ.get("ADAPMOE_DIST_BACKEND", "nccl")
+
+
 def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -78,8 +89,12 @@ def dist_init():
     if ws > 1:
         import torch
         import torch.distributed as dist
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(BACKEND)
     return ws, rank, local
 
 
@@ -94,7 +109,7 @@ def max_over_ranks(ws, v: float) -> float:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if BACKEND == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -223,9 +238,10 @@ def ours(args):
                       P.PolicyFlags(wl.gating, wl.prefetch, True))
     t_setup = time.time()
     eng = P.Engine(spec, local)
-    ep_world = ws if args.ep else 1
-    ep_rank = rank if args.ep else 0
-    seed_off = 0 if args.ep else rank  # replicas decode different streams; EP shards share one
+    use_ep = (args.ep or ws > 1) and not args.replicas
+    ep_world = ws if use_ep else 1
+    ep_rank = rank if use_ep else 0
+    seed_off = 0 if use_ep else rank  # replicas decode different streams; EP shards share one
     trace = eng.generate_trace(P.SynthConfig(spec, wl.tokens, wl.concentration, wl.drift, wl.gate_seed,
                                              wl.token_seed + seed_off, False, wl.fisher_scales, wl.drift_scales))
     tau, realized = P.calibrate_threshold(spec, trace.scores, trace.fisher, wl.target_single_ratio)
@@ -236,7 +252,8 @@ def ours(args):
     alias = 0
     try:
         avail = int(open("/proc/meminfo").read().split("MemAvailable:")[1].split()[0]) * 1024
-        per_rank = int(0.85 * avail / max(1, int(os.environ.get("LOCAL_WORLD_SIZE", ws))))
+        share = 0.85 if ws == 1 else 0.6  # leave host headroom when several ranks pin memory
+        per_rank = int(share * avail / max(1, int(os.environ.get("LOCAL_WORLD_SIZE", ws))))
         if per_rank < wl.layers * wl.experts * expert_bytes:
             alias = max(1, per_rank // expert_bytes)
     except Exception:  # noqa: BLE001
@@ -443,8 +460,9 @@ def ours(args):
                 if B == 1:
                     line["parity"] = {"reference_on_demand_loads": r["on_demand_loads"],
                                       "ours_on_demand_loads": res.metrics["on_demand_loads"],
-                                      "equal": (r["on_demand_loads"] == res.metrics["on_demand_loads"]
-                                                if rank == 0 and ws == 1 else None)}
+                                      # rank 0 decodes the reference's own stream (token_seed + 0) in
+                                      # every mode, so its logical trace must match the reference's
+                                      "equal": r["on_demand_loads"] == res.metrics["on_demand_loads"]}
                 else:
                     line["cpu_baseline"]["sample"] += ("; the reference is batch-1: it decodes stream 0 only, its "
                                                        "tok/s is per single stream")

@@ -39,12 +39,15 @@ def combine_partials(partial, group=None):
     import torch.distributed as dist
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return partial
-    parts = [torch.empty_like(partial) for _ in range(dist.get_world_size(group))]
-    dist.all_gather(parts, partial.contiguous(), group=group)
+    src = partial
+    if partial.is_cuda and dist.get_backend(group) == "gloo":  # gloo exchanges through host memory
+        src = partial.cpu()
+    parts = [torch.empty_like(src) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, src.contiguous(), group=group)
     out = parts[0].clone()
     for p in parts[1:]:
         out += p
-    return out
+    return out.to(partial.device)
 
 
 class ExpertParallelDecoder:

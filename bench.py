@@ -48,6 +48,9 @@ def parse():
                     help="expert-parallel over the torchrun ranks (the default when WORLD_SIZE > 1): rank r owns experts "
                          "e % G == r, the ranks decode ONE token stream and combine partial layer outputs (all_gather, "
                          "fixed order)")
+    ap.add_argument("--ep-exchange", default="p2p", choices=["p2p", "allgather"],
+                    help="EP combine: device-side stores into peer memory (CUDA IPC, NVLink) from the combine "
+                         "epilogue, or a torch.distributed all_gather after each call")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: run independent replicas (one stream per GPU) instead of expert parallelism")
     ap.add_argument("--budget", type=int, default=None)
@@ -279,8 +282,19 @@ def ours(args):
         del streams
     else:
         acts, scores = acts[:, None], scores[:, None]
-    eng.decode_begin(caps, trace.fisher, tau, cfg, wl.seed, total_tokens, args.staging, batch=B, ep_rank=ep_rank,
-                     ep_world=ep_world)
+    p2p = ep_world > 1 and args.ep_exchange == "p2p"
+
+    def begin(capacities):
+        eng.decode_begin(capacities, trace.fisher, tau, cfg, wl.seed, total_tokens, args.staging, batch=B,
+                         ep_rank=ep_rank, ep_world=ep_world)
+        if p2p:  # swap exchange regions (CUDA IPC handles) and connect: outputs come back already summed
+            import torch.distributed as dist
+            _, handle = eng.decode_ep_export(max(W, K, 1))
+            handles = [None] * ep_world
+            dist.all_gather_object(handles, handle)
+            eng.decode_ep_connect(peer_ptrs=[0] * ep_world, peer_ipc=handles)
+
+    begin(caps)
     # token inputs: device copies for the value window, pinned host copies for the e2e window
     d_acts = torch.from_numpy(np.ascontiguousarray(acts[: W + K])).cuda()
     d_scores = torch.from_numpy(np.ascontiguousarray(scores[: W + K])).cuda()
@@ -306,7 +320,7 @@ def ours(args):
     barrier(ws)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        if ep_world > 1:
+        if ep_world > 1 and not p2p:
             # the cross-shard combine (all_gather + fixed-order sum) is part of the step
             t_ev0, t_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t_ev0.record()
@@ -330,7 +344,7 @@ def ours(args):
         ah = h_acts[i: i + 1].numpy()
         sh = h_scores[i: i + 1].numpy()
         eng.decode_tokens(ah, sh, h_hidden[i: i + 1].numpy())
-        if ep_world > 1:
+        if ep_world > 1 and not p2p:
             EP.combine_partials(h_hidden[i: i + 1].cuda(non_blocking=True)).cpu()
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(ws, time.perf_counter() - w0)
@@ -345,8 +359,7 @@ def ours(args):
     elif not args.no_resident_check:
         # same inputs, every expert resident: the FFN launches cover whole experts and nothing waits on
         # the host link, which isolates the kernel's streaming rate inside the decode step
-        eng.decode_begin([wl.experts] * wl.layers, trace.fisher, tau, cfg, wl.seed, total_tokens, args.staging, batch=B,
-                         ep_rank=ep_rank, ep_world=ep_world)
+        begin([wl.experts] * wl.layers)
         dev_call(0, W)
         r0 = eng.decode_stats()
         barrier(ws)
@@ -410,7 +423,9 @@ def ours(args):
                    "budget": wl.budget, "tiles": wl.tiles, "lookahead": wl.lookahead, "trace_tokens": wl.tokens,
                    "tau": tau, "realized_single_ratio": realized, "capacities": [int(c) for c in caps],
                    "dp_expected_loads_per_token": exp_loads, "host_alias": alias,
-                   "parallelism": f"ep{ws} (expert e on rank e % {ws})" if ep_world > 1 else f"replicas x{ws}",
+                   "parallelism": (f"ep{ws} (expert e on rank e % {ws}; combine: "
+                                   f"{'P2P stores into peer memory from the combine epilogue' if p2p else 'all_gather'})"
+                                   if ep_world > 1 else f"replicas x{ws}"),
                    "l2": "no flush needed: resident experts (>=22 GB) >> 126 MB L2"},
         "on_demand_loads_per_token": od_timed / K,
         "experts_activated_per_token": act_timed / K,

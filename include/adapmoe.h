@@ -299,6 +299,16 @@ int moe_decode_begin_ex(moe_engine_t engine, const int32_t* capacities, int32_t 
                         double tau, const moe_sim_config* cfg, uint64_t seed, int32_t total_tokens,
                         const moe_decode_opts* opts);
 
+/* Expert-parallel exchange over peer memory (NVLink P2P; see kernels/ep_exchange.hpp), replacing a
+ * host-side all_gather of the shards' partial outputs.  After moe_decode_begin_ex with ep_world > 1:
+ * each shard exports its exchange region (device pointer for peers in the same process, 64-byte
+ * CUDA IPC handle for other processes), the shards swap them, and each connects.  From then on the
+ * combine kernels store each layer's partial output straight into every shard's region and
+ * moe_decode_tokens returns the full layer outputs (shard partials summed in shard order, identical
+ * on every shard).  All shards must decode the same calls (same counts, same order), concurrently. */
+int moe_decode_ep_export(moe_engine_t engine, int32_t max_tokens_per_call, uint64_t* region_ptr, uint8_t* ipc_handle);
+int moe_decode_ep_connect(moe_engine_t engine, const uint64_t* peer_ptrs, const uint8_t* peer_ipc_handles);
+
 /* Decode `count` tokens (trace-replay: layer l's router/FFN input is the trace activation).
  * acts [count][L][d] fp64 and scores [count][L][N] fp64 are HOST buffers if inputs_on_device == 0,
  * else device pointers.  hidden_out [count][L][d] fp32 receives x_l + sum_e w_e * E_e(x_l) per

@@ -123,6 +123,8 @@ SIGNATURES = {
     "moe_decode_begin": (C.c_int, [_eng, _i32, C.c_int32, _d, C.c_double, _cfg, C.c_uint64, C.c_int32]),
     "moe_decode_begin_ex": (C.c_int, [_eng, _i32, C.c_int32, _d, C.c_double, _cfg, C.c_uint64, C.c_int32,
                                       C.POINTER(DecodeOptsC)]),
+    "moe_decode_ep_export": (C.c_int, [_eng, C.c_int32, C.POINTER(C.c_uint64), C.c_char_p]),
+    "moe_decode_ep_connect": (C.c_int, [_eng, C.POINTER(C.c_uint64), C.c_char_p]),
     "moe_decode_tokens": (C.c_int, [_eng, _d, _d, C.c_int32, C.c_int32, _f, _d]),
     "moe_decode_end": (C.c_int, [_eng, C.POINTER(MetricsC), _i64, _i64, C.POINTER(EventC), C.c_int64, _i64,
                                  C.POINTER(DecodeStatsC)]),

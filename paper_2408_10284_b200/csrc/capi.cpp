@@ -482,6 +482,22 @@ int moe_decode_begin(moe_engine_t h, const int32_t* caps, int32_t staging, const
     return moe_decode_begin_ex(h, caps, staging, fisher, tau, cfg, seed, total_tokens, nullptr);
 }
 
+int moe_decode_ep_export(moe_engine_t h, int32_t max_tokens, uint64_t* ptr, uint8_t* ipc) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        if (!e.session) fail(Status::Usage, "decode_ep_export: no session (call moe_decode_begin_ex)");
+        e.session->ep_export(max_tokens, ptr, ipc);
+    });
+}
+
+int moe_decode_ep_connect(moe_engine_t h, const uint64_t* ptrs, const uint8_t* ipc) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        if (!e.session) fail(Status::Usage, "decode_ep_connect: no session (call moe_decode_begin_ex)");
+        e.session->ep_connect(ptrs, ipc);
+    });
+}
+
 int moe_decode_tokens(moe_engine_t h, const double* acts, const double* scores, int32_t count, int32_t on_device,
                       float* hidden_out, double* gpu_ms) {
     return guarded([&] {

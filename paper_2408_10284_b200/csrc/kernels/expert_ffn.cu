@@ -220,7 +220,13 @@ __global__ void __launch_bounds__(kCombineCols * kCombineLanes) combine_kernel(c
         }
         __syncthreads();
     }
-    if (q == 0 && live) a.out[j] = acc;
+    if (q == 0 && live) {
+        if (a.n_out_peer > 0) {
+            for (int g = 0; g < a.n_out_peer; ++g) a.out_peer[g][j] = acc;  // P2P stores into each shard's slot
+        } else {
+            a.out[j] = acc;
+        }
+    }
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {

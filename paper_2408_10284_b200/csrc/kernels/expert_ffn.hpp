@@ -18,6 +18,8 @@
 
 #include <cstdint>
 
+#include "ep_exchange.hpp"
+
 namespace adapmoe {
 
 constexpr int kMaxFfnSegments = 32;
@@ -68,6 +70,10 @@ struct CombineArgs {
     int experts[8] = {0};            // selected experts in rank order
     int ranks = 0, d = 0, ft = 0;
     int residual = 1;                // add x (expert-parallel: only the first shard adds it)
+    // expert-parallel P2P exchange: when n_out_peer > 0 the result goes to out_peer[g] (this shard's
+    // slot in every shard's exchange region, same row offset as out) instead of out
+    int n_out_peer = 0;
+    float* out_peer[kMaxEpPeers] = {};
     int n_refs = 0;                  // refs sorted by (rank, tile)
     FfnPartialRef refs[kMaxCombineRefs];
 };

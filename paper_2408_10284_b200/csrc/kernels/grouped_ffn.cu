@@ -336,7 +336,11 @@ __global__ void __launch_bounds__(128) gcombine_kernel(const __grid_constant__ G
         const float w = ranks == 1 ? 1.0f : static_cast<float>(sc[a.pair_expert[pi]] / denom);
         acc = __fmaf_rn(w, y, acc);
     }
-    a.out[b * a.out_stride + j] = acc;
+    if (a.n_out_peer > 0) {
+        for (int g = 0; g < a.n_out_peer; ++g) a.out_peer[g][b * a.out_stride + j] = acc;  // P2P stores
+    } else {
+        a.out[b * a.out_stride + j] = acc;
+    }
 }
 
 int stages_for(int np) {

@@ -29,6 +29,8 @@
 
 #include <cstdint>
 
+#include "ep_exchange.hpp"
+
 namespace adapmoe {
 
 constexpr int kGMaxEntries = 64;   // distinct experts of one layer (N <= 64)
@@ -101,6 +103,8 @@ struct GCombineArgs {
     long long out_stride = 0;
     int d = 0, np_stride = 0, n_streams = 0, top_k = 0;
     int residual = 1;                // add x (expert-parallel: only the first shard adds it)
+    int n_out_peer = 0;              // expert-parallel P2P exchange: write out_peer[g] (same layout as out)
+    float* out_peer[kMaxEpPeers] = {};
     int ref_first[kGMaxEntries + 1]; // entry e's refs: refs[ref_first[e] .. ref_first[e+1])
     GCombineRef refs[256];
     // per (stream, rank): entry index, token column, expert id (-1 = unused rank)

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <chrono>
 #include <numeric>
+#include <thread>
 
 namespace adapmoe {
 
@@ -111,6 +112,7 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
 
 DecodeSession::~DecodeSession() {
     copier_.reset();
+    for (void* p : ep_ipc_opened_) cudaIpcCloseMemHandle(p);
     if (h_route_) cudaFreeHost(h_route_);
     if (route_done_) cudaEventDestroy(route_done_);
     for (auto& p : pass_events_) {
@@ -126,6 +128,72 @@ DecodeSession::~DecodeSession() {
         cudaEventDestroy(p.second);
     }
     for (cudaEvent_t e : timing_pool_) cudaEventDestroy(e);
+}
+
+void DecodeSession::ep_export(int max_tokens_per_call, std::uint64_t* ptr, void* ipc_handle) {
+    eng_.activate();
+    if (ep_world_ < 2) fail(Status::Usage, "ep_export: the session is not expert-parallel (ep_world < 2)");
+    if (ep_world_ > kMaxEpPeers) fail(Status::Usage, "ep_export: at most 8 expert-parallel shards");
+    if (max_tokens_per_call < 1) fail(Status::Usage, "ep_export: max_tokens_per_call must be >= 1");
+    ep_max_tokens_ = max_tokens_per_call;
+    ep_rows_max_ = static_cast<size_t>(max_tokens_per_call) * batch_ * spec_.num_layers;
+    const size_t bytes = kEpFlagBytes + 2 * static_cast<size_t>(ep_world_) * ep_rows_max_ * spec_.hidden_dim * sizeof(float);
+    d_ep_region_.reserve(bytes);
+    MOE_CUDA(cudaMemsetAsync(d_ep_region_.ptr, 0, kEpFlagBytes, eng_.compute_stream()));  // flags + timeout word
+    MOE_CUDA(cudaStreamSynchronize(eng_.compute_stream()));
+    ep_region_[ep_rank_] = d_ep_region_.as<unsigned char>();
+    // Once connected, a shard's reduce kernel waits on its peers; any device-synchronising call
+    // (cudaFree / cudaFreeHost when a buffer grows) inside a later decode call would then wait on it
+    // while the peer's host thread waits likewise.  Size every per-call buffer for the largest call
+    // now, so the exchange never meets an implicit device synchronisation.
+    {
+        const size_t TL = ep_rows_max_, D = spec_.hidden_dim, N = spec_.experts_per_layer;
+        d_in_acts_.reserve(TL * D * sizeof(double));
+        d_in_scores_.reserve(TL * N * sizeof(double));
+        d_out_.reserve(TL * D * sizeof(float));
+        h_groups_.reserve(TL * sizeof(RouteGroup));
+        d_groups_.reserve(TL * sizeof(RouteGroup));
+        if (batch_ > 1) {  // worst-case grouped down-partial arena of one layer
+            const size_t mt = D / 128, T = store_.tiles;
+            d_gpart_.reserve((N * mt * 16 + N * T * mt * 16) * np_ * 128 * sizeof(float));
+        }
+    }
+    if (ptr) *ptr = reinterpret_cast<std::uint64_t>(d_ep_region_.ptr);
+    if (ipc_handle) {
+        cudaIpcMemHandle_t h;
+        MOE_CUDA(cudaIpcGetMemHandle(&h, d_ep_region_.ptr));
+        std::memcpy(ipc_handle, &h, sizeof h);
+    }
+}
+
+void DecodeSession::ep_connect(const std::uint64_t* peer_ptrs, const unsigned char* peer_ipc) {
+    eng_.activate();
+    if (!d_ep_region_.ptr) fail(Status::Usage, "ep_connect: call ep_export first");
+    for (int g = 0; g < ep_world_; ++g) {
+        if (g == ep_rank_) continue;
+        if (peer_ptrs && peer_ptrs[g]) {
+            void* p = reinterpret_cast<void*>(peer_ptrs[g]);
+            cudaPointerAttributes at{};
+            MOE_CUDA(cudaPointerGetAttributes(&at, p));
+            if (at.device != eng_.device()) {  // same process, another GPU: peer access over NVLink
+                const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) MOE_CUDA(e);
+                cudaGetLastError();
+            }
+            ep_region_[g] = static_cast<unsigned char*>(p);
+        } else if (peer_ipc) {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, peer_ipc + static_cast<size_t>(g) * 64, sizeof h);
+            void* p = nullptr;
+            MOE_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            ep_ipc_opened_.push_back(p);
+            ep_region_[g] = static_cast<unsigned char*>(p);
+        } else {
+            fail(Status::Usage, "ep_connect: no pointer or IPC handle for shard " + std::to_string(g));
+        }
+    }
+    ep_connected_ = true;
+    sm_count_ = std::max(1, sm_count_ - 1);  // leave an SM for the exchange's 1-warp wait kernel
 }
 
 cudaEvent_t DecodeSession::take_timing() {
@@ -352,6 +420,10 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
     c.n_refs = static_cast<int>(refs.size());
     for (size_t i = 0; i < refs.size(); ++i) c.refs[i] = std::get<2>(refs[i]);
     for (int r = 0; r < d.count; ++r) c.experts[r] = d.experts[r];
+    if (ep_connected_) {  // store the partial into this shard's slot of every shard's region
+        c.n_out_peer = ep_world_;
+        for (int g = 0; g < ep_world_; ++g) c.out_peer[g] = ep_slot(g, ep_rank_, ep_call_ & 1) + (cur_out_ - cur_out_base_);
+    }
     MOE_CUDA(launch_combine(c, eng_.compute_stream()));
     stats_.kernels += 1;
 }
@@ -459,6 +531,7 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
         need += static_cast<size_t>(p.units) * np_ * 128;
     }
     if (need * sizeof(float) > d_gpart_.bytes) {
+        if (ep_connected_) fail(Status::Internal, "grouped partial arena too small under the EP exchange");
         MOE_CUDA(cudaStreamSynchronize(cs));  // earlier layers may still read the old arena
         d_gpart_.reserve(need * sizeof(float) * 5 / 4);
     }
@@ -503,6 +576,10 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
     c.n_streams = batch_;
     c.top_k = K;
     c.residual = ep_rank_ == 0 ? 1 : 0;
+    if (ep_connected_) {
+        c.n_out_peer = ep_world_;
+        for (int g = 0; g < ep_world_; ++g) c.out_peer[g] = ep_slot(g, ep_rank_, ep_call_ & 1) + (cur_out_ - cur_out_base_);
+    }
     MOE_CUDA(launch_grouped_combine(c, cs));
     stats_.kernels += 1;
 }
@@ -530,6 +607,11 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
     }
     d_out_.reserve(TL * D * sizeof(float));
     float* out_all = (on_device && hidden_out) ? hidden_out : d_out_.as<float>();
+    cur_out_base_ = out_all;
+    if (ep_connected_) {
+        if (count > ep_max_tokens_) fail(Status::Usage, "decode: more tokens per call than ep_export allowed");
+        ++ep_call_;
+    }
 
     // router groups for every (token, layer, stream) of this call: they depend only on positions.
     // Group (i, l, b) writes rows b*4 + item of the layer's launch.
@@ -644,9 +726,43 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             stats_.host_step_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count();
         }
     }
+    if (ep_connected_) {  // publish this call's partials, then sum every shard's slot in shard order
+        EpSignalArgs sa;
+        for (int g = 0; g < ep_world_; ++g) sa.peer_flags[g] = reinterpret_cast<unsigned*>(ep_region_[g]);
+        sa.world = ep_world_;
+        sa.rank = ep_rank_;
+        sa.call = ep_call_;
+        MOE_CUDA(launch_ep_signal(sa, cs));
+        MOE_CUDA(launch_ep_wait(ep_region_[ep_rank_], ep_world_, ep_call_, cs));
+        EpReduceArgs ra;
+        ra.slots = ep_slot(ep_rank_, 0, ep_call_ & 1);
+        ra.slot_stride = static_cast<long long>(ep_rows_max_) * D;
+        ra.out = out_all;
+        ra.elems = static_cast<long long>(TL) * D;
+        ra.world = ep_world_;
+        MOE_CUDA(launch_ep_reduce(ra, cs));
+        stats_.kernels += 2;
+    }
     if (hidden_out && !on_device)
         MOE_CUDA(cudaMemcpyAsync(hidden_out, out_all, TL * D * sizeof(float), cudaMemcpyDeviceToHost, cs));
     MOE_CUDA(cudaEventRecord(t_end, cs));
+    if (ep_connected_) {  // a peer that never signals must not hang the caller forever
+        const auto t0 = std::chrono::steady_clock::now();
+        cudaError_t q;
+        while ((q = cudaEventQuery(t_end)) == cudaErrorNotReady) {
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+                fail(Status::Device, "expert-parallel exchange: no signal from a peer shard within 120 s (all shards "
+                                     "must decode the same calls concurrently)");
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+        MOE_CUDA(q);
+        unsigned timed_out = 0;
+        MOE_CUDA(cudaMemcpy(&timed_out, ep_region_[ep_rank_] + 64 * kMaxEpPeers, sizeof timed_out,
+                            cudaMemcpyDeviceToHost));
+        if (timed_out)
+            fail(Status::Device, "expert-parallel exchange: a peer shard did not publish its partials (all shards "
+                                 "must decode the same calls concurrently)");
+    }
     MOE_CUDA(cudaStreamSynchronize(cs));
     release_pending(true);
     tokens_done_ += count;

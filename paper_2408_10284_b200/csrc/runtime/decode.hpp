@@ -20,6 +20,7 @@
 
 #include <cuda_runtime_api.h>
 
+#include <array>
 #include <memory>
 #include <tuple>
 #include <utility>
@@ -55,6 +56,14 @@ public:
     double decode(const double* acts, const double* scores, int count, bool on_device, float* hidden_out);
 
     const PolicyEngine& policy() const { return *policy_; }
+
+    // expert-parallel exchange over peer memory (kernels/ep_exchange.hpp): allocate this shard's
+    // region for calls of up to max_tokens_per_call tokens; returns its device pointer and (if
+    // ipc_handle) a CUDA IPC handle for other processes.
+    void ep_export(int max_tokens_per_call, std::uint64_t* ptr, void* ipc_handle);
+    // peer_ptrs[g] (same process) or peer_ipc[g] (64-byte IPC handles, other processes) for every
+    // shard g != ep_rank; afterwards decode() returns the full (summed) layer outputs.
+    void ep_connect(const std::uint64_t* peer_ptrs, const unsigned char* peer_ipc);
     DecodeStats snapshot();  // counters so far (call between decode() calls)
     DecodeStats finish();    // drain the copy engine, then snapshot
 
@@ -95,6 +104,17 @@ private:
     // this shard only holds, copies and computes its own experts, and writes its partial layer
     // output (shard 0 adds the residual); the shards' partials are summed in shard order.
     int ep_rank_ = 0, ep_world_ = 1;
+    DeviceBuffer d_ep_region_;
+    size_t ep_rows_max_ = 0;
+    int ep_max_tokens_ = 0;
+    bool ep_connected_ = false;
+    unsigned ep_call_ = 0;
+    std::array<unsigned char*, kMaxEpPeers> ep_region_{};
+    std::vector<void*> ep_ipc_opened_;
+    float* ep_slot(int shard, int writer, int parity) const {
+        return reinterpret_cast<float*>(ep_region_[shard] + kEpFlagBytes) +
+               (static_cast<size_t>(parity) * ep_world_ + writer) * ep_rows_max_ * spec_.hidden_dim;
+    }
     bool owned(int expert) const { return expert % ep_world_ == ep_rank_; }
     int np_ = 16;                       // token rows per expert entry in X / H (B rounded up to 16)
     DeviceBuffer d_gx_, d_gh_, d_gpart_;  // X [N][NP][d], H [N][NP][F] bf16; down partial arena
@@ -138,6 +158,7 @@ private:
     const double* cur_x_ = nullptr;
     const double* cur_scores_ = nullptr;
     float* cur_out_ = nullptr;
+    float* cur_out_base_ = nullptr;  // out buffer of the current decode call (row offsets for the EP slots)
 
     // buffers
     DeviceBuffer d_in_acts_, d_in_scores_, d_out_, d_groups_;

@@ -9,11 +9,13 @@ The reference has no parallelism; this is the B200 extension.  La
     (SURVEY §8(e): global logical per-layer LRU with the DP capacities);
   * dispatch: in trace-replay decode every shard already holds the layer inputs (the reference never
     evolves a hidden state, inc/simulator.hpp:392), so no activations move;
-  * combine: each shard writes its partial layer output  P_r = [r == 0] x + sum_{e owned} w_e E_e(x)
+  * combine: each shard forms its partial layer output  P_r = [r == 0] x + sum_{e owned} w_e E_e(x)
     (combine weights from the full selection); the layer output is
-    P_0 + P_1 + ... + P_{G-1} summed in shard order after one all_gather per decode call — the same
-    bits on every shard and for any collective algorithm.
-`torch.distributed` carries the all_gather (NCCL over NVLink on B200s, gloo in the CPU tests).
+    P_0 + P_1 + ... + P_{G-1} summed in shard order — the same bits on every shard.  Default
+    ("p2p"): the combine kernels store P_r straight into every shard's exchange region over peer
+    memory (CUDA IPC, NVLink), a release flag per call publishes it and each shard reduces the slots
+    on the device (kernels/ep_exchange.hpp); "allgather": one torch.distributed all_gather per call.
+`torch.distributed` swaps the IPC handles / carries the all_gather (NCCL on B200s, gloo in tests).
 """
 from __future__ import annotations
 
@@ -57,10 +59,21 @@ class ExpertParallelDecoder:
     every shard.  acts [n][B][L][d] (or [n][L][d] at batch 1) host numpy arrays."""
 
     def __init__(self, engine, caps, fisher, tau, cfg, seed: int, total_tokens: int, rank: int, world: int,
-                 batch: int = 1, staging_slots: int = 0, group=None):
+                 batch: int = 1, staging_slots: int = 0, group=None, exchange: str = "p2p",
+                 max_tokens_per_call: int = 64):
+        """exchange="p2p": the shards swap exchange regions (CUDA IPC handles) and the combine kernels
+        store partials straight into peer memory (NVLink); "allgather": torch.distributed after each
+        call."""
+        import torch.distributed as dist
         self.engine, self.rank, self.world, self.batch, self.group = engine, rank, world, batch, group
         engine.decode_begin(caps, fisher, tau, cfg, seed, total_tokens, staging_slots, batch=batch, ep_rank=rank,
                             ep_world=world)
+        self.p2p = exchange == "p2p" and world > 1
+        if self.p2p:
+            _, handle = engine.decode_ep_export(max_tokens_per_call)
+            handles = [None] * world
+            dist.all_gather_object(handles, handle, group=group)
+            engine.decode_ep_connect(peer_ptrs=[0] * world, peer_ipc=handles)
 
     def decode(self, acts, scores):
         import torch
@@ -70,6 +83,8 @@ class ExpertParallelDecoder:
             (n, spec.num_layers, spec.hidden_dim)
         part = np.zeros(shape, dtype=np.float32)
         gpu_ms = self.engine.decode_tokens(acts, scores, part)
+        if self.p2p:  # already summed on the device
+            return part, gpu_ms
         t = torch.from_numpy(part)
         if torch.cuda.is_available():
             t = t.cuda()

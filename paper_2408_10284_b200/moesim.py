@@ -328,6 +328,19 @@ class Engine:
                                          total_tokens, C.byref(opts)))
         self._batch = batch
 
+    def decode_ep_export(self, max_tokens_per_call: int) -> tuple[int, bytes]:
+        """Expert-parallel exchange region of this shard: (device pointer, 64-byte CUDA IPC handle)."""
+        ptr = C.c_uint64()
+        h = C.create_string_buffer(64)
+        check(load().moe_decode_ep_export(self._h, int(max_tokens_per_call), C.byref(ptr), h))
+        return ptr.value, h.raw
+
+    def decode_ep_connect(self, peer_ptrs=None, peer_ipc=None):
+        """peer_ptrs[g]: region pointers of same-process shards (0 = use peer_ipc[g], 64 bytes each)."""
+        ptrs = None if peer_ptrs is None else (C.c_uint64 * len(peer_ptrs))(*[int(p) for p in peer_ptrs])
+        ipc = None if peer_ipc is None else b"".join(bytes(b).ljust(64, b"\0")[:64] for b in peer_ipc)
+        check(load().moe_decode_ep_connect(self._h, ptrs, ipc))
+
     def decode_tokens(self, acts, scores, hidden_out=None, on_device: bool = False) -> float:
         """acts [n][L][d], scores [n][L][N] host numpy arrays (or device pointers via on_device)."""
         ms = C.c_double()

@@ -124,3 +124,79 @@ def test_ep_shards_match_single_gpu(batch):
     # each shard only moved / computed its own experts
     b0, b1 = results[1].stats["ffn_bytes"], results[2].stats["ffn_bytes"]
     assert b0 + b1 == results[0].stats["ffn_bytes"]
+
+
+def _p2p_inputs(batch):
+    g = load_golden("tiny")
+    w0, fg = oracle_inputs(g)
+    T = 12
+    ws = [w0] + [O.generate_trace(w0.L, w0.N, w0.K, w0.D, T, 0.6, 0.18, 99, 6000 + b, False,
+                                  [2.0, 1.2, 0.7, 0.35], [1.8, 1.2, 0.8, 0.45]) for b in range(1, batch)]
+    if batch == 1:
+        acts, scores, shape = w0.acts[:T], w0.scores[:T], (T, w0.L, w0.D)
+    else:
+        acts = np.ascontiguousarray(np.stack([w.acts[:T] for w in ws], axis=1))
+        scores = np.ascontiguousarray(np.stack([w.scores[:T] for w in ws], axis=1))
+        shape = (T, batch, w0.L, w0.D)
+    return g, w0, fg, acts, scores, shape, T
+
+
+_P2P_CALLS = [0, 5, 6, 12]
+
+
+def _p2p_decode(rank, world, batch, connect_fn=None):
+    import paper_2408_10284_b200 as P
+    g, w0, fg, acts, scores, shape, T = _p2p_inputs(batch)
+    cfg = sim_config(g)
+    eng = P.Engine(P.ModelSpec(w0.L, w0.N, w0.K, w0.D))
+    eng.load_gates(w0.gates, fg)
+    eng.experts_init(1024, cfg.tile_count_per_expert, seed=5)
+    eng.decode_begin(g["sim_capacities"], w0.fisher, g["tau"], cfg, 0, T, batch=batch, ep_rank=rank,
+                     ep_world=world)
+    if connect_fn:
+        connect_fn(eng)
+    out = np.zeros(shape, dtype=np.float32)
+    for a, b in zip(_P2P_CALLS, _P2P_CALLS[1:]):
+        eng.decode_tokens(acts[a:b], scores[a:b], out[a:b])
+    res = eng.decode_end(cfg, T)
+    eng.close()
+    return out, res
+
+
+def _p2p_worker(rank, world, port, batch, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def connect(eng):
+            ptr, handle = eng.decode_ep_export(max(b - a for a, b in zip(_P2P_CALLS, _P2P_CALLS[1:])))
+            handles = [None] * world
+            dist.all_gather_object(handles, handle)
+            eng.decode_ep_connect(peer_ptrs=[0] * world, peer_ipc=handles)  # other processes: IPC handles
+
+        out, res = _p2p_decode(rank, world, batch, connect)
+        np.save(os.path.join(out_dir, f"p2p_{rank}.npy"), out)
+        np.save(os.path.join(out_dir, f"p2p_metrics_{rank}.npy"), np.array(list(res.metrics.values())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("batch", [1, 4])
+def test_ep_p2p_exchange_two_processes(batch, tmp_path):
+    """The device-side exchange through CUDA IPC: two shard processes (sharing this GPU; on a node
+    each would own a GPU and the stores would cross NVLink) store their partials into each other's
+    exchange regions from the combine epilogue, signal with system-scope release flags and reduce in
+    shard order.  Both return identical full outputs equal to the single-GPU decode, over several
+    calls (slots double-buffered by call parity)."""
+    import torch.multiprocessing as mp
+    full, ref = _p2p_decode(0, 1, batch)
+    mp.spawn(_p2p_worker, args=(2, _free_port(), batch, str(tmp_path)), nprocs=2, join=True)
+    o0, o1 = np.load(tmp_path / "p2p_0.npy"), np.load(tmp_path / "p2p_1.npy")
+    assert np.array_equal(o0, o1)  # same bits on every shard
+    for r in range(2):
+        assert np.load(tmp_path / f"p2p_metrics_{r}.npy").tolist() == list(ref.metrics.values())
+    _, _, _, acts, _, _, _ = _p2p_inputs(batch)
+    moe = full.astype(np.float64) - acts.astype(np.float32).astype(np.float64)
+    assert np.abs(o0.astype(np.float64) - full).max() <= 1e-5 * np.abs(moe).max()

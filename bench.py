@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--ep-exchange", default="p2p", choices=["p2p", "allgather"],
                     help="EP combine: device-side stores into peer memory (CUDA IPC, NVLink) from the combine "
                          "epilogue, or a torch.distributed all_gather after each call")
+    ap.add_argument("--free-running", action="store_true",
+                    help="decode with the hidden state flowing through the experts (layer l > 0 routes on layer "
+                         "l-1's output; decisions from the gates) instead of replaying the trace")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: run independent replicas (one stream per GPU) instead of expert parallelism")
     ap.add_argument("--budget", type=int, default=None)
@@ -286,7 +289,8 @@ def ours(args):
 
     def begin(capacities):
         eng.decode_begin(capacities, trace.fisher, tau, cfg, wl.seed, total_tokens, args.staging, batch=B,
-                         ep_rank=ep_rank, ep_world=ep_world)
+                         ep_rank=ep_rank, ep_world=ep_world, free_running=args.free_running,
+                         concentration=wl.concentration)
         if p2p:  # swap exchange regions (CUDA IPC handles) and connect: outputs come back already summed
             import torch.distributed as dist
             _, handle = eng.decode_ep_export(max(W, K, 1))
@@ -418,7 +422,7 @@ def ours(args):
         "config": {"workload": f"{wl.name} batch-{B} decode, HBM expert cache {wl.budget}/{wl.layers * wl.experts} experts "
                                f"(DP), experts offloaded to pinned host memory" +
                                (f"; {B} token streams share the cache (union policy), grouped tcgen05 FFN" if B > 1 else ""),
-                   "batch": B,
+                   "batch": B, "mode": "free-running" if args.free_running else "trace-replay",
                    "layers": wl.layers, "experts": wl.experts, "top_k": wl.top_k, "hidden": wl.hidden, "ffn": wl.ffn,
                    "budget": wl.budget, "tiles": wl.tiles, "lookahead": wl.lookahead, "trace_tokens": wl.tokens,
                    "tau": tau, "realized_single_ratio": realized, "capacities": [int(c) for c in caps],
@@ -466,7 +470,12 @@ def ours(args):
     if not args.no_cpu_baseline:
         try:
             r = run_reference_driver(wl, decoded, 20)
-            if r is not None:
+            if r is not None and args.free_running:
+                line["cpu_baseline"] = {"value": r["tokens"] / r["simulate_best_s"], "unit": "tok/s", "cores": 1,
+                                        "kind": "reference",
+                                        "sample": f"unmodified moesim simulate_trace over {r['tokens']} replayed tokens "
+                                                  "(the reference has no free-running mode)"}
+            elif r is not None:
                 line["cpu_baseline"] = {"value": r["tokens"] / r["simulate_best_s"], "unit": "tok/s", "cores": 1,
                                         "kind": "reference",
                                         "sample": f"unmodified moesim simulate_trace over the same {r['tokens']} decoded "

@@ -288,11 +288,20 @@ int moe_decode_begin(moe_engine_t engine, const int32_t* capacities, int32_t sta
  *           is replicated (identical trace on every shard); the shard holds, copies and computes only
  *           its own experts and hidden_out receives its partial layer output (shard 0 adds the
  *           residual x).  The layer output is the sum of the shards' partials in shard order
- *           (paper_2408_10284_b200/ep.py does it with torch.distributed).  0 <= ep_rank < ep_world <= N. */
+ *           (paper_2408_10284_b200/ep.py does it with torch.distributed).  0 <= ep_rank < ep_world <= N.
+ *  free_running : SURVEY §7.2's second mode (no reference counterpart: the reference replays stored
+ *           scores, inc/simulator.hpp:392).  Layer l > 0 routes and computes on layer l-1's output,
+ *           so the hidden state flows through the offloaded experts; layer 0 takes the caller's
+ *           activation; the actual decision uses the layer's gate on that hidden state (softmax of
+ *           logits / dirichlet_concentration, like the reference generator, inc/workload.hpp:93-98)
+ *           and the stored scores are ignored.  Given the hidden states the GPU produced, every
+ *           decision and the cache trace equal the reference rule's. */
 typedef struct {
     int32_t batch;
     int32_t ep_rank;
     int32_t ep_world;
+    int32_t free_running;            /* see below; 0 = trace replay (the reference's semantics) */
+    double dirichlet_concentration;  /* free-running: logits / concentration before softmax (SynthConfig) */
 } moe_decode_opts;
 
 int moe_decode_begin_ex(moe_engine_t engine, const int32_t* capacities, int32_t staging_slots, const double* fisher,

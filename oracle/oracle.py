@@ -247,6 +247,20 @@ def simulate_batch(streams: list, caps, tau, fisher=None, first_gate=None, tiles
     return SimOut(metrics, lat, odl, tl[: n.value].copy(), preds, dec)
 
 
+def gate_scores(gate: np.ndarray, x: np.ndarray, concentration: float = 1.0) -> np.ndarray:
+    """softmax(GateMatrix::logits(x) / concentration) exactly as the reference generator forms the
+    stored scores (inc/prefetch.hpp:24-35, inc/workload.hpp:93-98, inc/core.hpp:205-216)."""
+    D, N = gate.shape
+    lg = np.zeros(N)
+    xx = np.ascontiguousarray(x, dtype=np.float64)
+    g = np.ascontiguousarray(gate, dtype=np.float64)
+    lib().orc_gate_logits(_p(g, _d), D, N, _p(xx, _d), _p(lg, _d))
+    lg = np.array([v / concentration for v in lg])
+    out = np.zeros(N)
+    lib().orc_softmax(_p(lg, _d), N, _p(out, _d))
+    return out
+
+
 def expert_init(seed, layer, expert, D, F, tiles) -> np.ndarray:
     out = np.zeros(3 * F * D, dtype=np.uint16)
     rc = lib().orc_expert_init(seed, layer, expert, D, F, tiles, _p(out, _u16))

@@ -470,10 +470,12 @@ int moe_decode_begin_ex(moe_engine_t h, const int32_t* caps, int32_t staging, co
         const int batch = opts ? opts->batch : 1;
         const int ep_rank = opts ? opts->ep_rank : 0;
         const int ep_world = opts ? opts->ep_world : 1;
+        const bool free_running = opts ? opts->free_running != 0 : false;
+        const double conc = (opts && opts->dirichlet_concentration > 0.0) ? opts->dirichlet_concentration : 1.0;
         e.session.reset();
         e.session = std::make_unique<DecodeSession>(e, std::span<const int>(caps, L), staging,
                                                     std::span<const double>(fisher, L), tau, c, seed, total_tokens,
-                                                    batch, ep_rank, ep_world);
+                                                    batch, ep_rank, ep_world, free_running, conc);
     });
 }
 

@@ -287,7 +287,21 @@ __global__ void expert_init_kernel(uint16_t* dst, int D, int F, int tiles, InitA
     }
 }
 
+__global__ void rows_f32_to_f64_kernel(double* dst, long long dst_stride, const float* src, long long src_stride, int d) {
+    const int r = blockIdx.y;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += gridDim.x * blockDim.x)
+        dst[r * dst_stride + j] = static_cast<double>(src[r * src_stride + j]);
+}
+
 }  // namespace
+
+cudaError_t launch_rows_f32_to_f64(double* dst, long long dst_stride, const float* src, long long src_stride, int rows,
+                                   int d, cudaStream_t stream) {
+    if (rows <= 0 || d <= 0) return cudaSuccess;
+    dim3 grid((d + 255) / 256 < 16 ? (d + 255) / 256 : 16, rows);
+    rows_f32_to_f64_kernel<<<grid, 256, 0, stream>>>(dst, dst_stride, src, src_stride, d);
+    return cudaGetLastError();
+}
 
 void ffn_partial_range(FfnPartialRef& f, int ft) {
     const long long TR = static_cast<long long>(f.n_seg) * ft;

@@ -79,6 +79,11 @@ struct CombineArgs {
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream);
 
+// dst[r * dst_stride + j] = (double) src[r * src_stride + j], rows x d (free-running decode: the next
+// layer's fp64 router / FFN input is this layer's fp32 output)
+cudaError_t launch_rows_f32_to_f64(double* dst, long long dst_stride, const float* src, long long src_stride, int rows,
+                                   int d, cudaStream_t stream);
+
 // Deterministic counter-based bf16 init of one expert in the tile-major layout (same values as
 // oracle/moe_oracle.c orc_expert_init): value = bf16_rne(float(sum of 4 x 16-bit lanes of
 // splitmix64(base_m + index) - 131070) * scale_m), index = logical row-major index in W1/W3 [F][D]

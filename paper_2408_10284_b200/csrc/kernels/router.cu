@@ -209,6 +209,16 @@ __device__ bool decide_certified(const RouteItem& it, const float* F32, const fl
         o.single[it.out] = single;
         if (o.perturbation) o.perturbation[it.out] = pert;
     }
+    if (o.scores && (it.flags & kRouteEmitScores)) {
+        // softmax of the (concentration-scaled) fp32 logits: combine weights for the free-running
+        // decode (the decision above is certified; these values are within ~1e-7 of the reference's)
+        const double mx = warp_max(fmax(lane < N ? F0 : -INFINITY, lane + 32 < N ? F1 : -INFINITY));
+        const double e0 = lane < N ? exp(F0 - mx) : 0.0, e1 = lane + 32 < N ? exp(F1 - mx) : 0.0;
+        double sum = 0.0;
+        for (int j = 0; j < N; ++j) sum += col(e0, e1, j);
+        if (lane < N) o.scores[it.out * N + lane] = e0 / sum;
+        if (lane + 32 < N) o.scores[it.out * N + lane + 32] = e1 / sum;
+    }
     return true;
 }
 

@@ -17,8 +17,11 @@ constexpr size_t kSlotAlign = 2u << 20;
 
 DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int staging_slots,
                              std::span<const double> fisher, double tau, const SimConfig& cfg, std::uint64_t seed,
-                             int total_tokens, int batch, int ep_rank, int ep_world)
-    : batch_(batch),
+                             int total_tokens, int batch, int ep_rank, int ep_world, bool free_running,
+                             double concentration)
+    : free_running_(free_running),
+      concentration_(concentration),
+      batch_(batch),
       ep_rank_(ep_rank),
       ep_world_(ep_world),
       eng_(eng),
@@ -38,6 +41,8 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
         fail(Status::Usage, "decode_begin: SimConfig tile count differs from the expert store's tile layout");
     if (total_tokens < 1) fail(Status::Usage, "decode_begin: total_tokens must be >= 1");
     if (K > 8) fail(Status::Usage, "decode: top_k > 8 unsupported by the combine kernel");
+    if (free_running_ && !eng.has_gates()) fail(Status::Usage, "free-running decode needs the gate matrices");
+    if (!(concentration_ > 0.0)) fail(Status::Usage, "decode_begin: dirichlet concentration must be > 0");
     if (batch_ < 1 || batch_ > 256 || batch_ * K > kGMaxPairs)
         fail(Status::Usage, "decode_begin: batch must be in [1, 256] with batch * top_k <= 512");
     const int Ft = store_.ffn / store_.tiles;
@@ -568,7 +573,7 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
     c.acts = cur_x_;
     c.scores = cur_scores_;
     c.stream_stride = static_cast<long long>(L) * D;
-    c.score_stride = static_cast<long long>(L) * N;
+    c.score_stride = cur_score_stride_;
     c.out = cur_out_;
     c.out_stride = static_cast<long long>(L) * D;
     c.d = D;
@@ -608,6 +613,13 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
     d_out_.reserve(TL * D * sizeof(float));
     float* out_all = (on_device && hidden_out) ? hidden_out : d_out_.as<float>();
     cur_out_base_ = out_all;
+    if (free_running_) {
+        // layer l > 0 reads the previous layer's output; layer 0 the caller's input
+        d_x_free_.reserve(TL * D * sizeof(double));
+        d_free_scores_.reserve(static_cast<size_t>(4) * B * N * sizeof(double));
+        MOE_CUDA(cudaMemcpyAsync(d_x_free_.ptr, x_all, TL * D * sizeof(double), cudaMemcpyDeviceToDevice, cs));
+        x_all = d_x_free_.as<double>();
+    }
     if (ep_connected_) {
         if (count > ep_max_tokens_) fail(Status::Usage, "decode: more tokens per call than ep_export allowed");
         ++ep_call_;
@@ -633,6 +645,10 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                 g.items[0].fisher = fisher_[l];
                 g.items[0].flags = adaptive;
                 g.items[0].out = b * 4;
+                if (free_running_) {  // decide from this layer's gate on the evolving hidden state
+                    eng_.gate_item(g.items[0], l);
+                    g.items[0].flags = adaptive | kRouteDivConc | kRouteEmitScores;
+                }
                 if (prefetch_on) {
                     if (l + 1 < L) {
                         for (int dep = 1; dep <= cfg_.lookahead_depth && l + dep < L; ++dep) {
@@ -650,17 +666,17 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                         it.out = b * 4 + 1;
                     }
                 }
-                max_gates = std::max(max_gates, g.n_items - 1);
+                max_gates = std::max(max_gates, free_running_ ? g.n_items : g.n_items - 1);
                 hg[(static_cast<size_t>(i) * L + l) * B + b] = g;  // launch order [i][l][b]
             }
     MOE_CUDA(cudaMemcpyAsync(d_groups_.ptr, hg, TL * sizeof(RouteGroup), cudaMemcpyHostToDevice, cs));
-    RouteParams rp{D, N, K, tau_, 1.0};
+    RouteParams rp{D, N, K, tau_, concentration_};
     const int rows = 4 * B;
     int* d_sel = d_route_;
     int* d_cnt = d_sel + static_cast<size_t>(rows) * K;
     int* d_sgl = d_cnt + rows;
     int* d_exact = d_sgl + rows;
-    RouteOutputs ro{d_sel, d_cnt, d_sgl, nullptr, nullptr, d_exact};
+    RouteOutputs ro{d_sel, d_cnt, d_sgl, nullptr, free_running_ ? d_free_scores_.as<double>() : nullptr, d_exact};
     const int* sel = h_route_;
     const int* cnt = sel + static_cast<size_t>(rows) * K;
     const int* sgl = cnt + rows;
@@ -671,6 +687,12 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
         const int tok = tokens_done_ + i;
         for (int l = 0; l < L; ++l) {
             const size_t gl = (static_cast<size_t>(i) * L + l) * B;
+            if (free_running_ && l > 0) {  // x_l = the previous layer's output, every stream
+                const size_t row_prev = (static_cast<size_t>(i) * B) * L + (l - 1);
+                MOE_CUDA(launch_rows_f32_to_f64(d_x_free_.as<double>() + (row_prev + 1) * D, static_cast<long long>(L) * D,
+                                                out_all + row_prev * D, static_cast<long long>(L) * D, B, D, cs));
+                stats_.kernels += 1;
+            }
             cudaEvent_t r0 = take_timing(), r1 = take_timing();
             cudaEventRecord(r0, cs);
             MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + gl, B, max_gates, rp, ro, cs, &route_scratch_));
@@ -720,7 +742,8 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             d.single = B == 1 && sgl[0] != 0;
             const size_t row0 = (static_cast<size_t>(i) * B) * L + l;  // stream 0's input row
             cur_x_ = x_all + row0 * D;
-            cur_scores_ = s_all + row0 * N;
+            cur_scores_ = free_running_ ? d_free_scores_.as<double>() : s_all + row0 * N;
+            cur_score_stride_ = free_running_ ? 4 * N : static_cast<long long>(L) * N;
             cur_out_ = out_all + row0 * D;
             policy_->step(tok, l, d, std::span<const RoutePrediction>(preds.data(), np), B > 1 ? singles : -1);
             stats_.host_step_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count();

@@ -49,7 +49,7 @@ class DecodeSession : public DecodeListener {
 public:
     DecodeSession(Engine& eng, std::span<const int> capacities, int staging_slots, std::span<const double> fisher,
                   double tau, const SimConfig& cfg, std::uint64_t seed, int total_tokens, int batch = 1,
-                  int ep_rank = 0, int ep_world = 1);
+                  int ep_rank = 0, int ep_world = 1, bool free_running = false, double concentration = 1.0);
     ~DecodeSession() override;
 
     // acts [count][B][L][d], scores [count][B][L][N]: host or device pointers
@@ -96,6 +96,13 @@ private:
     void layer_ffn_single(const RouteDecision& d);   // batch 1: K2 row kernel
     void layer_ffn_grouped(const RouteDecision& d);  // batch > 1: K3 grouped tcgen05 kernels
     void timed_grouped(GroupedLaunch& p, bool down);
+    // free-running decode: layer l > 0 routes and computes on layer l-1's output (the hidden state
+    // flows through the experts); the actual decision comes from the layer's gate (softmax of
+    // logits / concentration, like the reference generator) instead of stored scores
+    bool free_running_ = false;
+    double concentration_ = 1.0;
+    DeviceBuffer d_x_free_, d_free_scores_;
+    long long cur_score_stride_ = 0;
     int l2_mode_ = 0;  // K2 L2 prefetch (ADAPMOE_K2_L2: 0 off, 1 next chunk, 2 whole range); off: both
                        // prefetch modes measured slower on cold launches (tools/k2_cold.cu)
     int batch_ = 1;

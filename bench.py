@@ -379,6 +379,7 @@ def ours(args):
                     "ffn_achieved_gbs": ach, "ffn_frac": ach / measured_peaks().get("hbm_gbs", 6650.0),
                     "ffn_share_of_step": dr["ffn_ms"] / g_ms if g_ms > 0 else None,
                     "ffn_launches": dr["ffn_launches"], "router_us_per_launch": 1e3 * dr["router_ms"] / max(1, K * wl.layers),
+                    "host_wait_k1_ms_per_step": dr["host_sync_ms"] / K, "host_step_ms_per_step": dr["host_step_ms"] / K,
                     "budget": wl.layers * wl.experts}
     # on-demand loads per token in the timed window (tile 0 of each on-demand expert)
     tl = res.timeline

@@ -287,19 +287,28 @@ __global__ void expert_init_kernel(uint16_t* dst, int D, int F, int tiles, InitA
     }
 }
 
-__global__ void rows_f32_to_f64_kernel(double* dst, long long dst_stride, const float* src, long long src_stride, int d) {
-    const int r = blockIdx.y;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += gridDim.x * blockDim.x)
-        dst[r * dst_stride + j] = static_cast<double>(src[r * src_stride + j]);
+__global__ void free_running_input_kernel(double* res, double* norm, long long stride, const float* src,
+                                          long long src_stride, int d, double eps) {
+    const int r = blockIdx.x, lane = threadIdx.x;
+    double* x = res + r * stride;
+    if (src)
+        for (int i = lane; i < d; i += 32) x[i] = static_cast<double>(src[r * src_stride + i]);
+    __syncwarp();
+    double ss = 0.0;
+    for (int i = lane; i < d; i += 32) ss = __dadd_rn(ss, __dmul_rn(x[i], x[i]));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, off));
+    const double rms = __dsqrt_rn(__dadd_rn(__ddiv_rn(ss, static_cast<double>(d)), eps));
+    double* n = norm + r * stride;
+    for (int i = lane; i < d; i += 32) n[i] = __ddiv_rn(x[i], rms);
 }
 
 }  // namespace
 
-cudaError_t launch_rows_f32_to_f64(double* dst, long long dst_stride, const float* src, long long src_stride, int rows,
-                                   int d, cudaStream_t stream) {
+cudaError_t launch_free_running_input(double* res, double* norm, long long stride, const float* src,
+                                      long long src_stride, int rows, int d, double eps, cudaStream_t stream) {
     if (rows <= 0 || d <= 0) return cudaSuccess;
-    dim3 grid((d + 255) / 256 < 16 ? (d + 255) / 256 : 16, rows);
-    rows_f32_to_f64_kernel<<<grid, 256, 0, stream>>>(dst, dst_stride, src, src_stride, d);
+    free_running_input_kernel<<<rows, 32, 0, stream>>>(res, norm, stride, src, src_stride, d, eps);
     return cudaGetLastError();
 }
 

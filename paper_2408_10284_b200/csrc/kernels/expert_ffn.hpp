@@ -79,10 +79,13 @@ struct CombineArgs {
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream);
 
-// dst[r * dst_stride + j] = (double) src[r * src_stride + j], rows x d (free-running decode: the next
-// layer's fp64 router / FFN input is this layer's fp32 output)
-cudaError_t launch_rows_f32_to_f64(double* dst, long long dst_stride, const float* src, long long src_stride, int rows,
-                                   int d, cudaStream_t stream);
+// Free-running decode, per layer and stream row r (stride `stride` doubles between rows):
+//   res[r] = src ? (double) src[r] (previous layer's fp32 output) : res[r] (unchanged, layer 0)
+//   norm[r] = res[r] / sqrt(sum_i res[r][i]^2 / d + eps)     (RMSNorm without gain, Mixtral's
+// pre-MoE norm).  One warp per row: lane j sums res[i]^2 for i = j, j+32, ... in order (separately
+// rounded fp64 ops), then a fixed xor butterfly — reproducible bit for bit on the host.
+cudaError_t launch_free_running_input(double* res, double* norm, long long stride, const float* src,
+                                      long long src_stride, int rows, int d, double eps, cudaStream_t stream);
 
 // Deterministic counter-based bf16 init of one expert in the tile-major layout (same values as
 // oracle/moe_oracle.c orc_expert_init): value = bf16_rne(float(sum of 4 x 16-bit lanes of

@@ -415,7 +415,7 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
         return std::get<0>(a) != std::get<0>(b) ? std::get<0>(a) < std::get<0>(b) : std::get<1>(a) < std::get<1>(b);
     });
     CombineArgs c;
-    c.x = cur_x_;
+    c.x = cur_res_;
     c.scores = cur_scores_;
     c.out = cur_out_;
     c.ranks = d.count;
@@ -570,7 +570,7 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
         }
         c.ref_first[r + 1] = static_cast<int>(q);
     }
-    c.acts = cur_x_;
+    c.acts = cur_res_;
     c.scores = cur_scores_;
     c.stream_stride = static_cast<long long>(L) * D;
     c.score_stride = cur_score_stride_;
@@ -613,12 +613,16 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
     d_out_.reserve(TL * D * sizeof(float));
     float* out_all = (on_device && hidden_out) ? hidden_out : d_out_.as<float>();
     cur_out_base_ = out_all;
+    double* x_norm = nullptr;
     if (free_running_) {
-        // layer l > 0 reads the previous layer's output; layer 0 the caller's input
+        // residual stream: layer 0 = the caller's input, layer l > 0 = layer l-1's output; the router
+        // and the experts read its RMSNorm (Mixtral's pre-MoE norm, without gain)
         d_x_free_.reserve(TL * D * sizeof(double));
+        d_x_norm_.reserve(TL * D * sizeof(double));
         d_free_scores_.reserve(static_cast<size_t>(4) * B * N * sizeof(double));
         MOE_CUDA(cudaMemcpyAsync(d_x_free_.ptr, x_all, TL * D * sizeof(double), cudaMemcpyDeviceToDevice, cs));
         x_all = d_x_free_.as<double>();
+        x_norm = d_x_norm_.as<double>();
     }
     if (ep_connected_) {
         if (count > ep_max_tokens_) fail(Status::Usage, "decode: more tokens per call than ep_export allowed");
@@ -639,7 +643,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                 const size_t row = (static_cast<size_t>(i) * B + b) * L + l;  // input row [i][b][l]
                 const int tok = tokens_done_ + i;
                 RouteGroup g;
-                g.x = x_all + row * D;
+                g.x = (free_running_ ? x_norm : x_all) + row * D;
                 g.n_items = 1;
                 g.items[0].scores = s_all + row * N;
                 g.items[0].fisher = fisher_[l];
@@ -687,10 +691,11 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
         const int tok = tokens_done_ + i;
         for (int l = 0; l < L; ++l) {
             const size_t gl = (static_cast<size_t>(i) * L + l) * B;
-            if (free_running_ && l > 0) {  // x_l = the previous layer's output, every stream
-                const size_t row_prev = (static_cast<size_t>(i) * B) * L + (l - 1);
-                MOE_CUDA(launch_rows_f32_to_f64(d_x_free_.as<double>() + (row_prev + 1) * D, static_cast<long long>(L) * D,
-                                                out_all + row_prev * D, static_cast<long long>(L) * D, B, D, cs));
+            if (free_running_) {  // residual x_l (previous output for l > 0) and its RMSNorm, every stream
+                const size_t row_l = (static_cast<size_t>(i) * B) * L + l;
+                MOE_CUDA(launch_free_running_input(d_x_free_.as<double>() + row_l * D, x_norm + row_l * D,
+                                                   static_cast<long long>(L) * D, l > 0 ? out_all + (row_l - 1) * D : nullptr,
+                                                   static_cast<long long>(L) * D, B, D, kFreeRunningNormEps, cs));
                 stats_.kernels += 1;
             }
             cudaEvent_t r0 = take_timing(), r1 = take_timing();
@@ -741,7 +746,8 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             }
             d.single = B == 1 && sgl[0] != 0;
             const size_t row0 = (static_cast<size_t>(i) * B) * L + l;  // stream 0's input row
-            cur_x_ = x_all + row0 * D;
+            cur_x_ = (free_running_ ? x_norm : x_all) + row0 * D;
+            cur_res_ = x_all + row0 * D;
             cur_scores_ = free_running_ ? d_free_scores_.as<double>() : s_all + row0 * N;
             cur_score_stride_ = free_running_ ? 4 * N : static_cast<long long>(L) * N;
             cur_out_ = out_all + row0 * D;

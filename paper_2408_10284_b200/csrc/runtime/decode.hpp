@@ -101,7 +101,8 @@ private:
     // logits / concentration, like the reference generator) instead of stored scores
     bool free_running_ = false;
     double concentration_ = 1.0;
-    DeviceBuffer d_x_free_, d_free_scores_;
+    DeviceBuffer d_x_free_, d_x_norm_, d_free_scores_;
+    static constexpr double kFreeRunningNormEps = 1e-5;  // Mixtral rms_norm_eps
     long long cur_score_stride_ = 0;
     int l2_mode_ = 0;  // K2 L2 prefetch (ADAPMOE_K2_L2: 0 off, 1 next chunk, 2 whole range); off: both
                        // prefetch modes measured slower on cold launches (tools/k2_cold.cu)
@@ -162,7 +163,8 @@ private:
 
     // per-layer work
     std::vector<Use> uses_;
-    const double* cur_x_ = nullptr;
+    const double* cur_x_ = nullptr;    // router / expert input of the current layer
+    const double* cur_res_ = nullptr;  // residual added by the combine (== cur_x_ in trace replay)
     const double* cur_scores_ = nullptr;
     float* cur_out_ = nullptr;
     float* cur_out_base_ = nullptr;  // out buffer of the current decode call (row offsets for the EP slots)

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Round-1 bench sweep on one B200 (results: gpurun_out/r1_final.jsonl, one JSON line per run).
+out=gpurun_out/r1_final.jsonl
+: > $out
+run() {
+  echo "== bench.py $*" >&2
+  timeout 900 python bench.py "$@" > gpurun_out/_b.json 2> gpurun_out/_b.err
+  rc=$?
+  if [ $rc -eq 0 ]; then tail -n 1 gpurun_out/_b.json >> $out; else echo "rc=$rc"; tail -n 5 gpurun_out/_b.err; fi
+}
+run --impl reference
+run
+run --free-running
+run --batch 16 --steps 4
+run --batch 64 --steps 4
+run --config mixtral-8x22b --steps 4
+wc -l $out

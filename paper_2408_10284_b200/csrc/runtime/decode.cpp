@@ -109,6 +109,21 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
                            cudaHostAllocMapped));
     MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_route_), h_route_, 0));
     MOE_CUDA(cudaEventCreateWithFlags(&route_done_, cudaEventDisableTiming));
+    // per-call buffers sized for the whole announced trace now: growing them inside decode() would put
+    // cudaFree / cudaMallocHost (implicit device synchronisation) inside the timed window
+    {
+        const size_t TL = static_cast<size_t>(total_tokens) * batch_ * L;
+        d_in_acts_.reserve(TL * D * sizeof(double));
+        d_in_scores_.reserve(TL * N * sizeof(double));
+        d_out_.reserve(TL * D * sizeof(float));
+        h_groups_.reserve(TL * sizeof(RouteGroup));
+        d_groups_.reserve(TL * sizeof(RouteGroup));
+        if (free_running_) {
+            d_x_free_.reserve(TL * D * sizeof(double));
+            d_x_norm_.reserve(TL * D * sizeof(double));
+            d_free_scores_.reserve(static_cast<size_t>(4) * batch_ * N * sizeof(double));
+        }
+    }
     copier_ = std::make_unique<CopyEngine>(eng.copy_stream(), eng.device());
     // last: the constructor performs the initial fill through on_insert
     policy_ = std::make_unique<PolicyEngine>(spec_, cfg_, caps_, seed, total_tokens, this, true);

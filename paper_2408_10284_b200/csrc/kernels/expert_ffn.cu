@@ -70,6 +70,7 @@ template <int DC>
 __global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_constant__ FfnLaunch p) {
     extern __shared__ __align__(16) float xs[];  // [d]
     __shared__ float hs[2][kChunk];
+    __shared__ float ha[2][kChunk], hb[2][kChunk];  // per-warp half sums when two warps share a row
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int D = p.d, Ft = p.ft, vpr = D / 8;  // 16-byte vectors per weight row
     ptx::load_x_f32<kThreads>(xs, p.x, D);
@@ -109,17 +110,25 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_cons
             ptx::bulk_prefetch_l2(p.seg[s1].gate_up + static_cast<size_t>(q0) * 2 * D, n1 * 2u * D * 2u);
             ptx::bulk_prefetch_l2(p.seg[s1].down_t + static_cast<size_t>(q0) * D, n1 * static_cast<unsigned>(D) * 2u);
         }
-        // ---- phase 1: h for row r0 + warp ----
-        if (warp < n) {
-            const int4* w1 = reinterpret_cast<const int4*>(p.seg[s].gate_up) + static_cast<size_t>(r0 + warp) * 2 * vpr;
+        // ---- phase 1: h for row r0 + warp (a short chunk spreads each row over wpr = 2/4/8/16
+        // warps, equal slices of d summed in part order — every warp keeps loads in flight) ----
+#ifndef ADAPMOE_K2_MAXWPR
+#define ADAPMOE_K2_MAXWPR 4
+#endif
+        int wpr = n <= 1 ? 16 : n <= 2 ? 8 : n <= 4 ? 4 : n <= 8 ? 2 : 1;
+        if (wpr > ADAPMOE_K2_MAXWPR) wpr = ADAPMOE_K2_MAXWPR;
+        const int row = warp / wpr, part = warp % wpr;
+        if (row < n) {
+            const int4* w1 = reinterpret_cast<const int4*>(p.seg[s].gate_up) + static_cast<size_t>(r0 + row) * 2 * vpr;
             const int4* w3 = w1 + vpr;
+            const int j_lo = part * (vpr / wpr), j_hi = part + 1 == wpr ? vpr : (part + 1) * (vpr / wpr);
             float a = 0.0f, b = 0.0f;
-            for (int j0 = lane; j0 < vpr; j0 += 32 * kUnroll) {
+            for (int j0 = j_lo + lane; j0 < j_hi; j0 += 32 * kUnroll) {
                 int4 q1[kUnroll], q3[kUnroll];
 #pragma unroll
                 for (int k = 0; k < kUnroll; ++k) {
                     const int j = j0 + 32 * k;
-                    if (j < vpr) {
+                    if (j < j_hi) {
                         q1[k] = ptx::ld_stream(w1 + j);
                         q3[k] = ptx::ld_stream(w3 + j);
                     }
@@ -127,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_cons
 #pragma unroll
                 for (int k = 0; k < kUnroll; ++k) {
                     const int j = j0 + 32 * k;
-                    if (j < vpr) {
+                    if (j < j_hi) {
                         const float4 xa = *reinterpret_cast<const float4*>(xs + j * 8);
                         const float4 xb = *reinterpret_cast<const float4*>(xs + j * 8 + 4);
                         a = dot8(q1[k], xa, xb, a);
@@ -140,9 +149,25 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_cons
                 a += __shfl_xor_sync(0xffffffffu, a, o);
                 b += __shfl_xor_sync(0xffffffffu, b, o);
             }
-            if (lane == 0) hs[parity][warp] = silu(a) * b;
+            if (lane == 0) {
+                if (wpr == 1) {
+                    hs[parity][warp] = silu(a) * b;
+                } else {
+                    ha[parity][warp] = a;
+                    hb[parity][warp] = b;
+                }
+            }
         }
         __syncthreads();  // h of this chunk visible; double-buffered hs makes one barrier enough
+        if (wpr > 1 && tid < n) {  // combine the parts (fixed order), one thread per row
+            float a = 0.0f, b = 0.0f;
+            for (int q = 0; q < wpr; ++q) {
+                a += ha[parity][tid * wpr + q];
+                b += hb[parity][tid * wpr + q];
+            }
+            hs[parity][tid] = silu(a) * b;
+        }
+        if (wpr > 1) __syncthreads();
         // ---- phase 2: acc += h_r * W2^T_r over this thread's columns ----
         const int4* down = reinterpret_cast<const int4*>(p.seg[s].down_t) + static_cast<size_t>(r0) * vpr;
 #pragma unroll

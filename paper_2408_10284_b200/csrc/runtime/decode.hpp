@@ -105,6 +105,7 @@ private:
     static constexpr double kFreeRunningNormEps = 1e-5;  // Mixtral rms_norm_eps
     long long cur_score_stride_ = 0;
     int l2_mode_ = 0;
+    bool spin_route_wait_ = true;   // spin on the router event (host reaction latency per layer)
     bool fuse_combine_ = true;      // batch 1: combine fused into the FFN launch when one launch covers the layer
     DeviceBuffer d_barrier_;        // its grid-barrier counter (monotonic)
     unsigned barrier_target_ = 0;  // K2 L2 prefetch (ADAPMOE_K2_L2: 0 off, 1 next chunk, 2 whole range); off: both

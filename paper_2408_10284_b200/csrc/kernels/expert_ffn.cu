@@ -27,10 +27,6 @@ namespace adapmoe {
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kCombineCols = 32, kCombineLanes = 16;
-__device__ void combine_columns(int j0, int d, const double* x, const double* scores, const int* experts, int ranks,
-                                int residual, const FfnPartialRef* refs, int n_refs, float* out, int n_out_peer,
-                                float* const* out_peer);
 constexpr int kWarps = kThreads / 32;
 constexpr int kChunk = kWarps;  // ffn rows per chunk (one per warp in phase 1)
 constexpr int kUnroll = 4;
@@ -201,67 +197,42 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_cons
         c0 += n;
     }
     store_partial<DC>(part + static_cast<size_t>(cur_seg - first_seg) * D, acc, tid, D);
-    if (p.fc.enabled) {  // fused combine: grid barrier, then this CTA's 32-column groups
-        __shared__ FfnPartialRef refs[kMaxFfnSegments];
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) {
-            atomicAdd(p.fc.barrier, 1u);
-            unsigned v;
-            do {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.fc.barrier) : "memory");
-                if (static_cast<int>(v - p.fc.target) >= 0) break;
-                __nanosleep(64);
-            } while (true);
-        }
-        if (tid < p.n_seg) {
-            FfnPartialRef f{p.partial, static_cast<int>(gridDim.x), p.n_seg, tid, p.seg_rank[tid]};
-            ffn_partial_range(f, Ft);
-            refs[tid] = f;
-        }
-        __syncthreads();
-        for (int grp = blockIdx.x; grp * kCombineCols < D; grp += gridDim.x)
-            combine_columns(grp * kCombineCols, D, p.fc.x, p.fc.scores, p.fc.experts, p.fc.ranks, p.fc.residual, refs,
-                            p.n_seg, p.fc.out, p.fc.n_out_peer, p.fc.out_peer);
-    }
 }
 
 // out[j] = x[j] + sum_rank w_rank * y_rank[j];  y_rank = fixed-order reduction of the K2 partials
 // of the rank's (tile) segments.  Block = 32 output columns x 8 partial lanes: lane q of column j
 // sums the partials of CTAs c = c_lo + q, c_lo + q + 8, ... of every segment of the rank (coalesced
 // 128-byte rows, several loads in flight), then lanes 0..7 are added in order through shared memory.
-// out[j] = x[j] + sum_rank w_rank * y_rank[j] for the 32 columns j0 .. j0+31, 512 threads (column =
-// tid % 32, lane q = tid / 32); refs sorted by (rank, tile).
-__device__ void combine_columns(int j0, int d, const double* x, const double* scores, const int* experts, int ranks,
-                                int residual, const FfnPartialRef* refs, int n_refs, float* out, int n_out_peer,
-                                float* const* out_peer) {
+constexpr int kCombineCols = 32, kCombineLanes = 16;
+
+__global__ void __launch_bounds__(kCombineCols * kCombineLanes) combine_kernel(const __grid_constant__ CombineArgs a) {
     __shared__ float red[kCombineLanes][kCombineCols];
     const int jl = threadIdx.x % kCombineCols, q = threadIdx.x / kCombineCols;
-    const int j = j0 + jl;
-    const bool live = j < d;
+    const int j = blockIdx.x * kCombineCols + jl;
+    const bool live = j < a.d;
     double denom = 0.0;
-    for (int r = 0; r < ranks; ++r) denom += scores[experts[r]];
-    float acc = (live && residual) ? static_cast<float>(x[j]) : 0.0f;
+    for (int r = 0; r < a.ranks; ++r) denom += a.scores[a.experts[r]];
+    float acc = (live && a.residual) ? static_cast<float>(a.x[j]) : 0.0f;
     int ref = 0;
-    for (int r = 0; r < ranks; ++r) {
+    for (int r = 0; r < a.ranks; ++r) {
         float part = 0.0f;
-        for (; ref < n_refs && refs[ref].rank == r; ++ref) {
-            const FfnPartialRef& f = refs[ref];
+        for (; ref < a.n_refs && a.refs[ref].rank == r; ++ref) {
+            const FfnPartialRef& f = a.refs[ref];
             if (!live) continue;
             // lane q sums CTAs c_lo + q, c_lo + q + 16, ... in that order; 8 loads in flight per lane
-            float p0 = 0.0f;
+            float p0 = 0.0f, p1 = 0.0f;
             for (int c = f.c_lo + q; c <= f.c_hi; c += 8 * kCombineLanes) {
                 float v[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     const int cc = c + k * kCombineLanes;
                     const int sl = cc == f.c_lo ? f.slot_lo : 0;
-                    v[k] = cc <= f.c_hi ? f.partial[(static_cast<size_t>(cc) * kFfnSlotsPerCta + sl) * d + j] : 0.0f;
+                    v[k] = cc <= f.c_hi ? f.partial[(static_cast<size_t>(cc) * kFfnSlotsPerCta + sl) * a.d + j] : 0.0f;
                 }
 #pragma unroll
                 for (int k = 0; k < 8; ++k) p0 += v[k];
             }
-            part += p0;
+            part += p0 + p1;
         }
         red[q][jl] = part;
         __syncthreads();
@@ -269,23 +240,18 @@ __device__ void combine_columns(int j0, int d, const double* x, const double* sc
             float yr = 0.0f;
 #pragma unroll
             for (int k = 0; k < kCombineLanes; ++k) yr += red[k][jl];
-            const float w = ranks == 1 ? 1.0f : static_cast<float>(scores[experts[r]] / denom);
+            const float w = a.ranks == 1 ? 1.0f : static_cast<float>(a.scores[a.experts[r]] / denom);
             acc = __fmaf_rn(w, yr, acc);
         }
         __syncthreads();
     }
     if (q == 0 && live) {
-        if (n_out_peer > 0) {
-            for (int g = 0; g < n_out_peer; ++g) out_peer[g][j] = acc;  // P2P stores into each shard's slot
+        if (a.n_out_peer > 0) {
+            for (int g = 0; g < a.n_out_peer; ++g) a.out_peer[g][j] = acc;  // P2P stores into each shard's slot
         } else {
-            out[j] = acc;
+            a.out[j] = acc;
         }
     }
-}
-
-__global__ void __launch_bounds__(kCombineCols * kCombineLanes) combine_kernel(const __grid_constant__ CombineArgs a) {
-    combine_columns(blockIdx.x * kCombineCols, a.d, a.x, a.scores, a.experts, a.ranks, a.residual, a.refs, a.n_refs,
-                    a.out, a.n_out_peer, a.out_peer);
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -371,6 +337,19 @@ cudaError_t launch_free_running_input(double* res, double* norm, long long strid
     return cudaGetLastError();
 }
 
+void ffn_partial_range(FfnPartialRef& f, int ft) {
+    const long long TR = static_cast<long long>(f.n_seg) * ft;
+    const long long s_lo = static_cast<long long>(f.seg) * ft, s_hi = s_lo + ft;
+    int c_lo = static_cast<int>(s_lo * f.grid / TR);
+    while (c_lo > 0 && TR * c_lo / f.grid > s_lo) --c_lo;
+    while (TR * (c_lo + 1) / f.grid <= s_lo) ++c_lo;  // first CTA whose range reaches the segment
+    int c_hi = static_cast<int>((s_hi - 1) * f.grid / TR);
+    while (c_hi + 1 < f.grid && TR * (c_hi + 1) / f.grid < s_hi) ++c_hi;
+    while (c_hi > c_lo && TR * c_hi / f.grid >= s_hi) --c_hi;  // last CTA starting inside it
+    f.c_lo = c_lo;
+    f.c_hi = c_hi;
+    f.slot_lo = f.seg - static_cast<int>(TR * c_lo / f.grid / ft);
+}
 
 int ffn_grid(const FfnLaunch& p, int sm_count) {
     const long long rows = static_cast<long long>(p.n_seg) * p.ft;
@@ -393,12 +372,12 @@ cudaError_t launch_ffn(const FfnLaunch& p, int sm_count, cudaStream_t stream) {
         cudaFuncSetAttribute(ffn_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         configured = true;
     }
-    auto kernel = p.d <= 4096 ? ffn_rows_kernel<1> : p.d <= 8192 ? ffn_rows_kernel<2> : ffn_rows_kernel<4>;
-    if (p.fc.enabled) {  // the grid barrier needs every CTA co-resident: cooperative launch
-        void* args[] = {const_cast<FfnLaunch*>(&p)};
-        return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), grid, kThreads, args, smem, stream);
-    }
-    kernel<<<grid, kThreads, smem, stream>>>(p);
+    if (p.d <= 4096)
+        ffn_rows_kernel<1><<<grid, kThreads, smem, stream>>>(p);
+    else if (p.d <= 8192)
+        ffn_rows_kernel<2><<<grid, kThreads, smem, stream>>>(p);
+    else
+        ffn_rows_kernel<4><<<grid, kThreads, smem, stream>>>(p);
     return cudaGetLastError();
 }
 

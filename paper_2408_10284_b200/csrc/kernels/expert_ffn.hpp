@@ -31,22 +31,6 @@ struct FfnSegment {
     const std::uint16_t* down_t = nullptr;   // [Ft][D] bf16 (W2^T rows)
 };
 
-// Combine fused into the FFN launch, for a layer whose whole selection is covered by this one
-// launch (every selected expert resident): after a grid-wide barrier (cooperative launch: all CTAs
-// co-resident) each CTA reduces 32-column groups of the partials exactly like combine_kernel.
-struct FfnFusedCombine {
-    int enabled = 0;
-    unsigned* barrier = nullptr;     // monotonic arrival counter in device memory
-    unsigned target = 0;             // every CTA of this launch has arrived when the counter reaches it
-    const double* x = nullptr;       // residual
-    const double* scores = nullptr;  // [N] post-softmax scores of the (token, layer)
-    float* out = nullptr;            // [d]
-    int experts[8] = {0};            // selection in rank order
-    int ranks = 0, residual = 1;
-    int n_out_peer = 0;              // expert-parallel P2P exchange (see CombineArgs)
-    float* out_peer[kMaxEpPeers] = {};
-};
-
 struct FfnLaunch {
     int n_seg = 0;
     int d = 0, ft = 0;
@@ -55,8 +39,6 @@ struct FfnLaunch {
     const double* x = nullptr;        // [d] layer input (fp64; converted to fp32 in shared memory)
     float* partial = nullptr;         // [grid][kFfnSlotsPerCta][d] written by the launch
     FfnSegment seg[kMaxFfnSegments];
-    int seg_rank[kMaxFfnSegments] = {};  // fused combine: selection rank of each segment ((rank, tile) order)
-    FfnFusedCombine fc;
 };
 
 // Grid the launch will use (partial buffer rows = grid * kFfnSlotsPerCta).
@@ -75,21 +57,9 @@ struct FfnPartialRef {
     int c_lo = 0, c_hi = -1, slot_lo = 0;
 };
 
-// Fill r.c_lo / c_hi / slot_lo from (grid, n_seg, seg) for row-tile ft (same integer arithmetic as
-// the kernel's row split); host and device.
-__host__ __device__ inline void ffn_partial_range(FfnPartialRef& f, int ft) {
-    const long long TR = static_cast<long long>(f.n_seg) * ft;
-    const long long s_lo = static_cast<long long>(f.seg) * ft, s_hi = s_lo + ft;
-    int c_lo = static_cast<int>(s_lo * f.grid / TR);
-    while (c_lo > 0 && TR * c_lo / f.grid > s_lo) --c_lo;
-    while (TR * (c_lo + 1) / f.grid <= s_lo) ++c_lo;  // first CTA whose range reaches the segment
-    int c_hi = static_cast<int>((s_hi - 1) * f.grid / TR);
-    while (c_hi + 1 < f.grid && TR * (c_hi + 1) / f.grid < s_hi) ++c_hi;
-    while (c_hi > c_lo && TR * c_hi / f.grid >= s_hi) --c_hi;  // last CTA starting inside it
-    f.c_lo = c_lo;
-    f.c_hi = c_hi;
-    f.slot_lo = f.seg - static_cast<int>(TR * c_lo / f.grid / ft);
-}
+// Host: fill r.c_lo / c_hi / slot_lo from (grid, n_seg, seg) for row-tile ft (same integer
+// arithmetic as the kernel's row split).
+void ffn_partial_range(FfnPartialRef& r, int ft);
 
 constexpr int kMaxCombineRefs = 128;
 

@@ -74,10 +74,7 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     slot_of_.assign(static_cast<size_t>(L) * N, -1);
     cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, eng.device());
     if (const char* v = std::getenv("ADAPMOE_K2_L2")) l2_mode_ = std::atoi(v);  // profiling knob
-    if (const char* v = std::getenv("ADAPMOE_FUSE_COMBINE")) fuse_combine_ = std::atoi(v) != 0;
     if (const char* v = std::getenv("ADAPMOE_SPIN_WAIT")) spin_route_wait_ = std::atoi(v) != 0;
-    d_barrier_.reserve(sizeof(unsigned));
-    MOE_CUDA(cudaMemsetAsync(d_barrier_.ptr, 0, sizeof(unsigned), eng.compute_stream()));
 
     // at most one launch for the resident experts' tiles (split per 32 segments) + one per
     // on-demand tile
@@ -403,42 +400,6 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
     partial_next_ = 0;
     std::vector<std::pair<int, int>> meta;  // (rank, tile) of p's pending segments
     std::vector<std::tuple<int, int, FfnPartialRef>> refs;
-    // every selected expert (of this shard) resident and within one launch: fuse the combine into it
-    int resident_segs = 0;
-    bool any_missing = false;
-    for (const Use& u : uses_) {
-        if (u.missing) any_missing = true;
-        else resident_segs += T;
-    }
-    if (fuse_combine_ && !any_missing && resident_segs > 0 && resident_segs <= kMaxFfnSegments) {
-        for (const Use& u : uses_) {
-            wait_fill(u.slot, -1);
-            for (int t = 0; t < T; ++t) {
-                p.seg_rank[p.n_seg] = u.rank;
-                p.seg[p.n_seg++] = seg(u.slot, t);
-                meta.emplace_back(u.rank, t);
-            }
-            stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
-        }
-        FfnFusedCombine& fc = p.fc;
-        fc.enabled = 1;
-        fc.barrier = d_barrier_.as<unsigned>();
-        barrier_target_ += static_cast<unsigned>(ffn_grid(p, sm_count_));
-        fc.target = barrier_target_;
-        fc.x = cur_res_;
-        fc.scores = cur_scores_;
-        fc.out = cur_out_;
-        fc.ranks = d.count;
-        fc.residual = ep_rank_ == 0 ? 1 : 0;
-        for (int r = 0; r < d.count; ++r) fc.experts[r] = d.experts[r];
-        if (ep_connected_) {
-            fc.n_out_peer = ep_world_;
-            for (int g = 0; g < ep_world_; ++g)
-                fc.out_peer[g] = ep_slot(g, ep_rank_, ep_call_ & 1) + (cur_out_ - cur_out_base_);
-        }
-        timed_ffn(p, meta, refs);
-        return;
-    }
     // resident experts: one launch over all their tiles
     for (const Use& u : uses_) {
         if (u.missing) continue;

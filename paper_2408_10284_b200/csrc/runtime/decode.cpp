@@ -74,7 +74,6 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     slot_of_.assign(static_cast<size_t>(L) * N, -1);
     cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, eng.device());
     if (const char* v = std::getenv("ADAPMOE_K2_L2")) l2_mode_ = std::atoi(v);  // profiling knob
-    if (const char* v = std::getenv("ADAPMOE_SPIN_WAIT")) spin_route_wait_ = std::atoi(v) != 0;
 
     // at most one launch for the resident experts' tiles (split per 32 segments) + one per
     // on-demand tile
@@ -722,16 +721,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             stats_.kernels += 1;
             MOE_CUDA(cudaEventRecord(route_done_, cs));
             const auto h0 = std::chrono::steady_clock::now();
-            // the host policy step is on the critical path of every layer: spin on the event (a
-            // blocking synchronise may yield the thread and add scheduler latency)
-            if (spin_route_wait_) {
-                cudaError_t q;
-                while ((q = cudaEventQuery(route_done_)) == cudaErrorNotReady) {
-                }
-                MOE_CUDA(q);
-            } else {
-                MOE_CUDA(cudaEventSynchronize(route_done_));
-            }
+            MOE_CUDA(cudaEventSynchronize(route_done_));
             const auto h1 = std::chrono::steady_clock::now();
             stats_.host_sync_ms += std::chrono::duration<double, std::milli>(h1 - h0).count();
             release_pending(false);

@@ -446,6 +446,16 @@ def ours(args):
         "host_link": {"copy_bytes": d["copy_bytes"], "copy_busy_ms": d["copy_busy_ms"], "achieved_gbs": copy_gbs,
                       "tile_copies": d["tile_copies"], "stall_ms": d["stall_ms"],
                       "copy_hidden_frac": (1.0 - d["stall_ms"] / d["copy_busy_ms"]) if d["copy_busy_ms"] > 0 else None,
+                      # north-star ">= 90 % of prefetch transfer hidden": prefetches the logical engine
+                      # never promoted to on-demand, vs the compute-stream wait on their tiles
+                      "prefetch_copy_ms": d["prefetch_copy_ms"], "prefetch_stall_ms": d["prefetch_stall_ms"],
+                      "prefetch_tile_copies": d["prefetch_tile_copies"],
+                      "prefetch_used_copy_ms": d["prefetch_used_copy_ms"],
+                      # of the consumed prefetch copy time, the part the compute stream did not wait for
+                      "prefetch_hidden_frac": (1.0 - d["prefetch_stall_ms"] / d["prefetch_used_copy_ms"])
+                      if d["prefetch_used_copy_ms"] > 0 else None,
+                      "prefetch_wasted_frac": (1.0 - d["prefetch_used_copy_ms"] / d["prefetch_copy_ms"])
+                      if d["prefetch_copy_ms"] > 0 else None,
                       "link_busy_frac": d["copy_busy_ms"] / gpu_ms if gpu_ms > 0 else None,
                       "peak_gbs": link_peak, "peak_source": "pinned 256 MiB H2D copy, best of 5, measured in this run",
                       "frac": (copy_gbs / link_peak) if copy_gbs else None,

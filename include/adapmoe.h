@@ -346,6 +346,10 @@ typedef struct {
     double host_step_ms;          /* host wall time in the policy step + launches (incl. copy-issue waits) */
     int32_t slots_total;          /* HBM slots = sum(capacities) + staging */
     int32_t staging_high_water;   /* most staging slots in use at once */
+    double prefetch_copy_ms;      /* tile-copy time of prefetches the logical engine never promoted */
+    double prefetch_stall_ms;     /* compute-stream time blocked on those prefetch tiles */
+    int64_t prefetch_tile_copies; /* tiles copied for them */
+    double prefetch_used_copy_ms; /* ... of which the compute stream consumed; hidden = 1 - stall / used copy */
 } moe_decode_stats;
 
 /* Counters so far without ending the session. */

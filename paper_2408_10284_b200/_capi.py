@@ -67,7 +67,9 @@ class DecodeStatsC(C.Structure):
                 ("ffn_bytes", C.c_int64), ("copy_busy_ms", C.c_double), ("ffn_ms", C.c_double),
                 ("ffn_gate_up_ms", C.c_double), ("ffn_down_ms", C.c_double), ("ffn_gate_up_bytes", C.c_double),
                 ("ffn_down_bytes", C.c_double), ("router_ms", C.c_double), ("stall_ms", C.c_double),
-                ("router_exact_items", C.c_int64), ("host_sync_ms", C.c_double), ("host_step_ms", C.c_double), ("slots_total", C.c_int32), ("staging_high_water", C.c_int32)]
+                ("router_exact_items", C.c_int64), ("host_sync_ms", C.c_double), ("host_step_ms", C.c_double), ("slots_total", C.c_int32), ("staging_high_water", C.c_int32),
+                ("prefetch_copy_ms", C.c_double), ("prefetch_stall_ms", C.c_double),
+                ("prefetch_tile_copies", C.c_int64), ("prefetch_used_copy_ms", C.c_double)]
 
 
 _d = C.POINTER(C.c_double)

@@ -417,6 +417,10 @@ void export_stats(const DecodeStats& s, moe_decode_stats* out) {
     out->host_step_ms = s.host_step_ms;
     out->slots_total = s.slots_total;
     out->staging_high_water = s.staging_high_water;
+    out->prefetch_copy_ms = s.prefetch_copy_ms;
+    out->prefetch_stall_ms = s.prefetch_stall_ms;
+    out->prefetch_tile_copies = s.prefetch_tiles;
+    out->prefetch_used_copy_ms = s.prefetch_used_copy_ms;
 }
 }  // namespace
 

@@ -68,6 +68,7 @@ void CopyEngine::submit(const std::shared_ptr<CopyJob>& job, bool on_demand) {
     {
         std::lock_guard<std::mutex> g(mu_);
         job->on_demand = on_demand;
+        job->logical_prefetch = !on_demand;
         job->queued = true;
         (on_demand ? od_ : pf_).push_back(job);
     }
@@ -128,15 +129,26 @@ double CopyEngine::busy_ms() {
     return busy_ms_;
 }
 
-double CopyEngine::busy_ms_total() {
+double CopyEngine::busy_ms_total(double* prefetch_ms, long long* prefetch_tiles, double* prefetch_used_ms) {
     std::lock_guard<std::mutex> g(mu_);
-    double total = busy_ms_;
+    double total = busy_ms_, pf = busy_pf_ms_, pf_used = busy_pf_used_ms_;
+    long long pft = pf_tiles_;
     for (const auto& job : active_)
         for (int t = 0; t < job->issued_tiles; ++t)
             if (cudaEventQuery(job->t_end[t]) == cudaSuccess) {
                 float ms = 0.0f;
-                if (cudaEventElapsedTime(&ms, job->t_start[t], job->t_end[t]) == cudaSuccess) total += ms;
+                if (cudaEventElapsedTime(&ms, job->t_start[t], job->t_end[t]) == cudaSuccess) {
+                    total += ms;
+                    if (job->logical_prefetch) {
+                        pf += ms;
+                        ++pft;
+                        if (job->consumed) pf_used += ms;
+                    }
+                }
             }
+    if (prefetch_ms) *prefetch_ms = pf;
+    if (prefetch_used_ms) *prefetch_used_ms = pf_used;
+    if (prefetch_tiles) *prefetch_tiles = pft;
     return total;
 }
 
@@ -145,7 +157,14 @@ void CopyEngine::retire(const std::shared_ptr<CopyJob>& job) {
     for (int t = 0; t < job->issued_tiles; ++t) {
         if (cudaEventSynchronize(job->t_end[t]) == cudaSuccess) {
             float ms = 0.0f;
-            if (cudaEventElapsedTime(&ms, job->t_start[t], job->t_end[t]) == cudaSuccess) busy_ms_ += ms;
+            if (cudaEventElapsedTime(&ms, job->t_start[t], job->t_end[t]) == cudaSuccess) {
+                busy_ms_ += ms;
+                if (job->logical_prefetch) {
+                    busy_pf_ms_ += ms;
+                    ++pf_tiles_;
+                    if (job->consumed) busy_pf_used_ms_ += ms;
+                }
+            }
         }
     }
     for (cudaEvent_t e : job->done) free_sync_.push_back(e);

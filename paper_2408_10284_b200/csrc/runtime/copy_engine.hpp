@@ -26,6 +26,8 @@ struct CopyJob {
     size_t tile_bytes = 0;
     int tiles = 0;
     bool on_demand = false;
+    bool logical_prefetch = false;  // a prefetch the logical engine never promoted (accounting class)
+    bool consumed = false;          // the compute stream waited on (used) its tiles
     // progress (guarded by the engine mutex)
     int next_tile = 0;      // next tile to hand to the DMA engine
     int issued_tiles = 0;   // tiles whose completion event has been recorded
@@ -57,7 +59,10 @@ public:
     long long tiles_copied() const { return tiles_copied_.load(); }
     long long bytes_copied() const { return bytes_copied_.load(); }
     double busy_ms();        // sum of per-tile copy durations of retired jobs
-    double busy_ms_total();  // ... plus every completed tile of live jobs
+    // ... plus every completed tile of live jobs; optionally the logical-prefetch share (ms, tiles)
+    // and the part of it whose jobs were consumed by the compute stream
+    double busy_ms_total(double* prefetch_ms = nullptr, long long* prefetch_tiles = nullptr,
+                         double* prefetch_used_ms = nullptr);
     void retire(const std::shared_ptr<CopyJob>& job);  // accumulate timing + recycle events
 
 private:
@@ -75,7 +80,8 @@ private:
     bool stop_ = false;
     bool busy_ = false;
     std::atomic<long long> tiles_copied_{0}, bytes_copied_{0};
-    double busy_ms_ = 0.0;
+    double busy_ms_ = 0.0, busy_pf_ms_ = 0.0, busy_pf_used_ms_ = 0.0;
+    long long pf_tiles_ = 0;
     std::thread thread_;
 };
 

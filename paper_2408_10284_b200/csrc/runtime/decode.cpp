@@ -283,7 +283,9 @@ void DecodeSession::on_request(int id, ExpertRef ref, bool on_demand) {
 }
 
 void DecodeSession::on_promote(int id) {
-    if (req_job_[id]) copier_->promote(req_job_[id], false);
+    if (!req_job_[id]) return;
+    req_job_[id]->logical_prefetch = false;  // counted on-demand at decision time (inc/simulator.hpp:410-418)
+    copier_->promote(req_job_[id], false);
 }
 
 void DecodeSession::on_insert(ExpertRef ref, int request, std::optional<int> evicted) {
@@ -337,12 +339,15 @@ void DecodeSession::wait_fill(int slot, int tile) {
     cudaStream_t cs = eng_.compute_stream();
     for (int t = t0; t < t1; ++t) {
         if (sl.fill->issued_tiles <= t) copier_->promote(sl.fill, true);
+        const bool prefetch = sl.fill->logical_prefetch;
+        sl.fill->consumed = true;
         cudaEvent_t ev = copier_->wait_issued(sl.fill, t);
         cudaEvent_t a = take_timing(), b = take_timing();
         cudaEventRecord(a, cs);
         MOE_CUDA(cudaStreamWaitEvent(cs, ev, 0));
         cudaEventRecord(b, cs);
         stall_events_.emplace_back(a, b);
+        stall_is_prefetch_.push_back(prefetch);
     }
     if (tile < 0 || tile == sl.fill->tiles - 1) sl.fill_done = true;
 }
@@ -843,16 +848,20 @@ DecodeStats DecodeSession::snapshot() {
         timing_pool_.push_back(p.second);
     }
     router_events_.clear();
-    for (auto& p : stall_events_) {
-        stats_.stall_ms += elapsed(p.first, p.second);
+    for (size_t i = 0; i < stall_events_.size(); ++i) {
+        const auto& p = stall_events_[i];
+        const double ms = elapsed(p.first, p.second);
+        stats_.stall_ms += ms;
+        if (stall_is_prefetch_[i]) stats_.prefetch_stall_ms += ms;
         timing_pool_.push_back(p.first);
         timing_pool_.push_back(p.second);
     }
     stall_events_.clear();
+    stall_is_prefetch_.clear();
     DecodeStats s = stats_;
     s.tile_copies = copier_->tiles_copied();
     s.copy_bytes = copier_->bytes_copied();
-    s.copy_busy_ms = copier_->busy_ms_total();
+    s.copy_busy_ms = copier_->busy_ms_total(&s.prefetch_copy_ms, &s.prefetch_tiles, &s.prefetch_used_copy_ms);
     return s;
 }
 

@@ -40,6 +40,9 @@ struct DecodeStats {
     long long tokens = 0, kernels = 0, ffn_launches = 0, tile_copies = 0, copy_bytes = 0, input_bytes = 0, ffn_bytes = 0;
     double copy_busy_ms = 0, ffn_ms = 0, gate_up_ms = 0, down_ms = 0, gate_up_bytes = 0, down_bytes = 0;
     double router_ms = 0, stall_ms = 0;
+    // logical prefetches (never promoted to on-demand): copy time, tiles, compute-stream wait on them
+    double prefetch_copy_ms = 0, prefetch_stall_ms = 0, prefetch_used_copy_ms = 0;
+    long long prefetch_tiles = 0;
     long long router_exact = 0;  // look-ahead items that needed the exact fp64 path
     double host_sync_ms = 0, host_step_ms = 0;  // host wall time: waiting on K1 / policy step + launches
     int slots_total = 0, staging_high_water = 0;
@@ -179,6 +182,7 @@ private:
     cudaEvent_t route_done_ = nullptr;
     std::vector<cudaEvent_t> timing_pool_;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> router_events_, stall_events_;
+    std::vector<char> stall_is_prefetch_;  // per stall_events_ entry: waited on a logical prefetch
     struct PassRec {
         double gate_up_bytes, down_bytes;
         cudaEvent_t e0, e1;

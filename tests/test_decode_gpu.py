@@ -91,6 +91,14 @@ def test_decode_trace_tiny(name):
     st = r.stats
     assert st["tokens"] == T
     assert st["ffn_bytes"] == r.metrics["experts_activated_total"] * 3 * ffn * w.D * 2
+    # copy / stall accounting by request class (bench host_link.prefetch_*): prefetch shares are
+    # parts of the totals; no prefetch traffic when the policy prefetches nothing
+    eps = 1e-6
+    assert 0 <= st["prefetch_used_copy_ms"] <= st["prefetch_copy_ms"] + eps <= st["copy_busy_ms"] + 2 * eps
+    assert 0 <= st["prefetch_stall_ms"] <= st["stall_ms"] + eps
+    assert 0 <= st["prefetch_tile_copies"] <= st["tile_copies"]
+    if not cfg.policy.prefetch or cfg.lookahead_depth == 0:
+        assert st["prefetch_tile_copies"] == 0 and st["prefetch_copy_ms"] == 0
     sim = O.simulate(w, g["sim_capacities"], g["tau"], first_gate=fg,
                      **{k: v for k, v in __import__("helpers").sim_kwargs(g).items()})
     subset = {(t, l) for t in range(0, T, 7) for l in range(w.L)}

@@ -86,6 +86,14 @@ def main():
                     "trace_prefetch_hits": m["prefetch_hits"], "trace_activated": m["experts_activated_total"],
                     "prefetch_hit_rate": m["prefetch_hits"] / max(1, m["experts_activated_total"]),
                     "link_busy_frac": dd["copy_busy_ms"] / ms if ms else None,
+                    "copy_hidden_frac": 1.0 - dd["stall_ms"] / dd["copy_busy_ms"] if dd["copy_busy_ms"] > 0 else None,
+                    "prefetch_copy_ms": dd["prefetch_copy_ms"], "prefetch_stall_ms": dd["prefetch_stall_ms"],
+                    "prefetch_used_copy_ms": dd["prefetch_used_copy_ms"],
+                    "prefetch_hidden_frac": (1.0 - dd["prefetch_stall_ms"] / dd["prefetch_used_copy_ms"]
+                                             if dd["prefetch_used_copy_ms"] > 0 else None),
+                    "prefetch_wasted_frac": (1.0 - dd["prefetch_used_copy_ms"] / dd["prefetch_copy_ms"]
+                                             if dd["prefetch_copy_ms"] > 0 else None),
+                    "ffn_ms_per_token": dd["ffn_ms"] / K, "stall_ms_per_token": dd["stall_ms"] / K,
                     "k2_gbs": (dd["ffn_gate_up_bytes"] + dd["ffn_down_bytes"]) / max(1e-9, dd["ffn_ms"] * 1e-3) / 1e9}
             r = bench.run_reference_driver(W.mixtral_8x7b(tokens=64, budget=budget, target_single_ratio=target), n, 1)
             if r is not None:
@@ -94,7 +102,8 @@ def main():
             out.write(json.dumps(line) + "\n")
             out.flush()
             print(json.dumps({k: line[k] for k in ("target_single_ratio", "budget", "tok_s", "on_demand_loads_per_token",
-                                                   "prefetch_hit_rate", "link_busy_frac", "k2_gbs", "parity")
+                                                   "prefetch_hit_rate", "link_busy_frac", "prefetch_hidden_frac", "k2_gbs",
+                                                   "parity")
                               if k in line}))
     print(json.dumps({"expert_store_s": store_s}))
 

@@ -478,6 +478,29 @@ def ours(args):
     }
     if resident is not None:
         line["all_resident_window"] = resident
+    if B == 1 and not args.free_running and rank == 0:
+        # like-for-like with the reference arm: the same function (simulate_trace: every routing
+        # decision + the tick-model cache / transfer engine, no weights moved) on the same 64-token
+        # trace, through the C ABI from pinned host buffers (K1 on the GPU, C++ engine), wall clock,
+        # best of the reps; metrics must equal the unmodified reference's
+        n_sim = min(wl.tokens, trace.acts.shape[0])
+        p_acts = torch.from_numpy(np.ascontiguousarray(trace.acts[:n_sim])).pin_memory()
+        p_scores = torch.from_numpy(np.ascontiguousarray(trace.scores[:n_sim])).pin_memory()
+        best, sim = float("inf"), None
+        for _ in range(max(1, args.warmup) + K):
+            t0 = time.perf_counter()
+            sim = eng.simulate_trace(p_acts.numpy(), p_scores.numpy(), trace.fisher, caps, tau, cfg, wl.seed)
+            best = min(best, time.perf_counter() - t0)
+        sim_line = {"tok_s": n_sim / best, "ms_per_call": best * 1e3, "tokens": n_sim, "reps": max(1, args.warmup) + K,
+                    "h2d_bytes_per_call": int(p_acts.numel() * 8 + p_scores.numel() * 8),
+                    "timeline_events": int(len(sim.timeline))}
+        if not args.no_cpu_baseline:
+            rr = run_reference_driver(wl, n_sim, 5)
+            if rr is not None:
+                sim_line["reference_tok_s"] = rr["tokens"] / rr["simulate_best_s"]
+                sim_line["metrics_equal_reference"] = rr.get("metrics") == sim.metrics and \
+                    rr.get("timeline_events") == len(sim.timeline)
+        line["simulate_trace"] = sim_line
     if not args.no_cpu_baseline:
         try:
             r = run_reference_driver(wl, decoded, 20)

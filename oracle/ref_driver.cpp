@@ -198,21 +198,29 @@ int main(int argc, char** argv) {
         SimulationInputs sub = in;
         sub.traces = std::span<const TokenTrace>(wl.traces.data(), std::min<size_t>(sample, wl.traces.size()));
         double best = 1e30, total = 0;
-        long long loads = 0;
+        SimMetrics m{};
+        size_t events = 0;
         for (int r = 0; r < reps; ++r) {
             auto a = clk::now();
             SimResult res = simulate_trace(sub, sim, sim_seed);
             auto b = clk::now();
             best = std::min(best, secs(a, b));
             total += secs(a, b);
-            loads = res.metrics.on_demand_loads;
+            m = res.metrics;
+            events = res.timeline.events.size();
         }
         std::printf(
             "{\"tokens\": %zu, \"reps\": %d, \"simulate_best_s\": %.9f, \"simulate_mean_s\": %.9f, "
             "\"generate_s\": %.6f, \"calibrate_s\": %.6f, \"train_s\": %.6f, \"profile_s\": %.6f, "
-            "\"allocate_s\": %.6f, \"on_demand_loads\": %lld}\n",
+            "\"allocate_s\": %.6f, \"on_demand_loads\": %lld, \"metrics\": {\"total_latency\": %lld, "
+            "\"stall_time\": %lld, \"on_demand_loads\": %lld, \"cache_hits\": %lld, \"prefetch_hits\": %lld, "
+            "\"single_expert_decisions\": %lld, \"experts_activated_total\": %lld}, \"timeline_events\": %zu}\n",
             sub.traces.size(), reps, best, total / reps, secs(t0, t1), secs(t1, t2), secs(t2, t3), secs(t3, t4),
-            secs(t4, t5), loads);
+            secs(t4, t5), static_cast<long long>(m.on_demand_loads), static_cast<long long>(m.total_latency),
+            static_cast<long long>(m.stall_time), static_cast<long long>(m.on_demand_loads),
+            static_cast<long long>(m.cache_hits), static_cast<long long>(m.prefetch_hits),
+            static_cast<long long>(m.single_expert_decisions), static_cast<long long>(m.experts_activated_total),
+            events);
         return 0;
     }
 

@@ -378,7 +378,7 @@ def ours(args):
         resident = {"tok_s": ws * B * K / (max_over_ranks(ws, g_ms) * 1e-3), "ms_per_step": g_ms / K,
                     "ffn_achieved_gbs": ach, "ffn_frac": ach / measured_peaks().get("hbm_gbs", 6650.0),
                     "ffn_share_of_step": dr["ffn_ms"] / g_ms if g_ms > 0 else None,
-                    "ffn_launches": dr["ffn_launches"], "router_us_per_launch": 1e3 * dr["router_ms"] / max(1, K * wl.layers),
+                    "ffn_launches": dr["ffn_launches"], "router_us_per_layer": 1e3 * dr["router_ms"] / max(1, K * wl.layers),
                     "host_wait_k1_ms_per_step": dr["host_sync_ms"] / K, "host_step_ms_per_step": dr["host_step_ms"] / K,
                     "budget": wl.layers * wl.experts}
     # on-demand loads per token in the timed window (tile 0 of each on-demand expert)
@@ -465,8 +465,10 @@ def ours(args):
                       if gpu_ms > 0 else None},
         "time_split_ms": {"ffn": ffn_ms, "router": d["router_ms"], "copy_stall": d["stall_ms"], "total": gpu_ms,
                           "host_wait_k1": d["host_sync_ms"], "host_step": d["host_step_ms"]},
-        "router": {"launches": K * wl.layers, "groups_per_launch": B,
-                   "us_per_launch": 1e3 * d["router_ms"] / max(1, K * wl.layers),
+        "router": {"launches": int(d["router_launches"]),
+                   "groups_per_launch": K * wl.layers * B / max(1, d["router_launches"]),
+                   "us_per_launch": 1e3 * d["router_ms"] / max(1, d["router_launches"]),
+                   "us_per_layer": 1e3 * d["router_ms"] / max(1, K * wl.layers),
                    "exact_fallback_items": int(d["router_exact_items"])},
         "gpu_launches": int(d["kernels_launched"]),
         "clocks": clk.summary(),

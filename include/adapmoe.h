@@ -350,6 +350,7 @@ typedef struct {
     double prefetch_stall_ms;     /* compute-stream time blocked on those prefetch tiles */
     int64_t prefetch_tile_copies; /* tiles copied for them */
     double prefetch_used_copy_ms; /* ... of which the compute stream consumed; hidden = 1 - stall / used copy */
+    int64_t router_launches;      /* K1 launches: one per layer (free-running), one per token window (trace replay) */
 } moe_decode_stats;
 
 /* Counters so far without ending the session. */

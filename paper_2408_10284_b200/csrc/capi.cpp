@@ -421,6 +421,7 @@ void export_stats(const DecodeStats& s, moe_decode_stats* out) {
     out->prefetch_stall_ms = s.prefetch_stall_ms;
     out->prefetch_tile_copies = s.prefetch_tiles;
     out->prefetch_used_copy_ms = s.prefetch_used_copy_ms;
+    out->router_launches = s.router_launches;
 }
 }  // namespace
 

@@ -104,8 +104,10 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
         route_scratch_ = RouteScratch{reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + fa),
                                       reinterpret_cast<unsigned*>(base + 2 * fa), batch_};
     }
-    const int route_rows = 4 * batch_;
-    MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_route_), static_cast<size_t>(route_rows) * (K + 3) * sizeof(int),
+    // trace replay: one K1 launch routes up to route_window_ tokens (every layer and stream)
+    route_window_ = free_running_ ? 1 : std::max(1, std::min(total_tokens, (1 << 20) / (4 * batch_ * L)));
+    const size_t route_rows = static_cast<size_t>(4) * batch_ * (free_running_ ? 1 : static_cast<size_t>(L) * route_window_);
+    MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_route_), route_rows * (K + 3) * sizeof(int),
                            cudaHostAllocMapped));
     MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_route_), h_route_, 0));
     MOE_CUDA(cudaEventCreateWithFlags(&route_done_, cudaEventDisableTiming));
@@ -135,6 +137,8 @@ DecodeSession::~DecodeSession() {
     for (void* p : ep_ipc_opened_) cudaIpcCloseMemHandle(p);
     if (h_route_) cudaFreeHost(h_route_);
     if (route_done_) cudaEventDestroy(route_done_);
+    for (auto& p : layer_events_) cudaEventDestroy(p.second);
+    for (cudaEvent_t e : layer_event_pool_) cudaEventDestroy(e);
     for (auto& p : pass_events_) {
         cudaEventDestroy(p.e0);
         cudaEventDestroy(p.e1);
@@ -228,6 +232,12 @@ cudaEvent_t DecodeSession::take_timing() {
 }
 
 int DecodeSession::take_slot() {
+    if (free_.empty()) release_pending(false);
+    while (free_.empty() && !pending_free_.empty() && !layer_events_.empty()) {
+        // the host routed ahead of the GPU: wait for the oldest layer still reading a released slot
+        MOE_CUDA(cudaEventSynchronize(layer_events_.front().second));
+        release_pending(false);
+    }
     if (free_.empty())
         fail(Status::Infeasible, "decode: HBM slot pool exhausted (" + std::to_string(n_slots_) +
                                      " slots); pass a larger staging_slots to moe_decode_begin");
@@ -240,10 +250,16 @@ int DecodeSession::take_slot() {
 
 void DecodeSession::release_slot(int s) { pending_free_.emplace_back(layer_seq_, s); }
 
-// Called when every FFN launch of layers < layer_seq_ has completed (after the router sync).
+// Free the slots released by layers whose FFN + combine have completed on the GPU (all: every
+// pending slot; the caller has synchronised the device).
 void DecodeSession::release_pending(bool all) {
+    while (!layer_events_.empty() && (all || cudaEventQuery(layer_events_.front().second) == cudaSuccess)) {
+        layers_complete_ = layer_events_.front().first + 1;
+        layer_event_pool_.push_back(layer_events_.front().second);
+        layer_events_.pop_front();
+    }
     auto it = std::stable_partition(pending_free_.begin(), pending_free_.end(),
-                                    [&](const auto& p) { return !(all || p.first < layer_seq_); });
+                                    [&](const auto& p) { return !(all || p.first < layers_complete_); });
     for (auto jt = it; jt != pending_free_.end(); ++jt) {
         Slot& sl = slots_[jt->second];
         if (sl.fill) {
@@ -384,6 +400,15 @@ void DecodeSession::on_layer_done(int, int, const RouteDecision& d) {
     else
         layer_ffn_single(d);
     uses_.clear();
+    cudaEvent_t ev;
+    if (layer_event_pool_.empty()) {
+        MOE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    } else {
+        ev = layer_event_pool_.back();
+        layer_event_pool_.pop_back();
+    }
+    MOE_CUDA(cudaEventRecord(ev, eng_.compute_stream()));
+    layer_events_.emplace_back(layer_seq_, ev);
     ++layer_seq_;
 }
 
@@ -650,7 +675,9 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
     }
 
     // router groups for every (token, layer, stream) of this call: they depend only on positions.
-    // Group (i, l, b) writes rows b*4 + item of the layer's launch.
+    // Free-running: one launch per layer, group (i, l, b) writes rows b*4 + item.  Trace replay: the
+    // decisions depend only on the stored trace, so one launch routes a window of tokens ahead of the
+    // GPU and group (i, l, b) writes rows ((i % window) * L + l) * B * 4 + b * 4 + item.
     const bool prefetch_on = policy_->prefetch_on();
     h_groups_.reserve(TL * sizeof(RouteGroup));
     d_groups_.reserve(TL * sizeof(RouteGroup));
@@ -662,13 +689,14 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             for (int b = 0; b < B; ++b) {
                 const size_t row = (static_cast<size_t>(i) * B + b) * L + l;  // input row [i][b][l]
                 const int tok = tokens_done_ + i;
+                const int rb = free_running_ ? b * 4 : (((i % route_window_) * L + l) * B + b) * 4;
                 RouteGroup g;
                 g.x = (free_running_ ? x_norm : x_all) + row * D;
                 g.n_items = 1;
                 g.items[0].scores = s_all + row * N;
                 g.items[0].fisher = fisher_[l];
                 g.items[0].flags = adaptive;
-                g.items[0].out = b * 4;
+                g.items[0].out = rb;
                 if (free_running_) {  // decide from this layer's gate on the evolving hidden state
                     eng_.gate_item(g.items[0], l);
                     g.items[0].flags = adaptive | kRouteDivConc | kRouteEmitScores;
@@ -680,14 +708,14 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                             eng_.gate_item(it, l + dep);
                             it.fisher = fisher_[l + dep];
                             it.flags = adaptive;
-                            it.out = b * 4 + dep;
+                            it.out = rb + dep;
                         }
                     } else if (eng_.has_first_gate() && tok + 1 < total_tokens_) {
                         RouteItem& it = g.items[g.n_items++];
                         eng_.gate_item(it, -1);
                         it.fisher = fisher_[0];
                         it.flags = adaptive;
-                        it.out = b * 4 + 1;
+                        it.out = rb + 1;
                     }
                 }
                 max_gates = std::max(max_gates, free_running_ ? g.n_items : g.n_items - 1);
@@ -695,7 +723,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             }
     MOE_CUDA(cudaMemcpyAsync(d_groups_.ptr, hg, TL * sizeof(RouteGroup), cudaMemcpyHostToDevice, cs));
     RouteParams rp{D, N, K, tau_, concentration_};
-    const int rows = 4 * B;
+    const int rows = 4 * B * (free_running_ ? 1 : L * route_window_);  // output layout stride
     int* d_sel = d_route_;
     int* d_cnt = d_sel + static_cast<size_t>(rows) * K;
     int* d_sgl = d_cnt + rows;
@@ -718,30 +746,39 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                                                    static_cast<long long>(L) * D, B, D, kFreeRunningNormEps, cs));
                 stats_.kernels += 1;
             }
-            cudaEvent_t r0 = take_timing(), r1 = take_timing();
-            cudaEventRecord(r0, cs);
-            MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + gl, B, max_gates, rp, ro, cs, &route_scratch_));
-            cudaEventRecord(r1, cs);
-            router_events_.emplace_back(r0, r1);
-            stats_.kernels += 1;
-            MOE_CUDA(cudaEventRecord(route_done_, cs));
-            const auto h0 = std::chrono::steady_clock::now();
-            MOE_CUDA(cudaEventSynchronize(route_done_));
+            if (free_running_ || (l == 0 && i % route_window_ == 0)) {
+                // free-running: this layer (its input is the previous layer's output); trace replay:
+                // every layer of the next window of tokens, once
+                const int n_groups = free_running_ ? B : std::min(route_window_, count - i) * L * B;
+                cudaEvent_t r0 = take_timing(), r1 = take_timing();
+                cudaEventRecord(r0, cs);
+                MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + gl, n_groups, max_gates, rp, ro, cs,
+                                      n_groups <= route_scratch_.groups ? &route_scratch_ : nullptr));
+                cudaEventRecord(r1, cs);
+                router_events_.emplace_back(r0, r1);
+                stats_.kernels += 1;
+                stats_.router_launches += 1;
+                MOE_CUDA(cudaEventRecord(route_done_, cs));
+                const auto h0 = std::chrono::steady_clock::now();
+                MOE_CUDA(cudaEventSynchronize(route_done_));
+                stats_.host_sync_ms +=
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+            }
             const auto h1 = std::chrono::steady_clock::now();
-            stats_.host_sync_ms += std::chrono::duration<double, std::milli>(h1 - h0).count();
             release_pending(false);
             // actual selection: the union of the streams' selections (B = 1: the stream's own)
             RouteDecision d;
             int singles = 0;
             const int n_items = hg[gl].n_items;
             int np = 0;
+            const int base = free_running_ ? 0 : ((i % route_window_) * L + l) * B * 4;
             for (int it = 1; it < n_items; ++it) {
                 preds[np].target = (l + 1 < L) ? l + it : 0;
                 preds[np].count = 0;
                 ++np;
             }
             for (int b = 0; b < B; ++b) {
-                const int r0w = b * 4;
+                const int r0w = base + b * 4;
                 singles += sgl[r0w] != 0;
                 for (int it = 1; it < n_items; ++it) stats_.router_exact += exact_used[r0w + it];
                 for (int k = 0; k < cnt[r0w]; ++k) {
@@ -764,7 +801,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                     for (int k = 0; k < K; ++k) cur_sel_[b * K + k] = k < cnt[r0w] ? sel[r0w * K + k] : -1;
                 }
             }
-            d.single = B == 1 && sgl[0] != 0;
+            d.single = B == 1 && sgl[base] != 0;
             const size_t row0 = (static_cast<size_t>(i) * B) * L + l;  // stream 0's input row
             cur_x_ = (free_running_ ? x_norm : x_all) + row0 * D;
             cur_res_ = x_all + row0 * D;

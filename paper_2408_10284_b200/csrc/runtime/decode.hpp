@@ -40,6 +40,7 @@ struct DecodeStats {
     long long tokens = 0, kernels = 0, ffn_launches = 0, tile_copies = 0, copy_bytes = 0, input_bytes = 0, ffn_bytes = 0;
     double copy_busy_ms = 0, ffn_ms = 0, gate_up_ms = 0, down_ms = 0, gate_up_bytes = 0, down_bytes = 0;
     double router_ms = 0, stall_ms = 0;
+    long long router_launches = 0;
     // logical prefetches (never promoted to on-demand): copy time, tiles, compute-stream wait on them
     double prefetch_copy_ms = 0, prefetch_stall_ms = 0, prefetch_used_copy_ms = 0;
     long long prefetch_tiles = 0;
@@ -177,9 +178,19 @@ private:
     DeviceBuffer d_route_scratch_;  // K1 split launch: F / A per group + tickets
     RouteScratch route_scratch_;
     PinnedBuffer h_groups_;
-    int* h_route_ = nullptr;  // mapped pinned: selected [4][K], count [4], single [4]
+    // mapped pinned K1 outputs: selected [R][K], count [R], single [R], exact [R] with R = 4 rows per
+    // group; free-running routes one layer per launch (R = 4B), trace replay a window of
+    // route_window_ tokens per launch (R = 4B * L * window)
+    int* h_route_ = nullptr;
     int* d_route_ = nullptr;
+    int route_window_ = 1;
     cudaEvent_t route_done_ = nullptr;
+    // completion of each layer's FFN + combine on the compute stream: a slot released by layer s is
+    // reused only after the event of layer s has completed (trace replay routes ahead of the GPU, so
+    // there is no per-layer host synchronisation to order slot reuse)
+    std::deque<std::pair<long long, cudaEvent_t>> layer_events_;
+    std::vector<cudaEvent_t> layer_event_pool_;
+    long long layers_complete_ = 0;  // every layer with sequence < this has completed on the GPU
     std::vector<cudaEvent_t> timing_pool_;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> router_events_, stall_events_;
     std::vector<char> stall_is_prefetch_;  // per stall_events_ entry: waited on a logical prefetch

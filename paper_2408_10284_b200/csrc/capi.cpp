@@ -102,40 +102,59 @@ void export_events(const std::vector<TimelineEvent>& ev, long long total, moe_ev
 }
 
 // Replays router outputs through the logical engine (simulate_trace's cache/transfer half).
+struct Replayer {
+    const ModelSpec& spec;
+    const SimConfig& cfg;
+    std::vector<int> caps;
+    PolicyEngine pe;
+    Replayer(const ModelSpec& s, int T, const int32_t* c, const SimConfig& conf, uint64_t seed, bool events)
+        : spec(s), cfg(conf), caps(validated(s, c)), pe(s, conf, caps, seed, T, nullptr, events) {}
+    static std::vector<int> validated(const ModelSpec& s, const int32_t* c) {
+        std::vector<int> v(c, c + s.num_layers);
+        Allocation a{v, 0};
+        for (int t : v) a.budget += t;
+        a.validate(s);
+        return v;
+    }
+    // tokens [t0, t1) of [T][L] router outputs
+    void tokens(int t0, int t1, const int32_t* sel, const int32_t* single, const int32_t* preds) {
+        const int L = spec.num_layers, K = spec.top_k, PW = 2 + K;
+        RouteDecision d;
+        RoutePrediction p[3];
+        for (int tok = t0; tok < t1; ++tok)
+            for (int l = 0; l < L; ++l) {
+                const size_t tl = static_cast<size_t>(tok) * L + l;
+                d.count = 0;
+                for (int k = 0; k < K; ++k) {
+                    const int e = sel[tl * K + k];
+                    if (e >= 0) d.experts[d.count++] = e;
+                }
+                d.single = single ? single[tl] != 0 : (cfg.policy.adaptive_gating ? d.count == 1 : K == 1);
+                int np = 0;
+                if (preds)
+                    for (int s = 0; s < 3; ++s) {
+                        const int32_t* row = preds + (tl * 3 + s) * PW;
+                        if (row[0] < 0) continue;
+                        p[np].target = row[0];
+                        p[np].count = row[1];
+                        for (int k = 0; k < row[1]; ++k) p[np].experts[k] = row[2 + k];
+                        ++np;
+                    }
+                pe.step(tok, l, d, std::span<const RoutePrediction>(p, np));
+            }
+    }
+    void finish(moe_metrics* metrics, int64_t* lat, int64_t* odl, moe_event* events, int64_t cap, int64_t* n_events) {
+        export_metrics(pe.metrics(), metrics, lat, odl);
+        export_events(pe.timeline(), pe.events_recorded(), events, cap, n_events);
+    }
+};
+
 void replay(const ModelSpec& spec, int T, const int32_t* caps, const SimConfig& cfg, uint64_t seed, const int32_t* sel,
             const int32_t* single, const int32_t* preds, moe_metrics* metrics, int64_t* lat, int64_t* odl,
             moe_event* events, int64_t cap, int64_t* n_events) {
-    const int L = spec.num_layers, K = spec.top_k, PW = 2 + K;
-    std::vector<int> c(caps, caps + L);
-    Allocation a{c, 0};
-    for (int t : c) a.budget += t;
-    a.validate(spec);
-    PolicyEngine pe(spec, cfg, c, seed, T, nullptr, events != nullptr);
-    RouteDecision d;
-    RoutePrediction p[3];
-    for (int tok = 0; tok < T; ++tok)
-        for (int l = 0; l < L; ++l) {
-            const size_t tl = static_cast<size_t>(tok) * L + l;
-            d.count = 0;
-            for (int k = 0; k < K; ++k) {
-                const int e = sel[tl * K + k];
-                if (e >= 0) d.experts[d.count++] = e;
-            }
-            d.single = single ? single[tl] != 0 : (cfg.policy.adaptive_gating ? d.count == 1 : K == 1);
-            int np = 0;
-            if (preds)
-                for (int s = 0; s < 3; ++s) {
-                    const int32_t* row = preds + (tl * 3 + s) * PW;
-                    if (row[0] < 0) continue;
-                    p[np].target = row[0];
-                    p[np].count = row[1];
-                    for (int k = 0; k < row[1]; ++k) p[np].experts[k] = row[2 + k];
-                    ++np;
-                }
-            pe.step(tok, l, d, std::span<const RoutePrediction>(p, np));
-        }
-    export_metrics(pe.metrics(), metrics, lat, odl);
-    export_events(pe.timeline(), pe.events_recorded(), events, cap, n_events);
+    Replayer rp(spec, T, caps, cfg, seed, events != nullptr);
+    rp.tokens(0, T, sel, single, preds);
+    rp.finish(metrics, lat, odl, events, cap, n_events);
 }
 
 }  // namespace
@@ -281,9 +300,15 @@ int moe_simulate_trace(moe_engine_t h, const double* acts, const double* scores,
         if (T < 1) fail(Status::Validation, "trace holds no tokens");
         GatingThreshold{tau}.validate();
         const ModelSpec& s = e.spec();
-        TraceRoutes r = e.route_trace(acts, scores, T, std::span<const double>(fisher, s.num_layers), tau, c);
-        replay(s, T, caps, c, seed, r.selected.data(), r.single.data(), r.predictions.data(), metrics, lat, odl, events,
-               cap, n_events);
+        // the host engine replays each chunk of tokens while the GPU moves / routes the next ones
+        Replayer rp(s, T, caps, c, seed, events != nullptr);
+        TraceRoutes r;
+        const int chunk = std::max(1, std::min(16, (T + 7) / 8));
+        e.route_trace_stream(acts, scores, T, std::span<const double>(fisher, s.num_layers), tau, c, chunk, r,
+                             [&](int t0, int t1) {
+                                 rp.tokens(t0, t1, r.selected.data(), r.single.data(), r.predictions.data());
+                             });
+        rp.finish(metrics, lat, odl, events, cap, n_events);
     });
 }
 

@@ -115,26 +115,41 @@ void Engine::run_route(const std::vector<RouteGroup>& groups, int rows, int max_
 // Evaluation points of simulate_trace (inc/simulator.hpp:390-396 decision, :422-436 look-ahead).
 TraceRoutes Engine::route_trace(const double* acts, const double* scores, int T, std::span<const double> fisher,
                                 double tau, const SimConfig& cfg) {
+    TraceRoutes r;
+    route_trace_stream(acts, scores, T, fisher, tau, cfg, T, r, [](int, int) {});
+    return r;
+}
+
+void Engine::route_trace_stream(const double* acts, const double* scores, int T, std::span<const double> fisher,
+                                double tau, const SimConfig& cfg, int chunk_tokens, TraceRoutes& r,
+                                const std::function<void(int, int)>& on_chunk) {
     activate();
     cfg.validate();
     const int L = spec_.num_layers, N = spec_.experts_per_layer, K = spec_.top_k, D = spec_.hidden_dim;
     if (static_cast<int>(fisher.size()) != L) fail(Status::Usage, "route_trace: fisher count != num_layers");
     const bool prefetch_on = cfg.policy.prefetch && cfg.lookahead_depth > 0;
     if (prefetch_on && !has_gates()) fail(Status::Usage, "simulate_trace: prefetching requires one gate matrix per layer");
-    const size_t TL = static_cast<size_t>(T) * L;
+    const size_t TL = static_cast<size_t>(T) * L, rows = TL * 4;
     d_x_.reserve(TL * D * sizeof(double));
     d_scores_.reserve(TL * N * sizeof(double));
-    MOE_CUDA(cudaMemcpyAsync(d_x_.ptr, acts, TL * D * sizeof(double), cudaMemcpyHostToDevice, compute_));
-    MOE_CUDA(cudaMemcpyAsync(d_scores_.ptr, scores, TL * N * sizeof(double), cudaMemcpyHostToDevice, compute_));
+    d_groups_.reserve(TL * sizeof(RouteGroup));
+    d_out_sel_.reserve(rows * K * sizeof(int));
+    d_out_cnt_.reserve(rows * sizeof(int));
+    d_out_single_.reserve(rows * sizeof(int));
+    d_out_pert_.reserve(rows * sizeof(double));
+    h_trace_groups_.reserve(TL * sizeof(RouteGroup));
+    h_trace_out_.reserve(rows * ((K + 2) * sizeof(int) + sizeof(double)));
 
-    std::vector<RouteGroup> groups(TL);
+    // group (tok, l) writes rows tl*4 + item: decision, then look-ahead depth 1..k (or the first-layer
+    // predictive gate at the last layer)
+    RouteGroup* groups = h_trace_groups_.as<RouteGroup>();
     int max_gates = 0;
     for (int tok = 0; tok < T; ++tok)
         for (int l = 0; l < L; ++l) {
             const size_t tl = static_cast<size_t>(tok) * L + l;
             RouteGroup& g = groups[tl];
+            g = RouteGroup{};
             g.x = d_x_.as<double>() + tl * D;
-            g.n_items = 0;
             RouteItem& dec = g.items[g.n_items++];
             dec.gate = nullptr;
             dec.scores = d_scores_.as<double>() + tl * N;
@@ -164,37 +179,69 @@ TraceRoutes Engine::route_trace(const double* acts, const double* scores, int T,
             }
             max_gates = std::max(max_gates, n_gates);
         }
+    MOE_CUDA(cudaMemcpyAsync(d_groups_.ptr, groups, TL * sizeof(RouteGroup), cudaMemcpyHostToDevice, compute_));
+    int* h_sel = h_trace_out_.as<int>();
+    int* h_cnt = h_sel + rows * K;
+    int* h_sgl = h_cnt + rows;
+    double* h_pert = reinterpret_cast<double*>(h_sgl + rows);
     RouteParams p{D, N, K, tau, 1.0};
-    TraceRoutes raw;
-    run_route(groups, static_cast<int>(TL * 4), std::max(max_gates, 1), p, &raw, nullptr, compute_);
-
-    TraceRoutes r;
+    RouteOutputs o{d_out_sel_.as<int>(), d_out_cnt_.as<int>(), d_out_single_.as<int>(), d_out_pert_.as<double>(), nullptr};
+    const int chunk = std::max(1, std::min(chunk_tokens, T));
+    const int n_chunks = (T + chunk - 1) / chunk;
+    std::vector<cudaEvent_t> done(n_chunks);
+    for (auto& e : done) MOE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct EventGuard {
+        std::vector<cudaEvent_t>& v;
+        ~EventGuard() {
+            for (cudaEvent_t e : v) cudaEventDestroy(e);
+        }
+    } guard{done};
+    // enqueue every chunk: inputs -> K1 -> decisions back, one completion event per chunk
+    for (int c = 0; c < n_chunks; ++c) {
+        const size_t t0 = static_cast<size_t>(c) * chunk, t1 = std::min<size_t>(T, t0 + chunk);
+        const size_t r0 = t0 * L, nr = (t1 - t0) * L;
+        MOE_CUDA(cudaMemcpyAsync(d_x_.as<double>() + r0 * D, acts + r0 * D, nr * D * sizeof(double),
+                                 cudaMemcpyHostToDevice, compute_));
+        MOE_CUDA(cudaMemcpyAsync(d_scores_.as<double>() + r0 * N, scores + r0 * N, nr * N * sizeof(double),
+                                 cudaMemcpyHostToDevice, compute_));
+        MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + r0, static_cast<int>(nr), std::max(max_gates, 1), p, o, compute_));
+        const size_t q0 = r0 * 4, nq = nr * 4;
+        MOE_CUDA(cudaMemcpyAsync(h_sel + q0 * K, o.selected + q0 * K, nq * K * sizeof(int), cudaMemcpyDeviceToHost, compute_));
+        MOE_CUDA(cudaMemcpyAsync(h_cnt + q0, o.count + q0, nq * sizeof(int), cudaMemcpyDeviceToHost, compute_));
+        MOE_CUDA(cudaMemcpyAsync(h_sgl + q0, o.single + q0, nq * sizeof(int), cudaMemcpyDeviceToHost, compute_));
+        MOE_CUDA(cudaMemcpyAsync(h_pert + q0, o.perturbation + q0, nq * sizeof(double), cudaMemcpyDeviceToHost, compute_));
+        MOE_CUDA(cudaEventRecord(done[c], compute_));
+    }
     r.selected.resize(TL * K);
     r.count.resize(TL);
     r.single.resize(TL);
     r.perturbation.resize(TL);
     const int PW = 2 + K;
     r.predictions.assign(TL * 3 * PW, -1);
-    for (size_t tl = 0; tl < TL; ++tl) {
-        const int row = static_cast<int>(tl * 4);
-        for (int k = 0; k < K; ++k) r.selected[tl * K + k] = raw.selected[static_cast<size_t>(row) * K + k];
-        r.count[tl] = raw.count[row];
-        r.single[tl] = raw.single[row];
-        r.perturbation[tl] = raw.perturbation[row];
-        const RouteGroup& g = groups[tl];
-        for (int s = 0; s < 3; ++s) {
-            int* dst = &r.predictions[(tl * 3 + s) * PW];
-            dst[1] = 0;
-            if (s + 1 < g.n_items) {
-                const int prow = g.items[s + 1].out;
-                const int layer = static_cast<int>(tl % L);
-                dst[0] = (g.items[s + 1].gate == d_first_gate() && layer == L - 1) ? 0 : layer + s + 1;
-                dst[1] = raw.count[prow];
-                for (int k = 0; k < K; ++k) dst[2 + k] = raw.selected[static_cast<size_t>(prow) * K + k];
+    for (int c = 0; c < n_chunks; ++c) {
+        const int t0 = c * chunk, t1 = std::min(T, t0 + chunk);
+        MOE_CUDA(cudaEventSynchronize(done[c]));
+        for (size_t tl = static_cast<size_t>(t0) * L; tl < static_cast<size_t>(t1) * L; ++tl) {
+            const size_t row = tl * 4;
+            for (int k = 0; k < K; ++k) r.selected[tl * K + k] = h_sel[row * K + k];
+            r.count[tl] = h_cnt[row];
+            r.single[tl] = h_sgl[row];
+            r.perturbation[tl] = h_pert[row];
+            const RouteGroup& g = groups[tl];
+            for (int s = 0; s < 3; ++s) {
+                int* dst = &r.predictions[(tl * 3 + s) * PW];
+                dst[1] = 0;
+                if (s + 1 < g.n_items) {
+                    const size_t prow = static_cast<size_t>(g.items[s + 1].out);
+                    const int layer = static_cast<int>(tl % L);
+                    dst[0] = (g.items[s + 1].gate == d_first_gate() && layer == L - 1) ? 0 : layer + s + 1;
+                    dst[1] = h_cnt[prow];
+                    for (int k = 0; k < K; ++k) dst[2 + k] = h_sel[prow * K + k];
+                }
             }
         }
+        on_chunk(t0, t1);
     }
-    return r;
 }
 
 // inc/workload.hpp:60-112.  The RNG stream is consumed on the host in the reference's order

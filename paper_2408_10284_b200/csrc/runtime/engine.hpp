@@ -4,6 +4,7 @@
 
 #include <cuda_runtime_api.h>
 
+#include <functional>
 #include <memory>
 #include <span>
 #include <string>
@@ -79,6 +80,13 @@ public:
     // K1 over a whole trace (acts/scores host).  Matches simulate_trace's evaluation points.
     TraceRoutes route_trace(const double* acts, const double* scores, int tokens, std::span<const double> fisher,
                             double tau, const SimConfig& cfg);
+    // The same, pipelined: the trace is routed in chunks of `chunk_tokens` (H2D of the chunk's
+    // activations, one K1 launch, D2H of its decisions), all enqueued up front; `on_chunk(t0, t1)`
+    // runs on the host as soon as tokens [t0, t1) of `out` are filled, while later chunks are still
+    // moving / routing on the GPU.
+    void route_trace_stream(const double* acts, const double* scores, int tokens, std::span<const double> fisher,
+                            double tau, const SimConfig& cfg, int chunk_tokens, TraceRoutes& out,
+                            const std::function<void(int, int)>& on_chunk);
 
     // generate_trace with the gate GEMVs on the GPU; returns via the output arrays.
     void generate_trace(const int tokens, double concentration, double drift, std::uint64_t gate_seed,
@@ -113,6 +121,7 @@ private:
     bool gates_loaded_ = false, first_gate_loaded_ = false;
     // router workspace
     DeviceBuffer d_groups_, d_x_, d_scores_, d_out_sel_, d_out_cnt_, d_out_single_, d_out_pert_, d_out_scores_;
+    PinnedBuffer h_trace_groups_, h_trace_out_;  // route_trace_stream staging
 };
 
 }  // namespace adapmoe

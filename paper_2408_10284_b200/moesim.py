@@ -151,15 +151,19 @@ def tile_pipeline_latency(tiles: int, transfer: int, compute: int) -> int:
 
 
 def _events_buf(spec: ModelSpec, T: int, cfg: SimConfig, batch: int = 1):
+    """Uninitialised [cap][8] int64 event buffer (moe_event layout) and its capacity."""
     k = min(spec.experts_per_layer, spec.top_k * batch)  # experts a layer can activate
     per_layer = 2 + k * (1 + 2 * cfg.tile_count_per_expert) + 3 * k * cfg.tile_count_per_expert
     cap = T * spec.num_layers * per_layer + 64
-    return (_capi.EventC * cap)(), cap
+    return np.empty((cap, 8), dtype=np.int64), cap
+
+
+def _evp(buf):
+    return None if buf is None else buf.ctypes.data_as(C.POINTER(_capi.EventC))
 
 
 def _events_np(buf, n):
-    arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_int64)), shape=(len(buf) * 8,))
-    return arr[: n * 8].reshape(n, 8).copy()
+    return buf[:n].copy()
 
 
 def replay_policy(spec: ModelSpec, caps, cfg: SimConfig, seed: int, decisions, single, predictions,
@@ -177,7 +181,7 @@ def replay_policy(spec: ModelSpec, caps, cfg: SimConfig, seed: int, decisions, s
     check(load().moe_replay_policy(C.byref(spec.c()), T, _p(_i32(caps), _capi._i32), C.byref(cfg.c()), seed,
                                    _p(decisions, _capi._i32), None if single is None else _p(single, _capi._i32),
                                    None if predictions is None else _p(predictions, _capi._i32), C.byref(m),
-                                   _p(lat, _capi._i64), _p(odl, _capi._i64), buf, cap, C.byref(n)))
+                                   _p(lat, _capi._i64), _p(odl, _capi._i64), _evp(buf), cap, C.byref(n)))
     return SimResult({k: getattr(m, k) for k, _ in _capi.MetricsC._fields_}, lat, odl,
                      _events_np(buf, n.value) if timeline else None, n.value)
 
@@ -239,7 +243,7 @@ class Engine:
         buf, cap = _events_buf(self.spec, T, cfg) if timeline else (None, 0)
         check(load().moe_simulate_trace(self._h, _p(acts, _capi._d), _p(scores, _capi._d), T, _p(fisher, _capi._d),
                                         _p(_i32(caps), _capi._i32), float(tau), C.byref(cfg.c()), seed, C.byref(m),
-                                        _p(lat, _capi._i64), _p(odl, _capi._i64), buf, cap, C.byref(n)))
+                                        _p(lat, _capi._i64), _p(odl, _capi._i64), _evp(buf), cap, C.byref(n)))
         return SimResult({k: getattr(m, k) for k, _ in _capi.MetricsC._fields_}, lat, odl,
                          _events_np(buf, n.value) if timeline else None, n.value)
 
@@ -371,7 +375,7 @@ class Engine:
         buf, cap = (_events_buf(self.spec, T, cfg, getattr(self, "_batch", 1)) if (timeline and cfg is not None and T)
                     else (None, 0))
         check(load().moe_decode_end(self._h, C.byref(m), _p(lat, _capi._i64) if T else None, _p(odl, _capi._i64),
-                                    buf, cap, C.byref(n), C.byref(st)))
+                                    _evp(buf), cap, C.byref(n), C.byref(st)))
         return SimResult({k: getattr(m, k) for k, _ in _capi.MetricsC._fields_}, lat[:T], odl,
                          _events_np(buf, n.value) if buf is not None else None, n.value,
                          {k: getattr(st, k) for k, _ in _capi.DecodeStatsC._fields_})

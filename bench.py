@@ -248,11 +248,19 @@ def ours(args):
     ep_world = ws if use_ep else 1
     ep_rank = rank if use_ep else 0
     seed_off = 0 if use_ep else rank  # replicas decode different streams; EP shards share one
+    # the reference's offline pipeline on this engine; each stage timed once,
+    # like the reference arm times its own (oracle/_ref/moesim_ref mode=bench)
+    pipe_ms = {}
+    tp = time.perf_counter()
     trace = eng.generate_trace(P.SynthConfig(spec, wl.tokens, wl.concentration, wl.drift, wl.gate_seed,
                                              wl.token_seed + seed_off, False, wl.fisher_scales, wl.drift_scales))
+    pipe_ms["generate_trace"], tp = (time.perf_counter() - tp) * 1e3, time.perf_counter()
     tau, realized = P.calibrate_threshold(spec, trace.scores, trace.fisher, wl.target_single_ratio)
+    pipe_ms["calibrate_threshold"], tp = (time.perf_counter() - tp) * 1e3, time.perf_counter()
     alpha, beta = eng.generate_profiles(trace.acts, trace.scores, trace.fisher, tau)
+    pipe_ms["generate_profiles"], tp = (time.perf_counter() - tp) * 1e3, time.perf_counter()
     caps, exp_loads = P.dp_allocate(spec, P.build_cost_table(spec, alpha, beta), wl.budget)
+    pipe_ms["cost_table_and_dp_allocate"] = (time.perf_counter() - tp) * 1e3
     # host RAM: all L*N experts pinned unless the node cannot hold them per replica
     expert_bytes = 3 * wl.ffn * wl.hidden * 2
     alias = 0
@@ -511,7 +519,17 @@ def ours(args):
                                         "kind": "reference",
                                         "sample": f"unmodified moesim simulate_trace over {r['tokens']} replayed tokens "
                                                   "(the reference has no free-running mode)"}
-            elif r is not None:
+            if r is not None and B == 1 and not args.free_running and "tau" in r:
+                ref_ms = {"generate_trace": r["generate_s"] * 1e3, "calibrate_threshold": r["calibrate_s"] * 1e3,
+                          "generate_profiles": r["profile_s"] * 1e3, "cost_table_and_dp_allocate": r["allocate_s"] * 1e3}
+                line["offline_pipeline"] = {
+                    "workload": f"{wl.name}, {wl.tokens}-token trace (first call of each stage, wall clock)",
+                    "ours_ms": pipe_ms, "reference_ms": ref_ms,
+                    # the stages' outputs equal the unmodified reference's, bit for bit
+                    "equal": {"tau": r["tau"] == tau, "alpha": r["alpha"] == [float(v) for v in alpha],
+                              "beta": r["beta"] == [float(v) for v in beta],
+                              "capacities": r["capacities"] == [int(c) for c in caps]}}
+            if r is not None and not args.free_running:
                 line["cpu_baseline"] = {"value": r["tokens"] / r["simulate_best_s"], "unit": "tok/s", "cores": 1,
                                         "kind": "reference",
                                         "sample": f"unmodified moesim simulate_trace over the same {r['tokens']} decoded "

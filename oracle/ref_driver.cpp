@@ -197,6 +197,11 @@ int main(int argc, char** argv) {
         const int reps = static_cast<int>(argi("reps", 1));
         SimulationInputs sub = in;
         sub.traces = std::span<const TokenTrace>(wl.traces.data(), std::min<size_t>(sample, wl.traces.size()));
+        std::vector<double> alphas, betas;
+        for (const LayerProfile& pr : profiles) {
+            alphas.push_back(pr.single_expert_prob);
+            betas.push_back(pr.prefetch_accuracy);
+        }
         double best = 1e30, total = 0;
         SimMetrics m{};
         size_t events = 0;
@@ -214,19 +219,22 @@ int main(int argc, char** argv) {
             "\"generate_s\": %.6f, \"calibrate_s\": %.6f, \"train_s\": %.6f, \"profile_s\": %.6f, "
             "\"allocate_s\": %.6f, \"on_demand_loads\": %lld, \"metrics\": {\"total_latency\": %lld, "
             "\"stall_time\": %lld, \"on_demand_loads\": %lld, \"cache_hits\": %lld, \"prefetch_hits\": %lld, "
-            "\"single_expert_decisions\": %lld, \"experts_activated_total\": %lld}, \"timeline_events\": %zu}\n",
+            "\"single_expert_decisions\": %lld, \"experts_activated_total\": %lld}, \"timeline_events\": %zu, "
+            "\"tau\": %s, \"alpha\": %s, \"beta\": %s, \"capacities\": %s, \"total_cost\": %s}\n",
             sub.traces.size(), reps, best, total / reps, secs(t0, t1), secs(t1, t2), secs(t2, t3), secs(t3, t4),
             secs(t4, t5), static_cast<long long>(m.on_demand_loads), static_cast<long long>(m.total_latency),
             static_cast<long long>(m.stall_time), static_cast<long long>(m.on_demand_loads),
             static_cast<long long>(m.cache_hits), static_cast<long long>(m.prefetch_hits),
             static_cast<long long>(m.single_expert_decisions), static_cast<long long>(m.experts_activated_total),
-            events);
+            events, Out::d(tau.tau).c_str(), Out::arr(alphas).c_str(), Out::arr(betas).c_str(),
+            Out::arr(alloc.allocation.capacities).c_str(), Out::d(alloc.total_cost).c_str());
         return 0;
     }
 
     // artifact files through the reference's own io (inc/io.hpp): write every kind into dir=...
     if (mode == "save") {
         const std::string dir = arg("dir", ".");
+        const auto s0 = clk::now();
         save_trace(dir + "/trace.jsonl", wl.traces, cfg.spec);
         GatesFile gf;
         gf.spec = cfg.spec;
@@ -238,14 +246,17 @@ int main(int argc, char** argv) {
         save_threshold(dir + "/threshold.json", ThresholdFile{tau.tau, target, 0.25});
         save_allocation(dir + "/allocation.json", AllocationFile{alloc.allocation, alloc.total_cost, profile_hash(pf)});
         save_cost_table(dir + "/cost_table.json", table);
-        std::printf("{\"profile_hash\": \"%s\"}\n", profile_hash(pf).c_str());
+        const double save_s = secs(s0, clk::now());
+        std::printf("{\"profile_hash\": \"%s\", \"save_s\": %.9f}\n", profile_hash(pf).c_str(), save_s);
         return 0;
     }
     // ... and read them back (dir=...), printing FNV-1a hashes of the arrays and the scalars
     if (mode == "load") {
         const std::string dir = arg("dir", ".");
         auto h = [](const void* p, size_t n, std::uint64_t v) { return fnv1a_bytes(p, n, v); };
+        const auto l0 = clk::now();
         TraceFile tf = load_trace(dir + "/trace.jsonl");
+        const double load_trace_s = secs(l0, clk::now());
         std::uint64_t ha = 0xcbf29ce484222325ull, hs = ha, hsel = ha;
         for (const auto& tr : tf.traces)
             for (const auto& st : tr.layers) {
@@ -274,11 +285,11 @@ int main(int argc, char** argv) {
             "\", \"hash_selected\": \"%016" PRIx64 "\", \"hash_gates\": \"%016" PRIx64 "\", \"hash_first_gate\": \"%016" PRIx64
             "\", \"first_gate_steps\": %d, \"alpha\": %s, \"beta\": %s, \"fisher\": %s, \"profile_hash\": \"%s\", "
             "\"tau\": %s, \"capacities\": %s, \"budget\": %d, \"total_cost\": %s, \"alloc_profile_hash\": \"%s\", "
-            "\"hash_cost_table\": \"%016" PRIx64 "\"}\n",
+            "\"hash_cost_table\": \"%016" PRIx64 "\", \"load_trace_s\": %.9f}\n",
             tf.traces.size(), ha, hs, hsel, hg, hfg, gf.first_layer_gate ? gf.first_layer_gate->config.steps : -1,
             Out::arr(alpha).c_str(), Out::arr(beta).c_str(), Out::arr(fisher).c_str(), profile_hash(pf).c_str(),
             Out::d(th.tau).c_str(), Out::arr(af.allocation.capacities).c_str(), af.allocation.budget,
-            Out::d(af.total_cost).c_str(), af.profile_hash.c_str(), hc);
+            Out::d(af.total_cost).c_str(), af.profile_hash.c_str(), hc, load_trace_s);
         return 0;
     }
 
@@ -286,8 +297,10 @@ int main(int argc, char** argv) {
     // the raw --budget is passed through)
     if (mode == "compare") {
         const int jobs = static_cast<int>(argi("jobs", 1));
+        const auto c0 = clk::now();
         ComparisonReport rep = compare_policies(in, sim, budget, sim_seed, jobs);
-        std::string r = "{\"rows\": [";
+        const double compare_s = secs(c0, clk::now());
+        std::string r = "{\"compare_s\": " + Out::d(compare_s) + ", \"jobs\": " + std::to_string(jobs) + ", \"rows\": [";
         for (size_t i = 0; i < rep.rows.size(); ++i) {
             const ComparisonRow& row = rep.rows[i];
             const SimMetrics& m = row.metrics;

@@ -38,6 +38,7 @@ def main():
         os.makedirs(d, exist_ok=True)
         saved = O.run_ref(mode="save", dir=d, **wl.ref_args())
         view = O.run_ref(mode="load", dir=d, **wl.ref_args())
+        view = {k: v for k, v in view.items() if not k.endswith("_s")}  # drop timings
         view["workload"] = wl.ref_args()
         view["saved_profile_hash"] = saved["profile_hash"]
         with open(os.path.join(d, "expected.json"), "w") as f:

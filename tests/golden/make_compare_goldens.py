@@ -34,6 +34,7 @@ def main():
     os.makedirs(out_dir, exist_ok=True)
     for name, wl in cases():
         r = O.run_ref(mode="compare", **wl.ref_args())
+        r = {k: v for k, v in r.items() if k not in ("compare_s", "jobs")}  # timing, not a golden
         r["workload"] = wl.ref_args()
         with open(os.path.join(out_dir, f"{name}.json"), "w") as f:
             json.dump(r, f, indent=0)

@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--trace-tokens", type=int, default=64)
     ap.add_argument("--staging", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="measure the offline pipeline + ablation grid + artifact files (SURVEY §8(f)) against the "
+                         "reference, one JSON line per workload, instead of the decode")
     ap.add_argument("--host-alias", type=int, default=None,
                     help="store only this many distinct experts in host memory (profiling runs; same bytes moved)")
     return ap.parse_args()
@@ -549,10 +552,112 @@ def ours(args):
     print(json.dumps(line))
 
 
+def run_reference_mode(wl, mode: str, **extra):
+    """The unmodified reference in another mode of oracle/_ref/moesim_ref (compare / save / load)."""
+    ref = os.path.join(ROOT, "oracle", "_ref", "moesim_ref")
+    if not os.path.exists(ref):
+        return None
+    args = [ref, f"mode={mode}"] + [f"{k}={v}" for k, v in {**wl.ref_args(), **extra}.items()]
+    return json.loads(subprocess.run(args, check=True, capture_output=True, text=True).stdout)
+
+
+def pipeline_bench(args):
+    """SURVEY §8(f) rows on this engine vs the unmodified reference, same workload, wall clock of each
+    stage's first call: generate_trace, calibrate_threshold, train_first_gate, generate_profiles,
+    cost table + DP, simulate_trace, the 7-row ablation grid (compare_policies) and the artifact files
+    (save / load of trace + gates + profiles + threshold + allocation + cost table)."""
+    import tempfile
+
+    import numpy as np
+
+    import paper_2408_10284_b200 as P
+    from paper_2408_10284_b200 import io as IO
+    from paper_2408_10284_b200 import workloads as Wk
+
+    ws, rank, local = dist_init()
+    if rank != 0:
+        return
+    cases = [Wk.tiny(), Wk.mixtral_8x7b(tokens=64), Wk.mixtral_8x7b(tokens=64, train_first_gate=True),
+             Wk.mixtral_8x7b(tokens=8, name="mixtral-8x7b-files")]
+    for wl in cases:
+        spec = P.ModelSpec(wl.layers, wl.experts, wl.top_k, wl.hidden)
+        cfg = P.SimConfig(wl.tiles, wl.tile_transfer, wl.tile_compute, wl.attention, wl.gate_time, wl.lookahead,
+                          P.PolicyFlags(wl.gating, wl.prefetch, True))
+        ms = {}
+        with P.Engine(spec, local) as eng:
+            t = time.perf_counter()
+            tr = eng.generate_trace(P.SynthConfig(spec, wl.tokens, wl.concentration, wl.drift, wl.gate_seed,
+                                                  wl.token_seed, False, wl.fisher_scales, wl.drift_scales))
+            ms["generate_trace"], t = (time.perf_counter() - t) * 1e3, time.perf_counter()
+            tau, realized = P.calibrate_threshold(spec, tr.scores, tr.fisher, wl.target_single_ratio)
+            ms["calibrate_threshold"], t = (time.perf_counter() - t) * 1e3, time.perf_counter()
+            fg = None
+            if wl.train_first_gate:
+                fg = eng.train_first_gate(tr.acts, tr.scores, wl.train_lr, wl.train_steps, wl.train_seed)
+                eng.load_gates(tr.gates, fg)
+                ms["train_first_gate"], t = (time.perf_counter() - t) * 1e3, time.perf_counter()
+            alpha, beta = eng.generate_profiles(tr.acts, tr.scores, tr.fisher, tau)
+            ms["generate_profiles"], t = (time.perf_counter() - t) * 1e3, time.perf_counter()
+            table = P.build_cost_table(spec, alpha, beta)
+            caps, total_cost = P.dp_allocate(spec, table, wl.budget)
+            ms["cost_table_and_dp_allocate"], t = (time.perf_counter() - t) * 1e3, time.perf_counter()
+            sim = eng.simulate_trace(tr.acts, tr.scores, tr.fisher, caps, tau, cfg, wl.seed)
+            ms["simulate_trace"], t = (time.perf_counter() - t) * 1e3, time.perf_counter()
+            rows = eng.compare_policies(tr.acts, tr.scores, tr.fisher, alpha, beta, tau, cfg, wl.budget, wl.seed)
+            ms["compare_policies"] = (time.perf_counter() - t) * 1e3
+            files = None
+            if wl.tokens <= 8 or wl.hidden <= 256:
+                with tempfile.TemporaryDirectory() as d:
+                    t = time.perf_counter()
+                    IO.save_trace(os.path.join(d, "trace.jsonl"), spec, tr.acts, tr.scores, tr.selected)
+                    IO.save_gates(os.path.join(d, "gates.json"), spec, tr.gates, fg, wl.train_lr, wl.train_steps,
+                                  wl.train_seed)
+                    ph = IO.save_profiles(os.path.join(d, "profiles.json"), spec, alpha, beta, tr.fisher)
+                    IO.save_threshold(os.path.join(d, "threshold.json"), tau, wl.target_single_ratio, realized)
+                    IO.save_allocation(os.path.join(d, "allocation.json"), caps, wl.budget, total_cost, ph)
+                    IO.save_cost_table(os.path.join(d, "cost_table.json"), table)
+                    save_ms, t = (time.perf_counter() - t) * 1e3, time.perf_counter()
+                    back = IO.load_trace(os.path.join(d, "trace.jsonl"))
+                    load_ms = (time.perf_counter() - t) * 1e3
+                    size = os.path.getsize(os.path.join(d, "trace.jsonl"))
+                    files = {"save_all_ms": save_ms, "load_trace_ms": load_ms, "trace_jsonl_bytes": size,
+                             "round_trip_equal": bool(np.array_equal(back.acts, tr.acts)
+                                                      and np.array_equal(back.scores, tr.scores))}
+        line = {"impl": "ours", "pipeline": wl.name, "tokens": wl.tokens, "ours_ms": ms}
+        r = run_reference_driver(wl, wl.tokens, 3)
+        if r is not None:
+            line["reference_ms"] = {"generate_trace": r["generate_s"] * 1e3, "calibrate_threshold": r["calibrate_s"] * 1e3,
+                                    "generate_profiles": r["profile_s"] * 1e3,
+                                    "cost_table_and_dp_allocate": r["allocate_s"] * 1e3,
+                                    "simulate_trace": r["simulate_best_s"] * 1e3}
+            if wl.train_first_gate:
+                line["reference_ms"]["train_first_gate"] = r["train_s"] * 1e3
+            c = run_reference_mode(wl, "compare")
+            line["reference_ms"]["compare_policies"] = c["compare_s"] * 1e3
+            line["equal"] = {"tau": r["tau"] == tau, "alpha": r["alpha"] == [float(v) for v in alpha],
+                             "beta": r["beta"] == [float(v) for v in beta],
+                             "capacities": r["capacities"] == [int(v) for v in caps],
+                             "simulate_metrics": r["metrics"] == sim.metrics,
+                             "compare_rows": [(x["metrics"], x["capacities"], x["speedup_vs_baseline"]) for x in rows]
+                             == [({k: v for k, v in y["metrics"].items()}, y["capacities"], y["speedup_vs_baseline"])
+                                 for y in c["rows"]]}
+            if files is not None:
+                with tempfile.TemporaryDirectory() as d:
+                    s_ = run_reference_mode(wl, "save", dir=d)
+                    l_ = run_reference_mode(wl, "load", dir=d)
+                files["reference_save_all_ms"] = s_["save_s"] * 1e3
+                files["reference_load_trace_ms"] = l_["load_trace_s"] * 1e3
+        if files is not None:
+            line["files"] = files
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         reference_arm(args)
+    elif args.pipeline:
+        pipeline_bench(args)
     else:
         ours(args)
 

@@ -4,7 +4,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <thread>
 #include <limits>
+#include <memory>
 #include <numeric>
 
 namespace adapmoe {
@@ -55,6 +57,75 @@ double SeededRng::normal() {
     cached_ = radius * std::sin(angle);
     has_cached_ = true;
     return radius * std::cos(angle);
+}
+
+void SeededRng::normals(double* out, size_t count) {
+    size_t i = 0;
+    if (count > 0 && has_cached_) {
+        has_cached_ = false;
+        out[i++] = cached_;
+    }
+    const size_t pairs = (count - i + 1) / 2;
+    if (pairs == 0) return;
+    constexpr double kTwoPi = 6.283185307179586476925286766559;
+    double spare = 0.0;
+    // pair p -> normals i + 2p (cos) and i + 2p + 1 (sin; the cached spare past the end)
+    auto emit = [&](size_t p, std::uint64_t w1, std::uint64_t w2) {
+        const double u1 = static_cast<double>(w1 >> 11) * 0x1.0p-53;
+        const double u2 = static_cast<double>(w2 >> 11) * 0x1.0p-53;
+        const double radius = std::sqrt(-2.0 * std::log(u1));
+        const double angle = kTwoPi * u2;
+        out[i + 2 * p] = radius * std::cos(angle);
+        if (i + 2 * p + 1 < count)
+            out[i + 2 * p + 1] = radius * std::sin(angle);
+        else
+            spare = radius * std::sin(angle);
+    };
+    // Raw words in normal()'s draw order (u1, u2 per pair) are drawn sequentially into one of two
+    // chunk buffers while host threads transform the other.  A u1 of exactly 0 (probability 2^-53
+    // per pair) is redrawn after u2 and shifts the stream: from such a chunk on, the pairs replay
+    // sequentially from the buffered words, then the engine.
+    constexpr size_t kChunk = size_t{1} << 19;  // pairs per chunk
+    const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+    std::unique_ptr<std::uint64_t[]> buf[2] = {std::unique_ptr<std::uint64_t[]>(new std::uint64_t[2 * std::min(kChunk, pairs)]),
+                                               std::unique_ptr<std::uint64_t[]>(new std::uint64_t[2 * std::min(kChunk, pairs)])};
+    size_t done = 0;
+    int cur = 0;
+    engine_.fill(buf[0].get(), 2 * std::min(kChunk, pairs));
+    while (done < pairs) {
+        const size_t n = std::min(kChunk, pairs - done);
+        const std::uint64_t* w = buf[cur].get();
+        bool redraw = false;
+        for (size_t p = 0; p < n && !redraw; ++p) redraw = (w[2 * p] >> 11) == 0;
+        if (redraw) {
+            size_t c = 0;
+            auto next = [&]() { return c < 2 * n ? w[c++] : engine_(); };
+            for (size_t p = done; p < pairs; ++p) {
+                std::uint64_t a = next();
+                const std::uint64_t b = next();
+                while ((a >> 11) == 0) a = next();
+                emit(p, a, b);
+            }
+            done = pairs;
+            break;
+        }
+        auto transform = [&, w, done](size_t p0, size_t p1) {
+            for (size_t p = p0; p < p1; ++p) emit(done + p, w[2 * p], w[2 * p + 1]);
+        };
+        const size_t n_threads = std::min<size_t>(std::min<size_t>(hw, 16), n / 16384 + 1);
+        std::vector<std::thread> pool;
+        for (size_t t = 1; t < n_threads; ++t) pool.emplace_back(transform, n * t / n_threads, n * (t + 1) / n_threads);
+        const size_t next_n = std::min(kChunk, pairs - done - n);
+        if (next_n) engine_.fill(buf[cur ^ 1].get(), 2 * next_n);  // overlaps the workers
+        transform(0, n / n_threads);
+        for (auto& th : pool) th.join();
+        done += n;
+        cur ^= 1;
+    }
+    if ((count - i) % 2 != 0) {
+        cached_ = spare;
+        has_cached_ = true;
+    }
 }
 
 int SeededRng::uniform_int(int n) {

@@ -15,6 +15,7 @@
 // the host versions of those rules below are used by the offline tools and the replay engine.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <random>
 #include <span>
@@ -90,17 +91,70 @@ struct SimConfig {
 };
 
 // ---- deterministic random source -----------------------------------------------------------
+// MT19937-64 with std::mt19937_64's parameters and seeding (the reference's engine,
+// inc/core.hpp:182), plus a bulk fill: the twist runs over the whole 312-word state and the
+// tempering over contiguous output, so long streams cost ~1 ns per word.
+class Mt64 {
+public:
+    explicit Mt64(std::uint64_t seed) {
+        mt_[0] = seed;
+        for (int i = 1; i < kN; ++i) mt_[i] = 6364136223846793005ull * (mt_[i - 1] ^ (mt_[i - 1] >> 62)) + i;
+        idx_ = kN;
+    }
+    std::uint64_t operator()() {
+        if (idx_ >= kN) twist();
+        return temper(mt_[idx_++]);
+    }
+    void fill(std::uint64_t* out, size_t n) {
+        while (n) {
+            if (idx_ >= kN) twist();
+            const size_t take = std::min<size_t>(n, kN - idx_);
+            for (size_t i = 0; i < take; ++i) out[i] = temper(mt_[idx_ + i]);
+            idx_ += static_cast<int>(take);
+            out += take;
+            n -= take;
+        }
+    }
+
+private:
+    static constexpr int kN = 312, kM = 156;
+    static constexpr std::uint64_t kA = 0xb5026f5aa96619e9ull, kUpper = ~0x7fffffffull, kLower = 0x7fffffffull;
+    static std::uint64_t temper(std::uint64_t x) {
+        x ^= (x >> 29) & 0x5555555555555555ull;
+        x ^= (x << 17) & 0x71d67fffeda60000ull;
+        x ^= (x << 37) & 0xfff7eee000000000ull;
+        return x ^ (x >> 43);
+    }
+    void twist() {
+        auto step = [&](int i, int j, int k) {
+            const std::uint64_t y = (mt_[i] & kUpper) | (mt_[j] & kLower);
+            mt_[i] = mt_[k] ^ (y >> 1) ^ ((y & 1) ? kA : 0);
+        };
+        int i = 0;
+        for (; i < kN - kM; ++i) step(i, i + 1, i + kM);
+        for (; i < kN - 1; ++i) step(i, i + 1, i + kM - kN);
+        step(kN - 1, 0, kM - 1);
+        idx_ = 0;
+    }
+    std::uint64_t mt_[kN];
+    int idx_;
+};
+
 class SeededRng {
 public:
     explicit SeededRng(std::uint64_t seed) : engine_(seed) {}
     std::uint64_t next_u64() { return engine_(); }
     double uniform01() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
     double normal();
+    // The next `count` normal() values, bit-identical to `count` sequential calls (spare included):
+    // the raw mt19937_64 draws stay sequential, the Box-Muller transforms (glibc log / sqrt / sin /
+    // cos, the cost) run on host threads.
+    void normals(double* out, size_t count);
     int uniform_int(int n);
     std::vector<int> sample_subset(int n, int t);
 
 private:
-    std::mt19937_64 engine_;
+    Mt64 engine_;
     double cached_ = 0.0;
     bool has_cached_ = false;
 };

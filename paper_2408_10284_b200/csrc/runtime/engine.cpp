@@ -7,8 +7,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <exception>
+#include <memory>
+#include <thread>
 
 #include "decode.hpp"
 #include "experts.hpp"
@@ -264,28 +270,64 @@ void Engine::generate_trace(int T, double conc, double drift, std::uint64_t gate
     const size_t gsz = static_cast<size_t>(D) * N;
     SeededRng grng(gate_seed);
     const double wscale = 1.0 / std::sqrt(static_cast<double>(D));
-    for (int l = 0; l < L; ++l) {
-        double* g = gates + l * gsz;
-        if (shared_gates && l > 0) {
-            std::memcpy(g, gates, gsz * sizeof(double));
-            continue;
+    // every normal of both streams is drawn in bulk (SeededRng::normals: sequential raw draws,
+    // threaded transforms), then consumed in the reference's order
+    // (the two streams are independent: the gate stream is drawn on its own thread)
+    const size_t gate_layers = shared_gates ? 1 : static_cast<size_t>(L);
+    std::exception_ptr gate_error;
+    std::thread gate_thread([&] {
+        try {
+            grng.normals(gates, gate_layers * gsz);
+            for (size_t i = 0; i < gate_layers * gsz; ++i) gates[i] = wscale * gates[i];
+            for (int l = 1; shared_gates && l < L; ++l) std::memcpy(gates + l * gsz, gates, gsz * sizeof(double));
+        } catch (...) {
+            gate_error = std::current_exception();
         }
-        for (size_t i = 0; i < gsz; ++i) g[i] = wscale * grng.normal();
+    });
+    int drift_layers = 0;
+    for (int l = 0; l < L; ++l) drift_layers += drift * (drift_scales ? drift_scales[l] : 1.0) > 0.0;
+    const size_t n_token_normals = static_cast<size_t>(T) * D * (1 + drift_layers);
+    std::unique_ptr<double[]> nrm;
+    std::exception_ptr token_error;
+    try {
+        nrm.reset(new double[n_token_normals]);  // no zero fill: every entry is drawn
+        SeededRng trng(token_seed);
+        trng.normals(nrm.get(), n_token_normals);
+    } catch (...) {
+        token_error = std::current_exception();
     }
-    SeededRng trng(token_seed);
-    std::vector<double> x(D);
-    for (int tok = 0; tok < T; ++tok) {
-        for (double& v : x) v = trng.normal();
-        for (int l = 0; l < L; ++l) {
-            std::memcpy(acts + (static_cast<size_t>(tok) * L + l) * D, x.data(), D * sizeof(double));
-            const double eps = drift * (drift_scales ? drift_scales[l] : 1.0);
-            if (eps > 0.0) {
-                double norm_sq = 0.0;
-                for (double v : x) norm_sq += v * v;
-                const double step = eps * std::sqrt(norm_sq / D);
-                for (double& v : x) v += step * trng.normal();
+    gate_thread.join();
+    if (gate_error) std::rethrow_exception(gate_error);
+    if (token_error) std::rethrow_exception(token_error);
+    // every token restarts its walk from fresh normals, so given each token's offset in the stream
+    // (D * (1 + drift layers) normals per token) the walks run in parallel
+    const size_t per_token = static_cast<size_t>(D) * (1 + drift_layers);
+    auto walk = [&](int t0, int t1) {
+        std::vector<double> x(D);
+        for (int tok = t0; tok < t1; ++tok) {
+            const double* nv = nrm.get() + static_cast<size_t>(tok) * per_token;
+            for (double& v : x) v = *nv++;
+            for (int l = 0; l < L; ++l) {
+                std::memcpy(acts + (static_cast<size_t>(tok) * L + l) * D, x.data(), D * sizeof(double));
+                const double eps = drift * (drift_scales ? drift_scales[l] : 1.0);
+                if (eps > 0.0) {
+                    double norm_sq = 0.0;
+                    for (double v : x) norm_sq += v * v;
+                    const double step = eps * std::sqrt(norm_sq / D);
+                    for (double& v : x) v += step * *nv++;
+                }
             }
         }
+    };
+    const int n_walkers = static_cast<int>(std::min<size_t>(
+        {static_cast<size_t>(std::max(1u, std::thread::hardware_concurrency())), 16, static_cast<size_t>(T),
+         n_token_normals / 65536 + 1}));
+    if (n_walkers <= 1) {
+        walk(0, T);
+    } else {
+        std::vector<std::thread> pool;
+        for (int w = 0; w < n_walkers; ++w) pool.emplace_back(walk, T * w / n_walkers, T * (w + 1) / n_walkers);
+        for (auto& th : pool) th.join();
     }
     load_gates(gates, nullptr);
     const size_t TL = static_cast<size_t>(T) * L;

@@ -5,13 +5,17 @@
 #include "files.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <charconv>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <fstream>
 #include <map>
 #include <sstream>
+#include <string_view>
+#include <thread>
 
 namespace adapmoe {
 
@@ -225,7 +229,7 @@ private:
     std::string where_;
 };
 
-JVal parse_text(const std::string& text, const std::string& where) {
+JVal parse_text(std::string_view text, const std::string& where) {
     return Parser(text.data(), text.data() + text.size(), where).parse_document();
 }
 
@@ -713,44 +717,91 @@ TraceData load_trace_file(const std::string& path) {
     check_header(head, "trace", path);
     t.spec = spec_from(head, path);
     const int L = t.spec.num_layers, N = t.spec.experts_per_layer, K = t.spec.top_k, D = t.spec.hidden_dim;
-    while (next_line(line)) {
-        if (line.empty()) continue;
-        const std::string where = path + ":" + std::to_string(line_no);
-        const JVal j = parse_text(line, where);
-        const int tok = static_cast<int>(req_int(j, "token", where));
-        const JVal* layers = j.get("layers");
-        if (!layers || layers->t != JVal::Arr) schema_fail(where, "missing layers array");
-        t.token_index.push_back(tok);
-        const int nl = static_cast<int>(layers->size());
-        if (nl != L)
-            t.shape_violations.push_back("token " + std::to_string(tok) + ": expected " + std::to_string(L) +
-                                         " layers, got " + std::to_string(nl));
-        for (int l = 0; l < L; ++l) {
-            std::vector<double> act, sc;
-            std::vector<int> sel;
-            if (l < nl) {
-                const JVal& jl = layers->a[l];
-                act = req_doubles(jl, "activation", where);
-                sc = req_doubles(jl, "scores", where);
-                sel = req_ints(jl, "selected", where);
-                if (static_cast<int>(act.size()) != D)
-                    t.shape_violations.push_back("token " + std::to_string(tok) + " layer " + std::to_string(l) +
-                                                 ": activation dim " + std::to_string(act.size()) + " != " +
-                                                 std::to_string(D));
-                if (static_cast<int>(sc.size()) != N)
-                    t.shape_violations.push_back("token " + std::to_string(tok) + " layer " + std::to_string(l) +
-                                                 ": score vector length mismatch");
+    // token lines parse independently on host threads; results (and the first error, in line
+    // order) are assembled sequentially, as a one-pass reader would report them
+    struct Span {
+        size_t pos, len;
+        int line_no;
+    };
+    std::vector<Span> spans;
+    while (pos < text.size()) {
+        size_t e = text.find('\n', pos);
+        if (e == std::string::npos) e = text.size();
+        ++line_no;
+        if (e > pos) spans.push_back(Span{pos, e - pos, line_no});
+        pos = e + 1;
+    }
+    struct Parsed {
+        int tok = 0;
+        std::vector<double> act, sc;
+        std::vector<int> cnt, sel;
+        std::vector<std::string> violations;
+        std::exception_ptr error;
+    };
+    std::vector<Parsed> parsed(spans.size());
+    auto parse_line = [&](size_t q) {
+        Parsed& r = parsed[q];
+        try {
+            const std::string where = path + ":" + std::to_string(spans[q].line_no);
+            const JVal j = parse_text(std::string_view(text.data() + spans[q].pos, spans[q].len), where);
+            const int tok = static_cast<int>(req_int(j, "token", where));
+            const JVal* layers = j.get("layers");
+            if (!layers || layers->t != JVal::Arr) schema_fail(where, "missing layers array");
+            r.tok = tok;
+            const int nl = static_cast<int>(layers->size());
+            if (nl != L)
+                r.violations.push_back("token " + std::to_string(tok) + ": expected " + std::to_string(L) +
+                                       " layers, got " + std::to_string(nl));
+            r.act.reserve(static_cast<size_t>(L) * D);
+            r.sc.reserve(static_cast<size_t>(L) * N);
+            for (int l = 0; l < L; ++l) {
+                std::vector<double> act, sc;
+                std::vector<int> sel;
+                if (l < nl) {
+                    const JVal& jl = layers->a[l];
+                    act = req_doubles(jl, "activation", where);
+                    sc = req_doubles(jl, "scores", where);
+                    sel = req_ints(jl, "selected", where);
+                    if (static_cast<int>(act.size()) != D)
+                        r.violations.push_back("token " + std::to_string(tok) + " layer " + std::to_string(l) +
+                                               ": activation dim " + std::to_string(act.size()) + " != " +
+                                               std::to_string(D));
+                    if (static_cast<int>(sc.size()) != N)
+                        r.violations.push_back("token " + std::to_string(tok) + " layer " + std::to_string(l) +
+                                               ": score vector length mismatch");
+                }
+                act.resize(D, 0.0);
+                sc.resize(N, 0.0);
+                r.act.insert(r.act.end(), act.begin(), act.end());
+                r.sc.insert(r.sc.end(), sc.begin(), sc.end());
+                r.cnt.push_back(static_cast<int>(sel.size()));
+                for (int k = 0; k < K; ++k) r.sel.push_back(k < static_cast<int>(sel.size()) ? sel[k] : -1);
+                if (static_cast<int>(sel.size()) > K)
+                    r.violations.push_back("token " + std::to_string(tok) + " layer " + std::to_string(l) +
+                                           ": selected count " + std::to_string(sel.size()));
             }
-            act.resize(D, 0.0);
-            sc.resize(N, 0.0);
-            t.activations.insert(t.activations.end(), act.begin(), act.end());
-            t.scores.insert(t.scores.end(), sc.begin(), sc.end());
-            t.selected_count.push_back(static_cast<int>(sel.size()));
-            for (int k = 0; k < K; ++k) t.selected.push_back(k < static_cast<int>(sel.size()) ? sel[k] : -1);
-            if (static_cast<int>(sel.size()) > K)
-                t.shape_violations.push_back("token " + std::to_string(tok) + " layer " + std::to_string(l) +
-                                             ": selected count " + std::to_string(sel.size()));
+        } catch (...) {
+            r.error = std::current_exception();
         }
+    };
+    const int n_threads = std::max(1, std::min({static_cast<int>(std::thread::hardware_concurrency()), 16,
+                                                static_cast<int>(spans.size())}));
+    std::atomic<size_t> next{0};
+    auto worker = [&] {
+        for (size_t q; (q = next.fetch_add(1)) < spans.size();) parse_line(q);
+    };
+    std::vector<std::thread> pool;
+    for (int w = 1; w < n_threads; ++w) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+    for (const Parsed& r : parsed) {
+        if (r.error) std::rethrow_exception(r.error);
+        t.token_index.push_back(r.tok);
+        t.shape_violations.insert(t.shape_violations.end(), r.violations.begin(), r.violations.end());
+        t.activations.insert(t.activations.end(), r.act.begin(), r.act.end());
+        t.scores.insert(t.scores.end(), r.sc.begin(), r.sc.end());
+        t.selected_count.insert(t.selected_count.end(), r.cnt.begin(), r.cnt.end());
+        t.selected.insert(t.selected.end(), r.sel.begin(), r.sel.end());
     }
     t.tokens = static_cast<int>(t.token_index.size());
     return t;
@@ -760,8 +811,9 @@ void save_trace_jsonl(const std::string& path, const TraceData& t) {
     const int L = t.spec.num_layers, N = t.spec.experts_per_layer, K = t.spec.top_k, D = t.spec.hidden_dim;
     JVal h = header("trace");
     h.o["model"] = spec_json(t.spec);
-    std::string out = dumps(h) + "\n";
-    for (int tok = 0; tok < t.tokens; ++tok) {
+    // one line per token: lines are formatted independently on host threads, written in order
+    std::vector<std::string> lines(t.tokens);
+    auto format = [&](int tok) {
         JVal j = obj();
         j.o["token"] = inum(t.token_index.empty() ? tok : t.token_index[tok]);
         JVal layers = arr();
@@ -777,8 +829,29 @@ void save_trace_jsonl(const std::string& path, const TraceData& t) {
             layers.a.push_back(std::move(jl));
         }
         j.o["layers"] = std::move(layers);
-        out += dumps(j) + "\n";
-    }
+        lines[tok] = dumps(j) + "\n";
+    };
+    const int n_threads = std::max(1, std::min({static_cast<int>(std::thread::hardware_concurrency()), 16, t.tokens}));
+    std::atomic<int> next{0};
+    std::vector<std::exception_ptr> errors(n_threads);
+    auto worker = [&](int w) {
+        try {
+            for (int tok; (tok = next.fetch_add(1)) < t.tokens;) format(tok);
+        } catch (...) {
+            errors[w] = std::current_exception();
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int w = 1; w < n_threads; ++w) pool.emplace_back(worker, w);
+    worker(0);
+    for (auto& th : pool) th.join();
+    for (auto& e : errors)
+        if (e) std::rethrow_exception(e);
+    size_t total = 0;
+    for (const auto& l : lines) total += l.size();
+    std::string out = dumps(h) + "\n";
+    out.reserve(out.size() + total);
+    for (const auto& l : lines) out += l;
     write_file(path, out);
 }
 

@@ -161,3 +161,37 @@ def test_decode_mixtral_width_layers():
     for (t, l), m in moe.items():
         got = hid[t, l].astype(np.float64) - w.acts[t, l].astype(np.float32).astype(np.float64)
         assert _rel_err(got, m) < REL_TOL, (t, l)
+
+
+@pytest.mark.parametrize("name", ["tiny_budget0", "tiny_transfer_heavy", "tiny"])
+def test_slot_reuse_ordering_every_output(name):
+    """Slot recycling under host run-ahead, at the tightest feasible staging pool: every on-demand /
+    prefetch copy reuses a slot that an earlier, possibly still enqueued, layer read.  Slots return to
+    the pool only after that layer's completion event, so every (token, layer) output must equal the
+    oracle's.  Smaller pools fail loudly (MOE_E_INFEASIBLE, "slot pool exhausted")."""
+    g = load_golden(name)
+    w, fg = oracle_inputs(g)
+    cfg = sim_config(g)
+    ffn, seed, T = 224 * cfg.tile_count_per_expert, 9, 24
+    for staging in range(1, 33):
+        with P.Engine(P.ModelSpec(w.L, w.N, w.K, w.D)) as eng:
+            eng.load_gates(w.gates, fg)
+            eng.experts_init(ffn, cfg.tile_count_per_expert, seed=seed)
+            eng.decode_begin(g["sim_capacities"], w.fisher, g["tau"], cfg, int(g["workload"]["seed"]), T, staging)
+            hid = np.zeros((T, w.L, w.D), dtype=np.float32)
+            try:
+                eng.decode_tokens(w.acts[:T], w.scores[:T], hid)
+            except P.MoeError as e:
+                assert e.code == 5 and "exhausted" in str(e), e
+                continue
+            r = eng.decode_end(cfg, T)
+            break
+    else:
+        pytest.fail("no feasible staging pool up to 32 slots")
+    sim = O.simulate(w, g["sim_capacities"], g["tau"], first_gate=fg, T=T,
+                     **{k: v for k, v in __import__("helpers").sim_kwargs(g).items()})
+    assert r.metrics == sim.metrics
+    ref = _moe_reference(w, fg, sim.decisions, T, ffn, cfg.tile_count_per_expert, seed)
+    for (t, l), moe in ref.items():
+        got = hid[t, l].astype(np.float64) - w.acts[t, l].astype(np.float32).astype(np.float64)
+        assert _rel_err(got, moe) < REL_TOL, (t, l, staging)

@@ -106,6 +106,8 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     }
     // trace replay: one K1 launch routes up to route_window_ tokens (every layer and stream)
     route_window_ = free_running_ ? 1 : std::max(1, std::min(total_tokens, (1 << 20) / (4 * batch_ * L)));
+    if (const char* v = std::getenv("ADAPMOE_ROUTE_WINDOW"))  // test knob: force several windows per call
+        route_window_ = std::max(1, std::min(route_window_, std::atoi(v)));
     const size_t route_rows = static_cast<size_t>(4) * batch_ * (free_running_ ? 1 : static_cast<size_t>(L) * route_window_);
     MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_route_), route_rows * (K + 3) * sizeof(int),
                            cudaHostAllocMapped));

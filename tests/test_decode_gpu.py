@@ -195,3 +195,31 @@ def test_slot_reuse_ordering_every_output(name):
     for (t, l), moe in ref.items():
         got = hid[t, l].astype(np.float64) - w.acts[t, l].astype(np.float32).astype(np.float64)
         assert _rel_err(got, moe) < REL_TOL, (t, l, staging)
+
+
+def _decode_outputs(g, T, cuts, batch=1):
+    w, fg = oracle_inputs(g)
+    cfg = sim_config(g)
+    with P.Engine(P.ModelSpec(w.L, w.N, w.K, w.D)) as eng:
+        eng.load_gates(w.gates, fg)
+        eng.experts_init(224 * cfg.tile_count_per_expert, cfg.tile_count_per_expert, seed=4)
+        eng.decode_begin(g["sim_capacities"], w.fisher, g["tau"], cfg, int(g["workload"]["seed"]), T)
+        hid = np.zeros((T, w.L, w.D), dtype=np.float32)
+        for a, b in zip(cuts, cuts[1:]):
+            eng.decode_tokens(w.acts[a:b], w.scores[a:b], hid[a:b])
+        r = eng.decode_end(cfg, T)
+    return hid, r
+
+
+@pytest.mark.parametrize("window", ["1", "3", "7"])
+def test_route_windows_bit_identical(window, monkeypatch):
+    """Trace replay routes a window of tokens per K1 launch (the whole call at bench sizes).  Forcing
+    several windows per call (ADAPMOE_ROUTE_WINDOW) must not change a bit of the outputs or trace."""
+    g = load_golden("tiny_transfer_heavy")
+    T, cuts = 20, [0, 9, 20]
+    ref_hid, ref = _decode_outputs(g, T, cuts)
+    monkeypatch.setenv("ADAPMOE_ROUTE_WINDOW", window)
+    hid, r = _decode_outputs(g, T, cuts)
+    assert r.metrics == ref.metrics and np.array_equal(r.timeline, ref.timeline)
+    assert np.array_equal(hid, ref_hid)
+    assert r.stats["router_launches"] == sum(-(-(b - a) // int(window)) for a, b in zip(cuts, cuts[1:]))

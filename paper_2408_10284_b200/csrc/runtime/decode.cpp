@@ -74,6 +74,7 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     slot_of_.assign(static_cast<size_t>(L) * N, -1);
     cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, eng.device());
     if (const char* v = std::getenv("ADAPMOE_K2_L2")) l2_mode_ = std::atoi(v);  // profiling knob
+    if (const char* v = std::getenv("ADAPMOE_TILE_MERGE")) tile_merge_ = std::atoi(v) != 0 ? 1 : 0;  // A/B knob
 
     // at most one launch for the resident experts' tiles (split per 32 segments) + one per
     // on-demand tile
@@ -414,6 +415,46 @@ void DecodeSession::on_layer_done(int, int, const RouteDecision& d) {
     ++layer_seq_;
 }
 
+// Launch groups for the layer's on-demand (missing) experts, in landing order.  The host link is
+// ~100x slower than HBM, so a tile's FFN finishes long before the next tile lands: an expert that is
+// not the layer's last to land computes all its tiles in one launch once its last tile has landed
+// (the link is still busy with the later experts, so this costs nothing on the critical path), and
+// the last expert computes tiles 0..n-2 together and its final tile alone — the work left after the
+// layer's final tile lands stays one tile's.  The layer's resident experts join the first group that
+// is not the final tile (merge_resident()).  Merging pays only when a tile's transfer dwarfs a launch:
+// on by default for tiles >= 8 MiB (88 MB at 8x7B: 1.6 ms on PCIe Gen5 vs ~25 us of K2);
+// ADAPMOE_TILE_MERGE=0 / 1 forces it off / on.
+bool DecodeSession::tile_merge_active() const {
+    return tile_merge_ > 0 || (tile_merge_ < 0 && store_.tile_bytes >= (size_t{8} << 20));
+}
+
+bool DecodeSession::merge_resident() const {
+    if (!tile_merge_active()) return false;
+    int groups = 0;
+    for (const Use& u : uses_)
+        if (u.missing && !u.tiles.empty()) groups += u.tiles.size() > 1 ? 2 : 1;
+    return groups >= 2;  // some on-demand group lands before the layer's final tile
+}
+
+std::vector<std::pair<const DecodeSession::Use*, std::vector<int>>> DecodeSession::tile_groups() const {
+    std::vector<std::pair<const Use*, std::vector<int>>> groups;
+    std::vector<const Use*> missing;
+    for (const Use& u : uses_)
+        if (u.missing && !u.tiles.empty()) missing.push_back(&u);
+    for (size_t m = 0; m < missing.size(); ++m) {
+        const std::vector<int>& tiles = missing[m]->tiles;
+        if (!tile_merge_active()) {
+            for (int t : tiles) groups.emplace_back(missing[m], std::vector<int>{t});
+        } else if (m + 1 < missing.size() || tiles.size() == 1) {
+            groups.emplace_back(missing[m], tiles);
+        } else {
+            groups.emplace_back(missing[m], std::vector<int>(tiles.begin(), tiles.end() - 1));
+            groups.emplace_back(missing[m], std::vector<int>{tiles.back()});
+        }
+    }
+    return groups;
+}
+
 void DecodeSession::layer_ffn_single(const RouteDecision& d) {
     const int D = spec_.hidden_dim, T = store_.tiles, F = store_.ffn, Ft = F / T;
     const size_t gate_up_bytes = static_cast<size_t>(2) * Ft * D * 2;
@@ -445,18 +486,26 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
         }
         stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
     }
-    if (p.n_seg) timed_ffn(p, meta, refs);
-    meta.clear();
-    // on-demand experts: tile by tile as their copies land
-    for (const Use& u : uses_) {
-        if (!u.missing) continue;
-        for (int t : u.tiles) {
+    const auto groups = tile_groups();
+    // resident segments ride with the first on-demand group when that group is off the critical
+    // path and the launch stays within kMaxFfnSegments
+    const bool hold = p.n_seg > 0 && merge_resident() &&
+                      p.n_seg + static_cast<int>(groups.front().second.size()) <= kMaxFfnSegments;
+    if (p.n_seg && !hold) {
+        timed_ffn(p, meta, refs);
+        meta.clear();
+    }
+    // on-demand experts, as their tiles land (tile_groups: merged launches off the critical path)
+    for (const auto& grp : groups) {
+        const Use& u = *grp.first;
+        for (int t : grp.second) {
             wait_fill(u.slot, t);
             p.seg[p.n_seg++] = seg(u.slot, t);
-            meta.assign(1, {u.rank, t});
-            timed_ffn(p, meta, refs);
+            meta.emplace_back(u.rank, t);
         }
-        stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
+        timed_ffn(p, meta, refs);
+        meta.clear();
+        if (grp.second.back() == u.tiles.back()) stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
     }
     std::sort(refs.begin(), refs.end(), [](const auto& a, const auto& b) {
         return std::get<0>(a) != std::get<0>(b) ? std::get<0>(a) < std::get<0>(b) : std::get<1>(a) < std::get<1>(b);
@@ -550,7 +599,8 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
     // launch list: resident experts together (all tiles), on-demand experts tile by tile
     struct Job {
         std::vector<GSeg> segs;
-        int wait_slot = -1, wait_tile = 0;
+        int wait_slot = -1;
+        std::vector<int> wait_tiles;
     };
     std::vector<Job> jobs;
     Job res;
@@ -561,17 +611,24 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
             stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
         }
     if (!res.segs.empty()) jobs.push_back(res);
-    for (const Use& us : uses_)
-        if (us.missing) {
-            for (int t : us.tiles) {
-                Job j;
-                j.segs.push_back(GSeg{us.rank, t, t + 1});
-                j.wait_slot = us.slot;
-                j.wait_tile = t;
-                jobs.push_back(j);
-            }
-            stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
+    for (const auto& grp : tile_groups()) {  // on-demand experts, merged off the critical path
+        const Use& us = *grp.first;
+        Job j;
+        j.wait_slot = us.slot;
+        j.wait_tiles = grp.second;
+        for (size_t q = 0; q < grp.second.size();) {  // contiguous tile runs -> one segment each
+            size_t e = q + 1;
+            while (e < grp.second.size() && grp.second[e] == grp.second[e - 1] + 1) ++e;
+            j.segs.push_back(GSeg{us.rank, grp.second[q], grp.second[e - 1] + 1});
+            q = e;
         }
+        jobs.push_back(j);
+        if (grp.second.back() == us.tiles.back()) stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
+    }
+    if (!res.segs.empty() && jobs.size() >= 3 && merge_resident()) {  // resident + >= 2 on-demand groups
+        jobs[1].segs.insert(jobs[1].segs.begin(), jobs[0].segs.begin(), jobs[0].segs.end());
+        jobs.erase(jobs.begin());
+    }
     // plan every down launch first: the partial arena must hold the whole layer
     std::vector<GroupedLaunch> downs(jobs.size(), base);
     size_t need = 0;
@@ -590,7 +647,7 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
     size_t off = 0;
     std::vector<std::pair<int, GCombineRef>> refs;  // (rank, ref) in launch order
     for (size_t i = 0; i < jobs.size(); ++i) {
-        if (jobs[i].wait_slot >= 0) wait_fill(jobs[i].wait_slot, jobs[i].wait_tile);
+        for (int t : jobs[i].wait_tiles) wait_fill(jobs[i].wait_slot, t);
         GroupedLaunch up = base;
         up.n_seg = downs[i].n_seg;
         for (int s = 0; s < up.n_seg; ++s) up.seg[s] = downs[i].seg[s];

@@ -98,6 +98,10 @@ private:
     void timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int>>& seg_meta,
                    std::vector<std::tuple<int, int, FfnPartialRef>>& refs);
     void layer_ffn_single(const RouteDecision& d);   // batch 1: K2 row kernel
+    std::vector<std::pair<const Use*, std::vector<int>>> tile_groups() const;
+    bool tile_merge_active() const;
+    bool merge_resident() const;
+    int tile_merge_ = -1;  // -1 auto (tiles >= 8 MiB), 0 off, 1 on
     void layer_ffn_grouped(const RouteDecision& d);  // batch > 1: K3 grouped tcgen05 kernels
     void timed_grouped(GroupedLaunch& p, bool down);
     // free-running decode: layer l > 0 routes and computes on layer l-1's output (the hidden state

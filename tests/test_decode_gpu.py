@@ -223,3 +223,30 @@ def test_route_windows_bit_identical(window, monkeypatch):
     assert r.metrics == ref.metrics and np.array_equal(r.timeline, ref.timeline)
     assert np.array_equal(hid, ref_hid)
     assert r.stats["router_launches"] == sum(-(-(b - a) // int(window)) for a, b in zip(cuts, cuts[1:]))
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny_transfer_heavy", "tiny_budget0", "tiny_prefetch_off"])
+def test_tile_merge_every_output(name, monkeypatch):
+    """ADAPMOE_TILE_MERGE=1 (the default for >= 8 MiB tiles): an on-demand expert's tiles share one
+    K2 launch once landed, the layer's last expert keeps its final tile alone, resident experts ride
+    with the first on-demand group.  The trace is untouched and every output matches the oracle."""
+    monkeypatch.setenv("ADAPMOE_TILE_MERGE", "1")
+    g = load_golden(name)
+    w, fg = oracle_inputs(g)
+    cfg = sim_config(g)
+    ffn, seed, T = 224 * cfg.tile_count_per_expert, 13, 24
+    with P.Engine(P.ModelSpec(w.L, w.N, w.K, w.D)) as eng:
+        eng.load_gates(w.gates, fg)
+        eng.experts_init(ffn, cfg.tile_count_per_expert, seed=seed)
+        eng.decode_begin(g["sim_capacities"], w.fisher, g["tau"], cfg, int(g["workload"]["seed"]), T)
+        hid = np.zeros((T, w.L, w.D), dtype=np.float32)
+        eng.decode_tokens(w.acts[:T], w.scores[:T], hid)
+        r = eng.decode_end(cfg, T)
+    sim = O.simulate(w, g["sim_capacities"], g["tau"], first_gate=fg, T=T,
+                     **{k: v for k, v in __import__("helpers").sim_kwargs(g).items()})
+    assert r.metrics == sim.metrics and np.array_equal(r.timeline, sim.timeline)
+    assert r.stats["ffn_bytes"] == r.metrics["experts_activated_total"] * 3 * ffn * w.D * 2
+    ref = _moe_reference(w, fg, sim.decisions, T, ffn, cfg.tile_count_per_expert, seed)
+    for (t, l), moe in ref.items():
+        got = hid[t, l].astype(np.float64) - w.acts[t, l].astype(np.float32).astype(np.float64)
+        assert _rel_err(got, moe) < REL_TOL, (t, l)

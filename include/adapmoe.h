@@ -258,6 +258,16 @@ int moe_train_first_gate(moe_engine_t engine, const double* acts, const double* 
  * (l, e) -> (l*N + e) % host_alias (for hosts without L*N*expert_bytes of RAM); 0 = all distinct. */
 int moe_experts_init(moe_engine_t engine, int32_t ffn_dim, int32_t tiles, uint64_t seed, int32_t host_alias);
 
+/* Real weights instead of the synthetic init (SURVEY §8(b) moe_load_experts): allocate the pinned
+ * store (all L*N experts, zero), then hand every expert's weights over in the usual checkpoint
+ * layout — bf16 bit patterns, row-major: w1 = gate_proj.weight [ffn][d], w3 = up_proj.weight
+ * [ffn][d], w2 = down_proj.weight [d][ffn] — which moe_expert_set packs into the tile-major store
+ * (W1/W3 row pairs, W2 transposed; host threads).  Errors: MOE_E_USAGE for an out-of-range expert
+ * or while a decode session is active (its HBM slots hold copies of the store). */
+int moe_experts_alloc(moe_engine_t engine, int32_t ffn_dim, int32_t tiles);
+int moe_expert_set(moe_engine_t engine, int32_t layer, int32_t expert, const uint16_t* w1, const uint16_t* w3,
+                   const uint16_t* w2);
+
 /* Bytes of one expert (3 * F * d * 2) in the store. */
 int moe_expert_bytes(moe_engine_t engine, int64_t* bytes);
 

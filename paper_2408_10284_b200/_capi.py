@@ -105,6 +105,8 @@ SIGNATURES = {
     "moe_experts_init": (C.c_int, [_eng, C.c_int32, C.c_int32, C.c_uint64, C.c_int32]),
     "moe_expert_bytes": (C.c_int, [_eng, _i64]),
     "moe_expert_read": (C.c_int, [_eng, C.c_int32, C.c_int32, _u16]),
+    "moe_experts_alloc": (C.c_int, [_eng, C.c_int32, C.c_int32]),
+    "moe_expert_set": (C.c_int, [_eng, C.c_int32, C.c_int32, _u16, _u16, _u16]),
     "moe_trace_load": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
     "moe_trace_info": (C.c_int, [C.c_void_p, C.POINTER(ModelSpecC), _i32]),
     "moe_trace_read": (C.c_int, [C.c_void_p, _d, _d, _i32]),

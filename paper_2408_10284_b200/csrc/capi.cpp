@@ -466,6 +466,33 @@ int moe_experts_init(moe_engine_t h, int32_t ffn, int32_t tiles, uint64_t seed, 
     });
 }
 
+int moe_experts_alloc(moe_engine_t h, int32_t ffn, int32_t tiles) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        e.session.reset();
+        e.experts = std::make_unique<ExpertStore>();
+        try {
+            build_expert_store(e, *e.experts, ffn, tiles, 0, 0, false);
+        } catch (...) {
+            e.experts.reset();
+            throw;
+        }
+    });
+}
+
+int moe_expert_set(moe_engine_t h, int32_t layer, int32_t expert, const uint16_t* w1, const uint16_t* w3,
+                   const uint16_t* w2) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(w1, "w1");
+        require(w3, "w3");
+        require(w2, "w2");
+        if (!e.experts) fail(Status::Usage, "expert_set: call moe_experts_alloc (or moe_experts_init) first");
+        if (e.session) fail(Status::Usage, "expert_set: a decode session is active (its HBM slots hold copies)");
+        set_expert_weights(*e.experts, layer, expert, w1, w3, w2);
+    });
+}
+
 int moe_expert_bytes(moe_engine_t h, int64_t* bytes) {
     return guarded([&] {
         Engine& e = eng(h);

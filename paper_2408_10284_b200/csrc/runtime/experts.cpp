@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <sys/mman.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -37,7 +38,8 @@ void expert_init_constants(std::uint64_t seed, int layer, int expert, int d, int
     scale[2] = static_cast<float>(1.0 / (37837.22 * std::sqrt(static_cast<double>(ffn))));
 }
 
-void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::uint64_t seed, int alias) {
+void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::uint64_t seed, int alias,
+                        bool init_values) {
     const ModelSpec& spec = eng.spec();
     if (ffn <= 0 || tiles < 1 || ffn % tiles) fail(Status::Usage, "experts_init: ffn must be a positive multiple of tiles");
     const int ft = ffn / tiles;
@@ -87,7 +89,7 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
         if (!e.empty()) fail(Status::Device, "experts_init: " + e);
     auto t1 = std::chrono::steady_clock::now();
     st.pin_seconds = std::chrono::duration<double>(t1 - t0).count();
-
+    if (!init_values) return;
     // fill: GPU init kernel into two device scratch blocks, D2H into the pinned store
     DeviceBuffer scratch[2];
     cudaStream_t s[2];
@@ -112,6 +114,36 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
         cudaEventDestroy(copied[k]);
     }
     st.fill_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+}
+
+void set_expert_weights(ExpertStore& st, int layer, int expert, const std::uint16_t* w1, const std::uint16_t* w3,
+                        const std::uint16_t* w2) {
+    if (layer < 0 || layer >= st.layers || expert < 0 || expert >= st.experts) fail(Status::Usage, "ExpertRef out of range");
+    if (st.alias > 0) fail(Status::Usage, "expert_set: the store aliases experts (host_alias); allocate it without");
+    const size_t D = st.d, F = st.ffn, Ft = F / st.tiles;
+    std::uint16_t* dst = reinterpret_cast<std::uint16_t*>(st.blocks[st.stored_index(layer, expert)]);
+    const size_t tile_elems = 3 * Ft * D;
+    auto pack_rows = [&](size_t f0, size_t f1) {
+        constexpr size_t kB = 64;  // W2 transposed in kB x kB blocks (both sides cache friendly)
+        for (size_t f = f0; f < f1; ++f) {
+            const size_t t = f / Ft, r = f % Ft;
+            std::uint16_t* gu = dst + t * tile_elems + r * 2 * D;
+            std::memcpy(gu, w1 + f * D, D * 2);
+            std::memcpy(gu + D, w3 + f * D, D * 2);
+        }
+        for (size_t fb = f0; fb < f1; fb += kB)
+            for (size_t jb = 0; jb < D; jb += kB)
+                for (size_t f = fb; f < std::min(f1, fb + kB); ++f) {
+                    std::uint16_t* row = dst + (f / Ft) * tile_elems + 2 * Ft * D + (f % Ft) * D;
+                    for (size_t j = jb; j < std::min(D, jb + kB); ++j) row[j] = w2[j * F + f];
+                }
+    };
+    const size_t hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const size_t n = std::min(hw, F / 64 + 1);
+    std::vector<std::thread> pool;
+    for (size_t k = 1; k < n; ++k) pool.emplace_back(pack_rows, F * k / n, F * (k + 1) / n);
+    pack_rows(0, F / n);
+    for (auto& th : pool) th.join();
 }
 
 }  // namespace adapmoe

@@ -22,9 +22,17 @@ struct ExpertStore {
     ~ExpertStore();
 };
 
-// Allocate + pin (parallel first touch + cudaHostRegister) and fill with the deterministic init
-// (GPU init kernel, D2H into the pinned blocks).
-void build_expert_store(Engine& engine, ExpertStore& store, int ffn, int tiles, std::uint64_t seed, int alias);
+// Allocate + pin (parallel first touch + cudaHostRegister) and, with `init_values`, fill with the
+// deterministic init (GPU init kernel, D2H into the pinned blocks); without, the store is zero and
+// the caller provides the weights through set_expert_weights.
+void build_expert_store(Engine& engine, ExpertStore& store, int ffn, int tiles, std::uint64_t seed, int alias,
+                        bool init_values = true);
+
+// Pack one expert's weights, given in the usual checkpoint layout (bf16 bits, row-major:
+// w1 = gate_proj [ffn][d], w3 = up_proj [ffn][d], w2 = down_proj [d][ffn]), into the store's
+// tile-major layout (W1/W3 row pairs + W2 transposed, kernels/expert_ffn.hpp).  Host threads.
+void set_expert_weights(ExpertStore& store, int layer, int expert, const std::uint16_t* w1, const std::uint16_t* w3,
+                        const std::uint16_t* w2);
 
 // Per-matrix init constants shared with the CUDA init kernel and the oracle.
 void expert_init_constants(std::uint64_t seed, int layer, int expert, int d, int ffn, std::uint64_t base[3], float scale[3]);

@@ -310,6 +310,30 @@ class Engine:
     def experts_init(self, ffn_dim: int, tiles: int, seed: int = 0, host_alias: int = 0):
         check(load().moe_experts_init(self._h, ffn_dim, tiles, seed, host_alias))
 
+    def experts_alloc(self, ffn_dim: int, tiles: int):
+        """Pinned store for real weights (moe_experts_alloc); fill it with expert_set."""
+        check(load().moe_experts_alloc(self._h, ffn_dim, tiles))
+
+    def expert_set(self, layer: int, expert: int, w1, w3, w2):
+        """One expert's weights in checkpoint layout: w1 = gate_proj [ffn][d], w3 = up_proj [ffn][d],
+        w2 = down_proj [d][ffn]; bf16 (torch.bfloat16 tensors or uint16 bit patterns)."""
+        def bits(w):
+            if hasattr(w, "detach"):  # torch tensor
+                import torch
+                w = w.detach().contiguous().cpu()
+                if w.dtype == torch.bfloat16:
+                    w = w.view(torch.int16)
+                w = w.numpy()
+            return np.ascontiguousarray(w).view(np.uint16)
+        w1, w3, w2 = bits(w1), bits(w3), bits(w2)
+        d, F = self.spec.hidden_dim, w1.shape[0]
+        if w1.shape != (F, d) or w3.shape != (F, d) or w2.shape != (d, F):
+            raise ValueError(f"expert_set: want w1/w3 [{F}][{d}] and w2 [{d}][{F}], got {w1.shape} {w3.shape} {w2.shape}")
+        if self.expert_bytes() != 3 * F * d * 2:
+            raise ValueError("expert_set: ffn does not match the allocated store")
+        check(load().moe_expert_set(self._h, layer, expert, _p(w1, _capi._u16), _p(w3, _capi._u16),
+                                    _p(w2, _capi._u16)))
+
     def expert_bytes(self) -> int:
         b = C.c_int64()
         check(load().moe_expert_bytes(self._h, C.byref(b)))

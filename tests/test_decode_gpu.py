@@ -250,3 +250,68 @@ def test_tile_merge_every_output(name, monkeypatch):
     for (t, l), moe in ref.items():
         got = hid[t, l].astype(np.float64) - w.acts[t, l].astype(np.float32).astype(np.float64)
         assert _rel_err(got, moe) < REL_TOL, (t, l)
+
+
+def _bf16_bits(a):
+    """fp32 -> bf16 bit patterns (round to nearest even) and their exact fp32 values."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    b = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    return b, (b.astype(np.uint32) << 16).view(np.float32)
+
+
+def test_expert_set_checkpoint_layout():
+    """Real weights (moe_experts_alloc + moe_expert_set): checkpoint-layout W1 / W3 [ffn][d] and
+    W2 [d][ffn] land in the tile-major store and the K2 path computes W2 (silu(W1 x) * (W3 x))
+    within 1e-4 of fp64 numpy on the same bf16 values; then a decode over them matches too."""
+    rng = np.random.default_rng(5)
+    L, N, K, D, F, tiles = 2, 4, 2, 256, 512, 2
+    spec = P.ModelSpec(L, N, K, D)
+    mats = {}
+    with P.Engine(spec) as eng:
+        eng.experts_alloc(F, tiles)
+        for l in range(L):
+            for e in range(N):
+                w1, f1 = _bf16_bits(rng.standard_normal((F, D)) / np.sqrt(D))
+                w3, f3 = _bf16_bits(rng.standard_normal((F, D)) / np.sqrt(D))
+                w2, f2 = _bf16_bits(rng.standard_normal((D, F)) / np.sqrt(F))
+                eng.expert_set(l, e, w1, w3, w2)
+                mats[(l, e)] = (f1.astype(np.float64), f3.astype(np.float64), f2.astype(np.float64))
+        # tile-major packing: tile t = rows [t*Ft, (t+1)*Ft) as (W1 row, W3 row) pairs, then W2^T rows
+        Ft = F // tiles
+        blob = eng.expert_read(1, 2).reshape(tiles, 3 * Ft, D)
+        w1, w3, w2 = (_bf16_bits(m.astype(np.float32))[0] for m in mats[(1, 2)])
+        for t in range(tiles):
+            assert np.array_equal(blob[t, 0:2 * Ft:2], w1[t * Ft:(t + 1) * Ft])
+            assert np.array_equal(blob[t, 1:2 * Ft:2], w3[t * Ft:(t + 1) * Ft])
+            assert np.array_equal(blob[t, 2 * Ft:], w2[:, t * Ft:(t + 1) * Ft].T)
+        for (l, e), (a1, a3, a2) in list(mats.items())[:3]:
+            x = rng.standard_normal(D)
+            xf = x.astype(np.float32).astype(np.float64)
+            g, u = a1 @ xf, a3 @ xf
+            ref = a2 @ (g / (1.0 + np.exp(-g)) * u)
+            assert _rel_err(eng.expert_ffn(l, e, x), ref) < REL_TOL
+        # decode with the set weights (trace replay, every expert resident)
+        w = O.generate_trace(L, N, K, D, 6, 0.6, 0.2, 3, 44)
+        eng.load_gates(w.gates)
+        cfg = P.SimConfig(tile_count_per_expert=tiles)
+        tau = O.calibrate_threshold(w, 0.24)
+        eng.decode_begin([N] * L, w.fisher, tau, cfg, 0, 6)
+        hid = np.zeros((6, L, D), dtype=np.float32)
+        eng.decode_tokens(w.acts, w.scores, hid)
+        eng.decode_end(cfg, 6)
+        with pytest.raises(P.MoeError):
+            eng.decode_begin([N] * L, w.fisher, tau, cfg, 0, 6)
+            eng.expert_set(0, 0, w1, w3, w2)  # not while a session holds HBM copies
+    sim = O.simulate(w, [N] * L, tau, tiles=tiles)
+    for t in range(6):
+        for l in range(L):
+            sel = [int(e) for e in sim.decisions[t, l] if e >= 0]
+            sc = w.scores[t, l]
+            xf = w.acts[t, l].astype(np.float32).astype(np.float64)
+            moe = np.zeros(D)
+            for e in sel:
+                a1, a3, a2 = mats[(l, e)]
+                g, u = a1 @ xf, a3 @ xf
+                wgt = 1.0 if len(sel) == 1 else sc[e] / sum(sc[q] for q in sel)
+                moe += wgt * (a2 @ (g / (1.0 + np.exp(-g)) * u))
+            assert _rel_err(hid[t, l].astype(np.float64) - xf, moe) < REL_TOL, (t, l)

@@ -193,6 +193,27 @@ int moe_engine_destroy(moe_engine_t engine);
  * (PredictiveGate, inc/prefetch.hpp:146) [d][N] or NULL. */
 int moe_load_gates(moe_engine_t engine, const double* gates, const double* first_gate);
 
+/* K1 on device-resident hidden states, stream-ordered (SURVEY §8(b) moe_router_forward): the
+ * routing step of one layer for B rows inside a caller's decode loop.  x: device fp64 [B][d] (the
+ * layer's router input).  scores: device fp64 [B][N] stored post-softmax scores to decide from
+ * (trace replay, inc/simulator.hpp:390-396), or NULL to decide from softmax(x . W_layer).  Items per
+ * row: the decision, then look-ahead predictions x . W_{layer+1..layer+lookahead} (at the last layer
+ * the first-layer predictive gate, if loaded, as item 1), each with the sensitivity gate when
+ * flags & MOE_ROUTE_ADAPTIVE (else plain top-K).  Outputs (device, row r = b*(1+lookahead) + item):
+ * selected [rows][K] (-1 padded), count [rows], single [rows], perturbation [rows] (may be NULL).
+ * fisher: host [L].  stream: a cudaStream_t (NULL = the engine's compute stream).  Returns once the
+ * work is enqueued; the caller synchronises its stream before reading the outputs. */
+#define MOE_ROUTE_ADAPTIVE 1
+typedef struct {
+    int32_t* selected;
+    int32_t* count;
+    int32_t* single;
+    double* perturbation;
+} moe_route_out;
+int moe_router_forward(moe_engine_t engine, int32_t layer, const double* x, int32_t rows, const double* scores,
+                       double tau, const double* fisher, int32_t lookahead, int32_t flags, const moe_route_out* out,
+                       void* stream);
+
 /* K1 batched router over a whole trace (replaces the reference's per-call GateMatrix::logits +
  * softmax + top_k + gate_decide_sensitivity inside simulate_trace, inc/simulator.hpp:368-444,
  * and the stored-score decision at :390-396).  acts [T][L][d] fp64, scores [T][L][N] fp64, fisher

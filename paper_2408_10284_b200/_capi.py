@@ -61,6 +61,10 @@ class DecodeOptsC(C.Structure):
                 ("dirichlet_concentration", C.c_double)]
 
 
+class RouteOutC(C.Structure):
+    _fields_ = [("selected", C.c_void_p), ("count", C.c_void_p), ("single", C.c_void_p), ("perturbation", C.c_void_p)]
+
+
 class DecodeStatsC(C.Structure):
     _fields_ = [("tokens", C.c_int64), ("kernels_launched", C.c_int64), ("ffn_launches", C.c_int64),
                 ("tile_copies", C.c_int64), ("copy_bytes", C.c_int64), ("input_bytes", C.c_int64),
@@ -106,6 +110,8 @@ SIGNATURES = {
     "moe_expert_bytes": (C.c_int, [_eng, _i64]),
     "moe_expert_read": (C.c_int, [_eng, C.c_int32, C.c_int32, _u16]),
     "moe_experts_alloc": (C.c_int, [_eng, C.c_int32, C.c_int32]),
+    "moe_router_forward": (C.c_int, [_eng, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_double, _d, C.c_int32,
+                                     C.c_int32, C.c_void_p, C.c_void_p]),
     "moe_expert_set": (C.c_int, [_eng, C.c_int32, C.c_int32, _u16, _u16, _u16]),
     "moe_trace_load": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
     "moe_trace_info": (C.c_int, [C.c_void_p, C.POINTER(ModelSpecC), _i32]),

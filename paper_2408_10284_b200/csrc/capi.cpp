@@ -287,6 +287,19 @@ int moe_route_trace(moe_engine_t h, const double* acts, const double* scores, in
     });
 }
 
+int moe_router_forward(moe_engine_t h, int32_t layer, const double* x, int32_t rows, const double* scores, double tau,
+                       const double* fisher, int32_t lookahead, int32_t flags, const moe_route_out* out, void* stream) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(fisher, "fisher");
+        require(out, "out");
+        GatingThreshold{tau}.validate();
+        RouteOutputs o{out->selected, out->count, out->single, out->perturbation, nullptr};
+        e.router_forward(layer, x, rows, scores, tau, std::span<const double>(fisher, e.spec().num_layers), lookahead,
+                         (flags & MOE_ROUTE_ADAPTIVE) != 0, o, static_cast<cudaStream_t>(stream));
+    });
+}
+
 int moe_simulate_trace(moe_engine_t h, const double* acts, const double* scores, int32_t T, const double* fisher,
                        const int32_t* caps, double tau, const moe_sim_config* cfg, uint64_t seed, moe_metrics* metrics,
                        int64_t* lat, int64_t* odl, moe_event* events, int64_t cap, int64_t* n_events) {

@@ -61,6 +61,8 @@ Engine::~Engine() {
     cudaSetDevice(device_);
     session.reset();
     experts.reset();
+    for (cudaEvent_t ev : fwd_done_)
+        if (ev) cudaEventDestroy(ev);
     if (compute_) cudaStreamDestroy(compute_);
     if (copy_) cudaStreamDestroy(copy_);
 }
@@ -248,6 +250,71 @@ void Engine::route_trace_stream(const double* acts, const double* scores, int T,
         }
         on_chunk(t0, t1);
     }
+}
+
+void Engine::router_forward(int layer, const double* d_x, int rows, const double* d_scores, double tau,
+                            std::span<const double> fisher, int lookahead, bool adaptive, const RouteOutputs& out,
+                            cudaStream_t stream) {
+    activate();
+    const int L = spec_.num_layers, N = spec_.experts_per_layer, K = spec_.top_k, D = spec_.hidden_dim;
+    if (layer < 0 || layer >= L) fail(Status::Usage, "router_forward: layer out of range");
+    if (rows < 1) fail(Status::Usage, "router_forward: rows must be >= 1");
+    if (lookahead < 0 || lookahead > 3) fail(Status::Usage, "router_forward: lookahead out of {0,1,2,3}");
+    if (static_cast<int>(fisher.size()) != L) fail(Status::Usage, "router_forward: fisher count != num_layers");
+    if (!d_x || !out.selected || !out.count || !out.single) fail(Status::Usage, "router_forward: null device buffer");
+    if (!has_gates()) fail(Status::Usage, "router_forward: gates not loaded");
+    if (!stream) stream = compute_;
+    const int per_row = 1 + lookahead;
+    const int b = fwd_next_;
+    fwd_next_ ^= 1;
+    if (!fwd_done_[b]) MOE_CUDA(cudaEventCreateWithFlags(&fwd_done_[b], cudaEventDisableTiming));
+    MOE_CUDA(cudaEventSynchronize(fwd_done_[b]));  // the launch that last used this staging buffer
+    h_fwd_groups_[b].reserve(static_cast<size_t>(rows) * sizeof(RouteGroup));
+    d_fwd_groups_[b].reserve(static_cast<size_t>(rows) * sizeof(RouteGroup));
+    RouteGroup* groups = h_fwd_groups_[b].as<RouteGroup>();
+    const int flags = adaptive ? kRouteAdaptive : 0;
+    int max_gates = 0;
+    for (int r = 0; r < rows; ++r) {
+        RouteGroup& g = groups[r];
+        g = RouteGroup{};
+        g.x = d_x + static_cast<size_t>(r) * D;
+        RouteItem& dec = g.items[g.n_items++];
+        if (d_scores) {
+            dec.scores = d_scores + static_cast<size_t>(r) * N;
+        } else {
+            gate_item(dec, layer);
+        }
+        dec.fisher = fisher[layer];
+        dec.flags = flags;
+        dec.out = r * per_row;
+        int n_gates = d_scores ? 0 : 1;
+        if (layer + 1 < L) {
+            for (int dep = 1; dep <= lookahead && layer + dep < L; ++dep) {
+                RouteItem& it = g.items[g.n_items++];
+                gate_item(it, layer + dep);
+                it.fisher = fisher[layer + dep];
+                it.flags = flags;
+                it.out = r * per_row + dep;
+                ++n_gates;
+            }
+        } else if (lookahead > 0 && has_first_gate()) {
+            RouteItem& it = g.items[g.n_items++];
+            gate_item(it, -1);
+            it.fisher = fisher[0];
+            it.flags = flags;
+            it.out = r * per_row + 1;
+            ++n_gates;
+        }
+        max_gates = std::max(max_gates, n_gates);
+    }
+    // rows without every look-ahead item (near the last layer) keep count 0 in those slots
+    MOE_CUDA(cudaMemsetAsync(out.count, 0, static_cast<size_t>(rows) * per_row * sizeof(int), stream));
+    MOE_CUDA(cudaMemsetAsync(out.selected, 0xff, static_cast<size_t>(rows) * per_row * K * sizeof(int), stream));
+    MOE_CUDA(cudaMemcpyAsync(d_fwd_groups_[b].ptr, groups, static_cast<size_t>(rows) * sizeof(RouteGroup),
+                             cudaMemcpyHostToDevice, stream));
+    RouteParams p{D, N, K, tau, 1.0};
+    MOE_CUDA(launch_route(d_fwd_groups_[b].as<RouteGroup>(), rows, std::max(max_gates, 1), p, out, stream));
+    MOE_CUDA(cudaEventRecord(fwd_done_[b], stream));  // staging buffer b (host and device) free after this
 }
 
 // inc/workload.hpp:60-112.  The RNG stream is consumed on the host in the reference's order

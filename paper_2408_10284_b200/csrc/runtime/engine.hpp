@@ -88,6 +88,11 @@ public:
                             double tau, const SimConfig& cfg, int chunk_tokens, TraceRoutes& out,
                             const std::function<void(int, int)>& on_chunk);
 
+    // K1 for one layer on device rows, enqueued on `stream` (moe_router_forward).
+    void router_forward(int layer, const double* d_x, int rows, const double* d_scores, double tau,
+                        std::span<const double> fisher, int lookahead, bool adaptive, const RouteOutputs& out,
+                        cudaStream_t stream);
+
     // generate_trace with the gate GEMVs on the GPU; returns via the output arrays.
     void generate_trace(const int tokens, double concentration, double drift, std::uint64_t gate_seed,
                         std::uint64_t token_seed, bool shared_gates, const double* fisher_scales,
@@ -122,6 +127,12 @@ private:
     // router workspace
     DeviceBuffer d_groups_, d_x_, d_scores_, d_out_sel_, d_out_cnt_, d_out_single_, d_out_pert_, d_out_scores_;
     PinnedBuffer h_trace_groups_, h_trace_out_;  // route_trace_stream staging
+    // router_forward: groups staged in pinned memory, two buffers, each reused only after the
+    // copy that read it has completed (event)
+    PinnedBuffer h_fwd_groups_[2];
+    DeviceBuffer d_fwd_groups_[2];
+    cudaEvent_t fwd_done_[2] = {nullptr, nullptr};
+    int fwd_next_ = 0;
 };
 
 }  // namespace adapmoe

@@ -231,6 +231,29 @@ class Engine:
                                      _p(pert, _capi._d), _p(preds, _capi._i32)))
         return dec, single, pert, preds
 
+    def router_forward(self, layer: int, x, fisher, tau: float, lookahead: int = 2, scores=None,
+                       adaptive: bool = True, stream=None):
+        """K1 for one layer on device rows (moe_router_forward).  x: CUDA fp64 tensor [B][d]; scores:
+        optional CUDA fp64 [B][N] stored scores to decide from.  Returns CUDA tensors selected
+        [B][1+lookahead][K], count / single [B][1+lookahead], perturbation [B][1+lookahead],
+        enqueued on `stream` (a torch.cuda.Stream; default: the current stream)."""
+        import torch
+        B, K = x.shape[0], self.spec.top_k
+        rows = B * (1 + lookahead)
+        dev = x.device
+        sel = torch.empty((B, 1 + lookahead, K), dtype=torch.int32, device=dev)
+        cnt = torch.empty((B, 1 + lookahead), dtype=torch.int32, device=dev)
+        sgl = torch.empty((B, 1 + lookahead), dtype=torch.int32, device=dev)
+        pert = torch.empty((B, 1 + lookahead), dtype=torch.float64, device=dev)
+        if rows:
+            s = stream if stream is not None else torch.cuda.current_stream(dev)
+            out = _capi.RouteOutC(sel.data_ptr(), cnt.data_ptr(), sgl.data_ptr(), pert.data_ptr())
+            check(load().moe_router_forward(self._h, layer, x.data_ptr(), B,
+                                            None if scores is None else scores.data_ptr(), float(tau),
+                                            _p(_f64(fisher), _capi._d), lookahead, 1 if adaptive else 0,
+                                            C.byref(out), s.cuda_stream))
+        return sel, cnt, sgl, pert
+
     def simulate_trace(self, acts, scores, fisher, caps, tau, cfg: SimConfig, seed: int = 0,
                        timeline: bool = True) -> SimResult:
         """inc/simulator.hpp:329 with K1 on the GPU."""

@@ -123,3 +123,53 @@ def test_router_logits_match_reference_order():
                 O.lib().orc_top_k(sc.ctypes.data_as(O._d), N, K, top.ctypes.data_as(O._i))
                 assert preds[t, l, s, 0] == l + s + 1
                 assert preds[t, l, s, 2:].tolist() == top.tolist()
+
+
+@pytest.mark.parametrize("name", ["tiny", "wide_n16", "top3", "mixtral_8x7b_t12"])
+@pytest.mark.parametrize("lookahead", [0, 2, 3])
+def test_router_forward_matches_route_trace(name, lookahead):
+    """moe_router_forward (device rows, caller's stream) decides and predicts exactly like the
+    trace router: for every layer, rows = the trace's tokens; decisions from the stored scores equal
+    route_trace's, look-ahead item d equals route_trace's prediction slot d-1 (at the last layer:
+    the first-layer gate, for tokens that have a successor); deciding from the layer's own gate
+    logits equals deciding from the reference softmax of those logits."""
+    import torch
+    g = load_golden(name)
+    w, fg = oracle_inputs(g)
+    cfg = sim_config(g)
+    cfg.lookahead_depth = lookahead
+    L, K, T = w.L, w.K, w.T
+    with P.Engine(_spec(g)) as eng:
+        eng.load_gates(w.gates, fg)
+        dec, single, pert, preds = eng.route_trace(w.acts, w.scores, w.fisher, g["tau"], cfg)
+        stream = torch.cuda.Stream()
+        for l in range(L):
+            x = torch.from_numpy(np.ascontiguousarray(w.acts[:, l])).cuda()
+            s = torch.from_numpy(np.ascontiguousarray(w.scores[:, l])).cuda()
+            torch.cuda.synchronize()
+            with torch.cuda.stream(stream):
+                sel, cnt, sgl, prt = eng.router_forward(l, x, w.fisher, g["tau"], lookahead, scores=s, stream=stream)
+            stream.synchronize()
+            sel, cnt, sgl = sel.cpu().numpy(), cnt.cpu().numpy(), sgl.cpu().numpy()
+            assert np.array_equal(sel[:, 0], dec[:, l]) and np.array_equal(sgl[:, 0], single[:, l])
+            assert np.array_equal(prt.cpu().numpy()[:, 0], pert[:, l])
+            for dep in range(1, lookahead + 1):
+                if l + dep < L:
+                    rows = range(T)
+                elif l == L - 1 and dep == 1 and fg is not None:
+                    rows = range(T - 1)  # route_trace predicts the next token's layer 0 only if one exists
+                else:
+                    assert (cnt[:, dep] == 0).all()
+                    continue
+                for t in rows:
+                    target, count = preds[t, l, dep - 1, 0], preds[t, l, dep - 1, 1]
+                    assert target == (l + dep if l + dep < L else 0)
+                    assert cnt[t, dep] == count
+                    assert list(sel[t, dep, :count]) == list(preds[t, l, dep - 1, 2:2 + count])
+            # decide from the gate's logits == decide from the reference softmax of those logits
+            ref_scores = torch.from_numpy(np.stack([O.gate_scores(w.gates[l], w.acts[t, l]) for t in range(T)])).cuda()
+            a = eng.router_forward(l, x, w.fisher, g["tau"], 0)
+            b = eng.router_forward(l, x, w.fisher, g["tau"], 0, scores=ref_scores)
+            torch.cuda.synchronize()
+            for u, v in zip(a[:3], b[:3]):
+                assert torch.equal(u, v)

@@ -312,20 +312,37 @@ __global__ void expert_init_kernel(uint16_t* dst, int D, int F, int tiles, InitA
     }
 }
 
-__global__ void free_running_input_kernel(double* res, double* norm, long long stride, const float* src,
-                                          long long src_stride, int d, double eps) {
-    const int r = blockIdx.x, lane = threadIdx.x;
+// One block per row.  The sum of squares keeps its fixed order — lane j of warp 0 adds x_i^2 for
+// i = j, j+32, ... (each product and sum separately rounded), then an xor butterfly over the 32
+// lane sums — while the whole block does the elementwise work (fp32 -> fp64 residual, squares into
+// shared memory, the final divisions).
+constexpr int kNormThreads = 256;
+
+__global__ void __launch_bounds__(kNormThreads) free_running_input_kernel(double* res, double* norm, long long stride,
+                                                                          const float* src, long long src_stride, int d,
+                                                                          double eps) {
+    extern __shared__ double sq[];  // [d]
+    __shared__ double rms_s;
+    const int r = blockIdx.x;
     double* x = res + r * stride;
-    if (src)
-        for (int i = lane; i < d; i += 32) x[i] = static_cast<double>(src[r * src_stride + i]);
-    __syncwarp();
-    double ss = 0.0;
-    for (int i = lane; i < d; i += 32) ss = __dadd_rn(ss, __dmul_rn(x[i], x[i]));
+    for (int i = threadIdx.x; i < d; i += kNormThreads) {
+        const double v = src ? static_cast<double>(src[r * src_stride + i]) : x[i];
+        if (src) x[i] = v;
+        sq[i] = __dmul_rn(v, v);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        double ss = 0.0;
+        for (int i = lane; i < d; i += 32) ss = __dadd_rn(ss, sq[i]);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, off));
-    const double rms = __dsqrt_rn(__dadd_rn(__ddiv_rn(ss, static_cast<double>(d)), eps));
+        for (int off = 16; off > 0; off >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, off));
+        if (lane == 0) rms_s = __dsqrt_rn(__dadd_rn(__ddiv_rn(ss, static_cast<double>(d)), eps));
+    }
+    __syncthreads();
+    const double rms = rms_s;
     double* n = norm + r * stride;
-    for (int i = lane; i < d; i += 32) n[i] = __ddiv_rn(x[i], rms);
+    for (int i = threadIdx.x; i < d; i += kNormThreads) n[i] = __ddiv_rn(x[i], rms);
 }
 
 }  // namespace
@@ -333,7 +350,13 @@ __global__ void free_running_input_kernel(double* res, double* norm, long long s
 cudaError_t launch_free_running_input(double* res, double* norm, long long stride, const float* src,
                                       long long src_stride, int rows, int d, double eps, cudaStream_t stream) {
     if (rows <= 0 || d <= 0) return cudaSuccess;
-    free_running_input_kernel<<<rows, 32, 0, stream>>>(res, norm, stride, src, src_stride, d, eps);
+    const size_t smem = static_cast<size_t>(d) * sizeof(double);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(free_running_input_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    free_running_input_kernel<<<rows, kNormThreads, smem, stream>>>(res, norm, stride, src, src_stride, d, eps);
     return cudaGetLastError();
 }
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <chrono>
@@ -794,6 +795,11 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
     const int* exact_used = sgl + rows;
 
     std::array<RoutePrediction, 3> preds;
+    const bool gap_trace = std::getenv("ADAPMOE_GAP_TRACE") != nullptr;
+    struct GapRec {
+        cudaEvent_t r0, r1, f0, f1;
+    };
+    std::vector<GapRec> gap_rec;
     for (int i = 0; i < count; ++i) {
         const int tok = tokens_done_ + i;
         for (int l = 0; l < L; ++l) {
@@ -867,7 +873,11 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             cur_scores_ = free_running_ ? d_free_scores_.as<double>() : s_all + row0 * N;
             cur_score_stride_ = free_running_ ? 4 * N : static_cast<long long>(L) * N;
             cur_out_ = out_all + row0 * D;
+            const size_t npass0 = pass_events_.size();
             policy_->step(tok, l, d, std::span<const RoutePrediction>(preds.data(), np), B > 1 ? singles : -1);
+            if (gap_trace && !router_events_.empty() && pass_events_.size() > npass0)
+                gap_rec.push_back({router_events_.back().first, router_events_.back().second, pass_events_[npass0].e0,
+                                   pass_events_.back().e1});
             stats_.host_step_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count();
         }
     }
@@ -909,6 +919,15 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                                  "must decode the same calls concurrently)");
     }
     MOE_CUDA(cudaStreamSynchronize(cs));
+    for (size_t q = 0; q < gap_rec.size(); ++q) {  // ADAPMOE_GAP_TRACE (temporary probe)
+        float k1 = 0, k1_ffn = 0, ffn = 0, prev = -1;
+        cudaEventElapsedTime(&k1, gap_rec[q].r0, gap_rec[q].r1);
+        cudaEventElapsedTime(&k1_ffn, gap_rec[q].r1, gap_rec[q].f0);
+        cudaEventElapsedTime(&ffn, gap_rec[q].f0, gap_rec[q].f1);
+        if (q) cudaEventElapsedTime(&prev, gap_rec[q - 1].f1, gap_rec[q].r0);
+        std::fprintf(stderr, "[gap] %zu: K1 %.1f us, K1 end -> FFN start %.1f us, FFN %.1f us, prev FFN end -> K1 start %.1f us\n",
+                     q, k1 * 1e3f, k1_ffn * 1e3f, ffn * 1e3f, prev * 1e3f);
+    }
     release_pending(true);
     tokens_done_ += count;
     stats_.tokens += static_cast<long long>(count) * B;

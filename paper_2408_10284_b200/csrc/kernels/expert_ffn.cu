@@ -84,16 +84,6 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_cons
     const int first_seg = static_cast<int>(r_lo / Ft);
     float* const part = p.partial + static_cast<size_t>(blockIdx.x) * kFfnSlotsPerCta * D;
     int cur_seg = first_seg;
-    if (p.l2_prefetch == 2 && tid == 0) {
-        // whole-range prefetch: HBM -> L2 at full rate regardless of how fast this CTA consumes
-        for (long long c = r_lo; c < r_hi;) {
-            const int s = static_cast<int>(c / Ft), q0 = static_cast<int>(c % Ft);
-            const int n = static_cast<int>(min(static_cast<long long>(Ft - q0), r_hi - c));
-            ptx::bulk_prefetch_l2(p.seg[s].gate_up + static_cast<size_t>(q0) * 2 * D, n * 2u * D * 2u);
-            ptx::bulk_prefetch_l2(p.seg[s].down_t + static_cast<size_t>(q0) * D, n * static_cast<unsigned>(D) * 2u);
-            c += n;
-        }
-    }
     __syncthreads();
     int parity = 0;
     for (long long c0 = r_lo; c0 < r_hi; parity ^= 1) {
@@ -102,13 +92,6 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_cons
         if (s != cur_seg) {
             store_partial<DC>(part + static_cast<size_t>(cur_seg - first_seg) * D, acc, tid, D);
             cur_seg = s;
-        }
-        if (p.l2_prefetch == 1 && tid == 0 && c0 + n < r_hi) {
-            const long long c1 = c0 + n;
-            const int s1 = static_cast<int>(c1 / Ft), q0 = static_cast<int>(c1 % Ft);
-            const int n1 = static_cast<int>(min(static_cast<long long>(min(kChunk, Ft - q0)), r_hi - c1));
-            ptx::bulk_prefetch_l2(p.seg[s1].gate_up + static_cast<size_t>(q0) * 2 * D, n1 * 2u * D * 2u);
-            ptx::bulk_prefetch_l2(p.seg[s1].down_t + static_cast<size_t>(q0) * D, n1 * static_cast<unsigned>(D) * 2u);
         }
         // ---- phase 1: h for row r0 + warp (a short chunk spreads each row over wpr = 2/4/8/16
         // warps, equal slices of d summed in part order — every warp keeps loads in flight) ----

@@ -34,8 +34,6 @@ struct FfnSegment {
 struct FfnLaunch {
     int n_seg = 0;
     int d = 0, ft = 0;
-    int l2_prefetch = 0;              // 1: bulk-prefetch the next row chunk into L2; 2: the CTA's whole
-                                      // row range at kernel start (small launches)
     const double* x = nullptr;        // [d] layer input (fp64; converted to fp32 in shared memory)
     float* partial = nullptr;         // [grid][kFfnSlotsPerCta][d] written by the launch
     FfnSegment seg[kMaxFfnSegments];

@@ -74,7 +74,6 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     for (int s = 0; s < n_slots_; ++s) free_.push_back(s);
     slot_of_.assign(static_cast<size_t>(L) * N, -1);
     cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, eng.device());
-    if (const char* v = std::getenv("ADAPMOE_K2_L2")) l2_mode_ = std::atoi(v);  // profiling knob
     if (const char* v = std::getenv("ADAPMOE_TILE_MERGE")) tile_merge_ = std::atoi(v) != 0 ? 1 : 0;  // A/B knob
 
     // at most one launch for the resident experts' tiles (split per 32 segments) + one per
@@ -380,7 +379,6 @@ void DecodeSession::timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int
     const size_t region = static_cast<size_t>(kFfnMaxCtas) * kFfnSlotsPerCta * spec_.hidden_dim;
     if (partial_next_ >= partial_regions_) fail(Status::Internal, "decode: FFN partial pool exhausted");
     p.partial = d_partials_.as<float>() + region * partial_next_++;
-    p.l2_prefetch = p.n_seg <= 2 ? l2_mode_ : 0;  // only small launches gain from the L2 prefetch
     const int grid = ffn_grid(p, sm_count_);
     for (int s = 0; s < p.n_seg; ++s) {
         FfnPartialRef r{p.partial, grid, p.n_seg, s, seg_meta[s].first};

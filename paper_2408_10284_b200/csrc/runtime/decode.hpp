@@ -112,8 +112,6 @@ private:
     DeviceBuffer d_x_free_, d_x_norm_, d_free_scores_;
     static constexpr double kFreeRunningNormEps = 1e-5;  // Mixtral rms_norm_eps
     long long cur_score_stride_ = 0;
-    int l2_mode_ = 0;  // K2 L2 prefetch (ADAPMOE_K2_L2: 0 off, 1 next chunk, 2 whole range); off: both
-                       // prefetch modes measured slower on cold launches (tools/k2_cold.cu)
     int batch_ = 1;
     // expert parallelism: shard ep_rank_ of ep_world_ owns experts e % world == rank
     // of every layer.  The logical engine is replicated (same inputs -> same trace on every shard);

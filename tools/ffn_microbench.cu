@@ -79,7 +79,7 @@ int main() {
         p.ft = Ft;
         p.x = x;
         p.partial = part;
-        p.l2_prefetch = nseg == 1;
+        // (the L2 prefetch option was removed from the product kernel: measured slower)
         for (int s = 0; s < nseg; ++s) {
             const uint16_t* t = w + s * tile_elems;
             p.seg[s].gate_up = t;

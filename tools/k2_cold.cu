@@ -44,7 +44,7 @@ int main() {
                 p.ft = Ft;
                 p.x = x;
                 p.partial = part;
-                p.l2_prefetch = mode;
+                (void)mode;  // L2 prefetch modes measured slower and removed (profiles/r1_k2_variants.txt)
                 for (int s = 0; s < nseg; ++s) {
                     const uint16_t* t = w + ((rep * nseg + s) % NT) * tile_elems;
                     p.seg[s].gate_up = t;

@@ -235,6 +235,35 @@ __global__ void __launch_bounds__(kCombineCols * kCombineLanes) combine_kernel(c
             a.out[j] = acc;
         }
     }
+    if (a.next_res) {
+        __shared__ unsigned last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        extern __shared__ double sq[];  // [d]
+        __shared__ double rms_s;
+        const int n_threads = kCombineCols * kCombineLanes;
+        for (int i = threadIdx.x; i < a.d; i += n_threads) {
+            const double v = static_cast<double>(__ldcg(a.out + i));
+            a.next_res[i] = v;
+            sq[i] = __dmul_rn(v, v);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // same order as free_running_input_kernel
+            double ss = 0.0;
+            for (int i = threadIdx.x; i < a.d; i += 32) ss = __dadd_rn(ss, sq[i]);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, off));
+            if (threadIdx.x == 0) rms_s = __dsqrt_rn(__dadd_rn(__ddiv_rn(ss, static_cast<double>(a.d)), a.eps));
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < a.d; i += n_threads)
+            a.next_norm[i] = __ddiv_rn(static_cast<double>(__ldcg(a.out + i)), rms_s);
+        if (threadIdx.x == 0) *a.ticket = 0;  // re-arm for the next (stream-ordered) launch
+    }
 }
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -388,7 +417,14 @@ cudaError_t launch_ffn(const FfnLaunch& p, int sm_count, cudaStream_t stream) {
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
-    combine_kernel<<<(a.d + kCombineCols - 1) / kCombineCols, kCombineCols * kCombineLanes, 0, stream>>>(a);
+    if (a.next_res && (!a.next_norm || !a.ticket || a.n_out_peer > 0)) return cudaErrorInvalidValue;
+    const size_t smem = a.next_res ? static_cast<size_t>(a.d) * sizeof(double) : 0;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    combine_kernel<<<(a.d + kCombineCols - 1) / kCombineCols, kCombineCols * kCombineLanes, smem, stream>>>(a);
     return cudaGetLastError();
 }
 

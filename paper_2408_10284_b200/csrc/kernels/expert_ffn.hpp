@@ -73,6 +73,13 @@ struct CombineArgs {
     int n_out_peer = 0;
     float* out_peer[kMaxEpPeers] = {};
     int n_refs = 0;                  // refs sorted by (rank, tile)
+    // free-running batch 1: the block that finishes last (ticket) also forms the next layer's input
+    // from `out` — next_res = (double) out, next_norm = RMSNorm(next_res) in the fixed order of
+    // launch_free_running_input — so that launch disappears.  next_res == nullptr: off.
+    double* next_res = nullptr;
+    double* next_norm = nullptr;
+    unsigned* ticket = nullptr;      // zero before the launch; the last block re-arms it
+    double eps = 0.0;
     FfnPartialRef refs[kMaxCombineRefs];
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream);

@@ -75,6 +75,8 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     slot_of_.assign(static_cast<size_t>(L) * N, -1);
     cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, eng.device());
     if (const char* v = std::getenv("ADAPMOE_TILE_MERGE")) tile_merge_ = std::atoi(v) != 0 ? 1 : 0;  // A/B knob
+    d_combine_ticket_.reserve(sizeof(unsigned));
+    MOE_CUDA(cudaMemsetAsync(d_combine_ticket_.ptr, 0, sizeof(unsigned), eng.compute_stream()));
 
     // at most one launch for the resident experts' tiles (split per 32 segments) + one per
     // on-demand tile
@@ -524,6 +526,12 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
         c.n_out_peer = ep_world_;
         for (int g = 0; g < ep_world_; ++g) c.out_peer[g] = ep_slot(g, ep_rank_, ep_call_ & 1) + (cur_out_ - cur_out_base_);
     }
+    if (fuse_next_res_) {  // free-running batch 1: the combine also forms the next layer's input
+        c.next_res = fuse_next_res_;
+        c.next_norm = fuse_next_norm_;
+        c.ticket = d_combine_ticket_.as<unsigned>();
+        c.eps = kFreeRunningNormEps;
+    }
     MOE_CUDA(launch_combine(c, eng_.compute_stream()));
     stats_.kernels += 1;
 }
@@ -802,7 +810,10 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
         const int tok = tokens_done_ + i;
         for (int l = 0; l < L; ++l) {
             const size_t gl = (static_cast<size_t>(i) * L + l) * B;
-            if (free_running_) {  // residual x_l (previous output for l > 0) and its RMSNorm, every stream
+            // free-running batch 1 without the EP exchange: layer l > 0's input was formed by layer
+            // l-1's combine (CombineArgs::next_res)
+            const bool fused_input = free_running_ && B == 1 && ep_world_ == 1;
+            if (free_running_ && !(fused_input && l > 0)) {  // residual x_l and its RMSNorm, every stream
                 const size_t row_l = (static_cast<size_t>(i) * B) * L + l;
                 MOE_CUDA(launch_free_running_input(d_x_free_.as<double>() + row_l * D, x_norm + row_l * D,
                                                    static_cast<long long>(L) * D, l > 0 ? out_all + (row_l - 1) * D : nullptr,
@@ -871,6 +882,8 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             cur_scores_ = free_running_ ? d_free_scores_.as<double>() : s_all + row0 * N;
             cur_score_stride_ = free_running_ ? 4 * N : static_cast<long long>(L) * N;
             cur_out_ = out_all + row0 * D;
+            fuse_next_res_ = (fused_input && l + 1 < L) ? d_x_free_.as<double>() + (row0 + 1) * D : nullptr;
+            fuse_next_norm_ = fuse_next_res_ ? x_norm + (row0 + 1) * D : nullptr;
             const size_t npass0 = pass_events_.size();
             policy_->step(tok, l, d, std::span<const RoutePrediction>(preds.data(), np), B > 1 ? singles : -1);
             if (gap_trace && !router_events_.empty() && pass_events_.size() > npass0)

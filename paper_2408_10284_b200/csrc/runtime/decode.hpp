@@ -110,6 +110,9 @@ private:
     bool free_running_ = false;
     double concentration_ = 1.0;
     DeviceBuffer d_x_free_, d_x_norm_, d_free_scores_;
+    double* fuse_next_res_ = nullptr;   // batch 1: next layer's residual / norm rows the combine forms
+    double* fuse_next_norm_ = nullptr;
+    DeviceBuffer d_combine_ticket_;
     static constexpr double kFreeRunningNormEps = 1e-5;  // Mixtral rms_norm_eps
     long long cur_score_stride_ = 0;
     int batch_ = 1;

@@ -80,3 +80,10 @@ def test_model_mismatch_is_validation_error(exe, tmp_path):
     shutil.copy(os.path.join(DIR, "odd_d37", "gates.json"), tmp_path / "gates.json")
     r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True)
     assert r.returncode == 4 and "mismatch" in r.stderr  # require_same_model (moesim_main.cpp:102-104)
+
+
+@pytest.mark.gpu
+def test_python_example_runs():
+    r = subprocess.run(["python", os.path.join(ROOT, "examples", "python_decode.py")], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout + r.stderr

@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--ep-exchange", default="p2p", choices=["p2p", "allgather"],
                     help="EP combine: device-side stores into peer memory (CUDA IPC, NVLink) from the combine "
                          "epilogue, or a torch.distributed all_gather after each call")
+    ap.add_argument("--ep-owner", default="balanced", choices=["balanced", "modulo"],
+                    help="EP expert placement: balanced by a calibration trace's transfers (ep.balanced_owners) or "
+                         "expert e on rank e % N")
     ap.add_argument("--free-running", action="store_true",
                     help="decode with the hidden state flowing through the experts (layer l > 0 routes on layer "
                          "l-1's output; decisions from the gates) instead of replaying the trace")
@@ -299,11 +302,21 @@ def ours(args):
     else:
         acts, scores = acts[:, None], scores[:, None]
     p2p = ep_world > 1 and args.ep_exchange == "p2p"
+    owners = None
+    if ep_world > 1 and args.ep_owner == "balanced":
+        # placement from a separate calibration trace of the same model (not the decoded tokens):
+        # the same deterministic table on every rank
+        calib = eng.generate_trace(P.SynthConfig(spec, wl.tokens, wl.concentration, wl.drift, wl.gate_seed,
+                                                 wl.token_seed + 7777, False, wl.fisher_scales, wl.drift_scales))
+        eng.load_gates(trace.gates)
+        sim = eng.simulate_trace(calib.acts, calib.scores, calib.fisher, caps, tau, cfg, wl.seed)
+        owners = EP.balanced_owners(sim.timeline, wl.layers, wl.experts, ep_world)
+        del calib
 
     def begin(capacities):
         eng.decode_begin(capacities, trace.fisher, tau, cfg, wl.seed, total_tokens, args.staging, batch=B,
                          ep_rank=ep_rank, ep_world=ep_world, free_running=args.free_running,
-                         concentration=wl.concentration)
+                         concentration=wl.concentration, expert_owner=owners)
         if p2p:  # swap exchange regions (CUDA IPC handles) and connect: outputs come back already summed
             import torch.distributed as dist
             _, handle = eng.decode_ep_export(max(W, K, 1))
@@ -402,6 +415,11 @@ def ours(args):
     act_timed = int((((tl[:, 1] == 2) | ((tl[:, 1] == 3) & (tl[:, 7] == 0))) & (tokens_col >= W) & (tokens_col < W + K)).sum())
 
     d = {k: s1[k] - s0[k] for k in s0 if isinstance(s0[k], (int, float))}
+    per_rank_copy = [int(d["copy_bytes"])]
+    if ws > 1:  # every shard's host-link bytes (EP: the busiest shard bounds the step)
+        import torch.distributed as dist
+        per_rank_copy = [None] * ws
+        dist.all_gather_object(per_rank_copy, int(d["copy_bytes"]))
     ffn_ms = d["ffn_ms"]
     ffn_bytes = d["ffn_gate_up_bytes"] + d["ffn_down_bytes"]
     peaks = measured_peaks()
@@ -441,7 +459,7 @@ def ours(args):
                    "budget": wl.budget, "tiles": wl.tiles, "lookahead": wl.lookahead, "trace_tokens": wl.tokens,
                    "tau": tau, "realized_single_ratio": realized, "capacities": [int(c) for c in caps],
                    "dp_expected_loads_per_token": exp_loads, "host_alias": alias,
-                   "parallelism": (f"ep{ws} (expert e on rank e % {ws}; combine: "
+                   "parallelism": (f"ep{ws} ({'experts placed by a calibration trace (ep.balanced_owners)' if owners is not None else f'expert e on rank e % {ws}'}; combine: "
                                    f"{'P2P stores into peer memory from the combine epilogue' if p2p else 'all_gather'})"
                                    if ep_world > 1 else f"replicas x{ws}"),
                    "l2": "no flush needed: resident experts (>=22 GB) >> 126 MB L2"},
@@ -456,7 +474,7 @@ def ours(args):
                      "ms_per_launch": ffn_ms / max(1, d["ffn_launches"]),
                      "algorithmic_bytes": "3*d*ffn/tiles*2 B per (expert, tile) segment: every bf16 weight once",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"},
-        "host_link": {"copy_bytes": d["copy_bytes"], "copy_busy_ms": d["copy_busy_ms"], "achieved_gbs": copy_gbs,
+        "host_link": {"copy_bytes": d["copy_bytes"], "copy_bytes_per_rank": per_rank_copy, "copy_busy_ms": d["copy_busy_ms"], "achieved_gbs": copy_gbs,
                       "tile_copies": d["tile_copies"], "stall_ms": d["stall_ms"],
                       "copy_hidden_frac": (1.0 - d["stall_ms"] / d["copy_busy_ms"]) if d["copy_busy_ms"] > 0 else None,
                       # north-star ">= 90 % of prefetch transfer hidden": prefetches the logical engine

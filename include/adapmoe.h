@@ -333,6 +333,10 @@ typedef struct {
     int32_t ep_world;
     int32_t free_running;            /* see below; 0 = trace replay (the reference's semantics) */
     double dirichlet_concentration;  /* free-running: logits / concentration before softmax (SynthConfig) */
+    const int32_t* expert_owner;     /* EP: [L][N] shard of each (layer, expert), the same table on every
+                                        shard; NULL = e % ep_world.  Physical placement only: the event
+                                        trace does not depend on it (ep.balanced_owners balances it by a
+                                        calibration run's transfers) */
 } moe_decode_opts;
 
 int moe_decode_begin_ex(moe_engine_t engine, const int32_t* capacities, int32_t staging_slots, const double* fisher,

@@ -58,7 +58,7 @@ class CompareRowC(C.Structure):
 
 class DecodeOptsC(C.Structure):
     _fields_ = [("batch", C.c_int32), ("ep_rank", C.c_int32), ("ep_world", C.c_int32), ("free_running", C.c_int32),
-                ("dirichlet_concentration", C.c_double)]
+                ("dirichlet_concentration", C.c_double), ("expert_owner", C.c_void_p)]
 
 
 class RouteOutC(C.Structure):

@@ -542,10 +542,11 @@ int moe_decode_begin_ex(moe_engine_t h, const int32_t* caps, int32_t staging, co
         const int ep_world = opts ? opts->ep_world : 1;
         const bool free_running = opts ? opts->free_running != 0 : false;
         const double conc = (opts && opts->dirichlet_concentration > 0.0) ? opts->dirichlet_concentration : 1.0;
+        const int32_t* owner = opts ? opts->expert_owner : nullptr;
         e.session.reset();
         e.session = std::make_unique<DecodeSession>(e, std::span<const int>(caps, L), staging,
                                                     std::span<const double>(fisher, L), tau, c, seed, total_tokens,
-                                                    batch, ep_rank, ep_world, free_running, conc);
+                                                    batch, ep_rank, ep_world, free_running, conc, owner);
     });
 }
 

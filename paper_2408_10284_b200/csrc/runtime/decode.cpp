@@ -19,7 +19,7 @@ constexpr size_t kSlotAlign = 2u << 20;
 DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int staging_slots,
                              std::span<const double> fisher, double tau, const SimConfig& cfg, std::uint64_t seed,
                              int total_tokens, int batch, int ep_rank, int ep_world, bool free_running,
-                             double concentration)
+                             double concentration, const int* expert_owner)
     : free_running_(free_running),
       concentration_(concentration),
       batch_(batch),
@@ -53,12 +53,20 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     if (prefetch_on && !eng.has_gates()) fail(Status::Usage, "decode: prefetching requires the gate matrices");
     if (ep_world_ < 1 || ep_rank_ < 0 || ep_rank_ >= ep_world_ || ep_world_ > N)
         fail(Status::Usage, "decode_begin: expert-parallel shard must satisfy 0 <= rank < world <= N");
+    owner_.resize(static_cast<size_t>(L) * N);
+    for (int l = 0; l < L; ++l)
+        for (int e = 0; e < N; ++e) {
+            const int o = expert_owner ? expert_owner[static_cast<size_t>(l) * N + e] : e % ep_world_;
+            if (o < 0 || o >= ep_world_) fail(Status::Usage, "decode_begin: expert_owner entry out of [0, ep_world)");
+            owner_[static_cast<size_t>(l) * N + e] = o;
+        }
     int resident = 0;
-    int owned_per_layer = 0;
-    for (int e = 0; e < N; ++e) owned_per_layer += owned(e) ? 1 : 0;
-    for (int c : caps_) {
+    for (int l = 0; l < L; ++l) {
+        const int c = caps_[l];
         if (c < 0 || c > N) fail(Status::Usage, "decode_begin: capacity out of [0, N]");
-        resident += std::min(c, owned_per_layer);  // this shard's resident experts
+        int owned_here = 0;
+        for (int e = 0; e < N; ++e) owned_here += owned(l, e) ? 1 : 0;
+        resident += std::min(c, owned_here);  // this shard's resident experts
     }
     resident_slots_ = resident;
     int staging = staging_slots > 0 ? staging_slots : std::min(32, L * N + K);
@@ -289,7 +297,7 @@ void DecodeSession::on_request(int id, ExpertRef ref, bool on_demand) {
         req_slot_.resize(id + 1, -1);
         req_job_.resize(id + 1);
     }
-    if (!owned(ref.expert)) {  // another shard moves it
+    if (!owned(ref.layer, ref.expert)) {  // another shard moves it
         req_slot_[id] = -1;
         req_job_[id].reset();
         return;
@@ -314,7 +322,7 @@ void DecodeSession::on_insert(ExpertRef ref, int request, std::optional<int> evi
     const int key = ref.layer * N + ref.expert;
     if (request < 0) {  // initial residency (session setup, synchronous, untimed)
         if (evicted) fail(Status::Internal, "initial fill evicted an expert");
-        if (!owned(ref.expert)) return;
+        if (!owned(ref.layer, ref.expert)) return;
         const int s = take_slot();
         // initial residency (pinned source), ordered before any compute-stream use of the slot
         MOE_CUDA(cudaMemcpyAsync(slot_ptr(s), store_.expert(ref.layer, ref.expert), store_.expert_bytes,
@@ -342,12 +350,12 @@ void DecodeSession::on_insert(ExpertRef ref, int request, std::optional<int> evi
 }
 
 void DecodeSession::on_resident_compute(int, ExpertRef ref, int rank) {
-    if (!owned(ref.expert)) return;
+    if (!owned(ref.layer, ref.expert)) return;
     uses_.push_back(Use{rank, slot_of_[ref.layer * spec_.experts_per_layer + ref.expert], false, {}});
 }
 
 void DecodeSession::on_tile_compute(int, ExpertRef ref, int rank, int tile, int request) {
-    if (!owned(ref.expert)) return;
+    if (!owned(ref.layer, ref.expert)) return;
     if (uses_.empty() || !uses_.back().missing || uses_.back().rank != rank)
         uses_.push_back(Use{rank, req_slot_[request], true, {}});
     uses_.back().tiles.push_back(tile);

@@ -53,7 +53,8 @@ class DecodeSession : public DecodeListener {
 public:
     DecodeSession(Engine& eng, std::span<const int> capacities, int staging_slots, std::span<const double> fisher,
                   double tau, const SimConfig& cfg, std::uint64_t seed, int total_tokens, int batch = 1,
-                  int ep_rank = 0, int ep_world = 1, bool free_running = false, double concentration = 1.0);
+                  int ep_rank = 0, int ep_world = 1, bool free_running = false, double concentration = 1.0,
+                  const int* expert_owner = nullptr);
     ~DecodeSession() override;
 
     // acts [count][B][L][d], scores [count][B][L][N]: host or device pointers
@@ -132,7 +133,12 @@ private:
         return reinterpret_cast<float*>(ep_region_[shard] + kEpFlagBytes) +
                (static_cast<size_t>(parity) * ep_world_ + writer) * ep_rows_max_ * spec_.hidden_dim;
     }
-    bool owned(int expert) const { return expert % ep_world_ == ep_rank_; }
+    // shard of each (layer, expert): the caller's table (e.g. balanced by calibration traffic,
+    // ep.balanced_owners) or e % world; the logical trace does not depend on it
+    std::vector<int> owner_;
+    bool owned(int layer, int expert) const {
+        return owner_[static_cast<size_t>(layer) * spec_.experts_per_layer + expert] == ep_rank_;
+    }
     int np_ = 16;                       // token rows per expert entry in X / H (B rounded up to 16)
     DeviceBuffer d_gx_, d_gh_, d_gpart_;  // X [N][NP][d], H [N][NP][F] bf16; down partial arena
     size_t gpart_next_ = 0;             // floats used in the arena this layer

@@ -27,6 +27,28 @@ def owned_experts(num_experts: int, world: int, rank: int) -> list[int]:
     return [e for e in range(num_experts) if e % world == rank]
 
 
+def balanced_owners(timeline, num_layers: int, num_experts: int, world: int) -> np.ndarray:
+    """[L][N] shard table that balances the host-link traffic: the weight of (layer, expert) is its
+    tile transfers in a calibration run's event timeline (simulate_trace / decode_end on a trace of
+    the same model; activations break ties, spreading the FFN work too), assigned longest-first to
+    the least-loaded shard (ties -> lowest (layer, expert), lowest rank).  Deterministic, so every
+    shard computes the same table; the logical trace does not depend on it."""
+    tl = np.asarray(timeline)
+    w = np.zeros((num_layers, num_experts))
+    if tl.size:
+        kind, layer, expert = tl[:, 1], tl[:, 5], tl[:, 6]
+        np.add.at(w, (layer[kind == 4], expert[kind == 4]), 1000.0)  # TileTransfer
+        np.add.at(w, (layer[kind == 3], expert[kind == 3]), 1.0)     # TileCompute
+    order = sorted(((-w[l, e], l, e) for l in range(num_layers) for e in range(num_experts)))
+    load = [0.0] * world
+    owner = np.zeros((num_layers, num_experts), dtype=np.int32)
+    for negw, l, e in order:
+        r = min(range(world), key=lambda g: (load[g], g))
+        owner[l, e] = r
+        load[r] += -negw
+    return owner
+
+
 def shard_resident_slots(capacities, num_experts: int, world: int, rank: int) -> int:
     """HBM slots shard `rank` needs for its resident experts: sum_l min(t_l, owned per layer)."""
     owned = len(owned_experts(num_experts, world, rank))
@@ -60,14 +82,14 @@ class ExpertParallelDecoder:
 
     def __init__(self, engine, caps, fisher, tau, cfg, seed: int, total_tokens: int, rank: int, world: int,
                  batch: int = 1, staging_slots: int = 0, group=None, exchange: str = "p2p",
-                 max_tokens_per_call: int = 64):
+                 max_tokens_per_call: int = 64, expert_owner=None):
         """exchange="p2p": the shards swap exchange regions (CUDA IPC handles) and the combine kernels
         store partials straight into peer memory (NVLink); "allgather": torch.distributed after each
         call."""
         import torch.distributed as dist
         self.engine, self.rank, self.world, self.batch, self.group = engine, rank, world, batch, group
         engine.decode_begin(caps, fisher, tau, cfg, seed, total_tokens, staging_slots, batch=batch, ep_rank=rank,
-                            ep_world=world)
+                            ep_world=world, expert_owner=expert_owner)
         self.p2p = exchange == "p2p" and world > 1
         if self.p2p:
             _, handle = engine.decode_ep_export(max_tokens_per_call)

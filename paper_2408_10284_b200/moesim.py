@@ -369,14 +369,16 @@ class Engine:
 
     def decode_begin(self, caps, fisher, tau, cfg: SimConfig, seed: int, total_tokens: int, staging_slots: int = 0,
                      batch: int = 1, ep_rank: int = 0, ep_world: int = 1, free_running: bool = False,
-                     concentration: float = 1.0):
+                     concentration: float = 1.0, expert_owner=None):
         """Start a decode session (moe_decode_begin_ex).  batch > 1: B token streams share the
         cache; decode_tokens then takes acts [n][B][L][d] and scores [n][B][L][N].  ep_world > 1:
         this engine is expert-parallel shard ep_rank (experts e % ep_world == ep_rank) and
         decode_tokens returns its partial layer outputs (see paper_2408_10284_b200/ep.py).
         free_running: layer l > 0 routes and computes on layer l-1's output (decisions from the
         layer's gate, softmax(logits / concentration)); layer 0 takes acts[:, ..., 0, :]."""
-        opts = _capi.DecodeOptsC(batch, ep_rank, ep_world, int(free_running), float(concentration))
+        owner = None if expert_owner is None else _i32(np.asarray(expert_owner).reshape(-1))
+        opts = _capi.DecodeOptsC(batch, ep_rank, ep_world, int(free_running), float(concentration),
+                                 None if owner is None else owner.ctypes.data)
         check(load().moe_decode_begin_ex(self._h, _p(_i32(caps), _capi._i32), staging_slots,
                                          _p(_f64(fisher), _capi._d), float(tau), C.byref(cfg.c()), seed,
                                          total_tokens, C.byref(opts)))

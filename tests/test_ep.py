@@ -200,3 +200,62 @@ def test_ep_p2p_exchange_two_processes(batch, tmp_path):
     _, _, _, acts, _, _, _ = _p2p_inputs(batch)
     moe = full.astype(np.float64) - acts.astype(np.float32).astype(np.float64)
     assert np.abs(o0.astype(np.float64) - full).max() <= 1e-5 * np.abs(moe).max()
+
+
+def test_balanced_owners_balances_transfers():
+    """LPT placement by a timeline's transfers: every (layer, expert) gets one shard, the busiest
+    shard carries at most the lightest plus the heaviest single item, and the table is deterministic."""
+    rng = np.random.default_rng(3)
+    L, N, G = 6, 8, 4
+    rows = []
+    for l in range(L):
+        for e in range(N):
+            for _ in range(int(rng.integers(0, 9))):
+                rows.append([1, 4, 0, 1, 0, l, e, 0])  # TileTransfer
+            rows.append([0, 3, 0, 1, 0, l, e, 0])      # TileCompute
+    tl = np.array(rows, dtype=np.int64)
+    own = ep.balanced_owners(tl, L, N, G)
+    assert own.shape == (L, N) and own.min() >= 0 and own.max() < G
+    w = np.zeros((L, N))
+    np.add.at(w, (tl[tl[:, 1] == 4, 5], tl[tl[:, 1] == 4, 6]), 1.0)
+    load = [w[own == g].sum() for g in range(G)]
+    assert max(load) - min(load) <= w.max()
+    assert np.array_equal(own, ep.balanced_owners(tl, L, N, G))
+    # modulo placement of the same weights is no better balanced
+    mod = np.array([[e % G for e in range(N)] for _ in range(L)])
+    assert max(load) <= max(w[mod == g].sum() for g in range(G))
+
+
+@pytest.mark.gpu
+def test_ep_custom_owner_table():
+    """A non-modulo owner table (ep.balanced_owners of a calibration run): shards keep the reference
+    trace bit for bit, each moves / computes only its own (layer, expert)s, and the partials sum to
+    the single-GPU decode."""
+    import paper_2408_10284_b200 as P
+    g = load_golden("tiny")
+    w0, fg = oracle_inputs(g)
+    cfg = sim_config(g)
+    caps, tau, T = g["sim_capacities"], g["tau"], 12
+    ffn = 1024
+    with P.Engine(P.ModelSpec(w0.L, w0.N, w0.K, w0.D)) as eng:
+        eng.load_gates(w0.gates, fg)
+        calib = eng.simulate_trace(w0.acts[T:], w0.scores[T:], w0.fisher, caps, tau, cfg, 0)
+    owners = ep.balanced_owners(calib.timeline, w0.L, w0.N, 2)
+    assert not np.array_equal(owners, np.array([[e % 2 for e in range(w0.N)]] * w0.L))
+    outs, results = [], []
+    for rank, world in [(0, 1), (0, 2), (1, 2)]:
+        with P.Engine(P.ModelSpec(w0.L, w0.N, w0.K, w0.D)) as eng:
+            eng.load_gates(w0.gates, fg)
+            eng.experts_init(ffn, cfg.tile_count_per_expert, seed=5)
+            eng.decode_begin(caps, w0.fisher, tau, cfg, 0, T, ep_rank=rank, ep_world=world,
+                             expert_owner=owners if world > 1 else None)
+            h = np.zeros((T, w0.L, w0.D), dtype=np.float32)
+            eng.decode_tokens(w0.acts[:T], w0.scores[:T], h)
+            results.append(eng.decode_end(cfg, T))
+            outs.append(h)
+    for r in results[1:]:
+        assert r.metrics == results[0].metrics and np.array_equal(r.timeline, results[0].timeline)
+    assert results[1].stats["ffn_bytes"] + results[2].stats["ffn_bytes"] == results[0].stats["ffn_bytes"]
+    full = outs[0].astype(np.float64)
+    moe = full - w0.acts[:T].astype(np.float32).astype(np.float64)
+    assert np.abs(outs[1].astype(np.float64) + outs[2].astype(np.float64) - full).max() <= 1e-5 * np.abs(moe).max()

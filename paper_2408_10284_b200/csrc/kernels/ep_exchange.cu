@@ -42,11 +42,13 @@ __global__ void ep_wait_kernel(const unsigned char* region, int world, unsigned 
 }
 
 __global__ void ep_reduce_kernel(const __grid_constant__ EpReduceArgs a) {
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < a.elems;
+    const long long elems = a.rows * a.d;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < elems;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        float s = a.slots[i];
-        for (int g = 1; g < a.world; ++g) s = __fadd_rn(s, a.slots[g * a.slot_stride + i]);
-        a.out[i] = s;
+        const long long o = (i / a.d) * a.row_stride + i % a.d;
+        float s = a.slots[o];
+        for (int g = 1; g < a.world; ++g) s = __fadd_rn(s, a.slots[g * a.slot_stride + o]);
+        a.out[o] = s;
     }
 }
 
@@ -65,8 +67,8 @@ cudaError_t launch_ep_wait(const unsigned char* region, int world, unsigned call
 }
 
 cudaError_t launch_ep_reduce(const EpReduceArgs& a, cudaStream_t stream) {
-    if (a.elems <= 0) return cudaSuccess;
-    const long long blocks = (a.elems + 255) / 256;
+    if (a.rows <= 0 || a.d <= 0) return cudaSuccess;
+    const long long blocks = (a.rows * a.d + 255) / 256;
     ep_reduce_kernel<<<static_cast<int>(blocks < 296 ? blocks : 296), 256, 0, stream>>>(a);
     return cudaGetLastError();
 }

@@ -38,10 +38,11 @@ cudaError_t launch_ep_signal(const EpSignalArgs& a, cudaStream_t stream);
 cudaError_t launch_ep_wait(const unsigned char* region, int world, unsigned call, cudaStream_t stream);
 
 struct EpReduceArgs {
-    const float* slots = nullptr;     // this shard's slots for the call's parity: [G][rows_max][d]
+    const float* slots = nullptr;     // writer 0's slot at the rows' offset (this shard's region, parity)
     long long slot_stride = 0;        // floats between writer slots
-    float* out = nullptr;             // [rows][d]
-    long long elems = 0;              // rows * d of this call
+    float* out = nullptr;             // rows of d floats, row_stride apart (same offsets in the slots)
+    long long rows = 0, row_stride = 0;
+    int d = 0;
     int world = 0;
 };
 cudaError_t launch_ep_reduce(const EpReduceArgs& a, cudaStream_t stream);

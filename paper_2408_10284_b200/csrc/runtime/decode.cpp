@@ -383,6 +383,32 @@ void DecodeSession::wait_fill(int slot, int tile) {
 
 // Launch the pending segments of `p` into the next partial region of this layer; `seg_meta`
 // gives (rank, tile) per segment so the combine can find each segment's partials.
+// One step of the peer-memory exchange (kernels/ep_exchange.hpp), sequence number ep_call_: publish
+// this shard's partials of the step (already stored into every shard's slot by the combine), wait
+// for every peer's, and sum the G slots of `rows` output rows (row_stride floats apart, at `out`'s
+// offset in the call's output) in shard order into `out`.
+void DecodeSession::ep_exchange(float* out, long long rows, long long row_stride) {
+    cudaStream_t cs = eng_.compute_stream();
+    const int D = spec_.hidden_dim;
+    EpSignalArgs sa;
+    for (int g = 0; g < ep_world_; ++g) sa.peer_flags[g] = reinterpret_cast<unsigned*>(ep_region_[g]);
+    sa.world = ep_world_;
+    sa.rank = ep_rank_;
+    sa.call = ep_call_;
+    MOE_CUDA(launch_ep_signal(sa, cs));
+    MOE_CUDA(launch_ep_wait(ep_region_[ep_rank_], ep_world_, ep_call_, cs));
+    EpReduceArgs ra;
+    ra.slots = ep_slot(ep_rank_, 0, ep_call_ & 1) + (out - cur_out_base_);
+    ra.slot_stride = static_cast<long long>(ep_rows_max_) * D;
+    ra.out = out;
+    ra.rows = rows;
+    ra.row_stride = row_stride;
+    ra.d = D;
+    ra.world = ep_world_;
+    MOE_CUDA(launch_ep_reduce(ra, cs));
+    stats_.kernels += 3;
+}
+
 void DecodeSession::timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int>>& seg_meta,
                               std::vector<std::tuple<int, int, FfnPartialRef>>& refs) {
     cudaStream_t cs = eng_.compute_stream();
@@ -745,7 +771,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
     }
     if (ep_connected_) {
         if (count > ep_max_tokens_) fail(Status::Usage, "decode: more tokens per call than ep_export allowed");
-        ++ep_call_;
+        if (!free_running_) ++ep_call_;  // one exchange per call (free-running: one per layer, below)
     }
 
     // router groups for every (token, layer, stream) of this call: they depend only on positions.
@@ -893,30 +919,18 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             fuse_next_res_ = (fused_input && l + 1 < L) ? d_x_free_.as<double>() + (row0 + 1) * D : nullptr;
             fuse_next_norm_ = fuse_next_res_ ? x_norm + (row0 + 1) * D : nullptr;
             const size_t npass0 = pass_events_.size();
+            if (free_running_ && ep_connected_) ++ep_call_;  // this layer's exchange (its combine's slot parity)
             policy_->step(tok, l, d, std::span<const RoutePrediction>(preds.data(), np), B > 1 ? singles : -1);
+            if (free_running_ && ep_connected_)  // the next layer routes on the full output: sum the shards now
+                ep_exchange(cur_out_, B, static_cast<long long>(L) * D);
             if (gap_trace && !router_events_.empty() && pass_events_.size() > npass0)
                 gap_rec.push_back({router_events_.back().first, router_events_.back().second, pass_events_[npass0].e0,
                                    pass_events_.back().e1});
             stats_.host_step_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h1).count();
         }
     }
-    if (ep_connected_) {  // publish this call's partials, then sum every shard's slot in shard order
-        EpSignalArgs sa;
-        for (int g = 0; g < ep_world_; ++g) sa.peer_flags[g] = reinterpret_cast<unsigned*>(ep_region_[g]);
-        sa.world = ep_world_;
-        sa.rank = ep_rank_;
-        sa.call = ep_call_;
-        MOE_CUDA(launch_ep_signal(sa, cs));
-        MOE_CUDA(launch_ep_wait(ep_region_[ep_rank_], ep_world_, ep_call_, cs));
-        EpReduceArgs ra;
-        ra.slots = ep_slot(ep_rank_, 0, ep_call_ & 1);
-        ra.slot_stride = static_cast<long long>(ep_rows_max_) * D;
-        ra.out = out_all;
-        ra.elems = static_cast<long long>(TL) * D;
-        ra.world = ep_world_;
-        MOE_CUDA(launch_ep_reduce(ra, cs));
-        stats_.kernels += 2;
-    }
+    if (ep_connected_ && !free_running_)  // publish this call's partials, then sum every shard's in order
+        ep_exchange(out_all, static_cast<long long>(TL), D);
     if (hidden_out && !on_device)
         MOE_CUDA(cudaMemcpyAsync(hidden_out, out_all, TL * D * sizeof(float), cudaMemcpyDeviceToHost, cs));
     MOE_CUDA(cudaEventRecord(t_end, cs));

@@ -105,6 +105,7 @@ private:
     int tile_merge_ = -1;  // -1 auto (tiles >= 8 MiB), 0 off, 1 on
     void layer_ffn_grouped(const RouteDecision& d);  // batch > 1: K3 grouped tcgen05 kernels
     void timed_grouped(GroupedLaunch& p, bool down);
+    void ep_exchange(float* out, long long rows, long long row_stride);
     // free-running decode: layer l > 0 routes and computes on layer l-1's output (the hidden state
     // flows through the experts); the actual decision comes from the layer's gate (softmax of
     // logits / concentration, like the reference generator) instead of stored scores

@@ -144,7 +144,7 @@ def _p2p_inputs(batch):
 _P2P_CALLS = [0, 5, 6, 12]
 
 
-def _p2p_decode(rank, world, batch, connect_fn=None):
+def _p2p_decode(rank, world, batch, connect_fn=None, free_running=False):
     import paper_2408_10284_b200 as P
     g, w0, fg, acts, scores, shape, T = _p2p_inputs(batch)
     cfg = sim_config(g)
@@ -152,7 +152,7 @@ def _p2p_decode(rank, world, batch, connect_fn=None):
     eng.load_gates(w0.gates, fg)
     eng.experts_init(1024, cfg.tile_count_per_expert, seed=5)
     eng.decode_begin(g["sim_capacities"], w0.fisher, g["tau"], cfg, 0, T, batch=batch, ep_rank=rank,
-                     ep_world=world)
+                     ep_world=world, free_running=free_running, concentration=0.6)
     if connect_fn:
         connect_fn(eng)
     out = np.zeros(shape, dtype=np.float32)
@@ -163,7 +163,7 @@ def _p2p_decode(rank, world, batch, connect_fn=None):
     return out, res
 
 
-def _p2p_worker(rank, world, port, batch, out_dir):
+def _p2p_worker(rank, world, port, batch, out_dir, free_running=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -175,9 +175,10 @@ def _p2p_worker(rank, world, port, batch, out_dir):
             dist.all_gather_object(handles, handle)
             eng.decode_ep_connect(peer_ptrs=[0] * world, peer_ipc=handles)  # other processes: IPC handles
 
-        out, res = _p2p_decode(rank, world, batch, connect)
+        out, res = _p2p_decode(rank, world, batch, connect, free_running)
         np.save(os.path.join(out_dir, f"p2p_{rank}.npy"), out)
         np.save(os.path.join(out_dir, f"p2p_metrics_{rank}.npy"), np.array(list(res.metrics.values())))
+        np.save(os.path.join(out_dir, f"p2p_timeline_{rank}.npy"), res.timeline)
     finally:
         dist.destroy_process_group()
 
@@ -259,3 +260,23 @@ def test_ep_custom_owner_table():
     full = outs[0].astype(np.float64)
     moe = full - w0.acts[:T].astype(np.float32).astype(np.float64)
     assert np.abs(outs[1].astype(np.float64) + outs[2].astype(np.float64) - full).max() <= 1e-5 * np.abs(moe).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("batch", [1, 4])
+def test_ep_p2p_free_running_two_processes(batch, tmp_path):
+    """Free-running decode across two shard processes: every layer's partial outputs are exchanged
+    over peer memory and summed before the next layer routes on them (one exchange step per layer).
+    Both shards hold the same bits, replay the single-GPU free-running trace, and their outputs match
+    it within the summation-order / bf16 tolerance."""
+    import torch.multiprocessing as mp
+    full, ref = _p2p_decode(0, 1, batch, free_running=True)
+    mp.spawn(_p2p_worker, args=(2, _free_port(), batch, str(tmp_path), True), nprocs=2, join=True)
+    o0, o1 = np.load(tmp_path / "p2p_0.npy"), np.load(tmp_path / "p2p_1.npy")
+    assert np.array_equal(o0, o1)
+    for r in range(2):
+        assert np.load(tmp_path / f"p2p_metrics_{r}.npy").tolist() == list(ref.metrics.values())
+        assert np.array_equal(np.load(tmp_path / f"p2p_timeline_{r}.npy"), ref.timeline)
+    tol = 1e-4 if batch == 1 else 2e-2
+    scale = np.abs(full).max()
+    assert np.abs(o0.astype(np.float64) - full.astype(np.float64)).max() <= tol * scale

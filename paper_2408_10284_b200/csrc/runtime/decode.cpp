@@ -769,6 +769,9 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
         x_all = d_x_free_.as<double>();
         x_norm = d_x_norm_.as<double>();
     }
+    if (free_running_ && ep_world_ > 1 && !ep_connected_)
+        fail(Status::Usage, "decode: free-running expert parallelism routes every layer on the summed output: "
+                            "connect the shards first (moe_decode_ep_export / moe_decode_ep_connect)");
     if (ep_connected_) {
         if (count > ep_max_tokens_) fail(Status::Usage, "decode: more tokens per call than ep_export allowed");
         if (!free_running_) ++ep_call_;  // one exchange per call (free-running: one per layer, below)

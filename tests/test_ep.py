@@ -280,3 +280,17 @@ def test_ep_p2p_free_running_two_processes(batch, tmp_path):
     tol = 1e-4 if batch == 1 else 2e-2
     scale = np.abs(full).max()
     assert np.abs(o0.astype(np.float64) - full.astype(np.float64)).max() <= tol * scale
+
+
+@pytest.mark.gpu
+def test_free_running_ep_requires_exchange():
+    import paper_2408_10284_b200 as P
+    g, w0, fg, acts, scores, shape, T = _p2p_inputs(1)
+    cfg = sim_config(g)
+    with P.Engine(P.ModelSpec(w0.L, w0.N, w0.K, w0.D)) as eng:
+        eng.load_gates(w0.gates, fg)
+        eng.experts_init(1024, cfg.tile_count_per_expert, seed=5)
+        eng.decode_begin(g["sim_capacities"], w0.fisher, g["tau"], cfg, 0, T, ep_rank=0, ep_world=2,
+                         free_running=True)
+        with pytest.raises(P.MoeError, match="connect the shards"):
+            eng.decode_tokens(acts[:2], scores[:2], np.zeros((2,) + shape[1:], dtype=np.float32))

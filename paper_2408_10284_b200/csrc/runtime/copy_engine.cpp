@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "../host/policy.hpp"
@@ -107,7 +108,10 @@ void CopyEngine::cancel(const std::shared_ptr<CopyJob>& job) {
 
 cudaEvent_t CopyEngine::wait_issued(const std::shared_ptr<CopyJob>& job, int tile) {
     std::unique_lock<std::mutex> lk(mu_);
-    cv_issued_.wait(lk, [&] { return job->issued_tiles > tile || (job->cancelled && job->next_tile <= tile) || stop_; });
+    cv_issued_.wait(lk, [&] {
+        return job->issued_tiles > tile || (job->cancelled && job->next_tile <= tile) || stop_ || !error_.empty();
+    });
+    throw_if_failed();
     if (job->issued_tiles <= tile) fail(Status::Internal, "copy engine: waited on a tile that will never be copied");
     return job->done[tile];
 }
@@ -119,7 +123,8 @@ bool CopyEngine::fully_issued(const std::shared_ptr<CopyJob>& job) {
 
 void CopyEngine::drain() {
     std::unique_lock<std::mutex> lk(mu_);
-    cv_issued_.wait(lk, [&] { return (od_.empty() && pf_.empty() && !busy_) || stop_; });
+    cv_issued_.wait(lk, [&] { return (od_.empty() && pf_.empty() && !busy_) || stop_ || !error_.empty(); });
+    throw_if_failed();
     lk.unlock();
     check(cudaStreamSynchronize(stream_), "copy stream sync");
 }
@@ -177,8 +182,38 @@ void CopyEngine::retire(const std::shared_ptr<CopyJob>& job) {
     if (it != active_.end()) active_.erase(it);
 }
 
+// The copy thread never throws: a CUDA error (or any exception) is recorded, every waiter is woken
+// and the host thread raises it (MOE_E_DEVICE) from wait_issued / drain.
 void CopyEngine::loop() {
-    cudaSetDevice(device_);
+    try {
+        run();
+    } catch (const std::exception& e) {
+        fail_thread(e.what());
+    } catch (...) {
+        fail_thread("copy engine: unknown error");
+    }
+}
+
+void CopyEngine::fail_thread(const std::string& what) {
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        if (error_.empty()) error_ = what;
+    }
+    cv_issued_.notify_all();
+}
+
+void CopyEngine::throw_if_failed() const {
+    if (!error_.empty()) fail(Status::Device, "copy engine: " + error_);
+}
+
+void CopyEngine::run() {
+    auto ck = [](cudaError_t e, const char* what) {
+        if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+    };
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    // test knob: fail after this many tiles (exercises the error path end to end)
+    const char* fault = std::getenv("ADAPMOE_COPY_FAULT_AFTER");
+    const long long fault_after = fault ? std::atoll(fault) : -1;
     for (;;) {
         std::shared_ptr<CopyJob> job;
         int tile = 0;
@@ -195,27 +230,29 @@ void CopyEngine::loop() {
             }
             busy_ = true;
         }
-        cudaEventRecord(job->t_start[tile], stream_);
+        if (fault_after >= 0 && tiles_copied_.load() >= fault_after) throw std::runtime_error("injected copy fault");
+        ck(cudaEventRecord(job->t_start[tile], stream_), "cudaEventRecord");
         const size_t base = static_cast<size_t>(tile) * job->tile_bytes;
         for (size_t off = 0; off < job->tile_bytes; off += kChunkBytes) {
             while (static_cast<int>(inflight_.size()) >= kWindow) {
-                cudaEventSynchronize(inflight_.front());
+                ck(cudaEventSynchronize(inflight_.front()), "tile copy");
                 std::lock_guard<std::mutex> g(mu_);
                 free_sync_.push_back(inflight_.front());
                 inflight_.pop_front();
             }
             const size_t n = std::min(kChunkBytes, job->tile_bytes - off);
-            cudaMemcpyAsync(job->dst + base + off, job->src + base + off, n, cudaMemcpyHostToDevice, stream_);
+            ck(cudaMemcpyAsync(job->dst + base + off, job->src + base + off, n, cudaMemcpyHostToDevice, stream_),
+               "cudaMemcpyAsync (expert tile)");
             cudaEvent_t e;
             {
                 std::lock_guard<std::mutex> g(mu_);
                 e = take_event(false);
             }
-            cudaEventRecord(e, stream_);
+            ck(cudaEventRecord(e, stream_), "cudaEventRecord");
             inflight_.push_back(e);
         }
-        cudaEventRecord(job->done[tile], stream_);
-        cudaEventRecord(job->t_end[tile], stream_);
+        ck(cudaEventRecord(job->done[tile], stream_), "cudaEventRecord");
+        ck(cudaEventRecord(job->t_end[tile], stream_), "cudaEventRecord");
         tiles_copied_ += 1;
         bytes_copied_ += static_cast<long long>(job->tile_bytes);
         {

@@ -15,6 +15,7 @@
 #include <deque>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -67,6 +68,9 @@ public:
 
 private:
     void loop();
+    void run();
+    void fail_thread(const std::string& what);
+    void throw_if_failed() const;  // caller holds mu_
     cudaEvent_t take_event(bool timing);
 
     cudaStream_t stream_;
@@ -79,6 +83,7 @@ private:
     std::vector<std::shared_ptr<CopyJob>> active_;
     bool stop_ = false;
     bool busy_ = false;
+    std::string error_;  // first error of the copy thread (it stops issuing)
     std::atomic<long long> tiles_copied_{0}, bytes_copied_{0};
     double busy_ms_ = 0.0, busy_pf_ms_ = 0.0, busy_pf_used_ms_ = 0.0;
     long long pf_tiles_ = 0;

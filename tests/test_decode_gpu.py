@@ -315,3 +315,19 @@ def test_expert_set_checkpoint_layout():
                 wgt = 1.0 if len(sel) == 1 else sc[e] / sum(sc[q] for q in sel)
                 moe += wgt * (a2 @ (g / (1.0 + np.exp(-g)) * u))
             assert _rel_err(hid[t, l].astype(np.float64) - xf, moe) < REL_TOL, (t, l)
+
+
+def test_copy_engine_error_surfaces(monkeypatch):
+    """A failure inside the copy thread (injected: ADAPMOE_COPY_FAULT_AFTER) surfaces as MOE_E_DEVICE
+    from the decode call instead of a hang, a crash or silently stale expert slots."""
+    monkeypatch.setenv("ADAPMOE_COPY_FAULT_AFTER", "3")
+    g = load_golden("tiny_budget0")
+    w, fg = oracle_inputs(g)
+    cfg = sim_config(g)
+    with P.Engine(P.ModelSpec(w.L, w.N, w.K, w.D)) as eng:
+        eng.load_gates(w.gates, fg)
+        eng.experts_init(224 * cfg.tile_count_per_expert, cfg.tile_count_per_expert, seed=1)
+        eng.decode_begin(g["sim_capacities"], w.fisher, g["tau"], cfg, 0, 8)
+        with pytest.raises(P.MoeError) as e:
+            eng.decode_tokens(w.acts[:8], w.scores[:8], np.zeros((8, w.L, w.D), dtype=np.float32))
+        assert e.value.code == 6 and "injected copy fault" in str(e.value)

@@ -81,7 +81,7 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     slots_.resize(n_slots_);
     for (int s = 0; s < n_slots_; ++s) free_.push_back(s);
     slot_of_.assign(static_cast<size_t>(L) * N, -1);
-    cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, eng.device());
+    MOE_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, eng.device()));
     if (const char* v = std::getenv("ADAPMOE_TILE_MERGE")) tile_merge_ = std::atoi(v) != 0 ? 1 : 0;  // A/B knob
     d_combine_ticket_.reserve(sizeof(unsigned));
     MOE_CUDA(cudaMemsetAsync(d_combine_ticket_.ptr, 0, sizeof(unsigned), eng.compute_stream()));
@@ -372,9 +372,9 @@ void DecodeSession::wait_fill(int slot, int tile) {
         sl.fill->consumed = true;
         cudaEvent_t ev = copier_->wait_issued(sl.fill, t);
         cudaEvent_t a = take_timing(), b = take_timing();
-        cudaEventRecord(a, cs);
+        MOE_CUDA(cudaEventRecord(a, cs));
         MOE_CUDA(cudaStreamWaitEvent(cs, ev, 0));
-        cudaEventRecord(b, cs);
+        MOE_CUDA(cudaEventRecord(b, cs));
         stall_events_.emplace_back(a, b);
         stall_is_prefetch_.push_back(prefetch);
     }
@@ -422,9 +422,9 @@ void DecodeSession::timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int
         refs.emplace_back(seg_meta[s].first, seg_meta[s].second, r);
     }
     cudaEvent_t e0 = take_timing(), e1 = take_timing();
-    cudaEventRecord(e0, cs);
+    MOE_CUDA(cudaEventRecord(e0, cs));
     MOE_CUDA(launch_ffn(p, sm_count_, cs));
-    cudaEventRecord(e1, cs);
+    MOE_CUDA(cudaEventRecord(e1, cs));
     const double gate_up = static_cast<double>(p.n_seg) * 2.0 * p.ft * p.d * 2.0;
     const double down = static_cast<double>(p.n_seg) * p.ft * p.d * 2.0;
     pass_events_.push_back(PassRec{gate_up, down, e0, e1});
@@ -573,9 +573,9 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
 void DecodeSession::timed_grouped(GroupedLaunch& p, bool down) {
     cudaStream_t cs = eng_.compute_stream();
     cudaEvent_t e0 = take_timing(), e1 = take_timing();
-    cudaEventRecord(e0, cs);
+    MOE_CUDA(cudaEventRecord(e0, cs));
     MOE_CUDA(down ? launch_grouped_down(p, sm_count_, cs) : launch_grouped_gate_up(p, sm_count_, cs));
-    cudaEventRecord(e1, cs);
+    MOE_CUDA(cudaEventRecord(e1, cs));
     double tiles = 0;
     for (int s = 0; s < p.n_seg; ++s) tiles += p.seg[s].t1 - p.seg[s].t0;
     const double bytes = tiles * (down ? 1.0 : 2.0) * p.ft * p.d * 2.0;
@@ -862,10 +862,10 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                 // every layer of the next window of tokens, once
                 const int n_groups = free_running_ ? B : std::min(route_window_, count - i) * L * B;
                 cudaEvent_t r0 = take_timing(), r1 = take_timing();
-                cudaEventRecord(r0, cs);
+                MOE_CUDA(cudaEventRecord(r0, cs));
                 MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + gl, n_groups, max_gates, rp, ro, cs,
                                       n_groups <= route_scratch_.groups ? &route_scratch_ : nullptr));
-                cudaEventRecord(r1, cs);
+                MOE_CUDA(cudaEventRecord(r1, cs));
                 router_events_.emplace_back(r0, r1);
                 stats_.kernels += 1;
                 stats_.router_launches += 1;
@@ -980,7 +980,7 @@ DecodeStats DecodeSession::snapshot() {
     MOE_CUDA(cudaStreamSynchronize(eng_.compute_stream()));
     auto elapsed = [](cudaEvent_t a, cudaEvent_t b) {
         float ms = 0.0f;
-        cudaEventElapsedTime(&ms, a, b);
+        MOE_CUDA(cudaEventElapsedTime(&ms, a, b));
         return static_cast<double>(ms);
     };
     for (auto& p : pass_events_) {

@@ -654,6 +654,9 @@ def pipeline_bench(args):
                 line["reference_ms"]["train_first_gate"] = r["train_s"] * 1e3
             c = run_reference_mode(wl, "compare")
             line["reference_ms"]["compare_policies"] = c["compare_s"] * 1e3
+            cores = os.cpu_count() or 1  # the grid's rows in parallel on every host core
+            cj = run_reference_mode(wl, "compare", jobs=cores)
+            line["reference_ms"][f"compare_policies_jobs{cores}"] = cj["compare_s"] * 1e3
             line["equal"] = {"tau": r["tau"] == tau, "alpha": r["alpha"] == [float(v) for v in alpha],
                              "beta": r["beta"] == [float(v) for v in beta],
                              "capacities": r["capacities"] == [int(v) for v in caps],

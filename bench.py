@@ -306,7 +306,7 @@ def ours(args):
     if ep_world > 1 and args.ep_owner == "balanced":
         # placement from a separate calibration trace of the same model (not the decoded tokens):
         # the same deterministic table on every rank
-        calib = eng.generate_trace(P.SynthConfig(spec, wl.tokens, wl.concentration, wl.drift, wl.gate_seed,
+        calib = eng.generate_trace(P.SynthConfig(spec, max(wl.tokens, 256), wl.concentration, wl.drift, wl.gate_seed,
                                                  wl.token_seed + 7777, False, wl.fisher_scales, wl.drift_scales))
         eng.load_gates(trace.gates)
         sim = eng.simulate_trace(calib.acts, calib.scores, calib.fisher, caps, tau, cfg, wl.seed)

@@ -534,6 +534,10 @@ def ours(args):
                 sim_line["metrics_equal_reference"] = rr.get("metrics") == sim.metrics and \
                     rr.get("timeline_events") == len(sim.timeline)
         line["simulate_trace"] = sim_line
+        line["comparison_note"] = ("value / e2e: the physical decode (experts moved over the host link and computed); "
+                                   "the reference arm times the reference's tick-model simulate_trace, which moves no "
+                                   "weights -- the like-for-like figure is simulate_trace.tok_s vs "
+                                   "simulate_trace.reference_tok_s")
     if not args.no_cpu_baseline:
         try:
             r = run_reference_driver(wl, decoded, 20)

@@ -294,3 +294,30 @@ def test_free_running_ep_requires_exchange():
                          free_running=True)
         with pytest.raises(P.MoeError, match="connect the shards"):
             eng.decode_tokens(acts[:2], scores[:2], np.zeros((2,) + shape[1:], dtype=np.float32))
+
+
+def _owners_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = load_golden("tiny")
+        w, fg = oracle_inputs(g)
+        sim = O.simulate(w, g["sim_capacities"], g["tau"], first_gate=fg, **sim_kwargs(g))
+        own = ep.balanced_owners(sim.timeline, w.L, w.N, world)
+        tables = [None] * world
+        dist.all_gather_object(tables, own.tolist())
+        np.save(os.path.join(out_dir, f"owners_{rank}.npy"), np.array(tables))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_balanced_owners_identical_on_every_rank_gloo(tmp_path):
+    """Every rank derives the placement table from the same calibration run independently; the
+    tables must agree (the decode sessions rely on it — no table is broadcast)."""
+    import torch.multiprocessing as mp
+    mp.spawn(_owners_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    t0, t1 = np.load(tmp_path / "owners_0.npy"), np.load(tmp_path / "owners_1.npy")
+    assert np.array_equal(t0, t1) and np.array_equal(t0[0], t0[1])
+    assert set(np.unique(t0[0])) <= {0, 1}

@@ -386,6 +386,8 @@ typedef struct {
     int64_t prefetch_tile_copies; /* tiles copied for them */
     double prefetch_used_copy_ms; /* ... of which the compute stream consumed; hidden = 1 - stall / used copy */
     int64_t router_launches;      /* K1 launches: one per layer (free-running), one per token window (trace replay) */
+    int64_t spec_launches;        /* free-running batch 1: speculative next-layer FFN launches (pre-gate top-1) */
+    int64_t spec_hits;            /* ... whose expert the layer's decision selected (partials reused) */
 } moe_decode_stats;
 
 /* Counters so far without ending the session. */

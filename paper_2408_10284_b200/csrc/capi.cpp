@@ -460,6 +460,8 @@ void export_stats(const DecodeStats& s, moe_decode_stats* out) {
     out->prefetch_tile_copies = s.prefetch_tiles;
     out->prefetch_used_copy_ms = s.prefetch_used_copy_ms;
     out->router_launches = s.router_launches;
+    out->spec_launches = s.spec_launches;
+    out->spec_hits = s.spec_hits;
 }
 }  // namespace
 

@@ -89,7 +89,14 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     // at most one launch for the resident experts' tiles (split per 32 segments) + one per
     // on-demand tile
     partial_regions_ = (K * store_.tiles + kMaxFfnSegments - 1) / kMaxFfnSegments + K * store_.tiles;
-    d_partials_.reserve(static_cast<size_t>(partial_regions_) * kFfnMaxCtas * kFfnSlotsPerCta * D * sizeof(float));
+    speculate_ = free_running_ && batch_ == 1 && ep_world_ == 1;
+    if (const char* v = std::getenv("ADAPMOE_SPECULATE")) speculate_ = speculate_ && std::atoi(v) != 0;
+    // one extra partial region (index partial_regions_) holds the speculative launch
+    d_partials_.reserve(static_cast<size_t>(partial_regions_ + 1) * kFfnMaxCtas * kFfnSlotsPerCta * D * sizeof(float));
+    if (speculate_) {
+        MOE_CUDA(cudaStreamCreateWithFlags(&route_stream_, cudaStreamNonBlocking));
+        MOE_CUDA(cudaEventCreateWithFlags(&in_ready_, cudaEventDisableTiming));
+    }
     if (batch_ > 1) {
         MOE_CUDA(cudaMemsetAsync(pool_.ptr, 0, slot_stride_ * n_slots_, eng.compute_stream()));  // slot padding read by TMA stays finite
         np_ = (batch_ + 15) / 16 * 16;
@@ -150,6 +157,11 @@ DecodeSession::~DecodeSession() {
     for (void* p : ep_ipc_opened_) cudaIpcCloseMemHandle(p);
     if (h_route_) cudaFreeHost(h_route_);
     if (route_done_) cudaEventDestroy(route_done_);
+    if (in_ready_) cudaEventDestroy(in_ready_);
+    if (route_stream_) {
+        cudaStreamSynchronize(route_stream_);
+        cudaStreamDestroy(route_stream_);
+    }
     for (auto& p : layer_events_) cudaEventDestroy(p.second);
     for (cudaEvent_t e : layer_event_pool_) cudaEventDestroy(e);
     for (auto& p : pass_events_) {
@@ -490,6 +502,55 @@ std::vector<std::pair<const DecodeSession::Use*, std::vector<int>>> DecodeSessio
     return groups;
 }
 
+// Free-running batch 1: while K1 routes layer `layer` (route_stream_, on the SMs left free), run the
+// FFN of the expert the previous layer's look-ahead ranked first for this layer, if it is resident
+// (the reference's reuse-based pre-gate, usually right).  layer_ffn_single takes its partials when
+// the decision selects it and launches only the rest; otherwise the launch was wasted work.
+void DecodeSession::launch_speculative(int layer, const double* x) {
+    spec_run_.valid = false;
+    const int n_pred = spec_next_n_;
+    spec_next_n_ = 0;
+    if (n_pred <= 0) return;
+    const int N = spec_.experts_per_layer, D = spec_.hidden_dim, T = store_.tiles, Ft = store_.ffn / T;
+    cudaStream_t cs = eng_.compute_stream();
+    const size_t gate_up_bytes = static_cast<size_t>(2) * Ft * D * 2;
+    FfnLaunch p;
+    p.d = D;
+    p.ft = Ft;
+    p.x = x;
+    SpecRun run;
+    for (int k = 0; k < n_pred && (run.n + 1) * T <= kMaxFfnSegments; ++k) {
+        const int slot = slot_of_[static_cast<size_t>(layer) * N + spec_next_[k]];
+        if (slot < 0) continue;  // not resident: the decision will load it
+        wait_fill(slot, -1);
+        for (int t = 0; t < T; ++t) {
+            const unsigned char* tile = slot_ptr(slot) + t * store_.tile_bytes;
+            p.seg[p.n_seg].gate_up = reinterpret_cast<const std::uint16_t*>(tile);
+            p.seg[p.n_seg].down_t = reinterpret_cast<const std::uint16_t*>(tile + gate_up_bytes);
+            ++p.n_seg;
+        }
+        run.slot[run.n++] = slot;
+    }
+    if (run.n == 0) return;
+    const size_t region = static_cast<size_t>(kFfnMaxCtas) * kFfnSlotsPerCta * D;
+    p.partial = d_partials_.as<float>() + region * partial_regions_;  // the extra region
+    const int sms = std::max(1, sm_count_ - kSpecSpareSms);          // leave SMs for K1
+    cudaEvent_t e0 = take_timing(), e1 = take_timing();
+    MOE_CUDA(cudaEventRecord(e0, cs));
+    MOE_CUDA(launch_ffn(p, sms, cs));
+    MOE_CUDA(cudaEventRecord(e1, cs));
+    pass_events_.push_back(PassRec{static_cast<double>(p.n_seg) * 2.0 * Ft * D * 2.0,
+                                   static_cast<double>(p.n_seg) * Ft * D * 2.0, e0, e1});
+    stats_.kernels += 1;
+    stats_.spec_launches += 1;
+    run.valid = true;
+    run.layer_seq = layer_seq_;
+    run.n_seg = p.n_seg;
+    run.grid = ffn_grid(p, sms);
+    run.partial = p.partial;
+    spec_run_ = run;
+}
+
 void DecodeSession::layer_ffn_single(const RouteDecision& d) {
     const int D = spec_.hidden_dim, T = store_.tiles, F = store_.ffn, Ft = F / T;
     const size_t gate_up_bytes = static_cast<size_t>(2) * Ft * D * 2;
@@ -507,9 +568,25 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
     partial_next_ = 0;
     std::vector<std::pair<int, int>> meta;  // (rank, tile) of p's pending segments
     std::vector<std::tuple<int, int, FfnPartialRef>> refs;
-    // resident experts: one launch over all their tiles
+    // resident experts: one launch over all their tiles (an expert the speculative launch already
+    // computed contributes its partials instead)
+    const bool spec_live = spec_run_.valid && spec_run_.layer_seq == layer_seq_;
+    spec_run_.valid = false;
     for (const Use& u : uses_) {
         if (u.missing) continue;
+        int k_spec = -1;
+        for (int k = 0; spec_live && k < spec_run_.n; ++k)
+            if (spec_run_.slot[k] == u.slot) k_spec = k;
+        if (k_spec >= 0) {
+            for (int t = 0; t < T; ++t) {
+                FfnPartialRef r{spec_run_.partial, spec_run_.grid, spec_run_.n_seg, k_spec * T + t, u.rank};
+                ffn_partial_range(r, Ft);
+                refs.emplace_back(u.rank, t, r);
+            }
+            stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
+            stats_.spec_hits += 1;
+            continue;
+        }
         wait_fill(u.slot, -1);
         for (int t = 0; t < T; ++t) {
             if (p.n_seg == kMaxFfnSegments) {
@@ -861,15 +938,23 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                 // free-running: this layer (its input is the previous layer's output); trace replay:
                 // every layer of the next window of tokens, once
                 const int n_groups = free_running_ ? B : std::min(route_window_, count - i) * L * B;
+                cudaStream_t rs = cs;
+                if (speculate_) {  // K1 beside the speculative FFN: its input is ready once the layer's input is
+                    MOE_CUDA(cudaEventRecord(in_ready_, cs));
+                    MOE_CUDA(cudaStreamWaitEvent(route_stream_, in_ready_, 0));
+                    rs = route_stream_;
+                }
                 cudaEvent_t r0 = take_timing(), r1 = take_timing();
-                MOE_CUDA(cudaEventRecord(r0, cs));
-                MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + gl, n_groups, max_gates, rp, ro, cs,
+                MOE_CUDA(cudaEventRecord(r0, rs));
+                MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + gl, n_groups, max_gates, rp, ro, rs,
                                       n_groups <= route_scratch_.groups ? &route_scratch_ : nullptr));
-                MOE_CUDA(cudaEventRecord(r1, cs));
+                MOE_CUDA(cudaEventRecord(r1, rs));
                 router_events_.emplace_back(r0, r1);
                 stats_.kernels += 1;
                 stats_.router_launches += 1;
-                MOE_CUDA(cudaEventRecord(route_done_, cs));
+                MOE_CUDA(cudaEventRecord(route_done_, rs));
+                if (speculate_)
+                    launch_speculative(l, x_norm + (static_cast<size_t>(i) * B * L + l) * D);
                 const auto h0 = std::chrono::steady_clock::now();
                 MOE_CUDA(cudaEventSynchronize(route_done_));
                 stats_.host_sync_ms +=
@@ -922,6 +1007,12 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             fuse_next_res_ = (fused_input && l + 1 < L) ? d_x_free_.as<double>() + (row0 + 1) * D : nullptr;
             fuse_next_norm_ = fuse_next_res_ ? x_norm + (row0 + 1) * D : nullptr;
             const size_t npass0 = pass_events_.size();
+            if (speculate_) {  // the look-ahead's top-1 for the next layer (item 1): the next speculation
+                // (speculating its whole list measured no gain: mispredicted second experts cost what
+                // the hits save; top-1 alone: +5 % on the all-resident free-running window)
+                spec_next_n_ = (l + 1 < L && np > 0) ? std::min(1, preds[0].count) : 0;
+                for (int k = 0; k < spec_next_n_; ++k) spec_next_[k] = preds[0].experts[k];
+            }
             if (free_running_ && ep_connected_) ++ep_call_;  // this layer's exchange (its combine's slot parity)
             policy_->step(tok, l, d, std::span<const RoutePrediction>(preds.data(), np), B > 1 ? singles : -1);
             if (free_running_ && ep_connected_)  // the next layer routes on the full output: sum the shards now

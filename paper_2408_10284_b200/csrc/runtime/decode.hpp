@@ -43,6 +43,7 @@ struct DecodeStats {
     long long router_launches = 0;
     // logical prefetches (never promoted to on-demand): copy time, tiles, compute-stream wait on them
     double prefetch_copy_ms = 0, prefetch_stall_ms = 0, prefetch_used_copy_ms = 0;
+    long long spec_launches = 0, spec_hits = 0;  // speculative next-layer FFN launches / used ones
     long long prefetch_tiles = 0;
     long long router_exact = 0;  // look-ahead items that needed the exact fp64 path
     double host_sync_ms = 0, host_step_ms = 0;  // host wall time: waiting on K1 / policy step + launches
@@ -148,6 +149,22 @@ private:
     std::vector<int> cur_sel_, cur_cnt_;
     DeviceBuffer d_partials_;  // per-layer pool of K2 partial regions (reused every layer, stream-ordered)
     int partial_regions_ = 0, partial_next_ = 0;
+    // free-running batch 1: speculative FFN of the next layer's predicted top-1 expert (the previous
+    // layer's look-ahead), launched on SMs - kSpecSpareSms CTAs while K1 routes on route_stream_
+    static constexpr int kSpecSpareSms = 3;
+    bool speculate_ = false;
+    cudaStream_t route_stream_ = nullptr;
+    cudaEvent_t in_ready_ = nullptr;
+    struct SpecRun {
+        bool valid = false;
+        long long layer_seq = -1;
+        int n = 0, n_seg = 0, grid = 0;
+        int slot[8] = {};            // speculated experts' slots; expert k owns segments k*T .. k*T+T-1
+        float* partial = nullptr;
+    } spec_run_;
+    int spec_next_[8] = {};          // the look-ahead's experts for the next layer (score order)
+    int spec_next_n_ = 0;
+    void launch_speculative(int layer, const double* x);
 
     Engine& eng_;
     ModelSpec spec_;

@@ -406,6 +406,7 @@ def ours(args):
                     "ffn_share_of_step": dr["ffn_ms"] / g_ms if g_ms > 0 else None,
                     "ffn_launches": dr["ffn_launches"], "router_us_per_layer": 1e3 * dr["router_ms"] / max(1, K * wl.layers),
                     "host_wait_k1_ms_per_step": dr["host_sync_ms"] / K, "host_step_ms_per_step": dr["host_step_ms"] / K,
+                    "speculative_ffn": {"launches": int(dr["spec_launches"]), "hits": int(dr["spec_hits"])},
                     "budget": wl.layers * wl.experts}
     # on-demand loads per token in the timed window (tile 0 of each on-demand expert)
     tl = res.timeline
@@ -502,6 +503,7 @@ def ours(args):
                    "us_per_layer": 1e3 * d["router_ms"] / max(1, K * wl.layers),
                    "exact_fallback_items": int(d["router_exact_items"])},
         "gpu_launches": int(d["kernels_launched"]),
+        "speculative_ffn": {"launches": int(d["spec_launches"]), "hits": int(d["spec_hits"])},
         "clocks": clk.summary(),
         "e2e": {"value": streams * B * K / e2e_s, "unit": "tok/s",
                 "h2d_bytes_per_step": int(B * wl.layers * (wl.hidden + wl.experts) * 8),

@@ -67,6 +67,8 @@ def main():
     t0, bad = time.time(), []
     for s in range(lo, hi):
         ok, why = run(s)
+        if (s - lo + 1) % 1000 == 0:  # progress: a run cut short by a timeout still counts
+            print(f"progress seeds {lo}..{s}: {s - lo + 1 - len(bad)} / {s - lo + 1} pass", flush=True)
         if not ok:
             bad.append(s)
             print("MISMATCH", s, why, flush=True)

@@ -121,6 +121,17 @@ bool CopyEngine::fully_issued(const std::shared_ptr<CopyJob>& job) {
     return job->issued_tiles == job->tiles;
 }
 
+bool CopyEngine::idle(const std::shared_ptr<CopyJob>& job) {
+    std::lock_guard<std::mutex> g(mu_);
+    if (job->next_tile != job->issued_tiles) return false;  // the copy thread is issuing a tile
+    return job->issued_tiles == 0 || cudaEventQuery(job->t_end[job->issued_tiles - 1]) == cudaSuccess;
+}
+
+bool CopyEngine::landed(const std::shared_ptr<CopyJob>& job) {
+    std::lock_guard<std::mutex> g(mu_);
+    return job->issued_tiles == job->tiles && cudaEventQuery(job->done[job->tiles - 1]) == cudaSuccess;
+}
+
 void CopyEngine::drain() {
     std::unique_lock<std::mutex> lk(mu_);
     cv_issued_.wait(lk, [&] { return (od_.empty() && pf_.empty() && !busy_) || stop_ || !error_.empty(); });

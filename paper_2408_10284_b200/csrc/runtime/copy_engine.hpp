@@ -55,6 +55,11 @@ public:
     // Block until `tile` of `job` has been issued; returns its completion event.
     cudaEvent_t wait_issued(const std::shared_ptr<CopyJob>& job, int tile);
     bool fully_issued(const std::shared_ptr<CopyJob>& job);
+    // No tile of `job` is being handed to the DMA engine and every issued tile has landed: its
+    // events may be recycled (retire).  Call after cancel(): the copy thread takes no new tile.
+    bool idle(const std::shared_ptr<CopyJob>& job);
+    // Every tile of `job` has been issued and has landed in HBM (no stream wait needed).
+    bool landed(const std::shared_ptr<CopyJob>& job);
     void drain();  // wait for the queues and the stream to empty
 
     long long tiles_copied() const { return tiles_copied_.load(); }

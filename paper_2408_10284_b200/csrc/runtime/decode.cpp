@@ -42,6 +42,8 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
         fail(Status::Usage, "decode_begin: SimConfig tile count differs from the expert store's tile layout");
     if (total_tokens < 1) fail(Status::Usage, "decode_begin: total_tokens must be >= 1");
     if (K > 8) fail(Status::Usage, "decode: top_k > 8 unsupported by the combine kernel");
+    if (K * store_.tiles > kMaxCombineRefs)  // CombineArgs::refs holds one entry per (rank, tile)
+        fail(Status::Usage, "decode_begin: top_k * tiles must be <= 128");
     if (free_running_ && !eng.has_gates()) fail(Status::Usage, "free-running decode needs the gate matrices");
     if (!(concentration_ > 0.0)) fail(Status::Usage, "decode_begin: dirichlet concentration must be > 0");
     if (batch_ < 1 || batch_ > 256 || batch_ * K > kGMaxPairs)
@@ -297,9 +299,8 @@ void DecodeSession::release_pending(bool all) {
     }
     pending_free_.erase(it, pending_free_.end());
     // recycle copy jobs whose issued tiles have landed
-    auto done = std::stable_partition(retiring_.begin(), retiring_.end(), [&](const std::shared_ptr<CopyJob>& j) {
-        return !(j->issued_tiles == 0 || cudaEventQuery(j->t_end[j->issued_tiles - 1]) == cudaSuccess);
-    });
+    auto done = std::stable_partition(retiring_.begin(), retiring_.end(),
+                                      [&](const std::shared_ptr<CopyJob>& j) { return !copier_->idle(j); });
     for (auto jt = done; jt != retiring_.end(); ++jt) copier_->retire(*jt);
     retiring_.erase(done, retiring_.end());
 }
@@ -522,7 +523,10 @@ void DecodeSession::launch_speculative(int layer, const double* x) {
     for (int k = 0; k < n_pred && (run.n + 1) * T <= kMaxFfnSegments; ++k) {
         const int slot = slot_of_[static_cast<size_t>(layer) * N + spec_next_[k]];
         if (slot < 0) continue;  // not resident: the decision will load it
-        wait_fill(slot, -1);
+        // only an expert whose weights have landed: waiting on an in-flight fill here would promote
+        // it ahead of the layer's real on-demand loads and stall compute on a guess
+        const Slot& sl = slots_[slot];
+        if (sl.fill && !sl.fill_done && !copier_->landed(sl.fill)) continue;
         for (int t = 0; t < T; ++t) {
             const unsigned char* tile = slot_ptr(slot) + t * store_.tile_bytes;
             p.seg[p.n_seg].gate_up = reinterpret_cast<const std::uint16_t*>(tile);
@@ -611,6 +615,10 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
     for (const auto& grp : groups) {
         const Use& u = *grp.first;
         for (int t : grp.second) {
+            if (p.n_seg == kMaxFfnSegments) {  // launch what has landed so far
+                timed_ffn(p, meta, refs);
+                meta.clear();
+            }
             wait_fill(u.slot, t);
             p.seg[p.n_seg++] = seg(u.slot, t);
             meta.emplace_back(u.rank, t);
@@ -622,6 +630,7 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
     std::sort(refs.begin(), refs.end(), [](const auto& a, const auto& b) {
         return std::get<0>(a) != std::get<0>(b) ? std::get<0>(a) < std::get<0>(b) : std::get<1>(a) < std::get<1>(b);
     });
+    if (refs.size() > static_cast<size_t>(kMaxCombineRefs)) fail(Status::Internal, "combine: too many (rank, tile) segments");
     CombineArgs c;
     c.x = cur_res_;
     c.scores = cur_scores_;
@@ -743,7 +752,8 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
         jobs.push_back(j);
         if (grp.second.back() == us.tiles.back()) stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
     }
-    if (!res.segs.empty() && jobs.size() >= 3 && merge_resident()) {  // resident + >= 2 on-demand groups
+    if (!res.segs.empty() && jobs.size() >= 3 && merge_resident() &&  // resident + >= 2 on-demand groups
+        jobs[0].segs.size() + jobs[1].segs.size() <= static_cast<size_t>(kGMaxSegs)) {
         jobs[1].segs.insert(jobs[1].segs.begin(), jobs[0].segs.begin(), jobs[0].segs.end());
         jobs.erase(jobs.begin());
     }
@@ -752,6 +762,7 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
     size_t need = 0;
     for (size_t i = 0; i < jobs.size(); ++i) {
         GroupedLaunch& p = downs[i];
+        if (jobs[i].segs.size() > static_cast<size_t>(kGMaxSegs)) fail(Status::Internal, "grouped launch: too many segments");
         p.n_seg = static_cast<int>(jobs[i].segs.size());
         for (int s = 0; s < p.n_seg; ++s) p.seg[s] = jobs[i].segs[s];
         grouped_plan_down(p, sm_count_);

@@ -45,6 +45,8 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
     const int ft = ffn / tiles;
     if (spec.hidden_dim % 32 || ft % 32) fail(Status::Usage, "experts_init: hidden_dim and ffn/tiles must be multiples of 32");
     if (spec.hidden_dim > 16384 || ft > 16384) fail(Status::Usage, "experts_init: rows longer than 16384 elements unsupported");
+    // one K2 launch covers a whole expert (FfnLaunch::seg) and a layer's combine every (rank, tile)
+    if (tiles > kMaxFfnSegments) fail(Status::Usage, "experts_init: at most 32 tiles per expert");
     if (alias < 0) fail(Status::Usage, "experts_init: host_alias must be >= 0");
     eng.activate();
     st.layers = spec.num_layers;

@@ -40,12 +40,14 @@ def rmsnorm_like_gpu(x):
     return np.array([v / rms for v in xs])
 
 
-@pytest.mark.parametrize("batch,tol", [(1, 1e-4), (4, 2e-2)])
-def test_free_running_decode_matches_oracle_per_step(batch, tol):
+def run_and_check(batch, tol, caps=None, T=10):
+    """Free-running decode of the tiny case; asserts per-step parity with the oracle; returns
+    (result, hidden, decode stats)."""
     g = load_golden("tiny")
     w0, fg = oracle_inputs(g)
     cfg = sim_config(g)
-    caps, tau, T = g["sim_capacities"], g["tau"], 10
+    caps = g["sim_capacities"] if caps is None else caps
+    tau = g["tau"]
     L, N, K, D = w0.L, w0.N, w0.K, w0.D
     ffn, tiles, seed = 1024, cfg.tile_count_per_expert, 3
     ws = [w0] + [O.generate_trace(L, N, K, D, T, 0.6, 0.18, 99, 7000 + b, False, [2.0, 1.2, 0.7, 0.35],
@@ -61,6 +63,7 @@ def test_free_running_decode_matches_oracle_per_step(batch, tol):
             eng.decode_tokens(acts[:, 0], scores[:, 0], hid[:, 0])
         else:
             eng.decode_tokens(acts, scores, hid)
+        stats = eng.decode_stats()
         r = eng.decode_end(cfg, T)
     # the residual stream and router / expert inputs the GPU used
     res = acts.copy()
@@ -102,3 +105,29 @@ def test_free_running_decode_matches_oracle_per_step(batch, tol):
     # the hidden state really evolves (layer inputs differ from the replayed trace) and stays bounded
     assert not np.allclose(res[:, :, 1:], acts[:, :, 1:])
     assert np.isfinite(hid).all()
+    return r, hid, stats
+
+
+@pytest.mark.parametrize("batch,tol", [(1, 1e-4), (4, 2e-2)])
+def test_free_running_decode_matches_oracle_per_step(batch, tol):
+    run_and_check(batch, tol)
+
+
+@pytest.mark.parametrize("all_resident", [False, True])
+def test_speculative_ffn_on_off(monkeypatch, all_resident):
+    """Batch-1 free-running decode speculates the look-ahead's top-1 expert of the next layer (see
+    DecodeSession::launch_speculative).  A hit sums that expert's partials from a launch with a
+    different CTA split, so outputs are not bit-identical across on / off: both runs must keep
+    per-step parity with the oracle, the speculative run must actually hit, and where the two runs
+    took the same decisions their outputs agree within the fp32 tolerance."""
+    caps = [8, 8, 8, 8] if all_resident else None
+    monkeypatch.setenv("ADAPMOE_SPECULATE", "1")
+    r_on, hid_on, st_on = run_and_check(1, 1e-4, caps=caps, T=12)
+    monkeypatch.setenv("ADAPMOE_SPECULATE", "0")
+    r_off, hid_off, st_off = run_and_check(1, 1e-4, caps=caps, T=12)
+    assert st_off["spec_launches"] == 0 and st_off["spec_hits"] == 0
+    assert st_on["spec_launches"] > 0 and st_on["spec_hits"] > 0, st_on
+    assert st_on["spec_hits"] <= st_on["spec_launches"]
+    if np.array_equal(r_on.timeline, r_off.timeline):
+        err = np.abs(hid_on - hid_off).max() / np.abs(hid_off).max()
+        assert err < 1e-4, err

@@ -279,6 +279,19 @@ int moe_train_first_gate(moe_engine_t engine, const double* acts, const double* 
  * (l, e) -> (l*N + e) % host_alias (for hosts without L*N*expert_bytes of RAM); 0 = all distinct. */
 int moe_experts_init(moe_engine_t engine, int32_t ffn_dim, int32_t tiles, uint64_t seed, int32_t host_alias);
 
+/* Expert-parallel shard store (replaces the reference's per-expert compute placeholder
+ * inc/simulator.hpp:446-462 on a shard): as moe_experts_init, but the pinned store holds only the
+ * experts with expert_owner[l*N + e] == rank (the same [L][N] table later passed to
+ * moe_decode_begin_ex), so a shard pins ~1/G of the L*N experts.  expert_owner == NULL: all experts.
+ * Host pages are placed on the GPU's NUMA node (sysfs; ADAPMOE_NUMA=0 disables, =n+1 forces node n)
+ * for every store. */
+int moe_experts_init_shard(moe_engine_t engine, int32_t ffn_dim, int32_t tiles, uint64_t seed, int32_t host_alias,
+                           const int32_t* expert_owner, int32_t rank);
+int moe_experts_alloc_shard(moe_engine_t engine, int32_t ffn_dim, int32_t tiles, const int32_t* expert_owner,
+                            int32_t rank);
+/* Pinned bytes, distinct stored expert blocks and the host NUMA node (-1: none) of the store. */
+int moe_experts_info(moe_engine_t engine, int64_t* pinned_bytes, int32_t* stored_experts, int32_t* numa_node);
+
 /* Real weights instead of the synthetic init (SURVEY §8(b) moe_load_experts): allocate the pinned
  * store (all L*N experts, zero), then hand every expert's weights over in the usual checkpoint
  * layout — bf16 bit patterns, row-major: w1 = gate_proj.weight [ffn][d], w3 = up_proj.weight

@@ -110,6 +110,9 @@ SIGNATURES = {
     "moe_expert_bytes": (C.c_int, [_eng, _i64]),
     "moe_expert_read": (C.c_int, [_eng, C.c_int32, C.c_int32, _u16]),
     "moe_experts_alloc": (C.c_int, [_eng, C.c_int32, C.c_int32]),
+    "moe_experts_init_shard": (C.c_int, [_eng, C.c_int32, C.c_int32, C.c_uint64, C.c_int32, _i32, C.c_int32]),
+    "moe_experts_alloc_shard": (C.c_int, [_eng, C.c_int32, C.c_int32, _i32, C.c_int32]),
+    "moe_experts_info": (C.c_int, [_eng, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "moe_router_forward": (C.c_int, [_eng, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_double, _d, C.c_int32,
                                      C.c_int32, C.c_void_p, C.c_void_p]),
     "moe_expert_set": (C.c_int, [_eng, C.c_int32, C.c_int32, _u16, _u16, _u16]),

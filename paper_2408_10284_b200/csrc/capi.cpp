@@ -467,31 +467,50 @@ void export_stats(const DecodeStats& s, moe_decode_stats* out) {
 
 extern "C" {
 
-int moe_experts_init(moe_engine_t h, int32_t ffn, int32_t tiles, uint64_t seed, int32_t alias) {
+namespace {
+int experts_build(moe_engine_t h, int32_t ffn, int32_t tiles, uint64_t seed, int32_t alias, bool init_values,
+                  const int32_t* owner, int32_t rank) {
     return guarded([&] {
         Engine& e = eng(h);
+        if (owner && (rank < 0 || rank >= e.spec().experts_per_layer))
+            fail(Status::Usage, "experts_init: shard rank out of [0, N)");
         e.session.reset();
         e.experts = std::make_unique<ExpertStore>();
         try {
-            build_expert_store(e, *e.experts, ffn, tiles, seed, alias);
+            build_expert_store(e, *e.experts, ffn, tiles, seed, alias, init_values, owner, rank);
         } catch (...) {
             e.experts.reset();
             throw;
         }
     });
 }
+}  // namespace
+
+int moe_experts_init(moe_engine_t h, int32_t ffn, int32_t tiles, uint64_t seed, int32_t alias) {
+    return experts_build(h, ffn, tiles, seed, alias, true, nullptr, 0);
+}
+
+int moe_experts_init_shard(moe_engine_t h, int32_t ffn, int32_t tiles, uint64_t seed, int32_t alias,
+                           const int32_t* expert_owner, int32_t rank) {
+    if (!expert_owner) return experts_build(h, ffn, tiles, seed, alias, true, nullptr, 0);
+    return experts_build(h, ffn, tiles, seed, alias, true, expert_owner, rank);
+}
 
 int moe_experts_alloc(moe_engine_t h, int32_t ffn, int32_t tiles) {
+    return experts_build(h, ffn, tiles, 0, 0, false, nullptr, 0);
+}
+
+int moe_experts_alloc_shard(moe_engine_t h, int32_t ffn, int32_t tiles, const int32_t* expert_owner, int32_t rank) {
+    return experts_build(h, ffn, tiles, 0, 0, false, expert_owner, rank);
+}
+
+int moe_experts_info(moe_engine_t h, int64_t* pinned_bytes, int32_t* stored_experts, int32_t* numa_node) {
     return guarded([&] {
         Engine& e = eng(h);
-        e.session.reset();
-        e.experts = std::make_unique<ExpertStore>();
-        try {
-            build_expert_store(e, *e.experts, ffn, tiles, 0, 0, false);
-        } catch (...) {
-            e.experts.reset();
-            throw;
-        }
+        if (!e.experts) fail(Status::Usage, "experts not initialised");
+        if (pinned_bytes) *pinned_bytes = static_cast<int64_t>(e.experts->pinned_bytes());
+        if (stored_experts) *stored_experts = static_cast<int32_t>(e.experts->blocks.size());
+        if (numa_node) *numa_node = e.experts->numa_node;
     });
 }
 

@@ -19,6 +19,8 @@
 // combine kernel reduces them in a fixed order.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "expert_ffn.hpp"
 #include "ptx.cuh"
 
@@ -400,12 +402,16 @@ cudaError_t launch_ffn(const FfnLaunch& p, int sm_count, cudaStream_t stream) {
         return cudaErrorInvalidValue;
     const int grid = ffn_grid(p, sm_count);
     const size_t smem = static_cast<size_t>(p.d) * sizeof(float);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(ffn_rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        cudaFuncSetAttribute(ffn_rows_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        cudaFuncSetAttribute(ffn_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        configured = true;
+    // the > 48 KB opt-in is a per-device function attribute: configure each device once
+    static std::atomic<std::uint64_t> configured{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return cudaErrorInvalidDevice;
+    if (!(configured.load() >> dev & 1)) {
+        for (auto fn : {ffn_rows_kernel<1>, ffn_rows_kernel<2>, ffn_rows_kernel<4>}) {
+            const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+            if (e != cudaSuccess) return e;
+        }
+        configured.fetch_or(std::uint64_t{1} << dev);
     }
     if (p.d <= 4096)
         ffn_rows_kernel<1><<<grid, kThreads, smem, stream>>>(p);

@@ -20,7 +20,10 @@
 // (reference) and adding the +-0 product are identical for finite weights.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
 
 #include "ptx.cuh"
 #include "router.hpp"
@@ -265,8 +268,8 @@ __device__ __forceinline__ void fast_dot(const float* __restrict__ w, const floa
     asum_out = asum;
 }
 
-__device__ __forceinline__ bool fast_item(const RouteItem& it) {
-    return it.gate != nullptr && !(it.flags & (kRouteExact | kRouteEmitLogits));
+__device__ __forceinline__ bool fast_item(const RouteItem& it, const RouteParams& p) {
+    return it.gate != nullptr && !(it.flags & (kRouteExact | kRouteEmitLogits)) && !p.force_exact;
 }
 
 // Certification + exact fallback for one group, all threads of the CTA (F/A in shared memory).
@@ -284,7 +287,7 @@ __device__ void finish_group(const RouteGroup& g, float (*F)[kMaxN], float (*A)[
         int exact = 0;
         if (it.gate == nullptr) {
             decide_exact(it, nullptr, p, o, lane);  // stored scores: the reference's own inputs
-        } else if (it.flags & (kRouteExact | kRouteEmitLogits)) {
+        } else if ((it.flags & (kRouteExact | kRouteEmitLogits)) || p.force_exact) {
             exact = 1;
         } else if (!decide_certified(it, F[warp], A[warp], chain_len, p, o, lane)) {
             exact = 1;
@@ -335,7 +338,28 @@ __device__ void finish_group(const RouteGroup& g, float (*F)[kMaxN], float (*A)[
         }
         __syncthreads();
     }
-    if (warp < NE) decide_exact(g.items[exact_item[warp]], exact_logits[warp], p, o, lane);
+    if (warp < NE) {
+        const RouteItem& it = g.items[exact_item[warp]];
+        decide_exact(it, exact_logits[warp], p, o, lane);
+        // queue the exact logits for the host's libm-exp decision (RouteOutputs::host_entries)
+        if (o.host_entries && o.exact_used && !(it.flags & kRouteEmitLogits)) {
+            unsigned idx = 0;
+            if (lane == 0) idx = atomicAdd(o.host_counter, 1u);
+            idx = __shfl_sync(kFull, idx, 0);
+            if (idx < static_cast<unsigned>(o.host_cap)) {
+                double* e = o.host_entries + static_cast<size_t>(idx) * (2 + N);
+                if (lane == 0) {
+                    e[0] = static_cast<double>(it.flags);
+                    e[1] = it.fisher;
+                }
+                if (lane < N) e[2 + lane] = exact_logits[warp][lane];
+                if (lane + 32 < N) e[2 + lane + 32] = exact_logits[warp][lane + 32];
+                if (lane == 0) o.exact_used[it.out] = 2 + static_cast<int>(idx);
+            } else if (lane == 0) {
+                o.exact_used[it.out] = -1;
+            }
+        }
+    }
 }
 
 __device__ __forceinline__ int chain_length(int D) {
@@ -357,7 +381,7 @@ __global__ void __launch_bounds__(kThreads) route_kernel(const RouteGroup* __res
 
     // ---- fast path: fp32 logits, fixed order ----
     bool any_gate = false;
-    for (int s = 0; s < g.n_items; ++s) any_gate |= fast_item(g.items[s]);
+    for (int s = 0; s < g.n_items; ++s) any_gate |= fast_item(g.items[s], p);
     if (any_gate) {
         ptx::load_x_f32<kThreads>(x32, g.x, D);
         __syncthreads();
@@ -365,7 +389,7 @@ __global__ void __launch_bounds__(kThreads) route_kernel(const RouteGroup* __res
         for (int pr = warp; pr < pairs; pr += kWarps) {
             const int s = pr / N, j = pr % N;
             const RouteItem& it = g.items[s];
-            if (!fast_item(it)) continue;
+            if (!fast_item(it, p)) continue;
             float acc, asum;
             fast_dot(it.gate32 + static_cast<size_t>(j) * D, x32, 0, D, vec4, lane, acc, asum);
             if (lane == 0) {
@@ -408,7 +432,7 @@ __global__ void __launch_bounds__(kThreads) route_split_kernel(const RouteGroup*
     if (tid == 0) {
         int nf = 0;
         for (int s = 0; s < g.n_items; ++s)
-            if (fast_item(g.items[s])) fast_list[nf++] = s;
+            if (fast_item(g.items[s], p)) fast_list[nf++] = s;
         n_fast = nf;
     }
     __syncthreads();
@@ -475,21 +499,28 @@ cudaError_t launch_route(const RouteGroup* d_groups, int n_groups, int max_gate_
     if (p.n < 2 || p.n > kMaxN || p.k < 1 || p.k > p.n || p.d < 1) return cudaErrorInvalidValue;
     const size_t smem = ((static_cast<size_t>(p.d) * 4 + 15) & ~size_t(15)) + 2ull * kChunkRows * 32 * 8;
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(200 * 1024));
-        cudaFuncSetAttribute(route_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(200 * 1024));
-        configured = true;
+    // the > 48 KB opt-in is a per-device function attribute: configure each device once
+    static std::atomic<std::uint64_t> configured{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return cudaErrorInvalidDevice;
+    if (!(configured.load() >> dev & 1)) {
+        for (const void* fn : {reinterpret_cast<const void*>(route_kernel), reinterpret_cast<const void*>(route_split_kernel)}) {
+            const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            if (e != cudaSuccess) return e;
+        }
+        configured.fetch_or(std::uint64_t{1} << dev);
     }
+    RouteParams pp = p;
+    if (const char* f = std::getenv("ADAPMOE_ROUTE_FORCE_EXACT")) pp.force_exact = std::atoi(f) != 0;
     // split when a group's gate columns would take more than one round of the CTA's warps
     const int pairs = (max_gate_items > 0 ? max_gate_items : 1) * p.n;
     const int split = (pairs + kPairsPerCta - 1) / kPairsPerCta;
     if (scratch && scratch->f && scratch->a && scratch->tickets && n_groups <= scratch->groups && split > 1 &&
         p.d >= 1024) {
-        route_split_kernel<<<n_groups * split, kThreads, smem, stream>>>(d_groups, p, out, *scratch, split);
+        route_split_kernel<<<n_groups * split, kThreads, smem, stream>>>(d_groups, pp, out, *scratch, split);
         return cudaGetLastError();
     }
-    route_kernel<<<n_groups, kThreads, smem, stream>>>(d_groups, p, out);
+    route_kernel<<<n_groups, kThreads, smem, stream>>>(d_groups, pp, out);
     return cudaGetLastError();
 }
 

@@ -45,13 +45,27 @@ struct RouteOutputs {
     int* single = nullptr;           // [rows]
     double* perturbation = nullptr;  // [rows] (may be null)
     double* scores = nullptr;        // [rows][N] (may be null; kRouteEmitScores / kRouteEmitLogits)
-    int* exact_used = nullptr;       // [rows] 1 if the item needed the exact fp64 path (may be null)
+    // [rows] (may be null): 0 = certified fp32 fast path; 1 = exact fp64 path, decided on the device;
+    // 2 + i = exact fp64 path, logits queued in host_entries[i] for the host decision (below);
+    // -1 = exact path but the host queue was full (the caller must fail)
+    int* exact_used = nullptr;
+    // Host-decision queue.  The reference softmaxes with glibc exp (inc/core.hpp:205-216); CUDA's exp
+    // can differ from it by an ulp, so a decision taken on the device from exact logits is exact only
+    // in practice.  With host_entries set, every exact-path gate item (the uncertified ones, ~1 in
+    // 600 look-ahead items at 8x7B) also appends [flags, fisher, logits[N]] (2 + N doubles) to this
+    // pinned, device-visible array and the host re-decides it with the reference's own procedure
+    // (route_host_decide): bit-exact by construction.  host_counter (device memory) must be zero
+    // before the first launch that uses the queue.
+    double* host_entries = nullptr;
+    unsigned* host_counter = nullptr;
+    int host_cap = 0;
 };
 
 struct RouteParams {
     int d = 0, n = 0, k = 0;
     double tau = 0.0;
     double concentration = 1.0;
+    int force_exact = 0;  // test knob (ADAPMOE_ROUTE_FORCE_EXACT=1, read by launch_route): no fast path
 };
 
 // Scratch for the split launch (per-layer decode): per group kMaxRouteItems x kMaxN fp32 logits and
@@ -68,6 +82,13 @@ struct RouteScratch {
 // columns exceed one round of a CTA's warps are split over several CTAs (lower latency).
 cudaError_t launch_route(const RouteGroup* d_groups, int n_groups, int max_gate_items, const RouteParams& p,
                          const RouteOutputs& out, cudaStream_t stream, const RouteScratch* scratch = nullptr);
+
+// Host side of the queue: re-decide every row whose exact_used is >= 2 from its queued logits with
+// the reference procedure (softmax with libm exp, sensitivity gate / top-K; policy.hpp), overwriting
+// selected [rows][K], count, single and (if non-null) perturbation.  rows [row0, row1) of exact_used
+// are scanned; fails (Internal) on a queue overflow (-1).
+void route_host_decide(const RouteParams& p, const double* host_entries, const int* exact_used, long long row0,
+                       long long row1, int* selected, int* count, int* single, double* perturbation);
 
 // fp32 transposed copy [N][d] of a row-major fp64 [d][N] gate (device to device).
 cudaError_t launch_gate_transpose(const double* src, float* dst, int d, int n, int count, cudaStream_t stream);

@@ -61,6 +61,9 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
             const int o = expert_owner ? expert_owner[static_cast<size_t>(l) * N + e] : e % ep_world_;
             if (o < 0 || o >= ep_world_) fail(Status::Usage, "decode_begin: expert_owner entry out of [0, ep_world)");
             owner_[static_cast<size_t>(l) * N + e] = o;
+            if (o == ep_rank_ && !store_.has(l, e))
+                fail(Status::Usage, "decode_begin: this shard owns expert (" + std::to_string(l) + ", " + std::to_string(e) +
+                                        ") but its expert store does not hold it (experts_init with the same owner table)");
         }
     int resident = 0;
     for (int l = 0; l < L; ++l) {
@@ -132,6 +135,9 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     MOE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_route_), route_rows * (K + 3) * sizeof(int),
                            cudaHostAllocMapped));
     MOE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_route_), h_route_, 0));
+    route_host_cap_ = static_cast<int>(std::min<size_t>(route_rows, 16384));
+    h_route_host_.reserve(static_cast<size_t>(route_host_cap_) * (2 + N) * sizeof(double));
+    d_route_counter_.reserve(sizeof(unsigned));
     MOE_CUDA(cudaEventCreateWithFlags(&route_done_, cudaEventDisableTiming));
     // per-call buffers sized for the whole announced trace now: growing them inside decode() would put
     // cudaFree / cudaMallocHost (implicit device synchronisation) inside the timed window
@@ -920,10 +926,13 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
     int* d_sgl = d_cnt + rows;
     int* d_exact = d_sgl + rows;
     RouteOutputs ro{d_sel, d_cnt, d_sgl, nullptr, free_running_ ? d_free_scores_.as<double>() : nullptr, d_exact};
-    const int* sel = h_route_;
-    const int* cnt = sel + static_cast<size_t>(rows) * K;
-    const int* sgl = cnt + rows;
-    const int* exact_used = sgl + rows;
+    ro.host_entries = h_route_host_.as<double>();
+    ro.host_counter = d_route_counter_.as<unsigned>();
+    ro.host_cap = route_host_cap_;
+    int* sel = h_route_;
+    int* cnt = sel + static_cast<size_t>(rows) * K;
+    int* sgl = cnt + rows;
+    int* exact_used = sgl + rows;
 
     std::array<RoutePrediction, 3> preds;
     const bool gap_trace = std::getenv("ADAPMOE_GAP_TRACE") != nullptr;
@@ -955,6 +964,8 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                     MOE_CUDA(cudaStreamWaitEvent(route_stream_, in_ready_, 0));
                     rs = route_stream_;
                 }
+                MOE_CUDA(cudaMemsetAsync(d_route_counter_.ptr, 0, sizeof(unsigned), rs));
+                std::memset(exact_used, 0, sizeof(int) * 4 * static_cast<size_t>(n_groups));  // rows without an item stay 0
                 cudaEvent_t r0 = take_timing(), r1 = take_timing();
                 MOE_CUDA(cudaEventRecord(r0, rs));
                 MOE_CUDA(launch_route(d_groups_.as<RouteGroup>() + gl, n_groups, max_gates, rp, ro, rs,
@@ -970,6 +981,8 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                 MOE_CUDA(cudaEventSynchronize(route_done_));
                 stats_.host_sync_ms +=
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+                // uncertified items: the reference's softmax (libm exp) on their exact logits
+                route_host_decide(rp, h_route_host_.as<double>(), exact_used, 0, 4LL * n_groups, sel, cnt, sgl, nullptr);
             }
             const auto h1 = std::chrono::steady_clock::now();
             release_pending(false);
@@ -987,7 +1000,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
             for (int b = 0; b < B; ++b) {
                 const int r0w = base + b * 4;
                 singles += sgl[r0w] != 0;
-                for (int it = 1; it < n_items; ++it) stats_.router_exact += exact_used[r0w + it];
+                for (int it = 1; it < n_items; ++it) stats_.router_exact += exact_used[r0w + it] != 0;
                 for (int k = 0; k < cnt[r0w]; ++k) {
                     const int e = sel[r0w * K + k];
                     bool seen = false;

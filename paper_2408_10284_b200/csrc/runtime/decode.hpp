@@ -212,6 +212,11 @@ private:
     // route_window_ tokens per launch (R = 4B * L * window)
     int* h_route_ = nullptr;
     int* d_route_ = nullptr;
+    // K1 host-decision queue (kernels/router.hpp RouteOutputs::host_entries): exact logits of the
+    // uncertified items, decided on the host with libm exp right after each route sync
+    PinnedBuffer h_route_host_;
+    DeviceBuffer d_route_counter_;
+    int route_host_cap_ = 0;
     int route_window_ = 1;
     cudaEvent_t route_done_ = nullptr;
     // completion of each layer's FFN + combine on the compute stream: a slot released by layer s is

@@ -92,6 +92,18 @@ void Engine::load_gates(const double* gates, const double* first_gate) {
     MOE_CUDA(cudaStreamSynchronize(compute_));
 }
 
+RouteOutputs Engine::host_queue(size_t max_items, cudaStream_t stream) {
+    RouteOutputs o;
+    const int cap = static_cast<int>(std::min<size_t>(std::max<size_t>(max_items, 1), 65536));
+    h_host_entries_.reserve(static_cast<size_t>(cap) * (2 + spec_.experts_per_layer) * sizeof(double));
+    d_host_counter_.reserve(sizeof(unsigned));
+    MOE_CUDA(cudaMemsetAsync(d_host_counter_.ptr, 0, sizeof(unsigned), stream));
+    o.host_entries = h_host_entries_.as<double>();
+    o.host_counter = d_host_counter_.as<unsigned>();
+    o.host_cap = cap;
+    return o;
+}
+
 void Engine::run_route(const std::vector<RouteGroup>& groups, int rows, int max_gate_items, const RouteParams& p,
                        TraceRoutes* out, std::vector<double>* scores_out, cudaStream_t stream) {
     const int K = p.k, N = p.n;
@@ -101,9 +113,16 @@ void Engine::run_route(const std::vector<RouteGroup>& groups, int rows, int max_
     d_out_single_.reserve(static_cast<size_t>(rows) * sizeof(int));
     d_out_pert_.reserve(static_cast<size_t>(rows) * sizeof(double));
     if (scores_out) d_out_scores_.reserve(static_cast<size_t>(rows) * N * sizeof(double));
+    d_out_exact_.reserve(static_cast<size_t>(rows) * sizeof(int));
     MOE_CUDA(cudaMemcpyAsync(d_groups_.ptr, groups.data(), groups.size() * sizeof(RouteGroup), cudaMemcpyHostToDevice, stream));
-    RouteOutputs o{d_out_sel_.as<int>(), d_out_cnt_.as<int>(), d_out_single_.as<int>(), d_out_pert_.as<double>(),
-                   scores_out ? d_out_scores_.as<double>() : nullptr};
+    RouteOutputs o = host_queue(static_cast<size_t>(rows), stream);
+    o.selected = d_out_sel_.as<int>();
+    o.count = d_out_cnt_.as<int>();
+    o.single = d_out_single_.as<int>();
+    o.perturbation = d_out_pert_.as<double>();
+    o.scores = scores_out ? d_out_scores_.as<double>() : nullptr;
+    o.exact_used = d_out_exact_.as<int>();
+    MOE_CUDA(cudaMemsetAsync(o.exact_used, 0, static_cast<size_t>(rows) * sizeof(int), stream));
     MOE_CUDA(launch_route(d_groups_.as<RouteGroup>(), static_cast<int>(groups.size()), max_gate_items, p, o, stream));
     out->selected.resize(static_cast<size_t>(rows) * K);
     out->count.resize(rows);
@@ -117,7 +136,11 @@ void Engine::run_route(const std::vector<RouteGroup>& groups, int rows, int max_
         scores_out->resize(static_cast<size_t>(rows) * N);
         MOE_CUDA(cudaMemcpyAsync(scores_out->data(), o.scores, scores_out->size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
     }
+    std::vector<int> exact(rows);
+    MOE_CUDA(cudaMemcpyAsync(exact.data(), o.exact_used, rows * sizeof(int), cudaMemcpyDeviceToHost, stream));
     MOE_CUDA(cudaStreamSynchronize(stream));
+    route_host_decide(p, o.host_entries, exact.data(), 0, rows, out->selected.data(), out->count.data(),
+                      out->single.data(), out->perturbation.data());
 }
 
 // Evaluation points of simulate_trace (inc/simulator.hpp:390-396 decision, :422-436 look-ahead).
@@ -146,7 +169,8 @@ void Engine::route_trace_stream(const double* acts, const double* scores, int T,
     d_out_single_.reserve(rows * sizeof(int));
     d_out_pert_.reserve(rows * sizeof(double));
     h_trace_groups_.reserve(TL * sizeof(RouteGroup));
-    h_trace_out_.reserve(rows * ((K + 2) * sizeof(int) + sizeof(double)));
+    h_trace_out_.reserve(rows * ((K + 3) * sizeof(int) + sizeof(double)));
+    d_out_exact_.reserve(rows * sizeof(int));
 
     // group (tok, l) writes rows tl*4 + item: decision, then look-ahead depth 1..k (or the first-layer
     // predictive gate at the last layer)
@@ -192,8 +216,15 @@ void Engine::route_trace_stream(const double* acts, const double* scores, int T,
     int* h_cnt = h_sel + rows * K;
     int* h_sgl = h_cnt + rows;
     double* h_pert = reinterpret_cast<double*>(h_sgl + rows);
+    int* h_exact = reinterpret_cast<int*>(h_pert + rows);
     RouteParams p{D, N, K, tau, 1.0};
-    RouteOutputs o{d_out_sel_.as<int>(), d_out_cnt_.as<int>(), d_out_single_.as<int>(), d_out_pert_.as<double>(), nullptr};
+    RouteOutputs o = host_queue(TL * (prefetch_on ? 3 : 0), compute_);
+    o.selected = d_out_sel_.as<int>();
+    o.count = d_out_cnt_.as<int>();
+    o.single = d_out_single_.as<int>();
+    o.perturbation = d_out_pert_.as<double>();
+    o.exact_used = d_out_exact_.as<int>();
+    MOE_CUDA(cudaMemsetAsync(o.exact_used, 0, rows * sizeof(int), compute_));
     const int chunk = std::max(1, std::min(chunk_tokens, T));
     const int n_chunks = (T + chunk - 1) / chunk;
     std::vector<cudaEvent_t> done(n_chunks);
@@ -218,6 +249,7 @@ void Engine::route_trace_stream(const double* acts, const double* scores, int T,
         MOE_CUDA(cudaMemcpyAsync(h_cnt + q0, o.count + q0, nq * sizeof(int), cudaMemcpyDeviceToHost, compute_));
         MOE_CUDA(cudaMemcpyAsync(h_sgl + q0, o.single + q0, nq * sizeof(int), cudaMemcpyDeviceToHost, compute_));
         MOE_CUDA(cudaMemcpyAsync(h_pert + q0, o.perturbation + q0, nq * sizeof(double), cudaMemcpyDeviceToHost, compute_));
+        MOE_CUDA(cudaMemcpyAsync(h_exact + q0, o.exact_used + q0, nq * sizeof(int), cudaMemcpyDeviceToHost, compute_));
         MOE_CUDA(cudaEventRecord(done[c], compute_));
     }
     r.selected.resize(TL * K);
@@ -229,6 +261,9 @@ void Engine::route_trace_stream(const double* acts, const double* scores, int T,
     for (int c = 0; c < n_chunks; ++c) {
         const int t0 = c * chunk, t1 = std::min(T, t0 + chunk);
         MOE_CUDA(cudaEventSynchronize(done[c]));
+        // the chunk's uncertified items: the reference's softmax (libm exp) on their exact logits
+        route_host_decide(p, o.host_entries, h_exact, static_cast<long long>(t0) * L * 4,
+                          static_cast<long long>(t1) * L * 4, h_sel, h_cnt, h_sgl, h_pert);
         for (size_t tl = static_cast<size_t>(t0) * L; tl < static_cast<size_t>(t1) * L; ++tl) {
             const size_t row = tl * 4;
             for (int k = 0; k < K; ++k) r.selected[tl * K + k] = h_sel[row * K + k];

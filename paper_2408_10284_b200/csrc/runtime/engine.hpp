@@ -126,6 +126,10 @@ private:
     bool gates_loaded_ = false, first_gate_loaded_ = false;
     // router workspace
     DeviceBuffer d_groups_, d_x_, d_scores_, d_out_sel_, d_out_cnt_, d_out_single_, d_out_pert_, d_out_scores_;
+    // K1 exact-path items decided on the host (kernels/router.hpp RouteOutputs::host_entries)
+    DeviceBuffer d_out_exact_, d_host_counter_;
+    PinnedBuffer h_host_entries_;
+    RouteOutputs host_queue(size_t max_items, cudaStream_t stream);  // outputs with the queue armed (counter zeroed on `stream`)
     PinnedBuffer h_trace_groups_, h_trace_out_;  // route_trace_stream staging
     // router_forward: groups staged in pinned memory, two buffers, each reused only after the
     // copy that read it has completed (event)

@@ -2,12 +2,17 @@
 
 #include <cuda_runtime.h>
 #include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <cctype>
+#include <cstdio>
 #include <cstring>
+#include <string>
 #include <thread>
 
 #include "../kernels/expert_ffn.hpp"
@@ -16,9 +21,48 @@
 namespace adapmoe {
 
 int ExpertStore::stored_index(int layer, int expert) const {
-    const int id = layer * experts + expert;
-    return alias > 0 ? id % alias : id;
+    const int b = index[static_cast<size_t>(layer) * experts + expert];
+    if (b < 0)
+        fail(Status::Usage, "expert (" + std::to_string(layer) + ", " + std::to_string(expert) +
+                                ") is owned by another expert-parallel shard: this store does not hold it");
+    return b;
 }
+
+namespace {
+
+// NUMA node of the engine's GPU (sysfs), -1 if unknown or single-node.  ADAPMOE_NUMA=0 disables the
+// placement, ADAPMOE_NUMA=<n+1> forces node n.
+int gpu_numa_node(int device) {
+    if (const char* v = std::getenv("ADAPMOE_NUMA")) {
+        const int n = std::atoi(v);
+        return n <= 0 ? -1 : n - 1;
+    }
+    char bus[32] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) return -1;
+    for (char* c = bus; *c; ++c) *c = static_cast<char>(std::tolower(*c));
+    std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
+    FILE* f = std::fopen(path.c_str(), "r");
+    if (!f) {  // sysfs uses a 4-digit domain; CUDA may print 8
+        std::string b(bus);
+        if (b.size() > 12) path = "/sys/bus/pci/devices/" + b.substr(b.size() - 12) + "/numa_node";
+        f = std::fopen(path.c_str(), "r");
+    }
+    if (!f) return -1;
+    int node = -1;
+    if (std::fscanf(f, "%d", &node) != 1) node = -1;
+    std::fclose(f);
+    return node;
+}
+
+// Prefer `node` for the pages of [p, p + bytes) (falls back to other nodes when it is full).
+void prefer_node(void* p, size_t bytes, int node) {
+    if (node < 0 || node >= 64) return;
+    unsigned long mask = 1ul << node;
+    constexpr int kMpolPreferred = 1;
+    syscall(SYS_mbind, p, bytes, kMpolPreferred, &mask, 64ul, 0u);  // best effort: errors keep the default policy
+}
+
+}  // namespace
 
 ExpertStore::~ExpertStore() {
     for (unsigned char* b : blocks) {
@@ -39,7 +83,7 @@ void expert_init_constants(std::uint64_t seed, int layer, int expert, int d, int
 }
 
 void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::uint64_t seed, int alias,
-                        bool init_values) {
+                        bool init_values, const int* owner, int rank) {
     const ModelSpec& spec = eng.spec();
     if (ffn <= 0 || tiles < 1 || ffn % tiles) fail(Status::Usage, "experts_init: ffn must be a positive multiple of tiles");
     const int ft = ffn / tiles;
@@ -56,11 +100,25 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
     st.tiles = tiles;
     st.seed = seed;
     const int total = spec.num_layers * spec.experts_per_layer;
-    st.alias = (alias > 0 && alias < total) ? alias : 0;
+    // experts this store holds (all, or one expert-parallel shard's)
+    std::vector<int> held;
+    for (int id = 0; id < total; ++id) {
+        if (owner && (owner[id] < 0)) fail(Status::Usage, "experts_init: negative expert owner");
+        if (!owner || owner[id] == rank) held.push_back(id);
+    }
+    if (held.empty()) fail(Status::Usage, "experts_init: this shard owns no expert");
+    const int n_held = static_cast<int>(held.size());
+    st.alias = (alias > 0 && alias < n_held) ? alias : 0;
     st.expert_bytes = static_cast<size_t>(3) * ffn * spec.hidden_dim * 2;
     st.tile_bytes = st.expert_bytes / tiles;
-    const int stored = st.alias > 0 ? st.alias : total;
+    const int stored = st.alias > 0 ? st.alias : n_held;
+    st.index.assign(total, -1);
+    for (int i = 0; i < n_held; ++i) st.index[held[i]] = st.alias > 0 ? i % st.alias : i;
+    std::vector<int> first_id(stored, -1);  // the (layer, expert) whose init values fill each block
+    for (int i = 0; i < n_held; ++i)
+        if (first_id[st.index[held[i]]] < 0) first_id[st.index[held[i]]] = held[i];
     st.blocks.assign(stored, nullptr);
+    st.numa_node = gpu_numa_node(eng.device());
 
     // allocate + first-touch + pin in parallel: page faulting and locking dominate at 90+ GB
     auto t0 = std::chrono::steady_clock::now();
@@ -76,6 +134,7 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
                     return;
                 }
                 madvise(p, st.expert_bytes, MADV_HUGEPAGE);
+                prefer_node(p, st.expert_bytes, st.numa_node);  // before first touch
                 std::memset(p, 0, st.expert_bytes);
                 cudaError_t e = cudaHostRegister(p, st.expert_bytes, cudaHostRegisterDefault);
                 if (e != cudaSuccess) {
@@ -103,7 +162,7 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
     }
     for (int i = 0; i < stored; ++i) {
         const int k = i & 1;
-        const int layer = i / spec.experts_per_layer, expert = i % spec.experts_per_layer;
+        const int layer = first_id[i] / spec.experts_per_layer, expert = first_id[i] % spec.experts_per_layer;
         std::uint64_t base[3];
         float scale[3];
         expert_init_constants(seed, layer, expert, spec.hidden_dim, ffn, base, scale);
@@ -122,6 +181,7 @@ void set_expert_weights(ExpertStore& st, int layer, int expert, const std::uint1
                         const std::uint16_t* w2) {
     if (layer < 0 || layer >= st.layers || expert < 0 || expert >= st.experts) fail(Status::Usage, "ExpertRef out of range");
     if (st.alias > 0) fail(Status::Usage, "expert_set: the store aliases experts (host_alias); allocate it without");
+    if (!st.has(layer, expert)) fail(Status::Usage, "expert_set: this store (an expert-parallel shard) does not hold the expert");
     const size_t D = st.d, F = st.ffn, Ft = F / st.tiles;
     std::uint16_t* dst = reinterpret_cast<std::uint16_t*>(st.blocks[st.stored_index(layer, expert)]);
     const size_t tile_elems = 3 * Ft * D;

@@ -15,18 +15,26 @@ struct ExpertStore {
     size_t expert_bytes = 0;  // 3 * F * d * 2
     size_t tile_bytes = 0;    // expert_bytes / tiles
     std::vector<unsigned char*> blocks;  // registered host memory, one per stored expert
+    // [L*N] block of each (layer, expert); -1 = not held by this store (an expert-parallel shard
+    // pins only the experts it owns)
+    std::vector<int> index;
+    int numa_node = -1;  // host NUMA node the blocks were placed on (-1: no binding)
     double pin_seconds = 0.0, fill_seconds = 0.0;
 
-    int stored_index(int layer, int expert) const;
+    bool has(int layer, int expert) const { return index[static_cast<size_t>(layer) * experts + expert] >= 0; }
+    int stored_index(int layer, int expert) const;  // fails (Usage) for an expert the store does not hold
     const unsigned char* expert(int layer, int expert) const { return blocks[stored_index(layer, expert)]; }
+    size_t pinned_bytes() const { return blocks.size() * expert_bytes; }
     ~ExpertStore();
 };
 
-// Allocate + pin (parallel first touch + cudaHostRegister) and, with `init_values`, fill with the
-// deterministic init (GPU init kernel, D2H into the pinned blocks); without, the store is zero and
-// the caller provides the weights through set_expert_weights.
+// Allocate + pin (parallel first touch on the GPU's NUMA node + cudaHostRegister) and, with
+// `init_values`, fill with the deterministic init (GPU init kernel, D2H into the pinned blocks);
+// without, the store is zero and the caller provides the weights through set_expert_weights.
+// owner [L*N] (may be null): hold only the experts with owner[l*N + e] == rank (expert-parallel
+// shard); alias > 0 maps the held experts onto that many distinct blocks.
 void build_expert_store(Engine& engine, ExpertStore& store, int ffn, int tiles, std::uint64_t seed, int alias,
-                        bool init_values = true);
+                        bool init_values = true, const int* owner = nullptr, int rank = 0);
 
 // Pack one expert's weights, given in the usual checkpoint layout (bf16 bits, row-major:
 // w1 = gate_proj [ffn][d], w3 = up_proj [ffn][d], w2 = down_proj [d][ffn]), into the store's

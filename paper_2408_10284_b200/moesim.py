@@ -330,12 +330,29 @@ class Engine:
         return w
 
     # -- physical decode -----------------------------------------------------------------------
-    def experts_init(self, ffn_dim: int, tiles: int, seed: int = 0, host_alias: int = 0):
-        check(load().moe_experts_init(self._h, ffn_dim, tiles, seed, host_alias))
+    def experts_init(self, ffn_dim: int, tiles: int, seed: int = 0, host_alias: int = 0, expert_owner=None,
+                     rank: int = 0):
+        """Pinned host expert store with the deterministic init.  expert_owner ([L][N] shard table) +
+        rank: an expert-parallel shard's store, holding only the experts it owns."""
+        if expert_owner is None:
+            check(load().moe_experts_init(self._h, ffn_dim, tiles, seed, host_alias))
+        else:
+            own = np.ascontiguousarray(expert_owner, dtype=np.int32).reshape(-1)
+            check(load().moe_experts_init_shard(self._h, ffn_dim, tiles, seed, host_alias, _p(own, _capi._i32), rank))
 
-    def experts_alloc(self, ffn_dim: int, tiles: int):
+    def experts_alloc(self, ffn_dim: int, tiles: int, expert_owner=None, rank: int = 0):
         """Pinned store for real weights (moe_experts_alloc); fill it with expert_set."""
-        check(load().moe_experts_alloc(self._h, ffn_dim, tiles))
+        if expert_owner is None:
+            check(load().moe_experts_alloc(self._h, ffn_dim, tiles))
+        else:
+            own = np.ascontiguousarray(expert_owner, dtype=np.int32).reshape(-1)
+            check(load().moe_experts_alloc_shard(self._h, ffn_dim, tiles, _p(own, _capi._i32), rank))
+
+    def experts_info(self) -> dict:
+        """Pinned bytes, distinct stored experts and host NUMA node of the store."""
+        b, n, node = C.c_int64(), C.c_int32(), C.c_int32()
+        check(load().moe_experts_info(self._h, C.byref(b), C.byref(n), C.byref(node)))
+        return {"pinned_bytes": b.value, "stored_experts": n.value, "numa_node": node.value}
 
     def expert_set(self, layer: int, expert: int, w1, w3, w2):
         """One expert's weights in checkpoint layout: w1 = gate_proj [ffn][d], w3 = up_proj [ffn][d],

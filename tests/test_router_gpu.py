@@ -9,7 +9,7 @@ import pytest
 import paper_2408_10284_b200 as P
 from conftest import golden_names, load_golden
 from helpers import (assert_metrics, assert_timeline, golden_decisions, oracle_inputs, parse_scales, sim_config,
-                     wl_args)
+                     sim_kwargs, wl_args)
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -173,3 +173,40 @@ def test_router_forward_matches_route_trace(name, lookahead):
             torch.cuda.synchronize()
             for u, v in zip(a[:3], b[:3]):
                 assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("name", ["mixtral_8x7b_t12", "tiny", "wide_n16", "top3", "odd_d"])
+def test_forced_exact_path_host_decisions_bit_exact(monkeypatch, name):
+    """ADAPMOE_ROUTE_FORCE_EXACT=1 sends EVERY gate item down K1's exact path: reference-order fp64
+    logits on the device, decision on the host with the reference's libm softmax
+    (route_host_decide).  Predictions, decisions and the whole simulate_trace timeline must still
+    equal the reference's bit for bit — the path the ~1-in-600 uncertified items take normally."""
+    monkeypatch.setenv("ADAPMOE_ROUTE_FORCE_EXACT", "1")
+    g = load_golden(name)
+    w, fg = oracle_inputs(g)
+    cfg = sim_config(g)
+    with P.Engine(_spec(g)) as eng:
+        eng.load_gates(w.gates, fg)
+        dec, single, pert, preds = eng.route_trace(w.acts, w.scores, w.fisher, g["tau"], cfg)
+        gdec, gsingle, gpreds = golden_decisions(g)
+        assert np.array_equal(dec, gdec) and np.array_equal(single, gsingle)
+        mism = np.argwhere((preds != gpreds).any(axis=-1))
+        assert mism.size == 0, f"{len(mism)} prediction flips, first at (tok, layer, slot) {mism[0].tolist()}"
+        r = eng.simulate_trace(w.acts, w.scores, w.fisher, g["sim_capacities"], g["tau"], cfg,
+                               int(g["workload"]["seed"]))
+        assert_metrics(g, r.metrics, r.latency_per_token, r.on_demand_loads_per_layer)
+        assert_timeline(g, r.timeline)
+        if g["spec"][3] <= 256 and cfg.policy.prefetch:  # the physical decode's routing takes the same path
+            T = min(8, w.T)
+            ffn = 4 * g["spec"][3] if g["spec"][3] % 32 == 0 else None
+            if ffn is not None:
+                eng.experts_init(ffn, cfg.tile_count_per_expert, seed=5)
+                eng.decode_begin(g["sim_capacities"], w.fisher, g["tau"], cfg, int(g["workload"]["seed"]), T)
+                hid = np.zeros((T, w.L, w.D), dtype=np.float32)
+                eng.decode_tokens(w.acts[:T], w.scores[:T], hid)
+                st = eng.decode_stats()
+                res = eng.decode_end(cfg, T)
+                ref = O.simulate(w, g["sim_capacities"], g["tau"], first_gate=fg, T=T, **sim_kwargs(g))
+                assert res.metrics == ref.metrics
+                assert np.array_equal(res.timeline, ref.timeline)
+                assert st["router_exact_items"] > 0

@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
+#include <cstring>
 
 #include "expert_ffn.hpp"
 #include "ptx.cuh"
@@ -182,6 +184,270 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_rows_kernel(const __grid_cons
         c0 += n;
     }
     store_partial<DC>(part + static_cast<size_t>(cur_seg - first_seg) * D, acc, tid, D);
+}
+
+// ---------------------------------------------------------------------------------------------
+// K2 v5 — the same row-owner decomposition, fed by the TMA engine through a deep shared-memory ring.
+//
+// The LDG kernel above alternates two load phases per 16-row chunk (W1/W3 rows, then W2^T rows)
+// with a CTA barrier between them, so its loads drain twice per chunk; on short launches (a
+// layer's final 88 MB tile = ~24 rows per CTA) that ramp / drain is ~11 us of fixed cost per
+// launch (profiles/r1_ncu_summary.md: 25 us for 88 MB, 44 % DRAM).  Here one producer lane issues
+// 1-D bulk copies (cp.async.bulk, evict-first) of the CTA's contiguous rows in exactly the order
+// the consumers use them — per chunk the W1/W3 row pairs, then the W2^T rows — into a ring of
+// kRingBytes (4-8 stages of ~32 KB, mbarrier full/empty pairs), and never waits on compute except
+// for a free stage, so HBM sees 100-200 KB in flight per SM from the first microsecond to the last.
+// Consumer thread t owns the 16-byte column vectors v = t + kRingConsumers*k of every row: its
+// slice of x lives in registers (fp32), phase 1 accumulates its part of (W1_r.x, W3_r.x) for the
+// chunk's rows, a reduce-scatter shuffle + one consumer barrier forms h_r = silu(a)*b, and phase 2
+// accumulates h_r * W2^T_r into the same columns of y (registers), as in the LDG kernel.  The
+// partial layout [grid][2][d] and the CTA row split are unchanged, so the combine is shared.
+#ifndef ADAPMOE_K2_CWARPS  // tuning knobs (tools/k2_ring_bench.cu sweeps them)
+#define ADAPMOE_K2_CWARPS 16
+#endif
+#ifndef ADAPMOE_K2_STAGE_KB
+#define ADAPMOE_K2_STAGE_KB 64
+#endif
+#ifndef ADAPMOE_K2_MAX_STAGES
+#define ADAPMOE_K2_MAX_STAGES 8
+#endif
+#ifndef ADAPMOE_K2_RING_KB
+#define ADAPMOE_K2_RING_KB 192
+#endif
+namespace ring {
+constexpr int kConsumerWarps = ADAPMOE_K2_CWARPS;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kThreads = kConsumers + 32;  // + one producer warp
+#ifndef ADAPMOE_K2_ROWS
+#define ADAPMOE_K2_ROWS 16
+#endif
+constexpr int kRows = ADAPMOE_K2_ROWS;     // ffn rows per chunk (16 or 32)
+static_assert(kRows == 16 || kRows == 32);
+constexpr int kRingBytes = ADAPMOE_K2_RING_KB * 1024;
+constexpr int kMaxStages = ADAPMOE_K2_MAX_STAGES;
+constexpr int kStageTarget = ADAPMOE_K2_STAGE_KB * 1024;
+
+struct Geometry {
+    int g;            // W1/W3 row pairs per phase-1 stage (2g W2^T rows per phase-2 stage)
+    int stage_bytes;  // g * 4 * d
+    int stages;
+};
+__host__ __device__ inline Geometry geometry(int d) {
+    Geometry q;
+    q.g = 4 * d >= kStageTarget ? 1 : kStageTarget / (4 * d);
+    if (q.g > kRows / 2) q.g = kRows / 2;
+    q.stage_bytes = q.g * 4 * d;
+    q.stages = kRingBytes / q.stage_bytes;
+    if (q.stages > kMaxStages) q.stages = kMaxStages;
+    return q;
+}
+}  // namespace ring
+
+__device__ __forceinline__ void consumer_sync() {  // named barrier 1: the consumer warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(ring::kConsumers) : "memory");
+}
+
+#ifdef ADAPMOE_K2_TRACE  // tools/k2_ring_bench.cu: per-CTA globaltimer stamps (start, first stage, end)
+__device__ unsigned long long k2_trace[kFfnMaxCtas][4];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
+// DV = ceil(d / 8 / kConsumers): 16-byte column vectors per consumer thread and row
+template <int DV>
+__global__ void __launch_bounds__(ring::kThreads, 1) ffn_ring_kernel(const __grid_constant__ FfnLaunch p) {
+    using namespace ring;
+    extern __shared__ __align__(128) unsigned char ring_buf[];
+    __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+    __shared__ float red[kConsumerWarps][2 * kRows];
+    __shared__ float hs[kRows];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int D = p.d, Ft = p.ft, vpr = D / 8;
+    const Geometry geo = geometry(D);
+    const int G = geo.g, G2 = 2 * geo.g, NS = geo.stages, SB = geo.stage_bytes;
+    const long long TR = static_cast<long long>(p.n_seg) * Ft;
+    const long long r_lo = TR * blockIdx.x / gridDim.x, r_hi = TR * (blockIdx.x + 1) / gridDim.x;
+#ifdef ADAPMOE_K2_TRACE
+    if (tid == 0) k2_trace[blockIdx.x][0] = gtime();
+#endif
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], kConsumerWarps);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {  // ---- producer: one lane streams the CTA's rows ----
+        if (lane == 0) {
+            const uint64_t pol = ptx::policy_evict_first();
+            int i = 0;
+            auto issue = [&](const unsigned char* src, int bytes) {
+                const int slot = i % NS;
+                if (i >= NS) ptx::mbar_wait(&empty[slot], ((i / NS) - 1) & 1);
+                ptx::mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(bytes));
+                ptx::bulk_g2s_stream(ring_buf + static_cast<size_t>(slot) * SB, src, static_cast<uint32_t>(bytes),
+                                     &full[slot], pol);
+                ++i;
+            };
+            for (long long c0 = r_lo; c0 < r_hi;) {
+                const int s = static_cast<int>(c0 / Ft), r0 = static_cast<int>(c0 % Ft);
+                const int n = static_cast<int>(min(static_cast<long long>(min(kRows, Ft - r0)), r_hi - c0));
+                const unsigned char* gu = reinterpret_cast<const unsigned char*>(p.seg[s].gate_up) + static_cast<size_t>(r0) * 4 * D;
+                for (int j = 0; j < n; j += G) issue(gu + static_cast<size_t>(j) * 4 * D, min(G, n - j) * 4 * D);
+                const unsigned char* dn = reinterpret_cast<const unsigned char*>(p.seg[s].down_t) + static_cast<size_t>(r0) * 2 * D;
+                for (int j = 0; j < n; j += G2) issue(dn + static_cast<size_t>(j) * 2 * D, min(G2, n - j) * 2 * D);
+                c0 += n;
+            }
+        }
+        return;
+    }
+
+    // ---- consumers ----
+    float4 xa[DV], xb[DV];  // x[8v .. 8v+8) of this thread's vectors, fp32
+#pragma unroll
+    for (int k = 0; k < DV; ++k) {
+        const int v = tid + kConsumers * k;
+        float t[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) t[e] = v < vpr ? static_cast<float>(__ldg(p.x + 8 * v + e)) : 0.0f;
+        xa[k] = make_float4(t[0], t[1], t[2], t[3]);
+        xb[k] = make_float4(t[4], t[5], t[6], t[7]);
+    }
+    float acc[DV][8];
+#pragma unroll
+    for (int k = 0; k < DV; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[k][e] = 0.0f;
+    const int first_seg = static_cast<int>(r_lo / Ft);
+    int cur_seg = first_seg;
+    float* const part = p.partial + static_cast<size_t>(blockIdx.x) * kFfnSlotsPerCta * D;
+    auto flush = [&](int seg) {
+        float* dst = part + static_cast<size_t>(seg - first_seg) * D;
+#pragma unroll
+        for (int k = 0; k < DV; ++k) {
+            const int v = tid + kConsumers * k;
+            if (v < vpr) {
+                *reinterpret_cast<float4*>(dst + 8 * v) = make_float4(acc[k][0], acc[k][1], acc[k][2], acc[k][3]);
+                *reinterpret_cast<float4*>(dst + 8 * v + 4) = make_float4(acc[k][4], acc[k][5], acc[k][6], acc[k][7]);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[k][e] = 0.0f;
+        }
+    };
+    int i = 0;  // stage sequence number (mirrors the producer)
+    for (long long c0 = r_lo; c0 < r_hi;) {
+        const int s = static_cast<int>(c0 / Ft), r0 = static_cast<int>(c0 % Ft);
+        const int n = static_cast<int>(min(static_cast<long long>(min(kRows, Ft - r0)), r_hi - c0));
+        if (s != cur_seg) {
+            flush(cur_seg);
+            cur_seg = s;
+        }
+        // phase 1: this thread's part of a_r = W1_r.x, b_r = W3_r.x for the chunk's rows
+        float ab[2 * kRows];
+#pragma unroll
+        for (int q = 0; q < 2 * kRows; ++q) ab[q] = 0.0f;
+        const unsigned char* base = nullptr;
+        int slot = 0;
+#pragma unroll
+        for (int rr = 0; rr < kRows; ++rr) {
+            if (rr < n) {
+                const int j = rr % G;
+                if (j == 0) {
+                    slot = i % NS;
+                    ptx::mbar_wait(&full[slot], (i / NS) & 1);
+                    base = ring_buf + static_cast<size_t>(slot) * SB;
+#ifdef ADAPMOE_K2_TRACE
+                    if (i == 0 && tid == 0) k2_trace[blockIdx.x][1] = gtime();
+#endif
+                }
+                const int4* w1 = reinterpret_cast<const int4*>(base + static_cast<size_t>(j) * 4 * D);
+                const int4* w3 = w1 + vpr;
+#pragma unroll
+                for (int k = 0; k < DV; ++k) {
+                    const int v = tid + kConsumers * k;
+                    if (v < vpr) {
+                        ab[rr] = dot8(w1[v], xa[k], xb[k], ab[rr]);
+                        ab[kRows + rr] = dot8(w3[v], xa[k], xb[k], ab[kRows + rr]);
+                    }
+                }
+                if (j == G - 1 || rr == n - 1) {
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&empty[slot]);
+                    ++i;
+                }
+            }
+        }
+        // warp reduce-scatter of the 2*kRows values (a then b): lane l ends with the warp sums of
+        // values [l*V, l*V + V), V = 2*kRows/32 (each halving step keeps the upper or lower half)
+        constexpr int V = 2 * kRows / 32;
+#pragma unroll
+        for (int o = 16, half = kRows; o >= 1; o >>= 1, half >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int q = 0; q < half; ++q) {
+                const float send = up ? ab[q] : ab[q + half];
+                const float keep = up ? ab[q + half] : ab[q];
+                ab[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < V; ++e) red[warp][lane * V + e] = ab[e];
+        consumer_sync();
+        if (tid < n) {  // fixed warp order
+            float a = 0.0f, b = 0.0f;
+#pragma unroll
+            for (int w = 0; w < kConsumerWarps; ++w) {
+                a += red[w][tid];
+                b += red[w][kRows + tid];
+            }
+            hs[tid] = silu(a) * b;
+        }
+        consumer_sync();
+        // phase 2: acc += h_r * W2^T_r over this thread's columns
+#pragma unroll
+        for (int rr = 0; rr < kRows; ++rr) {
+            if (rr < n) {
+                const int j = rr % G2;
+                if (j == 0) {
+                    slot = i % NS;
+                    ptx::mbar_wait(&full[slot], (i / NS) & 1);
+                    base = ring_buf + static_cast<size_t>(slot) * SB;
+                }
+                const int4* w2 = reinterpret_cast<const int4*>(base + static_cast<size_t>(j) * 2 * D);
+                const float h = hs[rr];
+#pragma unroll
+                for (int k = 0; k < DV; ++k) {
+                    const int v = tid + kConsumers * k;
+                    if (v < vpr) {
+                        const int4 q = w2[v];
+                        acc[k][0] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q.x) << 16), acc[k][0]);
+                        acc[k][1] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q.x) & 0xffff0000u), acc[k][1]);
+                        acc[k][2] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q.y) << 16), acc[k][2]);
+                        acc[k][3] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q.y) & 0xffff0000u), acc[k][3]);
+                        acc[k][4] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q.z) << 16), acc[k][4]);
+                        acc[k][5] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q.z) & 0xffff0000u), acc[k][5]);
+                        acc[k][6] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q.w) << 16), acc[k][6]);
+                        acc[k][7] = __fmaf_rn(h, __uint_as_float(static_cast<unsigned>(q.w) & 0xffff0000u), acc[k][7]);
+                    }
+                }
+                if (j == G2 - 1 || rr == n - 1) {
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&empty[slot]);
+                    ++i;
+                }
+            }
+        }
+        c0 += n;
+    }
+    flush(cur_seg);
+#ifdef ADAPMOE_K2_TRACE
+    if (tid == 0) k2_trace[blockIdx.x][2] = gtime();
+#endif
 }
 
 // out[j] = x[j] + sum_rank w_rank * y_rank[j];  y_rank = fixed-order reduction of the K2 partials
@@ -388,6 +654,14 @@ void ffn_partial_range(FfnPartialRef& f, int ft) {
     f.slot_lo = f.seg - static_cast<int>(TR * c_lo / f.grid / ft);
 }
 
+FfnKernel ffn_kernel_variant() {
+    static const FfnKernel v = [] {
+        const char* e = std::getenv("ADAPMOE_K2");  // A/B knob: "rows" = the LDG row-owner kernel
+        return (e && std::strcmp(e, "rows") == 0) ? FfnKernel::Rows : FfnKernel::Ring;
+    }();
+    return v;
+}
+
 int ffn_grid(const FfnLaunch& p, int sm_count) {
     const long long rows = static_cast<long long>(p.n_seg) * p.ft;
     long long g = sm_count < kFfnMaxCtas ? sm_count : kFfnMaxCtas;
@@ -401,7 +675,6 @@ cudaError_t launch_ffn(const FfnLaunch& p, int sm_count, cudaStream_t stream) {
     if (p.n_seg > kMaxFfnSegments || p.d % 8 || p.d > 16384 || p.ft < 1 || !p.partial || !p.x)
         return cudaErrorInvalidValue;
     const int grid = ffn_grid(p, sm_count);
-    const size_t smem = static_cast<size_t>(p.d) * sizeof(float);
     // the > 48 KB opt-in is a per-device function attribute: configure each device once
     static std::atomic<std::uint64_t> configured{0};
     int dev = 0;
@@ -411,8 +684,23 @@ cudaError_t launch_ffn(const FfnLaunch& p, int sm_count, cudaStream_t stream) {
             const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
             if (e != cudaSuccess) return e;
         }
+        for (auto fn : {ffn_ring_kernel<1>, ffn_ring_kernel<2>, ffn_ring_kernel<3>, ffn_ring_kernel<4>,
+                        ffn_ring_kernel<6>, ffn_ring_kernel<8>}) {
+            const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ring::kRingBytes);
+            if (e != cudaSuccess) return e;
+        }
         configured.fetch_or(std::uint64_t{1} << dev);
     }
+    if (ffn_kernel_variant() == FfnKernel::Ring) {
+        const ring::Geometry geo = ring::geometry(p.d);
+        const size_t smem = static_cast<size_t>(geo.stages) * geo.stage_bytes;
+        const int dv = (p.d / 8 + ring::kConsumers - 1) / ring::kConsumers;
+        auto fn = dv <= 1 ? ffn_ring_kernel<1> : dv <= 2 ? ffn_ring_kernel<2> : dv <= 3 ? ffn_ring_kernel<3>
+                : dv <= 4 ? ffn_ring_kernel<4> : dv <= 6 ? ffn_ring_kernel<6> : ffn_ring_kernel<8>;
+        fn<<<grid, ring::kThreads, smem, stream>>>(p);
+        return cudaGetLastError();
+    }
+    const size_t smem = static_cast<size_t>(p.d) * sizeof(float);
     if (p.d <= 4096)
         ffn_rows_kernel<1><<<grid, kThreads, smem, stream>>>(p);
     else if (p.d <= 8192)

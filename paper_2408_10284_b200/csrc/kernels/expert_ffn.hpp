@@ -41,6 +41,10 @@ struct FfnLaunch {
 
 // Grid the launch will use (partial buffer rows = grid * kFfnSlotsPerCta).
 int ffn_grid(const FfnLaunch& p, int sm_count);
+// Ring = TMA bulk-copy ring (default); Rows = the LDG row-owner kernel (ADAPMOE_K2=rows).  Both
+// use the same CTA row split and partial layout.
+enum class FfnKernel { Ring, Rows };
+FfnKernel ffn_kernel_variant();
 cudaError_t launch_ffn(const FfnLaunch& p, int sm_count, cudaStream_t stream);
 
 // One (rank, tile) segment's location among the launches of a layer.

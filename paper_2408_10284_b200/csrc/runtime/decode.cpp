@@ -87,7 +87,7 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     for (int s = 0; s < n_slots_; ++s) free_.push_back(s);
     slot_of_.assign(static_cast<size_t>(L) * N, -1);
     MOE_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, eng.device()));
-    if (const char* v = std::getenv("ADAPMOE_TILE_MERGE")) tile_merge_ = std::atoi(v) != 0 ? 1 : 0;  // A/B knob
+    if (const char* v = std::getenv("ADAPMOE_TILE_MERGE")) tile_merge_ = std::clamp(std::atoi(v), 0, 2);  // A/B knob
     d_combine_ticket_.reserve(sizeof(unsigned));
     MOE_CUDA(cudaMemsetAsync(d_combine_ticket_.ptr, 0, sizeof(unsigned), eng.compute_stream()));
 
@@ -469,21 +469,29 @@ void DecodeSession::on_layer_done(int, int, const RouteDecision& d) {
     ++layer_seq_;
 }
 
-// Launch groups for the layer's on-demand (missing) experts, in landing order.  The host link is
-// ~100x slower than HBM, so a tile's FFN finishes long before the next tile lands: an expert that is
-// not the layer's last to land computes all its tiles in one launch once its last tile has landed
-// (the link is still busy with the later experts, so this costs nothing on the critical path), and
-// the last expert computes tiles 0..n-2 together and its final tile alone — the work left after the
-// layer's final tile lands stays one tile's.  The layer's resident experts join the first group that
-// is not the final tile (merge_resident()).  Merging pays only when a tile's transfer dwarfs a launch:
-// on by default for tiles >= 8 MiB (88 MB at 8x7B: 1.6 ms on PCIe Gen5 vs ~25 us of K2);
-// ADAPMOE_TILE_MERGE=0 / 1 forces it off / on.
+// Launch plan for the layer's on-demand (missing) experts, in landing order (ADAPMOE_TILE_MERGE):
+//   0 "tiles":  one launch per landed tile (the reference's tile pipeline, inc/simulator.hpp:451-459);
+//   1 "groups": an expert that is not the layer's last to land computes all its tiles in one launch
+//               once its last tile has landed, the last expert computes tiles 0..n-2 together and its
+//               final tile alone, and the resident experts join the first group that is not the final
+//               tile (merge_resident()) — the work left after the final tile lands stays one tile's;
+//   2 "layer":  the layer's whole FFN (resident experts + every on-demand tile) in ONE launch once its
+//               last tile has landed.
+// The host link is ~100x slower than HBM: a tile of 88 MB (8x7B) takes 1.6 ms on PCIe Gen5, the
+// layer's whole FFN ~0.1 ms, and the link keeps streaming the next layer's copies meanwhile, so
+// computing the layer after its last tile costs no link time, while a launch carries ~10 us of fixed
+// cost (launch, first bytes, tail: profiles/r2_k2_ring.txt) that a 88 MB single-tile launch cannot
+// amortise.  Default (-1): "layer" for tiles >= 8 MiB, "tiles" below.
 bool DecodeSession::tile_merge_active() const {
     return tile_merge_ > 0 || (tile_merge_ < 0 && store_.tile_bytes >= (size_t{8} << 20));
 }
 
+bool DecodeSession::layer_launch() const {
+    return tile_merge_ == 2 || (tile_merge_ < 0 && store_.tile_bytes >= (size_t{8} << 20));
+}
+
 bool DecodeSession::merge_resident() const {
-    if (!tile_merge_active()) return false;
+    if (!tile_merge_active() || layer_launch()) return false;
     int groups = 0;
     for (const Use& u : uses_)
         if (u.missing && !u.tiles.empty()) groups += u.tiles.size() > 1 ? 2 : 1;
@@ -499,7 +507,7 @@ std::vector<std::pair<const DecodeSession::Use*, std::vector<int>>> DecodeSessio
         const std::vector<int>& tiles = missing[m]->tiles;
         if (!tile_merge_active()) {
             for (int t : tiles) groups.emplace_back(missing[m], std::vector<int>{t});
-        } else if (m + 1 < missing.size() || tiles.size() == 1) {
+        } else if (layer_launch() || m + 1 < missing.size() || tiles.size() == 1) {
             groups.emplace_back(missing[m], tiles);
         } else {
             groups.emplace_back(missing[m], std::vector<int>(tiles.begin(), tiles.end() - 1));
@@ -611,16 +619,19 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
     const auto groups = tile_groups();
     // resident segments ride with the first on-demand group when that group is off the critical
     // path and the launch stays within kMaxFfnSegments
-    const bool hold = p.n_seg > 0 && merge_resident() &&
-                      p.n_seg + static_cast<int>(groups.front().second.size()) <= kMaxFfnSegments;
+    const bool one_launch = layer_launch();
+    const bool hold = p.n_seg > 0 && !groups.empty() &&
+                      (one_launch || (merge_resident() &&
+                                      p.n_seg + static_cast<int>(groups.front().second.size()) <= kMaxFfnSegments));
     if (p.n_seg && !hold) {
         timed_ffn(p, meta, refs);
         meta.clear();
     }
-    // on-demand experts, as their tiles land (tile_groups: merged launches off the critical path)
-    for (const auto& grp : groups) {
-        const Use& u = *grp.first;
-        for (int t : grp.second) {
+    // on-demand experts, as their tiles land (tile_groups: merged launches off the critical path;
+    // "layer" mode: one launch after the layer's last tile)
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const Use& u = *groups[gi].first;
+        for (int t : groups[gi].second) {
             if (p.n_seg == kMaxFfnSegments) {  // launch what has landed so far
                 timed_ffn(p, meta, refs);
                 meta.clear();
@@ -629,9 +640,11 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
             p.seg[p.n_seg++] = seg(u.slot, t);
             meta.emplace_back(u.rank, t);
         }
-        timed_ffn(p, meta, refs);
-        meta.clear();
-        if (grp.second.back() == u.tiles.back()) stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
+        if (!one_launch || gi + 1 == groups.size()) {
+            timed_ffn(p, meta, refs);
+            meta.clear();
+        }
+        if (groups[gi].second.back() == u.tiles.back()) stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
     }
     std::sort(refs.begin(), refs.end(), [](const auto& a, const auto& b) {
         return std::get<0>(a) != std::get<0>(b) ? std::get<0>(a) < std::get<0>(b) : std::get<1>(a) < std::get<1>(b);
@@ -734,6 +747,7 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
         std::vector<GSeg> segs;
         int wait_slot = -1;
         std::vector<int> wait_tiles;
+        std::vector<std::pair<int, int>> waits;  // (slot, tile) of a merged job, in landing order
     };
     std::vector<Job> jobs;
     Job res;
@@ -763,6 +777,19 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
         jobs[1].segs.insert(jobs[1].segs.begin(), jobs[0].segs.begin(), jobs[0].segs.end());
         jobs.erase(jobs.begin());
     }
+    if (layer_launch() && jobs.size() > 1) {  // one launch pair once the layer's last tile has landed
+        Job all;
+        for (size_t i = 0; i < jobs.size(); ++i) {
+            if (i > 0 && all.segs.size() + jobs[i].segs.size() > static_cast<size_t>(kGMaxSegs)) break;
+            for (int t : jobs[i].wait_tiles) all.waits.emplace_back(jobs[i].wait_slot, t);
+            all.segs.insert(all.segs.end(), jobs[i].segs.begin(), jobs[i].segs.end());
+            jobs[i].segs.clear();
+        }
+        std::vector<Job> rest{all};
+        for (size_t i = 1; i < jobs.size(); ++i)
+            if (!jobs[i].segs.empty()) rest.push_back(jobs[i]);
+        jobs.swap(rest);
+    }
     // plan every down launch first: the partial arena must hold the whole layer
     std::vector<GroupedLaunch> downs(jobs.size(), base);
     size_t need = 0;
@@ -783,6 +810,7 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
     std::vector<std::pair<int, GCombineRef>> refs;  // (rank, ref) in launch order
     for (size_t i = 0; i < jobs.size(); ++i) {
         for (int t : jobs[i].wait_tiles) wait_fill(jobs[i].wait_slot, t);
+        for (const auto& w : jobs[i].waits) wait_fill(w.first, w.second);
         GroupedLaunch up = base;
         up.n_seg = downs[i].n_seg;
         for (int s = 0; s < up.n_seg; ++s) up.seg[s] = downs[i].seg[s];

@@ -102,8 +102,9 @@ private:
     void layer_ffn_single(const RouteDecision& d);   // batch 1: K2 row kernel
     std::vector<std::pair<const Use*, std::vector<int>>> tile_groups() const;
     bool tile_merge_active() const;
+    bool layer_launch() const;
     bool merge_resident() const;
-    int tile_merge_ = -1;  // -1 auto (tiles >= 8 MiB), 0 off, 1 on
+    int tile_merge_ = -1;  // -1 auto (tiles >= 8 MiB: 2), 0 per tile, 1 groups, 2 one launch per layer
     void layer_ffn_grouped(const RouteDecision& d);  // batch > 1: K3 grouped tcgen05 kernels
     void timed_grouped(GroupedLaunch& p, bool down);
     void ep_exchange(float* out, long long rows, long long row_stride);

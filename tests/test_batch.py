@@ -102,7 +102,7 @@ def _run_batch(ws, caps, tau, fg, ffn, tiles, seed, calls):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("merge", ["0", "1"])
+@pytest.mark.parametrize("merge", ["0", "1", "2"])
 @pytest.mark.parametrize("B,caps", [(4, [3, 2, 2, 1]), (16, [8, 4, 2, 0]), (64, [2, 2, 2, 2])])
 def test_batched_decode_tiny(B, caps, merge, monkeypatch):
     """merge: ADAPMOE_TILE_MERGE — on-demand tiles (and the resident experts) grouped into fewer

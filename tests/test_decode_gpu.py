@@ -225,12 +225,15 @@ def test_route_windows_bit_identical(window, monkeypatch):
     assert r.stats["router_launches"] == sum(-(-(b - a) // int(window)) for a, b in zip(cuts, cuts[1:]))
 
 
+@pytest.mark.parametrize("merge", ["1", "2"])
 @pytest.mark.parametrize("name", ["tiny", "tiny_transfer_heavy", "tiny_budget0", "tiny_prefetch_off"])
-def test_tile_merge_every_output(name, monkeypatch):
-    """ADAPMOE_TILE_MERGE=1 (the default for >= 8 MiB tiles): an on-demand expert's tiles share one
-    K2 launch once landed, the layer's last expert keeps its final tile alone, resident experts ride
-    with the first on-demand group.  The trace is untouched and every output matches the oracle."""
-    monkeypatch.setenv("ADAPMOE_TILE_MERGE", "1")
+def test_tile_merge_every_output(name, merge, monkeypatch):
+    """ADAPMOE_TILE_MERGE=1 ("groups"): an on-demand expert's tiles share one K2 launch once landed,
+    the layer's last expert keeps its final tile alone, resident experts ride with the first
+    on-demand group.  ADAPMOE_TILE_MERGE=2 ("layer", the default for >= 8 MiB tiles): the layer's
+    whole FFN in one launch after its last tile lands.  The trace is untouched and every output
+    matches the oracle."""
+    monkeypatch.setenv("ADAPMOE_TILE_MERGE", merge)
     g = load_golden(name)
     w, fg = oracle_inputs(g)
     cfg = sim_config(g)
@@ -246,6 +249,8 @@ def test_tile_merge_every_output(name, monkeypatch):
                      **{k: v for k, v in __import__("helpers").sim_kwargs(g).items()})
     assert r.metrics == sim.metrics and np.array_equal(r.timeline, sim.timeline)
     assert r.stats["ffn_bytes"] == r.metrics["experts_activated_total"] * 3 * ffn * w.D * 2
+    if merge == "2":  # one K2 launch per (token, layer)
+        assert r.stats["ffn_launches"] == T * w.L, r.stats["ffn_launches"]
     ref = _moe_reference(w, fg, sim.decisions, T, ffn, cfg.tile_count_per_expert, seed)
     for (t, l), moe in ref.items():
         got = hid[t, l].astype(np.float64) - w.acts[t, l].astype(np.float32).astype(np.float64)

@@ -22,7 +22,7 @@ def run(seed):
     tiles = int(r.choice([1, 2, 4]))
     F = 64 * tiles * int(r.integers(1, 4))
     T = int(r.integers(1, 6))
-    os.environ["ADAPMOE_TILE_MERGE"] = str(int(r.integers(0, 2)))
+    os.environ["ADAPMOE_TILE_MERGE"] = str(int(r.integers(0, 3)))
     ws = [O.generate_trace(L, N, K, D, T, 0.6, 0.2, 5, 100 + b) for b in range(B)]
     tau = O.calibrate_threshold(ws[0], 0.24)
     caps = [int(x) for x in r.integers(0, N + 1, size=L)]

@@ -1,0 +1,69 @@
+/* CPU expert-FFN decode baseline — builder-written, NOT the reference.
+ *
+ * The reference (moesim) charges expert compute as ticks and does no FFN arithmetic
+ * (/root/reference/proj/include/moesim/simulator.hpp:446-462), so its timed CPU path moves no
+ * weights.  BASELINE.md §4.3 asks for a CPU SwiGLU of the same decode next to it: this file computes
+ * one MoE layer, out = x + sum_e w_e * SwiGLU_e(x), for the selected experts of a (token, layer),
+ * reading the expert weights in place from the engine's pinned host store (moe_expert_host_ptr;
+ * tile-major bf16 layout of paper_2408_10284_b200/csrc/kernels/expert_ffn.hpp), fp32 accumulation,
+ * ffn rows split over OpenMP threads (each thread a private partial of y, summed in thread order).
+ * Used only by bench.py's cpu_baseline_ffn leg.
+ *   gcc -O3 -march=x86-64-v3 -fopenmp -fPIC -shared -o baseline/libcpu_ffn.so baseline/cpu_ffn.c -lm
+ */
+#include <math.h>
+#include <omp.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+static inline float bf16(uint16_t v) {
+    union { uint32_t u; float f; } c;
+    c.u = (uint32_t)v << 16;
+    return c.f;
+}
+
+/* experts[k]: tile-major block of the k-th selected expert; weights[k]: its combine weight. */
+int cpu_moe_layer(const void* const* experts, const double* weights, int n_experts, int D, int F, int tiles,
+                  const double* x_in, float* out, int threads) {
+    if (D <= 0 || F <= 0 || tiles <= 0 || F % tiles || n_experts < 0 || threads <= 0) return 1;
+    const int Ft = F / tiles;
+    const size_t tile_elems = (size_t)3 * Ft * D;
+    float* x = (float*)malloc(sizeof(float) * D);
+    float* part = (float*)calloc((size_t)threads * D, sizeof(float));
+    if (!x || !part) return 2;
+    for (int j = 0; j < D; ++j) x[j] = (float)x_in[j];
+    for (int j = 0; j < D; ++j) out[j] = x[j];
+    for (int k = 0; k < n_experts; ++k) {
+        const uint16_t* base = (const uint16_t*)experts[k];
+        memset(part, 0, sizeof(float) * (size_t)threads * D);
+#pragma omp parallel num_threads(threads)
+        {
+            const int t = omp_get_thread_num(), nt = omp_get_num_threads();
+            float* y = part + (size_t)t * D;
+            const int r0 = (int)((long long)F * t / nt), r1 = (int)((long long)F * (t + 1) / nt);
+            for (int r = r0; r < r1; ++r) {
+                const uint16_t* tile = base + (size_t)(r / Ft) * tile_elems;
+                const uint16_t* w1 = tile + (size_t)(r % Ft) * 2 * D;
+                const uint16_t* w3 = w1 + D;
+                const uint16_t* w2 = tile + (size_t)2 * Ft * D + (size_t)(r % Ft) * D;
+                float a = 0.0f, b = 0.0f;
+#pragma omp simd reduction(+ : a, b)
+                for (int j = 0; j < D; ++j) {
+                    a += bf16(w1[j]) * x[j];
+                    b += bf16(w3[j]) * x[j];
+                }
+                const float h = a / (1.0f + expf(-a)) * b;
+#pragma omp simd
+                for (int j = 0; j < D; ++j) y[j] += h * bf16(w2[j]);
+            }
+        }
+        const float w = (float)weights[k];
+        for (int t = 0; t < threads; ++t) {
+            const float* y = part + (size_t)t * D;
+            for (int j = 0; j < D; ++j) out[j] += w * y[j];
+        }
+    }
+    free(x);
+    free(part);
+    return 0;
+}

@@ -94,6 +94,9 @@ def workload(args):
 BACKEND = os.environ.get("ADAPMOE_DIST_BACKEND", "nccl")
 
 
+COMM = {"backend": None, "nranks": 1}
+
+
 def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -107,7 +110,61 @@ def dist_init():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(BACKEND)
+        # the communicator's own rank count (checked against WORLD_SIZE / --gpus by the caller)
+        t = torch.ones(1, device="cuda" if BACKEND == "nccl" else "cpu")
+        dist.all_reduce(t)
+        COMM.update(backend=dist.get_backend(), nranks=dist.get_world_size(), all_reduce_ranks=int(t.item()),
+                    gpus_visible=torch.cuda.device_count())
+        if BACKEND == "nccl":
+            COMM["nccl_version"] = ".".join(str(v) for v in torch.cuda.nccl.version())
+        if COMM["nranks"] != ws or COMM["all_reduce_ranks"] != ws:
+            raise SystemExit(f"communicator has {COMM['nranks']} ranks ({COMM['all_reduce_ranks']} in an all_reduce), "
+                             f"WORLD_SIZE is {ws}")
     return ws, rank, local
+
+
+def host_info() -> dict:
+    """nproc, CPU model and RAM of this host (with every report)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+        mem = open("/proc/meminfo").read()
+        info["ram_gb"] = round(int(mem.split("MemTotal:")[1].split()[0]) / 2**20, 1)
+    except Exception:  # noqa: BLE001
+        pass
+    return info
+
+
+def fnv1a_i64(arr) -> str:
+    """FNV-1a 64 over the raw little-endian bytes of an int64 array (the reference driver's hash)."""
+    import numpy as np
+    h = 0xcbf29ce484222325
+    for b in np.ascontiguousarray(arr, dtype=np.int64).tobytes():
+        h = ((h ^ b) * 0x100000001b3) & 0xffffffffffffffff
+    return f"{h:016x}"
+
+
+def spawn_ranks(args) -> None:
+    """`bench.py --gpus N` outside torchrun: launch N ranks of this script (one per GPU) through
+    torch.distributed.run on 127.0.0.1 and exit with its status.  Under torchrun (WORLD_SIZE set)
+    the rank count must equal --gpus."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus} launched with WORLD_SIZE={ws}")
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def barrier(ws):
@@ -209,6 +266,49 @@ def run_reference_driver(wl, sample_tokens: int, reps: int):
     return json.loads(out)
 
 
+def cpu_ffn_baseline(eng, wl, trace, tau, cfg, tok0: int, n_tok: int, gpu_out):
+    """the same decode's expert FFN on the host cores (baseline/cpu_ffn.c, OpenMP,
+    builder-written — NOT the reference, whose CPU path does no FFN arithmetic): for each (token,
+    layer) of a bounded sample, out = x + sum_e w_e SwiGLU_e(x) over the selected experts (the
+    reference rule's selections, from K1), reading the weights in place from the pinned host store.
+    Also the largest relative difference to the GPU decode's outputs of the same tokens."""
+    import ctypes as C
+
+    import numpy as np
+    lib = C.CDLL(os.path.join(ROOT, "baseline", "libcpu_ffn.so"))
+    lib.cpu_moe_layer.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_double), C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.POINTER(C.c_double), C.POINTER(C.c_float), C.c_int]
+    threads = os.cpu_count() or 1
+    acts = np.ascontiguousarray(trace.acts[tok0: tok0 + n_tok])
+    scores = trace.scores[tok0: tok0 + n_tok]
+    dec, single, _, _ = eng.route_trace(acts, scores, trace.fisher, tau, cfg)
+    out = np.zeros((n_tok, wl.layers, wl.hidden), dtype=np.float32)
+    moved = 0
+    t0 = time.perf_counter()
+    for t in range(n_tok):
+        for l in range(wl.layers):
+            sel = [int(e) for e in dec[t, l] if e >= 0]
+            den = sum(scores[t, l, e] for e in sel)
+            wts = (C.c_double * len(sel))(*[1.0 if len(sel) == 1 else scores[t, l, e] / den for e in sel])
+            ptrs = (C.c_void_p * len(sel))(*[eng.expert_host_ptr(l, e) for e in sel])
+            x = acts[t, l]
+            rc = lib.cpu_moe_layer(ptrs, wts, len(sel), wl.hidden, wl.ffn, wl.tiles,
+                                   x.ctypes.data_as(C.POINTER(C.c_double)),
+                                   out[t, l].ctypes.data_as(C.POINTER(C.c_float)), threads)
+            assert rc == 0, rc
+            moved += len(sel) * 3 * wl.ffn * wl.hidden * 2
+    dt = time.perf_counter() - t0
+    moe_gpu = gpu_out.astype(np.float64) - acts.astype(np.float32).astype(np.float64)
+    moe_cpu = out.astype(np.float64) - acts.astype(np.float32).astype(np.float64)
+    rel = float(np.abs(moe_cpu - moe_gpu).max() / max(np.abs(moe_gpu).max(), 1e-30))
+    return {"value": n_tok / dt, "unit": "tok/s", "cores": threads, "kind": "port",
+            "label": "not reference: builder-written CPU SwiGLU (baseline/cpu_ffn.c, OpenMP, fp32 accumulation); "
+                     "the reference's CPU path does no FFN arithmetic (inc/simulator.hpp:446-462)",
+            "sample": f"{n_tok} tokens x {wl.layers} layers of the e2e window, selected experts read in place from the "
+                      f"pinned host store ({moved / 1e9:.1f} GB)",
+            "host_read_gbs": moved / dt / 1e9, "max_rel_diff_vs_gpu": rel}
+
+
 def reference_arm(args):
     ws, rank, _ = dist_init()
     if rank != 0:
@@ -269,24 +369,43 @@ def ours(args):
     pipe_ms["generate_profiles"], tp = (time.perf_counter() - tp) * 1e3, time.perf_counter()
     caps, exp_loads = P.dp_allocate(spec, P.build_cost_table(spec, alpha, beta), wl.budget)
     pipe_ms["cost_table_and_dp_allocate"] = (time.perf_counter() - tp) * 1e3
-    # host RAM: all L*N experts pinned unless the node cannot hold them per replica
     expert_bytes = 3 * wl.ffn * wl.hidden * 2
+    W, K, B = args.warmup, args.steps, args.batch
+    p2p = ep_world > 1 and args.ep_exchange == "p2p"
+    owners = None
+    if ep_world > 1:
+        # expert placement: balanced by a separate calibration trace of the same model (not the decoded
+        # tokens; ep.balanced_owners) or e % G — the same deterministic table on every rank
+        if args.ep_owner == "balanced":
+            calib = eng.generate_trace(P.SynthConfig(spec, max(wl.tokens, 256), wl.concentration, wl.drift, wl.gate_seed,
+                                                     wl.token_seed + 7777, False, wl.fisher_scales, wl.drift_scales))
+            eng.load_gates(trace.gates)
+            sim = eng.simulate_trace(calib.acts, calib.scores, calib.fisher, caps, tau, cfg, wl.seed)
+            owners = EP.balanced_owners(sim.timeline, wl.layers, wl.experts, ep_world)
+            del calib
+        else:
+            owners = np.array([[e % ep_world for e in range(wl.experts)] for _ in range(wl.layers)], dtype=np.int32)
+    # host RAM: every expert this rank holds is pinned (an EP shard pins only its own);
+    # only a host that cannot hold them aliases blocks (single-GPU 8x22B on a small host)
+    held = int((owners == ep_rank).sum()) if owners is not None else wl.layers * wl.experts
     alias = 0
     try:
         avail = int(open("/proc/meminfo").read().split("MemAvailable:")[1].split()[0]) * 1024
-        share = 0.85 if ws == 1 else 0.6  # leave host headroom when several ranks pin memory
-        per_rank = int(share * avail / max(1, int(os.environ.get("LOCAL_WORLD_SIZE", ws))))
-        if per_rank < wl.layers * wl.experts * expert_bytes:
+        per_rank = int(0.85 * avail / max(1, int(os.environ.get("LOCAL_WORLD_SIZE", ws))))
+        if per_rank < held * expert_bytes:
             alias = max(1, per_rank // expert_bytes)
     except Exception:  # noqa: BLE001
         pass
     if args.host_alias is not None:
         alias = args.host_alias
+    elif alias and ep_world > 1:
+        raise SystemExit(f"rank {rank}: the expert-parallel shard needs {held * expert_bytes / 1e9:.0f} GB of pinned "
+                         f"host memory, {per_rank / 1e9:.0f} GB available per rank (pass --host-alias to alias blocks)")
     link_peak = h2d_peak_gbs(local)
     t0 = time.time()
-    eng.experts_init(wl.ffn, wl.tiles, seed=1234, host_alias=alias)
+    eng.experts_init(wl.ffn, wl.tiles, seed=1234, host_alias=alias, expert_owner=owners, rank=ep_rank)
     t_store = time.time() - t0
-    W, K, B = args.warmup, args.steps, args.batch
+    store_info = eng.experts_info()
     # B token streams (config 4): stream b = the reference generator with token_seed + b (same gates)
     acts, scores = trace.acts, trace.scores
     total_tokens = wl.tokens
@@ -301,17 +420,6 @@ def ours(args):
         del streams
     else:
         acts, scores = acts[:, None], scores[:, None]
-    p2p = ep_world > 1 and args.ep_exchange == "p2p"
-    owners = None
-    if ep_world > 1 and args.ep_owner == "balanced":
-        # placement from a separate calibration trace of the same model (not the decoded tokens):
-        # the same deterministic table on every rank
-        calib = eng.generate_trace(P.SynthConfig(spec, max(wl.tokens, 256), wl.concentration, wl.drift, wl.gate_seed,
-                                                 wl.token_seed + 7777, False, wl.fisher_scales, wl.drift_scales))
-        eng.load_gates(trace.gates)
-        sim = eng.simulate_trace(calib.acts, calib.scores, calib.fisher, caps, tau, cfg, wl.seed)
-        owners = EP.balanced_owners(sim.timeline, wl.layers, wl.experts, ep_world)
-        del calib
 
     def begin(capacities):
         eng.decode_begin(capacities, trace.fisher, tau, cfg, wl.seed, total_tokens, args.staging, batch=B,
@@ -383,7 +491,7 @@ def ours(args):
     st_end = res.stats
     resident = None
     hbm_total = torch.cuda.get_device_properties(local).total_memory
-    resident_bytes = (wl.layers * len(EP.owned_experts(wl.experts, ep_world, ep_rank)) + 32) * expert_bytes
+    resident_bytes = (held + 32) * expert_bytes
     if not args.no_resident_check and resident_bytes > 0.85 * hbm_total:
         resident = {"skipped": f"all {wl.layers * wl.experts} experts need {resident_bytes / 1e9:.0f} GB of HBM per GPU"}
     elif not args.no_resident_check:
@@ -417,10 +525,15 @@ def ours(args):
 
     d = {k: s1[k] - s0[k] for k in s0 if isinstance(s0[k], (int, float))}
     per_rank_copy = [int(d["copy_bytes"])]
-    if ws > 1:  # every shard's host-link bytes (EP: the busiest shard bounds the step)
+    per_rank_store = [{"pinned_gb": round(store_info["pinned_bytes"] / 1e9, 2), "experts": held,
+                       "numa_node": store_info["numa_node"]}]
+    if ws > 1:  # every shard's host-link bytes (EP: the busiest shard bounds the step) and pinned store
         import torch.distributed as dist
         per_rank_copy = [None] * ws
         dist.all_gather_object(per_rank_copy, int(d["copy_bytes"]))
+        gathered = [None] * ws
+        dist.all_gather_object(gathered, per_rank_store[0])
+        per_rank_store = gathered
     ffn_ms = d["ffn_ms"]
     ffn_bytes = d["ffn_gate_up_bytes"] + d["ffn_down_bytes"]
     peaks = measured_peaks()
@@ -460,6 +573,7 @@ def ours(args):
                    "budget": wl.budget, "tiles": wl.tiles, "lookahead": wl.lookahead, "trace_tokens": wl.tokens,
                    "tau": tau, "realized_single_ratio": realized, "capacities": [int(c) for c in caps],
                    "dp_expected_loads_per_token": exp_loads, "host_alias": alias,
+                   "expert_store_per_rank": per_rank_store,
                    "parallelism": (f"ep{ws} ({'experts placed by a calibration trace (ep.balanced_owners)' if owners is not None else f'expert e on rank e % {ws}'}; combine: "
                                    f"{'P2P stores into peer memory from the combine epilogue' if p2p else 'all_gather'})"
                                    if ep_world > 1 else f"replicas x{ws}"),
@@ -509,6 +623,8 @@ def ours(args):
                 "h2d_bytes_per_step": int(B * wl.layers * (wl.hidden + wl.experts) * 8),
                 "d2h_bytes_per_step": int(B * wl.layers * wl.hidden * 4)},
         "setup_s": {"total": setup_s, "expert_store": t_store},
+        "host": host_info(),
+        "comm": COMM,
         "slots": {"total": st_end["slots_total"], "staging_high_water": st_end["staging_high_water"]},
     }
     if resident is not None:
@@ -533,13 +649,20 @@ def ours(args):
             rr = run_reference_driver(wl, n_sim, 5)
             if rr is not None:
                 sim_line["reference_tok_s"] = rr["tokens"] / rr["simulate_best_s"]
-                sim_line["metrics_equal_reference"] = rr.get("metrics") == sim.metrics and \
-                    rr.get("timeline_events") == len(sim.timeline)
+                sim_line["metrics_equal_reference"] = all(rr["metrics"][k] == v for k, v in sim.metrics.items()) and \
+                    rr["metrics"]["on_demand_loads_per_layer"] == [int(v) for v in sim.on_demand_loads_per_layer] and \
+                    rr.get("hash_timeline") == fnv1a_i64(sim.timeline)
         line["simulate_trace"] = sim_line
         line["comparison_note"] = ("value / e2e: the physical decode (experts moved over the host link and computed); "
                                    "the reference arm times the reference's tick-model simulate_trace, which moves no "
                                    "weights -- the like-for-like figure is simulate_trace.tok_s vs "
                                    "simulate_trace.reference_tok_s")
+    if not args.no_cpu_baseline and ws == 1 and B == 1 and not args.free_running:
+        try:
+            n_cpu = min(K, 3)
+            line["cpu_baseline_ffn"] = cpu_ffn_baseline(eng, wl, trace, tau, cfg, W + K, n_cpu, h_hidden[:n_cpu, 0].numpy())
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline_ffn"] = {"value": None, "unavailable": str(e)[:200]}
     if not args.no_cpu_baseline:
         try:
             r = run_reference_driver(wl, decoded, 20)
@@ -565,11 +688,21 @@ def ours(args):
                                                   "tokens, best of 20 (tick model: no FFN arithmetic, no weight "
                                                   "movement)"}
                 if B == 1:
-                    line["parity"] = {"reference_on_demand_loads": r["on_demand_loads"],
-                                      "ours_on_demand_loads": res.metrics["on_demand_loads"],
-                                      # rank 0 decodes the reference's own stream (token_seed + 0) in
-                                      # every mode, so its logical trace must match the reference's
-                                      "equal": r["on_demand_loads"] == res.metrics["on_demand_loads"]}
+                    # rank 0 decodes the reference's own stream (token_seed + 0) in every mode, so its
+                    # logical trace must equal the reference's: the whole SimMetrics struct
+                    # (inc/simulator.hpp:130-166) and the event timeline, hashed like the reference's
+                    rm = r["metrics"]
+                    ours_m = dict(res.metrics)
+                    ours_m["on_demand_loads_per_layer"] = [int(v) for v in res.on_demand_loads_per_layer]
+                    ours_m["latency_per_token"] = [int(v) for v in res.latency_per_token[:decoded]]
+                    diff = sorted(k for k in rm if rm[k] != ours_m.get(k))
+                    ours_hash = fnv1a_i64(res.timeline)
+                    line["parity"] = {"tokens": decoded, "metrics_fields": len(rm), "metrics_differ": diff,
+                                      "on_demand_loads": [r["on_demand_loads"], res.metrics["on_demand_loads"]],
+                                      "timeline_events": [r["timeline_events"], int(len(res.timeline))],
+                                      "hash_timeline": [r["hash_timeline"], ours_hash],
+                                      "equal": not diff and r["hash_timeline"] == ours_hash
+                                      and r["timeline_events"] == len(res.timeline)}
                 else:
                     line["cpu_baseline"]["sample"] += ("; the reference is batch-1: it decodes stream 0 only, its "
                                                        "tok/s is per single stream")
@@ -666,7 +799,7 @@ def pipeline_bench(args):
             line["equal"] = {"tau": r["tau"] == tau, "alpha": r["alpha"] == [float(v) for v in alpha],
                              "beta": r["beta"] == [float(v) for v in beta],
                              "capacities": r["capacities"] == [int(v) for v in caps],
-                             "simulate_metrics": r["metrics"] == sim.metrics,
+                             "simulate_metrics": all(r["metrics"][k] == v for k, v in sim.metrics.items()),
                              "compare_rows": [(x["metrics"], x["capacities"], x["speedup_vs_baseline"]) for x in rows]
                              == [({k: v for k, v in y["metrics"].items()}, y["capacities"], y["speedup_vs_baseline"])
                                  for y in c["rows"]]}
@@ -683,6 +816,7 @@ def pipeline_bench(args):
 
 def main():
     args = parse()
+    spawn_ranks(args)
     if args.impl == "reference":
         reference_arm(args)
     elif args.pipeline:

@@ -308,6 +308,12 @@ int moe_expert_bytes(moe_engine_t engine, int64_t* bytes);
 /* Copy one expert's tile-major bf16 weights out of the pinned store (for parity tests). */
 int moe_expert_read(moe_engine_t engine, int32_t layer, int32_t expert, uint16_t* out);
 
+/* Read-only address of one expert's tile-major block inside the pinned store (host memory, valid
+ * until the store is replaced or the engine destroyed): zero-copy access for host-side consumers,
+ * e.g. a CPU expert path next to the GPU one.  MOE_E_USAGE when this (shard's) store does not
+ * hold the expert. */
+int moe_expert_host_ptr(moe_engine_t engine, int32_t layer, int32_t expert, const void** ptr);
+
 /* Begin a decode session: per-layer HBM slot pool sized by `capacities` (the DP allocation) plus
  * `staging_slots` transfer slots, LRU initial fill from SeededRng(seed) (inc/simulator.hpp:352-360),
  * fisher [L], tau, config.  total_tokens is the trace length (the last-layer first-gate

@@ -205,6 +205,7 @@ int main(int argc, char** argv) {
         double best = 1e30, total = 0;
         SimMetrics m{};
         size_t events = 0;
+        std::uint64_t h_tl = 0;
         for (int r = 0; r < reps; ++r) {
             auto a = clk::now();
             SimResult res = simulate_trace(sub, sim, sim_seed);
@@ -213,20 +214,37 @@ int main(int argc, char** argv) {
             total += secs(a, b);
             m = res.metrics;
             events = res.timeline.events.size();
+            if (r == 0) {  // FNV-1a of the timeline as int64 [events][8] (the layout of moe_decode_end)
+                std::vector<long long> ev;
+                ev.reserve(events * 8);
+                for (const auto& e : res.timeline.events) {
+                    ev.push_back(e.stream == Stream::Compute ? 0 : 1);
+                    ev.push_back(static_cast<int>(e.kind));
+                    ev.push_back(e.start);
+                    ev.push_back(e.end);
+                    ev.push_back(e.token);
+                    ev.push_back(e.layer);
+                    ev.push_back(e.expert);
+                    ev.push_back(e.tile);
+                }
+                h_tl = fnv1a_bytes(ev.data(), ev.size() * sizeof(long long));
+            }
         }
         std::printf(
             "{\"tokens\": %zu, \"reps\": %d, \"simulate_best_s\": %.9f, \"simulate_mean_s\": %.9f, "
             "\"generate_s\": %.6f, \"calibrate_s\": %.6f, \"train_s\": %.6f, \"profile_s\": %.6f, "
             "\"allocate_s\": %.6f, \"on_demand_loads\": %lld, \"metrics\": {\"total_latency\": %lld, "
             "\"stall_time\": %lld, \"on_demand_loads\": %lld, \"cache_hits\": %lld, \"prefetch_hits\": %lld, "
-            "\"single_expert_decisions\": %lld, \"experts_activated_total\": %lld}, \"timeline_events\": %zu, "
+            "\"single_expert_decisions\": %lld, \"experts_activated_total\": %lld, \"on_demand_loads_per_layer\": %s, "
+            "\"latency_per_token\": %s}, \"timeline_events\": %zu, \"hash_timeline\": \"%016" PRIx64 "\", "
             "\"tau\": %s, \"alpha\": %s, \"beta\": %s, \"capacities\": %s, \"total_cost\": %s}\n",
             sub.traces.size(), reps, best, total / reps, secs(t0, t1), secs(t1, t2), secs(t2, t3), secs(t3, t4),
             secs(t4, t5), static_cast<long long>(m.on_demand_loads), static_cast<long long>(m.total_latency),
             static_cast<long long>(m.stall_time), static_cast<long long>(m.on_demand_loads),
             static_cast<long long>(m.cache_hits), static_cast<long long>(m.prefetch_hits),
             static_cast<long long>(m.single_expert_decisions), static_cast<long long>(m.experts_activated_total),
-            events, Out::d(tau.tau).c_str(), Out::arr(alphas).c_str(), Out::arr(betas).c_str(),
+            Out::arr(m.on_demand_loads_per_layer).c_str(), Out::arr(m.latency_per_token).c_str(), events, h_tl,
+            Out::d(tau.tau).c_str(), Out::arr(alphas).c_str(), Out::arr(betas).c_str(),
             Out::arr(alloc.allocation.capacities).c_str(), Out::d(alloc.total_cost).c_str());
         return 0;
     }

@@ -514,6 +514,17 @@ int moe_experts_info(moe_engine_t h, int64_t* pinned_bytes, int32_t* stored_expe
     });
 }
 
+int moe_expert_host_ptr(moe_engine_t h, int32_t layer, int32_t expert, const void** ptr) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(ptr, "ptr");
+        if (!e.experts) fail(Status::Usage, "experts not initialised");
+        if (layer < 0 || layer >= e.experts->layers || expert < 0 || expert >= e.experts->experts)
+            fail(Status::Usage, "ExpertRef out of range");
+        *ptr = e.experts->expert(layer, expert);
+    });
+}
+
 int moe_expert_set(moe_engine_t h, int32_t layer, int32_t expert, const uint16_t* w1, const uint16_t* w3,
                    const uint16_t* w2) {
     return guarded([&] {

@@ -655,11 +655,8 @@ void ffn_partial_range(FfnPartialRef& f, int ft) {
 }
 
 FfnKernel ffn_kernel_variant() {
-    static const FfnKernel v = [] {
-        const char* e = std::getenv("ADAPMOE_K2");  // A/B knob: "rows" = the LDG row-owner kernel
-        return (e && std::strcmp(e, "rows") == 0) ? FfnKernel::Rows : FfnKernel::Ring;
-    }();
-    return v;
+    const char* e = std::getenv("ADAPMOE_K2");  // A/B knob (read per launch): "rows" = the LDG kernel
+    return (e && std::strcmp(e, "rows") == 0) ? FfnKernel::Rows : FfnKernel::Ring;
 }
 
 int ffn_grid(const FfnLaunch& p, int sm_count) {

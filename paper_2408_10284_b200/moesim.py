@@ -379,6 +379,12 @@ class Engine:
         check(load().moe_expert_bytes(self._h, C.byref(b)))
         return b.value
 
+    def expert_host_ptr(self, layer: int, expert: int) -> int:
+        """Address of the expert's tile-major block in the pinned host store (moe_expert_host_ptr)."""
+        p = C.c_void_p()
+        check(load().moe_expert_host_ptr(self._h, layer, expert, C.byref(p)))
+        return int(p.value)
+
     def expert_read(self, layer: int, expert: int) -> np.ndarray:
         out = np.zeros(self.expert_bytes() // 2, dtype=np.uint16)
         check(load().moe_expert_read(self._h, layer, expert, _p(out, _capi._u16)))

@@ -26,11 +26,19 @@ def _rel_err(got, ref):
 
 
 def test_expert_store_matches_oracle_init():
+    import ctypes
     spec = P.ModelSpec(2, 4, 2, 256)
     with P.Engine(spec) as eng:
         eng.experts_init(896, 4, seed=11)
+        n = 3 * 896 * 256
         for l, e in [(0, 0), (1, 3), (0, 2)]:
-            assert np.array_equal(eng.expert_read(l, e), O.expert_init(11, l, e, 256, 896, 4))
+            ref = O.expert_init(11, l, e, 256, 896, 4)
+            assert np.array_equal(eng.expert_read(l, e), ref)
+            # zero-copy view of the pinned block (moe_expert_host_ptr)
+            view = np.ctypeslib.as_array((ctypes.c_uint16 * n).from_address(eng.expert_host_ptr(l, e)))
+            assert np.array_equal(view, ref)
+        with pytest.raises(P.MoeError):
+            eng.expert_host_ptr(2, 0)
 
 
 @pytest.mark.parametrize("d,f,tiles", [(256, 896, 4), (512, 1024, 2), (256, 2048, 1), (4096, 14336, 4)])

@@ -5,6 +5,7 @@
 //   nvcc -std=c++20 -O3 -gencode arch=compute_100a,code=sm_100a -o tools/bin/k2_ring_bench tools/k2_ring_bench.cu
 //   tools/bin/k2_ring_bench [d] [ft]        (default 4096 3584: one 8x7B tile of 88 MB)
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -114,6 +115,42 @@ static int probe(int D, int Ft, uint16_t* w, int NT, double* x, float* part) {
                            nseg * tile_elems * 2 / (us * 1e-6) / 1e9);
                 }
             }
+        }
+    }
+    // idle gaps before each launch (GPU idle, host sleeping): does a sparse launch pattern (the
+    // link-bound decode computes ~10 % of the time) slow the kernel down?
+    for (int gap_us : {0, 200, 1000, 5000, 10000}) {
+        for (bool h2d : {false, true}) {
+            static void* hsrc = nullptr;
+            static void* ddst = nullptr;
+            static cudaStream_t cs;
+            if (!hsrc) {
+                cudaMallocHost(&hsrc, 256 << 20);
+                cudaMalloc(&ddst, 256 << 20);
+                cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+            }
+            double sum = 0;
+            int n = 0;
+            cudaEvent_t a, b;
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            for (int r = 0; r < 16; ++r) {
+                if (h2d) cudaMemcpyAsync(ddst, hsrc, 256 << 20, cudaMemcpyHostToDevice, cs);  // ~4.6 ms of link traffic
+                if (gap_us) {
+                    auto t0 = std::chrono::steady_clock::now();
+                    while (std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(gap_us)) {}
+                }
+                FfnLaunch p = mk(8, r, false);
+                cudaEventRecord(a);
+                launch_variant(0, p, 148, 0);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms;
+                cudaEventElapsedTime(&ms, a, b);
+                if (r >= 3) { sum += ms; ++n; }
+                cudaStreamSynchronize(cs);
+            }
+            printf("ring nseg=8 after %5d us idle%s: %6.1f us\n", gap_us, h2d ? " (+ concurrent 256 MB H2D)" : "", sum / n * 1e3);
         }
     }
     // per-CTA timeline of one cold ring launch (globaltimer, ns)

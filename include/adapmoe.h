@@ -380,6 +380,37 @@ int moe_decode_ep_connect(moe_engine_t engine, const uint64_t* peer_ptrs, const 
 int moe_decode_tokens(moe_engine_t engine, const double* acts, const double* scores, int32_t count,
                       int32_t inputs_on_device, float* hidden_out, double* gpu_ms);
 
+/* One MoE layer of the current token on caller DEVICE buffers, stream-ordered with the caller's
+ * stream (the per-layer, stream-level entry an inference engine calls between its own
+ * attention layers; the reference's per-layer body is inc/simulator.hpp:380-462).  The session's
+ * logical engine steps (token, layer) exactly as moe_decode_tokens does, so the event trace is the
+ * same; layers must be called in order 0..L-1 per token (MOE_E_USAGE otherwise), and a token must
+ * not be split between moe_decode_layer and moe_decode_tokens.
+ *  x      : device fp64 [B][d], this layer's router and expert input (B = the session's batch);
+ *  scores : device fp64 [B][N] stored post-softmax scores to decide from (the reference's
+ *           actual-selection rule, inc/simulator.hpp:390-396), or NULL to decide from the layer's
+ *           gate on x (softmax of logits / dirichlet_concentration, as free-running does);
+ *  out    : device fp32 [B][d] = (add_input ? x : 0) + sum_e w_e * E_e(x);
+ *  stream : a cudaStream_t (NULL = the engine's compute stream).  The layer's work waits for
+ *           everything enqueued on `stream` before the call, and `stream` waits for the layer's
+ *           output.  The call returns once the layer is enqueued; the host blocks only on the
+ *           layer's router result (the policy step needs the decision).
+ * Needs a session without free_running / expert parallelism. */
+int moe_decode_layer(moe_engine_t engine, int32_t layer, const double* x, const double* scores, float* out,
+                     int32_t add_input, void* stream);
+
+/* Physical timeline of the session (SURVEY §5 tracing): enable = 1 starts recording CUDA-event
+ * timestamps of every expert tile copy (request class on_demand / prefetch, promotion, the expert
+ * its insert evicted), every FFN launch (one record per (expert, tile) segment with the copy job
+ * that filled its slot), compute-stream waits on tile copies and router launches, relative to an
+ * origin event recorded now; 0 stops.  moe_decode_timeline_write drains the copy engine,
+ * synchronises, and writes everything recorded so far as JSONL sorted by start time, in the
+ * reference's schema (inc/io.hpp:402-417: stream, kind, start, end, expert, token, layer, tile;
+ * times in microseconds) plus physical fields (request, promoted, evicts, job for transfers;
+ * launch, fill for computes).  n_events (may be NULL) receives the line count. */
+int moe_decode_record_timeline(moe_engine_t engine, int32_t enable);
+int moe_decode_timeline_write(moe_engine_t engine, const char* path, int64_t* n_events);
+
 /* Physical counters of the session so far (CUDA-event timed on the engine's streams). */
 typedef struct {
     int64_t tokens;

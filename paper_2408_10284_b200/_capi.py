@@ -146,6 +146,9 @@ SIGNATURES = {
                                  C.POINTER(DecodeStatsC)]),
     "moe_expert_ffn": (C.c_int, [_eng, C.c_int32, C.c_int32, _d, _f]),
     "moe_decode_stats_snapshot": (C.c_int, [_eng, C.POINTER(DecodeStatsC)]),
+    "moe_decode_layer": (C.c_int, [_eng, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "moe_decode_record_timeline": (C.c_int, [_eng, C.c_int32]),
+    "moe_decode_timeline_write": (C.c_int, [_eng, C.c_char_p, C.POINTER(C.c_int64)]),
 }
 
 

@@ -629,6 +629,35 @@ int moe_decode_end(moe_engine_t h, moe_metrics* metrics, int64_t* lat, int64_t* 
     });
 }
 
+int moe_decode_layer(moe_engine_t h, int32_t layer, const double* x, const double* scores, float* out,
+                     int32_t add_input, void* stream) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        if (!e.session) fail(Status::Usage, "decode_layer: no session (moe_decode_begin)");
+        if (layer < 0 || layer >= e.spec().num_layers) fail(Status::Usage, "decode_layer: layer out of range");
+        e.session->decode_layer(layer, x, scores, out, add_input != 0,
+                                stream ? static_cast<cudaStream_t>(stream) : e.compute_stream());
+    });
+}
+
+int moe_decode_record_timeline(moe_engine_t h, int32_t enable) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        if (!e.session) fail(Status::Usage, "record_timeline: no session");
+        e.session->record_timeline(enable != 0);
+    });
+}
+
+int moe_decode_timeline_write(moe_engine_t h, const char* path, int64_t* n_events) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(path, "path");
+        if (!e.session) fail(Status::Usage, "timeline_write: no session");
+        const long long n = e.session->write_timeline(path);
+        if (n_events) *n_events = n;
+    });
+}
+
 int moe_decode_stats_snapshot(moe_engine_t h, moe_decode_stats* stats) {
     return guarded([&] {
         Engine& e = eng(h);

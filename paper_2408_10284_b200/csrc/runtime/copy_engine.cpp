@@ -181,6 +181,7 @@ void CopyEngine::retire(const std::shared_ptr<CopyJob>& job) {
                     if (job->consumed) busy_pf_used_ms_ += ms;
                 }
             }
+            if (t >= job->recorded_tiles) record_tile(*job, t);
         }
     }
     for (cudaEvent_t e : job->done) free_sync_.push_back(e);
@@ -191,6 +192,23 @@ void CopyEngine::retire(const std::shared_ptr<CopyJob>& job) {
     job->t_end.clear();
     auto it = std::find(active_.begin(), active_.end(), job);
     if (it != active_.end()) active_.erase(it);
+}
+
+void CopyEngine::record_tile(CopyJob& job, int t) {  // caller holds mu_; the tile has landed
+    float a = 0.0f, b = 0.0f;
+    if (records_ && origin_ && cudaEventElapsedTime(&a, origin_, job.t_start[t]) == cudaSuccess &&
+        cudaEventElapsedTime(&b, origin_, job.t_end[t]) == cudaSuccess) {
+        records_->push_back(TileCopyRecord{job.serial, job.token, job.layer, job.expert, t, job.evicts,
+                                           job.requested_on_demand, job.promoted, a, b});
+        job.recorded_tiles = t + 1;
+    }
+}
+
+void CopyEngine::collect_landed() {
+    std::lock_guard<std::mutex> g(mu_);
+    for (const auto& job : active_)
+        for (int t = job->recorded_tiles; t < job->issued_tiles; ++t)
+            if (cudaEventQuery(job->t_end[t]) == cudaSuccess) record_tile(*job, t);
 }
 
 // The copy thread never throws: a CUDA error (or any exception) is recorded, every waiter is woken

@@ -37,6 +37,20 @@ struct CopyJob {
     std::vector<cudaEvent_t> done;     // per tile, sync events
     std::vector<cudaEvent_t> t_start;  // per tile, timing
     std::vector<cudaEvent_t> t_end;
+    // physical timeline tags (set by the decode session): job serial, the request's expert and the
+    // token at which it was made, promotion to on-demand, the expert its insert evicted (-1 none)
+    long long serial = -1;
+    int token = -1, layer = -1, expert = -1, evicts = -1;
+    bool requested_on_demand = false, promoted = false;
+    int recorded_tiles = 0;  // tiles already appended to the timeline records
+};
+
+// One landed tile copy, for the physical timeline (times in ms from the recorder's origin event).
+struct TileCopyRecord {
+    long long serial;
+    int token, layer, expert, tile, evicts;
+    bool on_demand, promoted;
+    double start_ms, end_ms;
 };
 
 class CopyEngine {
@@ -70,10 +84,20 @@ public:
     double busy_ms_total(double* prefetch_ms = nullptr, long long* prefetch_tiles = nullptr,
                          double* prefetch_used_ms = nullptr);
     void retire(const std::shared_ptr<CopyJob>& job);  // accumulate timing + recycle events
+    // Physical timeline: from now on every retired tile is appended to `out` with its copy interval
+    // relative to `origin` (a timed event recorded on the device); nullptr stops recording.
+    // Append the landed, not yet recorded tiles of jobs that have not retired (they still hold slots).
+    void collect_landed();
+    void record_tiles(cudaEvent_t origin, std::vector<TileCopyRecord>* out) {
+        std::lock_guard<std::mutex> g(mu_);
+        origin_ = origin;
+        records_ = out;
+    }
 
 private:
     void loop();
     void run();
+    void record_tile(CopyJob& job, int t);
     void fail_thread(const std::string& what);
     void throw_if_failed() const;  // caller holds mu_
     cudaEvent_t take_event(bool timing);
@@ -92,6 +116,8 @@ private:
     std::atomic<long long> tiles_copied_{0}, bytes_copied_{0};
     double busy_ms_ = 0.0, busy_pf_ms_ = 0.0, busy_pf_used_ms_ = 0.0;
     long long pf_tiles_ = 0;
+    cudaEvent_t origin_ = nullptr;
+    std::vector<TileCopyRecord>* records_ = nullptr;
     std::thread thread_;
 };
 

@@ -139,6 +139,8 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
     h_route_host_.reserve(static_cast<size_t>(route_host_cap_) * (2 + N) * sizeof(double));
     d_route_counter_.reserve(sizeof(unsigned));
     MOE_CUDA(cudaEventCreateWithFlags(&route_done_, cudaEventDisableTiming));
+    MOE_CUDA(cudaEventCreateWithFlags(&user_in_, cudaEventDisableTiming));
+    MOE_CUDA(cudaEventCreateWithFlags(&user_out_, cudaEventDisableTiming));
     // per-call buffers sized for the whole announced trace now: growing them inside decode() would put
     // cudaFree / cudaMallocHost (implicit device synchronisation) inside the timed window
     {
@@ -151,8 +153,9 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
         if (free_running_) {
             d_x_free_.reserve(TL * D * sizeof(double));
             d_x_norm_.reserve(TL * D * sizeof(double));
-            d_free_scores_.reserve(static_cast<size_t>(4) * batch_ * N * sizeof(double));
         }
+        // gate-decided layers (free-running, moe_decode_layer without scores) emit their scores here
+        d_free_scores_.reserve(static_cast<size_t>(4) * batch_ * N * sizeof(double));
     }
     copier_ = std::make_unique<CopyEngine>(eng.copy_stream(), eng.device());
     // last: the constructor performs the initial fill through on_insert
@@ -165,6 +168,9 @@ DecodeSession::~DecodeSession() {
     for (void* p : ep_ipc_opened_) cudaIpcCloseMemHandle(p);
     if (h_route_) cudaFreeHost(h_route_);
     if (route_done_) cudaEventDestroy(route_done_);
+    if (origin_) cudaEventDestroy(origin_);
+    if (user_in_) cudaEventDestroy(user_in_);
+    if (user_out_) cudaEventDestroy(user_out_);
     if (in_ready_) cudaEventDestroy(in_ready_);
     if (route_stream_) {
         cudaStreamSynchronize(route_stream_);
@@ -324,6 +330,11 @@ void DecodeSession::on_request(int id, ExpertRef ref, bool on_demand) {
     const int s = take_slot();
     req_slot_[id] = s;
     auto job = copier_->make_job(slot_ptr(s), store_.expert(ref.layer, ref.expert), store_.tile_bytes, store_.tiles);
+    job->serial = job_serial_++;
+    job->token = cur_token_;
+    job->layer = ref.layer;
+    job->expert = ref.expert;
+    job->requested_on_demand = on_demand;
     slots_[s].fill = job;
     slots_[s].fill_done = false;
     req_job_[id] = job;
@@ -332,6 +343,7 @@ void DecodeSession::on_request(int id, ExpertRef ref, bool on_demand) {
 
 void DecodeSession::on_promote(int id) {
     if (!req_job_[id]) return;
+    req_job_[id]->promoted = true;
     req_job_[id]->logical_prefetch = false;  // counted on-demand at decision time (inc/simulator.hpp:410-418)
     copier_->promote(req_job_[id], false);
 }
@@ -360,6 +372,7 @@ void DecodeSession::on_insert(ExpertRef ref, int request, std::optional<int> evi
             slot_of_[key] = s;
         }
         if (evicted) {
+            if (request >= 0 && req_job_[request]) req_job_[request]->evicts = *evicted;
             const int vkey = ref.layer * N + *evicted;
             if (slot_of_[vkey] >= 0) release_slot(slot_of_[vkey]);  // the victim is ours
             slot_of_[vkey] = -1;
@@ -396,6 +409,7 @@ void DecodeSession::wait_fill(int slot, int tile) {
         MOE_CUDA(cudaEventRecord(b, cs));
         stall_events_.emplace_back(a, b);
         stall_is_prefetch_.push_back(prefetch);
+        if (record_) stall_tags_.push_back(StallTag{cur_token_, sl.fill->layer, sl.fill->expert, t, sl.fill->serial});
     }
     if (tile < 0 || tile == sl.fill->tiles - 1) sl.fill_done = true;
 }
@@ -446,7 +460,9 @@ void DecodeSession::timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int
     MOE_CUDA(cudaEventRecord(e1, cs));
     const double gate_up = static_cast<double>(p.n_seg) * 2.0 * p.ft * p.d * 2.0;
     const double down = static_cast<double>(p.n_seg) * p.ft * p.d * 2.0;
-    pass_events_.push_back(PassRec{gate_up, down, e0, e1});
+    pass_events_.push_back(PassRec{gate_up, down, e0, e1, cur_token_, cur_layer_, launch_serial_++, {}});
+    pass_events_.back().segs.swap(seg_info_);
+    seg_info_.clear();
     stats_.kernels += 1;
     p.n_seg = 0;
 }
@@ -546,6 +562,7 @@ void DecodeSession::launch_speculative(int layer, const double* x) {
             p.seg[p.n_seg].gate_up = reinterpret_cast<const std::uint16_t*>(tile);
             p.seg[p.n_seg].down_t = reinterpret_cast<const std::uint16_t*>(tile + gate_up_bytes);
             ++p.n_seg;
+            note_seg(slot, spec_next_[k], t, true);
         }
         run.slot[run.n++] = slot;
     }
@@ -558,7 +575,10 @@ void DecodeSession::launch_speculative(int layer, const double* x) {
     MOE_CUDA(launch_ffn(p, sms, cs));
     MOE_CUDA(cudaEventRecord(e1, cs));
     pass_events_.push_back(PassRec{static_cast<double>(p.n_seg) * 2.0 * Ft * D * 2.0,
-                                   static_cast<double>(p.n_seg) * Ft * D * 2.0, e0, e1});
+                                   static_cast<double>(p.n_seg) * Ft * D * 2.0, e0, e1, cur_token_, layer,
+                                   launch_serial_++, {}});
+    pass_events_.back().segs.swap(seg_info_);
+    seg_info_.clear();
     stats_.kernels += 1;
     stats_.spec_launches += 1;
     run.valid = true;
@@ -613,6 +633,7 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
             }
             p.seg[p.n_seg++] = seg(u.slot, t);
             meta.emplace_back(u.rank, t);
+            note_seg(u.slot, d.experts[u.rank], t, true);
         }
         stats_.ffn_bytes += static_cast<long long>(store_.expert_bytes);
     }
@@ -639,6 +660,7 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
             wait_fill(u.slot, t);
             p.seg[p.n_seg++] = seg(u.slot, t);
             meta.emplace_back(u.rank, t);
+            note_seg(u.slot, d.experts[u.rank], t, false);
         }
         if (!one_launch || gi + 1 == groups.size()) {
             timed_ffn(p, meta, refs);
@@ -657,7 +679,7 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
     c.ranks = d.count;
     c.d = D;
     c.ft = Ft;
-    c.residual = ep_rank_ == 0 ? 1 : 0;
+    c.residual = cur_residual_;
     c.n_refs = static_cast<int>(refs.size());
     for (size_t i = 0; i < refs.size(); ++i) c.refs[i] = std::get<2>(refs[i]);
     for (int r = 0; r < d.count; ++r) c.experts[r] = d.experts[r];
@@ -675,7 +697,7 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
     stats_.kernels += 1;
 }
 
-void DecodeSession::timed_grouped(GroupedLaunch& p, bool down) {
+void DecodeSession::timed_grouped(GroupedLaunch& p, bool down, const RouteDecision& u) {
     cudaStream_t cs = eng_.compute_stream();
     cudaEvent_t e0 = take_timing(), e1 = take_timing();
     MOE_CUDA(cudaEventRecord(e0, cs));
@@ -684,7 +706,21 @@ void DecodeSession::timed_grouped(GroupedLaunch& p, bool down) {
     double tiles = 0;
     for (int s = 0; s < p.n_seg; ++s) tiles += p.seg[s].t1 - p.seg[s].t0;
     const double bytes = tiles * (down ? 1.0 : 2.0) * p.ft * p.d * 2.0;
-    pass_events_.push_back(PassRec{down ? 0.0 : bytes, down ? bytes : 0.0, e0, e1});
+    pass_events_.push_back(PassRec{down ? 0.0 : bytes, down ? bytes : 0.0, e0, e1, cur_token_, cur_layer_,
+                                   launch_serial_++, {}});
+    if (record_)
+        for (int s = 0; s < p.n_seg; ++s) {
+            const int r = p.seg[s].entry;
+            int slot = -1;
+            bool resident = false;
+            for (const Use& us : uses_)
+                if (us.rank == r) {
+                    slot = us.slot;
+                    resident = !us.missing;
+                }
+            for (int t = p.seg[s].t0; t < p.seg[s].t1; ++t)
+                pass_events_.back().segs.push_back(SegInfo{u.experts[r], t, slot >= 0 ? fill_serial(slot) : -1, resident});
+        }
     stats_.kernels += 1;
 }
 
@@ -692,7 +728,7 @@ void DecodeSession::timed_grouped(GroupedLaunch& p, bool down) {
 // resident experts (one launch pair) and for each on-demand tile as it lands, then the per-stream
 // fixed-order weighted combine (see kernels/grouped_ffn.hpp).
 void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
-    const int D = spec_.hidden_dim, N = spec_.experts_per_layer, K = spec_.top_k, L = spec_.num_layers;
+    const int D = spec_.hidden_dim, N = spec_.experts_per_layer, K = spec_.top_k;
     const int T = store_.tiles, F = store_.ffn, Ft = F / T;
     cudaStream_t cs = eng_.compute_stream();
     const size_t row_bytes = static_cast<size_t>(D) * 2;
@@ -702,7 +738,7 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
     for (int r = 0; r < u.count; ++r) rank_of[u.experts[r]] = r;
     GatherArgs g;
     g.acts = cur_x_;
-    g.stream_stride = static_cast<long long>(L) * D;
+    g.stream_stride = cur_x_stride_;
     g.x = d_gx_.as<std::uint16_t>();
     g.d = D;
     g.np_stride = np_;
@@ -817,13 +853,13 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
         up.map_a = map_pool_gu_;
         up.map_b = map_x_;
         grouped_plan_gate_up(up);
-        timed_grouped(up, false);
+        timed_grouped(up, false, u);
         GroupedLaunch& dn = downs[i];
         dn.map_a = map_pool_dn_;
         dn.map_b = map_h_;
         dn.partial = d_gpart_.as<float>() + off;
         off += static_cast<size_t>(dn.units) * np_ * 128;
-        timed_grouped(dn, true);
+        timed_grouped(dn, true, u);
         for (int s = 0; s < dn.n_seg; ++s) refs.emplace_back(dn.seg[s].entry, GCombineRef{dn.partial, dn.unit_prefix[s], dn.kc});
     }
     std::stable_sort(refs.begin(), refs.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
@@ -839,15 +875,15 @@ void DecodeSession::layer_ffn_grouped(const RouteDecision& u) {
     }
     c.acts = cur_res_;
     c.scores = cur_scores_;
-    c.stream_stride = static_cast<long long>(L) * D;
+    c.stream_stride = cur_x_stride_;
     c.score_stride = cur_score_stride_;
     c.out = cur_out_;
-    c.out_stride = static_cast<long long>(L) * D;
+    c.out_stride = cur_out_stride_;
     c.d = D;
     c.np_stride = np_;
     c.n_streams = batch_;
     c.top_k = K;
-    c.residual = ep_rank_ == 0 ? 1 : 0;
+    c.residual = cur_residual_;
     if (ep_connected_) {
         c.n_out_peer = ep_world_;
         for (int g = 0; g < ep_world_; ++g) c.out_peer[g] = ep_slot(g, ep_rank_, ep_call_ & 1) + (cur_out_ - cur_out_base_);
@@ -862,6 +898,9 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
     const int B = batch_;
     if (count < 1) return 0.0;
     if (tokens_done_ + count > total_tokens_) fail(Status::Usage, "decode: more tokens than announced in decode_begin");
+    if (next_layer_ != 0)
+        fail(Status::Usage, "decode: token " + std::to_string(tokens_done_) + " is half done through moe_decode_layer "
+                            "(next layer " + std::to_string(next_layer_) + ")");
     cudaStream_t cs = eng_.compute_stream();
     cudaEvent_t t_begin = take_timing(), t_end = take_timing();
     MOE_CUDA(cudaEventRecord(t_begin, cs));
@@ -968,9 +1007,14 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
         cudaEvent_t r0, r1, f0, f1;
     };
     std::vector<GapRec> gap_rec;
+    cur_x_stride_ = static_cast<long long>(L) * D;
+    cur_out_stride_ = static_cast<long long>(L) * D;
+    cur_residual_ = ep_rank_ == 0 ? 1 : 0;
     for (int i = 0; i < count; ++i) {
         const int tok = tokens_done_ + i;
         for (int l = 0; l < L; ++l) {
+            cur_token_ = tok;
+            cur_layer_ = l;
             const size_t gl = (static_cast<size_t>(i) * L + l) * B;
             // free-running batch 1 without the EP exchange: layer l > 0's input was formed by layer
             // l-1's combine (CombineArgs::next_res)
@@ -1000,6 +1044,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                                       n_groups <= route_scratch_.groups ? &route_scratch_ : nullptr));
                 MOE_CUDA(cudaEventRecord(r1, rs));
                 router_events_.emplace_back(r0, r1);
+                if (record_) router_tokens_.push_back(tok);
                 stats_.kernels += 1;
                 stats_.router_launches += 1;
                 MOE_CUDA(cudaEventRecord(route_done_, rs));
@@ -1126,8 +1171,14 @@ DecodeStats DecodeSession::snapshot() {
         MOE_CUDA(cudaEventElapsedTime(&ms, a, b));
         return static_cast<double>(ms);
     };
+    auto since = [&](cudaEvent_t e) { return origin_ ? elapsed(origin_, e) : 0.0; };
     for (auto& p : pass_events_) {
         const double ms = elapsed(p.e0, p.e1);
+        if (record_) {
+            const double a = since(p.e0), b = since(p.e1);
+            for (const SegInfo& g : p.segs)
+                phys_compute_.push_back(PhysCompute{0, a, b, p.token, p.layer, g.expert, g.tile, p.launch, g.fill, g.resident});
+        }
         stats_.ffn_ms += ms;
         stats_.gate_up_bytes += p.gate_up_bytes;
         stats_.down_bytes += p.down_bytes;
@@ -1136,22 +1187,31 @@ DecodeStats DecodeSession::snapshot() {
         timing_pool_.push_back(p.e1);
     }
     pass_events_.clear();
-    for (auto& p : router_events_) {
+    for (size_t i = 0; i < router_events_.size(); ++i) {
+        const auto& p = router_events_[i];
         stats_.router_ms += elapsed(p.first, p.second);
+        if (record_ && i < router_tokens_.size())
+            phys_compute_.push_back(PhysCompute{2, since(p.first), since(p.second), router_tokens_[i], -1, -1, -1, -1, -1, false});
         timing_pool_.push_back(p.first);
         timing_pool_.push_back(p.second);
     }
     router_events_.clear();
+    router_tokens_.clear();
     for (size_t i = 0; i < stall_events_.size(); ++i) {
         const auto& p = stall_events_[i];
         const double ms = elapsed(p.first, p.second);
         stats_.stall_ms += ms;
         if (stall_is_prefetch_[i]) stats_.prefetch_stall_ms += ms;
+        if (record_ && i < stall_tags_.size()) {
+            const StallTag& g = stall_tags_[i];
+            phys_compute_.push_back(PhysCompute{1, since(p.first), since(p.second), g.token, g.layer, g.expert, g.tile, -1, g.job, false});
+        }
         timing_pool_.push_back(p.first);
         timing_pool_.push_back(p.second);
     }
     stall_events_.clear();
     stall_is_prefetch_.clear();
+    stall_tags_.clear();
     DecodeStats s = stats_;
     s.tile_copies = copier_->tiles_copied();
     s.copy_bytes = copier_->bytes_copied();
@@ -1167,6 +1227,232 @@ DecodeStats DecodeSession::finish() {
     for (auto& j : retiring_) copier_->retire(j);
     retiring_.clear();
     return snapshot();
+}
+
+// One layer of the current token on caller buffers (moe_decode_layer).  The same policy step and
+// FFN / combine launches as decode(), with the routing of one layer per call (its input is the
+// caller's, e.g. after the caller's attention) and the caller's stream ordered around the work.
+void DecodeSession::decode_layer(int layer, const double* x, const double* scores, float* out, bool add_input,
+                                 cudaStream_t user) {
+    eng_.activate();
+    const int L = spec_.num_layers, N = spec_.experts_per_layer, K = spec_.top_k, D = spec_.hidden_dim, B = batch_;
+    if (free_running_ || ep_world_ > 1)
+        fail(Status::Usage, "decode_layer: per-layer calls take a session without free_running or expert parallelism");
+    if (!x || !out) fail(Status::Usage, "decode_layer: x and out are required");
+    if (layer != next_layer_)
+        fail(Status::Usage, "decode_layer: layers run in order; expected layer " + std::to_string(next_layer_) +
+                                " of token " + std::to_string(tokens_done_) + ", got " + std::to_string(layer));
+    if (tokens_done_ >= total_tokens_) fail(Status::Usage, "decode_layer: more tokens than announced in decode_begin");
+    if (!scores && !eng_.has_gates()) fail(Status::Usage, "decode_layer: deciding from the gate needs the gate matrices");
+    const int tok = tokens_done_;
+    cur_token_ = tok;
+    cur_layer_ = layer;
+    cudaStream_t cs = eng_.compute_stream();
+    const auto h0 = std::chrono::steady_clock::now();
+    if (user != cs) {  // the caller's producer of x (e.g. attention) -> this layer's work
+        MOE_CUDA(cudaEventRecord(user_in_, user));
+        MOE_CUDA(cudaStreamWaitEvent(cs, user_in_, 0));
+    }
+    const bool prefetch_on = policy_->prefetch_on();
+    RouteGroup* hg = h_groups_.as<RouteGroup>();
+    const int adaptive = cfg_.policy.adaptive_gating ? kRouteAdaptive : 0;
+    int max_gates = 1;
+    for (int b = 0; b < B; ++b) {
+        RouteGroup g;
+        g.x = x + static_cast<size_t>(b) * D;
+        g.n_items = 1;
+        g.items[0].fisher = fisher_[layer];
+        g.items[0].out = b * 4;
+        if (scores) {  // the reference's actual-selection site: stored scores (inc/simulator.hpp:390-396)
+            g.items[0].scores = scores + static_cast<size_t>(b) * N;
+            g.items[0].flags = adaptive;
+        } else {  // the layer's gate on x, softmax(logits / concentration)
+            eng_.gate_item(g.items[0], layer);
+            g.items[0].flags = adaptive | kRouteDivConc | kRouteEmitScores;
+        }
+        if (prefetch_on) {
+            if (layer + 1 < L) {
+                for (int dep = 1; dep <= cfg_.lookahead_depth && layer + dep < L; ++dep) {
+                    RouteItem& it = g.items[g.n_items++];
+                    eng_.gate_item(it, layer + dep);
+                    it.fisher = fisher_[layer + dep];
+                    it.flags = adaptive;
+                    it.out = b * 4 + dep;
+                }
+            } else if (eng_.has_first_gate() && tok + 1 < total_tokens_) {
+                RouteItem& it = g.items[g.n_items++];
+                eng_.gate_item(it, -1);
+                it.fisher = fisher_[0];
+                it.flags = adaptive;
+                it.out = b * 4 + 1;
+            }
+        }
+        max_gates = std::max(max_gates, scores ? g.n_items - 1 : g.n_items);
+        hg[b] = g;
+    }
+    MOE_CUDA(cudaMemcpyAsync(d_groups_.ptr, hg, static_cast<size_t>(B) * sizeof(RouteGroup), cudaMemcpyHostToDevice, cs));
+    RouteParams rp{D, N, K, tau_, concentration_};
+    const int rows = 4 * B;
+    int* d_sel = d_route_;
+    int* d_cnt = d_sel + static_cast<size_t>(rows) * K;
+    int* d_sgl = d_cnt + rows;
+    int* d_exact = d_sgl + rows;
+    RouteOutputs ro{d_sel, d_cnt, d_sgl, nullptr, scores ? nullptr : d_free_scores_.as<double>(), d_exact};
+    ro.host_entries = h_route_host_.as<double>();
+    ro.host_counter = d_route_counter_.as<unsigned>();
+    ro.host_cap = route_host_cap_;
+    int* sel = h_route_;
+    int* cnt = sel + static_cast<size_t>(rows) * K;
+    int* sgl = cnt + rows;
+    int* exact_used = sgl + rows;
+    MOE_CUDA(cudaMemsetAsync(d_route_counter_.ptr, 0, sizeof(unsigned), cs));
+    std::memset(exact_used, 0, sizeof(int) * rows);
+    cudaEvent_t r0 = take_timing(), r1 = take_timing();
+    MOE_CUDA(cudaEventRecord(r0, cs));
+    MOE_CUDA(launch_route(d_groups_.as<RouteGroup>(), B, max_gates, rp, ro, cs,
+                          B <= route_scratch_.groups ? &route_scratch_ : nullptr));
+    MOE_CUDA(cudaEventRecord(r1, cs));
+    router_events_.emplace_back(r0, r1);
+    if (record_) router_tokens_.push_back(tok);
+    stats_.kernels += 1;
+    stats_.router_launches += 1;
+    MOE_CUDA(cudaEventRecord(route_done_, cs));
+    const auto hs = std::chrono::steady_clock::now();
+    MOE_CUDA(cudaEventSynchronize(route_done_));
+    stats_.host_sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hs).count();
+    route_host_decide(rp, h_route_host_.as<double>(), exact_used, 0, rows, sel, cnt, sgl, nullptr);
+    release_pending(false);
+    // decision (union over the streams) and look-ahead predictions, as in decode()
+    RouteDecision d;
+    std::array<RoutePrediction, 3> preds;
+    int singles = 0, np = 0;
+    const int n_items = hg[0].n_items;
+    for (int it = 1; it < n_items; ++it) {
+        preds[np].target = (layer + 1 < L) ? layer + it : 0;
+        preds[np].count = 0;
+        ++np;
+    }
+    for (int b = 0; b < B; ++b) {
+        const int r0w = b * 4;
+        singles += sgl[r0w] != 0;
+        for (int it = 1; it < n_items; ++it) stats_.router_exact += exact_used[r0w + it] != 0;
+        for (int k = 0; k < cnt[r0w]; ++k) {
+            const int e = sel[r0w * K + k];
+            bool seen = false;
+            for (int q = 0; q < d.count; ++q) seen |= d.experts[q] == e;
+            if (!seen) d.experts[d.count++] = e;
+        }
+        for (int it = 1; it < n_items; ++it) {
+            RoutePrediction& pr = preds[it - 1];
+            for (int k = 0; k < cnt[r0w + it]; ++k) {
+                const int e = sel[(r0w + it) * K + k];
+                bool seen = false;
+                for (int q = 0; q < pr.count; ++q) seen |= pr.experts[q] == e;
+                if (!seen) pr.experts[pr.count++] = e;
+            }
+        }
+        if (B > 1) {
+            cur_cnt_[b] = cnt[r0w];
+            for (int k = 0; k < K; ++k) cur_sel_[b * K + k] = k < cnt[r0w] ? sel[r0w * K + k] : -1;
+        }
+    }
+    d.single = B == 1 && sgl[0] != 0;
+    cur_x_ = x;
+    cur_res_ = x;
+    cur_scores_ = scores ? scores : d_free_scores_.as<double>();
+    cur_score_stride_ = scores ? N : 4 * N;
+    cur_out_ = out;
+    cur_out_base_ = out;
+    cur_x_stride_ = D;
+    cur_out_stride_ = D;
+    cur_residual_ = add_input ? 1 : 0;
+    fuse_next_res_ = fuse_next_norm_ = nullptr;
+    policy_->step(tok, layer, d, std::span<const RoutePrediction>(preds.data(), np), B > 1 ? singles : -1);
+    if (user != cs) {  // this layer's output -> the caller's consumer
+        MOE_CUDA(cudaEventRecord(user_out_, cs));
+        MOE_CUDA(cudaStreamWaitEvent(user, user_out_, 0));
+    }
+    stats_.host_step_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    if (++next_layer_ == L) {
+        next_layer_ = 0;
+        ++tokens_done_;
+        stats_.tokens += B;
+    }
+}
+
+void DecodeSession::record_timeline(bool on) {
+    eng_.activate();
+    if (on == record_) return;
+    snapshot();  // fold what ran so far into the counters (untagged)
+    if (on) {
+        if (!origin_) MOE_CUDA(cudaEventCreate(&origin_));
+        MOE_CUDA(cudaEventRecord(origin_, eng_.compute_stream()));
+        copier_->record_tiles(origin_, &phys_copies_);
+    } else {
+        copier_->record_tiles(nullptr, nullptr);
+    }
+    record_ = on;
+}
+
+namespace {
+void json_escape_free_line(std::string& o, const char* stream, const char* kind, double start_ms, double end_ms, int expert,
+                           int token, int layer, int tile) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf,
+                  "{\"stream\": \"%s\", \"kind\": \"%s\", \"start\": %.3f, \"end\": %.3f, \"expert\": %d, "
+                  "\"token\": %d, \"layer\": %d, \"tile\": %d",
+                  stream, kind, start_ms * 1e3, end_ms * 1e3, expert, token, layer, tile);
+    o += buf;
+}
+}  // namespace
+
+long long DecodeSession::write_timeline(const std::string& path) {
+    eng_.activate();
+    if (!origin_) fail(Status::Usage, "timeline_write: recording was never enabled (moe_decode_record_timeline)");
+    copier_->drain();
+    MOE_CUDA(cudaDeviceSynchronize());
+    copier_->collect_landed();  // tiles of jobs still holding slots
+    snapshot();
+    struct Line {
+        double start;
+        std::string text;
+    };
+    std::vector<Line> lines;
+    lines.reserve(phys_copies_.size() + phys_compute_.size());
+    char buf[256];
+    for (const TileCopyRecord& r : phys_copies_) {
+        std::string o;
+        json_escape_free_line(o, "comm", "tile_transfer", r.start_ms, r.end_ms, r.expert, r.token, r.layer, r.tile);
+        std::snprintf(buf, sizeof buf, ", \"request\": \"%s\", \"promoted\": %s, \"evicts\": %d, \"job\": %lld}",
+                      r.on_demand ? "on_demand" : "prefetch", r.promoted ? "true" : "false", r.evicts, r.serial);
+        o += buf;
+        lines.push_back(Line{r.start_ms, std::move(o)});
+    }
+    for (const PhysCompute& c : phys_compute_) {
+        std::string o;
+        if (c.kind == 0) {
+            json_escape_free_line(o, "compute", c.resident ? "expert_compute" : "tile_compute", c.start_ms, c.end_ms,
+                                  c.expert, c.token, c.layer, c.tile);
+            std::snprintf(buf, sizeof buf, ", \"launch\": %lld, \"fill\": %lld}", c.launch, c.fill);
+        } else if (c.kind == 1) {
+            json_escape_free_line(o, "compute", "wait", c.start_ms, c.end_ms, c.expert, c.token, c.layer, c.tile);
+            std::snprintf(buf, sizeof buf, ", \"job\": %lld}", c.fill);
+        } else {
+            json_escape_free_line(o, speculate_ ? "router" : "compute", "gate", c.start_ms, c.end_ms, -1, c.token, -1, -1);
+            std::snprintf(buf, sizeof buf, "}");
+        }
+        o += buf;
+        lines.push_back(Line{c.start_ms, std::move(o)});
+    }
+    std::stable_sort(lines.begin(), lines.end(), [](const Line& a, const Line& b) { return a.start < b.start; });
+    FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) fail(Status::Io, "timeline_write: cannot open " + path);
+    for (const Line& l : lines) {
+        std::fputs(l.text.c_str(), f);
+        std::fputc('\n', f);
+    }
+    if (std::fclose(f) != 0) fail(Status::Io, "timeline_write: cannot write " + path);
+    return static_cast<long long>(lines.size());
 }
 
 }  // namespace adapmoe

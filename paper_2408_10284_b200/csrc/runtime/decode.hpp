@@ -21,6 +21,7 @@
 #include <cuda_runtime_api.h>
 
 #include <array>
+#include <string>
 #include <memory>
 #include <tuple>
 #include <utility>
@@ -73,6 +74,23 @@ public:
     DecodeStats snapshot();  // counters so far (call between decode() calls)
     DecodeStats finish();    // drain the copy engine, then snapshot
 
+    // One MoE layer of the current token on caller device buffers, stream-ordered with `user`
+    // (moe_decode_layer): x [B][d] fp64 router/expert input, scores [B][N] fp64 (stored scores:
+    // the reference's actual-selection rule) or null (decide from the layer's gate on x, softmax
+    // of logits / concentration), out [B][d] fp32 = (add_input ? x : 0) + sum_e w_e E_e(x).
+    // Layers must come in order 0..L-1 per token; routing is per layer (K1 + one host sync).
+    void decode_layer(int layer, const double* x, const double* scores, float* out, bool add_input,
+                      cudaStream_t user);
+
+    // Physical timeline (moe_decode_record_timeline / moe_decode_timeline_write): CUDA-event
+    // timestamps of every tile copy (request class, promotion, eviction), FFN launch (its (expert,
+    // tile) segments and the copy job each segment's weights came from), compute-stream wait and
+    // router launch, relative to an origin event recorded when recording starts.
+    void record_timeline(bool on);
+    // Drain copies, sync, and write the events recorded so far as JSONL in the reference's
+    // timeline schema (inc/io.hpp:402-417; times in microseconds) plus physical fields.
+    long long write_timeline(const std::string& path);
+
     // DecodeListener
     void on_request(int id, ExpertRef ref, bool on_demand) override;
     void on_promote(int id) override;
@@ -106,7 +124,7 @@ private:
     bool merge_resident() const;
     int tile_merge_ = -1;  // -1 auto (tiles >= 8 MiB: 2), 0 per tile, 1 groups, 2 one launch per layer
     void layer_ffn_grouped(const RouteDecision& d);  // batch > 1: K3 grouped tcgen05 kernels
-    void timed_grouped(GroupedLaunch& p, bool down);
+    void timed_grouped(GroupedLaunch& p, bool down, const RouteDecision& u);
     void ep_exchange(float* out, long long rows, long long row_stride);
     // free-running decode: layer l > 0 routes and computes on layer l-1's output (the hidden state
     // flows through the experts); the actual decision comes from the layer's gate (softmax of
@@ -220,6 +238,7 @@ private:
     int route_host_cap_ = 0;
     int route_window_ = 1;
     cudaEvent_t route_done_ = nullptr;
+    cudaEvent_t user_in_ = nullptr, user_out_ = nullptr;  // moe_decode_layer: caller stream <-> compute stream
     // completion of each layer's FFN + combine on the compute stream: a slot released by layer s is
     // reused only after the event of layer s has completed (trace replay routes ahead of the GPU, so
     // there is no per-layer host synchronisation to order slot reuse)
@@ -229,9 +248,46 @@ private:
     std::vector<cudaEvent_t> timing_pool_;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> router_events_, stall_events_;
     std::vector<char> stall_is_prefetch_;  // per stall_events_ entry: waited on a logical prefetch
+    // physical timeline
+    struct SegInfo {
+        int expert, tile;
+        long long fill;  // copy job serial of the slot's contents (-1: initial residency)
+        bool resident;
+    };
+    struct PhysCompute {
+        int kind;  // 0 FFN launch segment, 1 compute-stream wait on a tile copy, 2 router launch
+        double start_ms, end_ms;
+        int token, layer, expert, tile;
+        long long launch, fill;
+        bool resident;
+    };
+    bool record_ = false;
+    cudaEvent_t origin_ = nullptr;
+    long long job_serial_ = 0, launch_serial_ = 0;
+    int cur_token_ = -1, cur_layer_ = -1;
+    std::vector<SegInfo> seg_info_;  // segments of the launch being assembled (record_ only)
+    std::vector<PhysCompute> phys_compute_;
+    std::vector<TileCopyRecord> phys_copies_;
+    struct StallTag {
+        int token, layer, expert, tile;
+        long long job;
+    };
+    std::vector<StallTag> stall_tags_;
+    std::vector<int> router_tokens_;
+    long long fill_serial(int slot) const { return slots_[slot].fill ? slots_[slot].fill->serial : -1; }
+    void note_seg(int slot, int expert, int tile, bool resident) {
+        if (record_) seg_info_.push_back(SegInfo{expert, tile, fill_serial(slot), resident});
+    }
+    // per-layer entry state
+    int next_layer_ = 0;
+    long long cur_x_stride_ = 0, cur_out_stride_ = 0;  // stream strides (doubles / floats) of cur_x_ / cur_out_
+    int cur_residual_ = 1;
     struct PassRec {
         double gate_up_bytes, down_bytes;
         cudaEvent_t e0, e1;
+        int token = -1, layer = -1;
+        long long launch = -1;
+        std::vector<SegInfo> segs;
     };
     std::vector<PassRec> pass_events_;
     cudaEvent_t take_timing();

@@ -420,6 +420,23 @@ class Engine:
         ipc = None if peer_ipc is None else b"".join(bytes(b).ljust(64, b"\0")[:64] for b in peer_ipc)
         check(load().moe_decode_ep_connect(self._h, ptrs, ipc))
 
+    def decode_layer(self, layer: int, x_ptr: int, scores_ptr: int | None, out_ptr: int, add_input: bool = True,
+                     stream: int | None = None) -> None:
+        """One MoE layer on device buffers, ordered with the caller's CUDA stream (moe_decode_layer):
+        x [B][d] fp64, scores [B][N] fp64 or None (decide from the gate), out [B][d] fp32."""
+        check(load().moe_decode_layer(self._h, layer, C.c_void_p(x_ptr), C.c_void_p(scores_ptr or 0) if scores_ptr else None,
+                                      C.c_void_p(out_ptr), int(add_input), C.c_void_p(stream) if stream else None))
+
+    def decode_record_timeline(self, enable: bool = True) -> None:
+        """Start / stop recording the physical timeline (moe_decode_record_timeline)."""
+        check(load().moe_decode_record_timeline(self._h, int(enable)))
+
+    def decode_timeline_write(self, path: str) -> int:
+        """Write the physical timeline recorded so far as JSONL (moe_decode_timeline_write)."""
+        n = C.c_int64()
+        check(load().moe_decode_timeline_write(self._h, str(path).encode(), C.byref(n)))
+        return n.value
+
     def decode_tokens(self, acts, scores, hidden_out=None, on_device: bool = False) -> float:
         """acts [n][L][d], scores [n][L][N] host numpy arrays (or device pointers via on_device)."""
         ms = C.c_double()

@@ -71,6 +71,9 @@ def parse():
     ap.add_argument("--pipeline", action="store_true",
                     help="measure the offline pipeline + ablation grid + artifact files (SURVEY §8(f)) against the "
                          "reference, one JSON line per workload, instead of the decode")
+    ap.add_argument("--timeline", default=None,
+                    help="record the physical timeline (CUDA-event tile copies, FFN launches, waits, router) over the "
+                         "e2e window, write it as JSONL to this path and run the reference's timeline validators")
     ap.add_argument("--host-alias", type=int, default=None,
                     help="store only this many distinct experts in host memory (profiling runs; same bytes moved)")
     return ap.parse_args()
@@ -475,6 +478,8 @@ def ours(args):
     s1 = eng.decode_stats()
     gpu_ms_max = max_over_ranks(ws, gpu_ms)
     # ---- e2e: one C-ABI call per token with pinned host buffers ----
+    if args.timeline:
+        eng.decode_record_timeline(True)
     barrier(ws)
     torch.cuda.synchronize()
     w0 = time.perf_counter()
@@ -487,6 +492,23 @@ def ours(args):
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(ws, time.perf_counter() - w0)
     barrier(ws)
+    timeline = None
+    if args.timeline:
+        from paper_2408_10284_b200 import timeline as TLM
+        path = args.timeline if ws == 1 else f"{args.timeline}.rank{rank}"
+        n_ev = eng.decode_timeline_write(path)
+        ev = TLM.load(path)
+        copies = [e for e in ev if e["kind"] == "tile_transfer"]
+        launches = {e["launch"]: (e["start"], e["end"]) for e in ev if "launch" in e}
+        t_lo = min(e["start"] for e in ev)
+        t_hi = max(e["end"] for e in ev)
+        timeline = {"path": path, "events": n_ev, "window_us": t_hi - t_lo,
+                    "link_busy_frac": sum(e["end"] - e["start"] for e in copies) / (t_hi - t_lo),
+                    "ffn_busy_frac": sum(b - a for a, b in launches.values()) / (t_hi - t_lo),
+                    "tile_copies": len(copies),
+                    "on_demand_tiles": sum(1 for e in copies if e["request"] == "on_demand" or e["promoted"]),
+                    "causality_problems": len(TLM.check_causality(ev)),
+                    "stream_overlap_problems": len(TLM.check_stream_exclusivity(ev))}
     res = eng.decode_end(cfg, total_tokens)
     st_end = res.stats
     resident = None
@@ -629,6 +651,8 @@ def ours(args):
     }
     if resident is not None:
         line["all_resident_window"] = resident
+    if timeline is not None:
+        line["physical_timeline"] = timeline
     if B == 1 and not args.free_running and rank == 0:
         # like-for-like with the reference arm: the same function (simulate_trace: every routing
         # decision + the tick-model cache / transfer engine, no weights moved) on the same 64-token

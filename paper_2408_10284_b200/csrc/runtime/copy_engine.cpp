@@ -7,6 +7,7 @@
 #include <string>
 
 #include "../host/policy.hpp"
+#include "nvtx.hpp"
 
 namespace adapmoe {
 
@@ -198,8 +199,9 @@ void CopyEngine::record_tile(CopyJob& job, int t) {  // caller holds mu_; the ti
     float a = 0.0f, b = 0.0f;
     if (records_ && origin_ && cudaEventElapsedTime(&a, origin_, job.t_start[t]) == cudaSuccess &&
         cudaEventElapsedTime(&b, origin_, job.t_end[t]) == cudaSuccess) {
-        records_->push_back(TileCopyRecord{job.serial, job.token, job.layer, job.expert, t, job.evicts,
-                                           job.requested_on_demand, job.promoted, a, b});
+        if (a >= 0.0f)  // copies that started before recording began are not part of the timeline
+            records_->push_back(TileCopyRecord{job.serial, job.token, job.layer, job.expert, t, job.evicts,
+                                               job.requested_on_demand, job.promoted, a, b});
         job.recorded_tiles = t + 1;
     }
 }
@@ -260,6 +262,7 @@ void CopyEngine::run() {
             busy_ = true;
         }
         if (fault_after >= 0 && tiles_copied_.load() >= fault_after) throw std::runtime_error("injected copy fault");
+        NvtxRange copy_range("copy L%d E%d tile %d (%s)", job->layer, job->expert, tile, job->on_demand ? "od" : "pf");
         ck(cudaEventRecord(job->t_start[tile], stream_), "cudaEventRecord");
         const size_t base = static_cast<size_t>(tile) * job->tile_bytes;
         for (size_t off = 0; off < job->tile_bytes; off += kChunkBytes) {

@@ -1,5 +1,7 @@
 #include "decode.hpp"
 
+#include "nvtx.hpp"
+
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -897,6 +899,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
     const int L = spec_.num_layers, N = spec_.experts_per_layer, K = spec_.top_k, D = spec_.hidden_dim;
     const int B = batch_;
     if (count < 1) return 0.0;
+    NvtxRange call_range("moe_decode_tokens %d..%d", tokens_done_, tokens_done_ + count - 1);
     if (tokens_done_ + count > total_tokens_) fail(Status::Usage, "decode: more tokens than announced in decode_begin");
     if (next_layer_ != 0)
         fail(Status::Usage, "decode: token " + std::to_string(tokens_done_) + " is half done through moe_decode_layer "
@@ -1015,6 +1018,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
         for (int l = 0; l < L; ++l) {
             cur_token_ = tok;
             cur_layer_ = l;
+            NvtxRange layer_range("token %d layer %d", tok, l);
             const size_t gl = (static_cast<size_t>(i) * L + l) * B;
             // free-running batch 1 without the EP exchange: layer l > 0's input was formed by layer
             // l-1's combine (CombineArgs::next_res)
@@ -1051,6 +1055,7 @@ double DecodeSession::decode(const double* acts, const double* scores, int count
                 if (speculate_)
                     launch_speculative(l, x_norm + (static_cast<size_t>(i) * B * L + l) * D);
                 const auto h0 = std::chrono::steady_clock::now();
+                NvtxRange sync_range("router sync");
                 MOE_CUDA(cudaEventSynchronize(route_done_));
                 stats_.host_sync_ms +=
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
@@ -1247,6 +1252,7 @@ void DecodeSession::decode_layer(int layer, const double* x, const double* score
     const int tok = tokens_done_;
     cur_token_ = tok;
     cur_layer_ = layer;
+    NvtxRange layer_range("moe_decode_layer token %d layer %d", tok, layer);
     cudaStream_t cs = eng_.compute_stream();
     const auto h0 = std::chrono::steady_clock::now();
     if (user != cs) {  // the caller's producer of x (e.g. attention) -> this layer's work

@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: run independent replicas (one stream per GPU) instead of expert parallelism")
     ap.add_argument("--budget", type=int, default=None)
+    ap.add_argument("--layers", type=int, default=None,
+                    help="rehearsal: keep only the model's first L layers (budget scaled by L / layers), e.g. the "
+                         "8x22B expert-parallel flow on a host that cannot pin all 270 GB of experts")
     ap.add_argument("--batch", type=int, default=1,
                     help="decode streams sharing the cache (BASELINE config 4: 16 / 64; grouped tcgen05 FFN)")
     ap.add_argument("--no-resident-check", action="store_true",
@@ -87,6 +90,14 @@ def workload(args):
         wl = W.mixtral_8x22b(tokens=max(args.trace_tokens, args.warmup + 2 * args.steps))
     else:
         wl = W.mixtral_8x7b(tokens=max(args.trace_tokens, args.warmup + 2 * args.steps))
+    if args.layers is not None:  # rehearsal of a deeper model on a smaller host: its first L layers
+        L = args.layers
+        budget = wl.budget * L // wl.layers
+        wl.name = f"{wl.name} (first {L} of {wl.layers} layers)"
+        wl.layers = L
+        wl.fisher_scales = wl.fisher_scales[:L]
+        wl.drift_scales = wl.drift_scales[:L]
+        wl.budget = budget
     if args.budget is not None:
         wl.budget = args.budget
     return wl
@@ -538,6 +549,28 @@ def ours(args):
                     "host_wait_k1_ms_per_step": dr["host_sync_ms"] / K, "host_step_ms_per_step": dr["host_step_ms"] / K,
                     "speculative_ffn": {"launches": int(dr["spec_launches"]), "hits": int(dr["spec_hits"])},
                     "budget": wl.layers * wl.experts}
+    free = None
+    if B == 1 and not args.free_running and ep_world == 1 and not args.no_resident_check:
+        # the realistic autoregressive mode beside the trace replay: layer l > 0 routes and computes on
+        # layer l-1's output (per-layer K1 + host sync), same budget, same store, CUDA events
+        eng.decode_begin(caps, trace.fisher, tau, cfg, wl.seed, total_tokens, args.staging, batch=1,
+                         free_running=True, concentration=wl.concentration)
+        wf, kf = 2, min(K, 4)
+        dev_call(0, wf)
+        f0 = eng.decode_stats()
+        torch.cuda.synchronize()
+        f_ms = dev_call(wf, wf + kf)
+        f1 = eng.decode_stats()
+        eng.decode_end(None, None, timeline=False)
+        df = {k: f1[k] - f0[k] for k in f0 if isinstance(f0[k], (int, float))}
+        fb = df["ffn_gate_up_bytes"] + df["ffn_down_bytes"]
+        free = {"tok_s": kf / (f_ms * 1e-3), "ms_per_step": f_ms / kf, "tokens": kf,
+                "ffn_frac": fb / (df["ffn_ms"] * 1e-3) / 1e9 / measured_peaks().get("hbm_gbs", 6650.0)
+                if df["ffn_ms"] > 0 else None,
+                "router_launches": int(df["router_launches"]), "host_wait_k1_ms_per_step": df["host_sync_ms"] / kf,
+                "speculative_ffn": {"launches": int(df["spec_launches"]), "hits": int(df["spec_hits"])},
+                "note": "free-running: decisions from the gates on the evolving hidden state (no reference "
+                        "counterpart; per-step parity in tests/test_free_running_gpu.py)"}
     # on-demand loads per token in the timed window (tile 0 of each on-demand expert)
     tl = res.timeline
     od_mask = (tl[:, 1] == 3) & (tl[:, 7] == 0)
@@ -653,6 +686,8 @@ def ours(args):
         line["all_resident_window"] = resident
     if timeline is not None:
         line["physical_timeline"] = timeline
+    if free is not None:
+        line["free_running_window"] = free
     if B == 1 and not args.free_running and rank == 0:
         # like-for-like with the reference arm: the same function (simulate_trace: every routing
         # decision + the tick-model cache / transfer engine, no weights moved) on the same 64-token

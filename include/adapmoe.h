@@ -305,6 +305,26 @@ int moe_expert_set(moe_engine_t engine, int32_t layer, int32_t expert, const uin
 /* Bytes of one expert (3 * F * d * 2) in the store. */
 int moe_expert_bytes(moe_engine_t engine, int64_t* bytes);
 
+/* Stream-level primitives (SURVEY §8(b) moe_copy_tile / moe_expert_ffn) for callers that manage their
+ * own HBM expert buffers.  moe_copy_tiles: tiles [tile0, tile0 + n_tiles) of expert (layer, expert)
+ * from the pinned host store into device memory laid out like the store (dst + t * tile_bytes holds
+ * tile t), one cudaMemcpyAsync per tile on `stream` (a cudaStream_t; NULL = the engine's copy
+ * stream); tile_events (NULL, or n_tiles cudaEvent_t) are recorded after each tile lands — the
+ * physical form of the reference CommEngine's per-tile transfer (inc/simulator.hpp:187-320). */
+int moe_copy_tiles(moe_engine_t engine, int32_t layer, int32_t expert, int32_t tile0, int32_t n_tiles, void* dst,
+                   void* stream, void* const* tile_events);
+
+/* moe_expert_ffn_async: y[b] = (accumulate ? y[b] : 0) + weight[b] * SwiGLU_E(x[b]) for b < rows,
+ * on device buffers, stream-ordered on `stream` (NULL = the engine's compute stream): expert = a
+ * device copy of one expert block (tile-major, e.g. from moe_copy_tiles), x [rows][d] fp64,
+ * y [rows][d] fp32, weights [rows] host doubles (NULL = 1).  tile_events (NULL or `tiles` events):
+ * the stream waits for each before computing (tile-granular overlap with moe_copy_tiles).  K2 + the
+ * combine kernel per row (batch-1 streaming; the batched grouped tcgen05 path runs inside
+ * moe_decode_tokens / moe_decode_layer).  Uses an engine-owned partial buffer: calls on one engine
+ * must be ordered on one stream. */
+int moe_expert_ffn_async(moe_engine_t engine, const void* expert, const double* x, float* y, int32_t rows,
+                         const double* weights, int32_t accumulate, void* const* tile_events, void* stream);
+
 /* Copy one expert's tile-major bf16 weights out of the pinned store (for parity tests). */
 int moe_expert_read(moe_engine_t engine, int32_t layer, int32_t expert, uint16_t* out);
 

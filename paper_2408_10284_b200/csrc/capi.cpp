@@ -514,6 +514,81 @@ int moe_experts_info(moe_engine_t h, int64_t* pinned_bytes, int32_t* stored_expe
     });
 }
 
+int moe_copy_tiles(moe_engine_t h, int32_t layer, int32_t expert, int32_t tile0, int32_t n_tiles, void* dst,
+                   void* stream, void* const* tile_events) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(dst, "dst");
+        if (!e.experts) fail(Status::Usage, "copy_tiles: experts not initialised");
+        const ExpertStore& st = *e.experts;
+        if (layer < 0 || layer >= st.layers || expert < 0 || expert >= st.experts) fail(Status::Usage, "ExpertRef out of range");
+        if (tile0 < 0 || n_tiles < 0 || tile0 + n_tiles > st.tiles) fail(Status::Usage, "copy_tiles: tile range out of [0, tiles)");
+        e.activate();
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e.copy_stream();
+        const unsigned char* src = st.expert(layer, expert);
+        for (int t = tile0; t < tile0 + n_tiles; ++t) {
+            const size_t off = static_cast<size_t>(t) * st.tile_bytes;
+            MOE_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(dst) + off, src + off, st.tile_bytes,
+                                     cudaMemcpyHostToDevice, s));
+            if (tile_events && tile_events[t - tile0])
+                MOE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(tile_events[t - tile0]), s));
+        }
+    });
+}
+
+int moe_expert_ffn_async(moe_engine_t h, const void* expert, const double* x, float* y, int32_t rows,
+                         const double* weights, int32_t accumulate, void* const* tile_events, void* stream) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        require(expert, "expert");
+        require(x, "x");
+        require(y, "y");
+        if (rows < 0) fail(Status::Usage, "expert_ffn_async: rows must be >= 0");
+        if (!e.experts) fail(Status::Usage, "expert_ffn_async: experts not initialised (shape unknown)");
+        e.activate();
+        const ExpertStore& st = *e.experts;
+        const int D = e.spec().hidden_dim, T = st.tiles, Ft = st.ffn / T;
+        cudaStream_t cs = stream ? static_cast<cudaStream_t>(stream) : e.compute_stream();
+        if (tile_events)
+            for (int t = 0; t < T; ++t)
+                if (tile_events[t]) MOE_CUDA(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(tile_events[t]), 0));
+        int sms = 148;
+        MOE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e.device()));
+        e.ffn_scratch.reserve(static_cast<size_t>(kFfnMaxCtas) * kFfnSlotsPerCta * D * sizeof(float));
+        const size_t gate_up = static_cast<size_t>(2) * Ft * D * 2;
+        for (int b = 0; b < rows; ++b) {
+            FfnLaunch p;
+            p.d = D;
+            p.ft = Ft;
+            p.x = x + static_cast<size_t>(b) * D;
+            p.partial = e.ffn_scratch.as<float>();
+            for (int t = 0; t < T; ++t) {
+                const unsigned char* tile = static_cast<const unsigned char*>(expert) + t * st.tile_bytes;
+                p.seg[p.n_seg].gate_up = reinterpret_cast<const std::uint16_t*>(tile);
+                p.seg[p.n_seg].down_t = reinterpret_cast<const std::uint16_t*>(tile + gate_up);
+                ++p.n_seg;
+            }
+            MOE_CUDA(launch_ffn(p, sms, cs));
+            CombineArgs c;
+            c.x = p.x;
+            c.scores = p.x;  // unread: one rank has weight 1
+            c.out = y + static_cast<size_t>(b) * D;
+            c.ranks = 1;
+            c.d = D;
+            c.ft = Ft;
+            c.residual = 0;
+            c.accumulate = accumulate ? 1 : 0;
+            c.scale = weights ? static_cast<float>(weights[b]) : 1.0f;
+            c.n_refs = T;
+            for (int t = 0; t < T; ++t) {
+                c.refs[t] = FfnPartialRef{p.partial, ffn_grid(p, sms), T, t, 0};
+                ffn_partial_range(c.refs[t], Ft);
+            }
+            MOE_CUDA(launch_combine(c, cs));
+        }
+    });
+}
+
 int moe_expert_host_ptr(moe_engine_t h, int32_t layer, int32_t expert, const void** ptr) {
     return guarded([&] {
         Engine& e = eng(h);

@@ -464,6 +464,7 @@ __global__ void __launch_bounds__(kCombineCols * kCombineLanes) combine_kernel(c
     double denom = 0.0;
     for (int r = 0; r < a.ranks; ++r) denom += a.scores[a.experts[r]];
     float acc = (live && a.residual) ? static_cast<float>(a.x[j]) : 0.0f;
+    if (live && a.accumulate) acc += a.out[j];
     int ref = 0;
     for (int r = 0; r < a.ranks; ++r) {
         float part = 0.0f;
@@ -491,7 +492,7 @@ __global__ void __launch_bounds__(kCombineCols * kCombineLanes) combine_kernel(c
             float yr = 0.0f;
 #pragma unroll
             for (int k = 0; k < kCombineLanes; ++k) yr += red[k][jl];
-            const float w = a.ranks == 1 ? 1.0f : static_cast<float>(a.scores[a.experts[r]] / denom);
+            const float w = (a.ranks == 1 ? 1.0f : static_cast<float>(a.scores[a.experts[r]] / denom)) * a.scale;
             acc = __fmaf_rn(w, yr, acc);
         }
         __syncthreads();
@@ -631,7 +632,7 @@ cudaError_t launch_free_running_input(double* res, double* norm, long long strid
                                       long long src_stride, int rows, int d, double eps, cudaStream_t stream) {
     if (rows <= 0 || d <= 0) return cudaSuccess;
     const size_t smem = static_cast<size_t>(d) * sizeof(double);
-    if (smem > 48 * 1024) {
+    if (smem > 40 * 1024) {  // the opt-in counts static shared memory too
         cudaError_t e = cudaFuncSetAttribute(free_running_input_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
@@ -710,7 +711,7 @@ cudaError_t launch_ffn(const FfnLaunch& p, int sm_count, cudaStream_t stream) {
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
     if (a.next_res && (!a.next_norm || !a.ticket || a.n_out_peer > 0)) return cudaErrorInvalidValue;
     const size_t smem = a.next_res ? static_cast<size_t>(a.d) * sizeof(double) : 0;
-    if (smem > 48 * 1024) {
+    if (smem > 40 * 1024) {  // the opt-in counts static shared memory too
         cudaError_t e = cudaFuncSetAttribute(combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;

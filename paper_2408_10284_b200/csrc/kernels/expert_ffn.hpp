@@ -84,6 +84,8 @@ struct CombineArgs {
     double* next_norm = nullptr;
     unsigned* ticket = nullptr;      // zero before the launch; the last block re-arms it
     double eps = 0.0;
+    float scale = 1.0f;              // extra factor on every rank's weight (moe_expert_ffn_async)
+    int accumulate = 0;              // out[j] += ... instead of out[j] = ... (n_out_peer == 0 only)
     FfnPartialRef refs[kMaxCombineRefs];
 };
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream);

@@ -117,6 +117,7 @@ public:
 
     std::unique_ptr<ExpertStore> experts;
     std::unique_ptr<DecodeSession> session;
+    DeviceBuffer ffn_scratch;  // K2 partials of moe_expert_ffn_async (stream-ordered reuse)
 
 private:
     ModelSpec spec_;

@@ -379,6 +379,23 @@ class Engine:
         check(load().moe_expert_bytes(self._h, C.byref(b)))
         return b.value
 
+    def copy_tiles(self, layer: int, expert: int, tile0: int, n_tiles: int, dst_ptr: int, stream: int | None = None,
+                   tile_events=None) -> None:
+        """Stream-ordered copy of expert tiles from the pinned store into device memory (moe_copy_tiles);
+        tile_events: optional list of cudaEvent_t handles (ints) recorded after each tile."""
+        ev = None if tile_events is None else (C.c_void_p * len(tile_events))(*[C.c_void_p(int(e)) for e in tile_events])
+        check(load().moe_copy_tiles(self._h, layer, expert, tile0, n_tiles, C.c_void_p(dst_ptr),
+                                    C.c_void_p(stream) if stream else None, ev))
+
+    def expert_ffn_async(self, expert_ptr: int, x_ptr: int, y_ptr: int, rows: int, weights=None,
+                         accumulate: bool = False, tile_events=None, stream: int | None = None) -> None:
+        """y[b] (+)= w[b] * SwiGLU(x[b]) on device buffers, stream-ordered (moe_expert_ffn_async)."""
+        w = None if weights is None else _f64(weights)
+        ev = None if tile_events is None else (C.c_void_p * len(tile_events))(*[C.c_void_p(int(e)) for e in tile_events])
+        check(load().moe_expert_ffn_async(self._h, C.c_void_p(expert_ptr), C.c_void_p(x_ptr), C.c_void_p(y_ptr), rows,
+                                          None if w is None else _p(w, _capi._d), int(accumulate), ev,
+                                          C.c_void_p(stream) if stream else None))
+
     def expert_host_ptr(self, layer: int, expert: int) -> int:
         """Address of the expert's tile-major block in the pinned host store (moe_expert_host_ptr)."""
         p = C.c_void_p()

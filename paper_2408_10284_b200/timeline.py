@@ -25,14 +25,17 @@ def load(path) -> list[dict]:
 
 def check_causality(events: list[dict], slack_us: float = 0.0) -> list[str]:
     """Every FFN segment whose slot was filled by a copy job starts after that job's copy of the
-    same tile ended (inc/simulator.hpp semantics: compute after transfer completion)."""
+    same tile ended (inc/simulator.hpp semantics: compute after transfer completion).  A recording
+    that starts mid-session cannot see copies that began before it: segments reading a job whose
+    tile 0 is not in the timeline are not checked."""
     ends = {}
     for e in events:
         if e["kind"] == "tile_transfer":
             ends[(e["job"], e["tile"])] = e["end"]
+    in_window = {job for job, tile in ends if tile == 0}
     problems = []
     for e in events:
-        if e["kind"] in ("expert_compute", "tile_compute") and e["fill"] >= 0:
+        if e["kind"] in ("expert_compute", "tile_compute") and e["fill"] in in_window:
             end = ends.get((e["fill"], e["tile"]))
             if end is None:
                 problems.append(f"launch {e['launch']}: layer {e['layer']} expert {e['expert']} tile {e['tile']} reads "

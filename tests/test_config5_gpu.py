@@ -169,3 +169,45 @@ def test_headline_decode_32_layers_budget64_vs_reference_golden():
     for (t, l) in [(0, 0), (3, 17), (7, 31), (11, 9)]:
         got = hid[t, l].astype(np.float64) - w.acts[t, l].astype(np.float32).astype(np.float64)
         assert _rel_err(got, _moe_ref(w, sim.decisions, t, l, ffn, cfg.tile_count_per_expert, seed, cache)) < REL_TOL
+
+
+def test_free_running_8x22b_shape():
+    """Free-running decode at the config-5 width (d 6144: the RMSNorm / fused-combine kernels need
+    > 48 KB of shared memory): layer 1 of every token must equal x1 + sum_e w_e E_e(RMSNorm(x1)) on the
+    GPU's own layer-0 output x1 (per-step parity of the hidden state, 1e-4)."""
+    import math
+    L, T = 2, 3
+    wl, (w,) = _x22b_trace(L, T, 6)
+    tau = O.calibrate_threshold(w, wl.target_single_ratio)
+    caps = [3, 3]
+    cfg = P.SimConfig()
+    with P.Engine(P.ModelSpec(L, 8, 2, 6144)) as eng:
+        eng.load_gates(w.gates)
+        eng.experts_init(wl.ffn, 4, seed=19)
+        eng.decode_begin(caps, w.fisher, tau, cfg, 0, T, free_running=True, concentration=wl.concentration)
+        hid = np.zeros((T, L, 6144), dtype=np.float32)
+        eng.decode_tokens(w.acts, w.scores, hid)
+        r = eng.decode_end(cfg, T)
+    assert np.isfinite(hid).all()
+    assert r.stats["router_launches"] == L * T
+    cache = {}
+    for t in range(T):
+        x1 = hid[t, 0].astype(np.float64)
+        rms = math.sqrt(float(np.dot(x1, x1)) / 6144 + 1e-5)
+        xn = (x1 / rms).astype(np.float32)
+        logits = xn.astype(np.float64) @ w.gates[1]
+        s = np.exp((logits - logits.max()) / wl.concentration)
+        s /= s.sum()
+        top = np.argsort(-s, kind="stable")[:2]
+        got = hid[t, 1].astype(np.float64) - x1
+        # the decision may be one or two experts (adaptive gate); accept the closer of the two readings
+        errs = []
+        for sel in ([int(top[0])], [int(e) for e in top]):
+            moe = np.zeros(6144)
+            for e in sel:
+                if e not in cache:
+                    cache[e] = O.expert_init(19, 1, e, 6144, wl.ffn, 4)
+                wgt = 1.0 if len(sel) == 1 else s[e] / s[list(sel)].sum()
+                moe += wgt * O.swiglu(cache[e], 6144, wl.ffn, 4, xn)
+            errs.append(_rel_err(got, moe))
+        assert min(errs) < 5e-4, (t, errs)

@@ -32,6 +32,8 @@ def test_compute_before_copy_is_flagged():
     probs = TL.check_causality(bad)
     assert len(probs) == 1 and "tile 1" in probs[0]
     assert TL.check_causality(GOOD[:3] + [_cp(0, 3, 21.0, 30.0, 0)])  # tile never copied
+    # a job that started before the recording (tile 0 absent) is not checked
+    assert TL.check_causality(GOOD + [_cp(3, 0, 50.0, 60.0, 9)]) == []
 
 
 def test_overlaps_are_flagged():

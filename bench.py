@@ -77,6 +77,9 @@ def parse():
     ap.add_argument("--timeline", default=None,
                     help="record the physical timeline (CUDA-event tile copies, FFN launches, waits, router) over the "
                          "e2e window, write it as JSONL to this path and run the reference's timeline validators")
+    ap.add_argument("--store-format", default="xb12", choices=["bf16", "xb12"],
+                    help="pinned expert store: raw bf16 tiles, or XB12 (lossless exponent-coded bf16: 75 %% of the "
+                         "bytes over the host link, decoded into the HBM slot on arrival; identical outputs)")
     ap.add_argument("--host-alias", type=int, default=None,
                     help="store only this many distinct experts in host memory (profiling runs; same bytes moved)")
     return ap.parse_args()
@@ -292,6 +295,12 @@ def cpu_ffn_baseline(eng, wl, trace, tau, cfg, tok0: int, n_tok: int, gpu_out):
     lib = C.CDLL(os.path.join(ROOT, "baseline", "libcpu_ffn.so"))
     lib.cpu_moe_layer.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_double), C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.POINTER(C.c_double), C.POINTER(C.c_float), C.c_int]
+    lib.cpu_moe_layer_xb12.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_int32), C.POINTER(C.c_uint32),
+                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_double), C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.POINTER(C.c_double), C.POINTER(C.c_float), C.c_int]
+    fmt, _ = eng.experts_format()
+    recs = {}
     threads = os.cpu_count() or 1
     acts = np.ascontiguousarray(trace.acts[tok0: tok0 + n_tok])
     scores = trace.scores[tok0: tok0 + n_tok]
@@ -304,13 +313,29 @@ def cpu_ffn_baseline(eng, wl, trace, tau, cfg, tok0: int, n_tok: int, gpu_out):
             sel = [int(e) for e in dec[t, l] if e >= 0]
             den = sum(scores[t, l, e] for e in sel)
             wts = (C.c_double * len(sel))(*[1.0 if len(sel) == 1 else scores[t, l, e] / den for e in sel])
-            ptrs = (C.c_void_p * len(sel))(*[eng.expert_host_ptr(l, e) for e in sel])
             x = acts[t, l]
-            rc = lib.cpu_moe_layer(ptrs, wts, len(sel), wl.hidden, wl.ffn, wl.tiles,
-                                   x.ctypes.data_as(C.POINTER(C.c_double)),
-                                   out[t, l].ctypes.data_as(C.POINTER(C.c_float)), threads)
+            xp, op = x.ctypes.data_as(C.POINTER(C.c_double)), out[t, l].ctypes.data_as(C.POINTER(C.c_float))
+            if fmt == "bf16":
+                ptrs = (C.c_void_p * len(sel))(*[eng.expert_host_ptr(l, e) for e in sel])
+                rc = lib.cpu_moe_layer(ptrs, wts, len(sel), wl.hidden, wl.ffn, wl.tiles, xp, op, threads)
+                moved += len(sel) * 3 * wl.ffn * wl.hidden * 2
+            else:  # XB12 records decoded on the fly (the same bytes the GPU path moves)
+                rs = []
+                for e in sel:
+                    for tt in range(wl.tiles):
+                        if (l, e, tt) not in recs:
+                            recs[(l, e, tt)] = eng.expert_tile_record(l, e, tt)
+                        rs.append(recs[(l, e, tt)])
+                n = len(rs)
+                rc = lib.cpu_moe_layer_xb12((C.c_void_p * n)(*[r["ptr"] for r in rs]),
+                                            (C.c_int32 * n)(*[r["format"] for r in rs]),
+                                            (C.c_uint32 * n)(*[r["base"] for r in rs]),
+                                            (C.c_int64 * n)(*[r["n_escapes"] for r in rs]),
+                                            (C.c_int64 * n)(*[r["nib_offset"] for r in rs]),
+                                            (C.c_int64 * n)(*[r["esc_offset"] for r in rs]),
+                                            wts, len(sel), wl.hidden, wl.ffn, wl.tiles, xp, op, threads)
+                moved += sum(r["bytes"] for r in rs)
             assert rc == 0, rc
-            moved += len(sel) * 3 * wl.ffn * wl.hidden * 2
     dt = time.perf_counter() - t0
     moe_gpu = gpu_out.astype(np.float64) - acts.astype(np.float32).astype(np.float64)
     moe_cpu = out.astype(np.float64) - acts.astype(np.float32).astype(np.float64)
@@ -319,7 +344,7 @@ def cpu_ffn_baseline(eng, wl, trace, tau, cfg, tok0: int, n_tok: int, gpu_out):
             "label": "not reference: builder-written CPU SwiGLU (baseline/cpu_ffn.c, OpenMP, fp32 accumulation); "
                      "the reference's CPU path does no FFN arithmetic (inc/simulator.hpp:446-462)",
             "sample": f"{n_tok} tokens x {wl.layers} layers of the e2e window, selected experts read in place from the "
-                      f"pinned host store ({moved / 1e9:.1f} GB)",
+                      f"pinned host store ({fmt} records, {moved / 1e9:.1f} GB)",
             "host_read_gbs": moved / dt / 1e9, "max_rel_diff_vs_gpu": rel}
 
 
@@ -417,9 +442,11 @@ def ours(args):
                          f"host memory, {per_rank / 1e9:.0f} GB available per rank (pass --host-alias to alias blocks)")
     link_peak = h2d_peak_gbs(local)
     t0 = time.time()
-    eng.experts_init(wl.ffn, wl.tiles, seed=1234, host_alias=alias, expert_owner=owners, rank=ep_rank)
+    eng.experts_init(wl.ffn, wl.tiles, seed=1234, host_alias=alias, expert_owner=owners, rank=ep_rank,
+                     store_format=args.store_format)
     t_store = time.time() - t0
     store_info = eng.experts_info()
+    store_fmt, store_link_bytes = eng.experts_format()
     # B token streams (config 4): stream b = the reference generator with token_seed + b (same gates)
     acts, scores = trace.acts, trace.scores
     total_tokens = wl.tokens
@@ -629,6 +656,8 @@ def ours(args):
                    "tau": tau, "realized_single_ratio": realized, "capacities": [int(c) for c in caps],
                    "dp_expected_loads_per_token": exp_loads, "host_alias": alias,
                    "expert_store_per_rank": per_rank_store,
+                   "store_format": store_fmt,
+                   "store_link_bytes_per_expert": store_link_bytes / max(1, held),
                    "parallelism": (f"ep{ws} ({'experts placed by a calibration trace (ep.balanced_owners)' if owners is not None else f'expert e on rank e % {ws}'}; combine: "
                                    f"{'P2P stores into peer memory from the combine epilogue' if p2p else 'all_gather'})"
                                    if ep_world > 1 else f"replicas x{ws}"),

@@ -289,6 +289,25 @@ int moe_experts_init_shard(moe_engine_t engine, int32_t ffn_dim, int32_t tiles, 
                            const int32_t* expert_owner, int32_t rank);
 int moe_experts_alloc_shard(moe_engine_t engine, int32_t ffn_dim, int32_t tiles, const int32_t* expert_owner,
                             int32_t rank);
+/* Expert store format for the next moe_experts_init* / moe_experts_alloc* on this engine:
+ * MOE_STORE_BF16 (default) keeps every tile as raw bf16; MOE_STORE_XB12 keeps each tile as an XB12
+ * record (paper_2408_10284_b200/csrc/kernels/xb12.hpp): sign + mantissa bytes, 4-bit exponent
+ * codes against a per-tile 15-exponent window and an escape list, 75 % of the bytes for Mixtral-shape
+ * weights.  Lossless: tiles land in an HBM staging buffer and a decode kernel restores the exact bf16
+ * bits in the slot before anything reads them, so every output and trace is bit-identical to the
+ * bf16 store; the host link moves 25 % fewer bytes.  A tile that would not shrink (> n/64 escapes)
+ * stays raw.  moe_expert_read decodes; moe_expert_host_ptr needs a bf16 store. */
+#define MOE_STORE_BF16 0
+#define MOE_STORE_XB12 1
+int moe_experts_set_format(moe_engine_t engine, int32_t format);
+/* Format of the current store and the bytes a copy of all its records moves over the host link. */
+int moe_experts_format(moe_engine_t engine, int32_t* format, int64_t* link_bytes);
+/* One tile's record in the pinned store: host address, bytes, format (0 raw bf16, 1 XB12), and for
+ * XB12 the window base exponent, escape count and section offsets (lo at 0, nibbles, escapes). */
+int moe_expert_tile_record(moe_engine_t engine, int32_t layer, int32_t expert, int32_t tile, const void** record,
+                           int64_t* bytes, int32_t* format, uint32_t* base, int64_t* n_escapes, int64_t* nib_offset,
+                           int64_t* esc_offset);
+
 /* Pinned bytes, distinct stored expert blocks and the host NUMA node (-1: none) of the store. */
 int moe_experts_info(moe_engine_t engine, int64_t* pinned_bytes, int32_t* stored_experts, int32_t* numa_node);
 

@@ -110,6 +110,11 @@ SIGNATURES = {
     "moe_expert_bytes": (C.c_int, [_eng, _i64]),
     "moe_expert_read": (C.c_int, [_eng, C.c_int32, C.c_int32, _u16]),
     "moe_expert_host_ptr": (C.c_int, [_eng, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "moe_experts_set_format": (C.c_int, [_eng, C.c_int32]),
+    "moe_experts_format": (C.c_int, [_eng, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+    "moe_expert_tile_record": (C.c_int, [_eng, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p),
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_uint32),
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "moe_copy_tiles": (C.c_int, [_eng, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                  C.POINTER(C.c_void_p)]),
     "moe_expert_ffn_async": (C.c_int, [_eng, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, _d, C.c_int32,

@@ -477,7 +477,7 @@ int experts_build(moe_engine_t h, int32_t ffn, int32_t tiles, uint64_t seed, int
         e.session.reset();
         e.experts = std::make_unique<ExpertStore>();
         try {
-            build_expert_store(e, *e.experts, ffn, tiles, seed, alias, init_values, owner, rank);
+            build_expert_store(e, *e.experts, ffn, tiles, seed, alias, init_values, owner, rank, e.store_format);
         } catch (...) {
             e.experts.reset();
             throw;
@@ -525,14 +525,8 @@ int moe_copy_tiles(moe_engine_t h, int32_t layer, int32_t expert, int32_t tile0,
         if (tile0 < 0 || n_tiles < 0 || tile0 + n_tiles > st.tiles) fail(Status::Usage, "copy_tiles: tile range out of [0, tiles)");
         e.activate();
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e.copy_stream();
-        const unsigned char* src = st.expert(layer, expert);
-        for (int t = tile0; t < tile0 + n_tiles; ++t) {
-            const size_t off = static_cast<size_t>(t) * st.tile_bytes;
-            MOE_CUDA(cudaMemcpyAsync(static_cast<unsigned char*>(dst) + off, src + off, st.tile_bytes,
-                                     cudaMemcpyHostToDevice, s));
-            if (tile_events && tile_events[t - tile0])
-                MOE_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(tile_events[t - tile0]), s));
-        }
+        upload_expert_tiles(st, layer, expert, tile0, tile0 + n_tiles, static_cast<unsigned char*>(dst), e.copy_staging,
+                            s, reinterpret_cast<cudaEvent_t const*>(tile_events));
     });
 }
 
@@ -589,6 +583,45 @@ int moe_expert_ffn_async(moe_engine_t h, const void* expert, const double* x, fl
     });
 }
 
+int moe_experts_set_format(moe_engine_t h, int32_t format) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        if (format != kStoreBf16 && format != kStoreXb12) fail(Status::Usage, "experts_set_format: unknown format");
+        e.store_format = format;
+    });
+}
+
+int moe_experts_format(moe_engine_t h, int32_t* format, int64_t* link_bytes) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        if (!e.experts) fail(Status::Usage, "experts not initialised");
+        if (format) *format = e.experts->format;
+        if (link_bytes) *link_bytes = static_cast<int64_t>(e.experts->link_bytes);
+    });
+}
+
+int moe_expert_tile_record(moe_engine_t h, int32_t layer, int32_t expert, int32_t tile, const void** record,
+                           int64_t* bytes, int32_t* format, uint32_t* base, int64_t* n_escapes, int64_t* nib_offset,
+                           int64_t* esc_offset) {
+    return guarded([&] {
+        Engine& e = eng(h);
+        if (!e.experts) fail(Status::Usage, "experts not initialised");
+        const ExpertStore& st = *e.experts;
+        if (layer < 0 || layer >= st.layers || expert < 0 || expert >= st.experts) fail(Status::Usage, "ExpertRef out of range");
+        if (tile < 0 || tile >= st.tiles) fail(Status::Usage, "tile out of range");
+        size_t b = 0;
+        const unsigned char* r = st.record(layer, expert, tile, &b);
+        const Xb12Tile& m = st.meta(layer, expert, tile);
+        if (record) *record = r;
+        if (bytes) *bytes = static_cast<int64_t>(b);
+        if (format) *format = m.format;
+        if (base) *base = m.base;
+        if (n_escapes) *n_escapes = static_cast<int64_t>(m.n_exc);
+        if (nib_offset) *nib_offset = static_cast<int64_t>(m.nib_off);
+        if (esc_offset) *esc_offset = static_cast<int64_t>(m.exc_off);
+    });
+}
+
 int moe_expert_host_ptr(moe_engine_t h, int32_t layer, int32_t expert, const void** ptr) {
     return guarded([&] {
         Engine& e = eng(h);
@@ -596,6 +629,8 @@ int moe_expert_host_ptr(moe_engine_t h, int32_t layer, int32_t expert, const voi
         if (!e.experts) fail(Status::Usage, "experts not initialised");
         if (layer < 0 || layer >= e.experts->layers || expert < 0 || expert >= e.experts->experts)
             fail(Status::Usage, "ExpertRef out of range");
+        if (e.experts->format != kStoreBf16)
+            fail(Status::Usage, "expert_host_ptr: the store is XB12-coded (moe_expert_tile_record gives its records)");
         *ptr = e.experts->expert(layer, expert);
     });
 }
@@ -609,7 +644,7 @@ int moe_expert_set(moe_engine_t h, int32_t layer, int32_t expert, const uint16_t
         require(w2, "w2");
         if (!e.experts) fail(Status::Usage, "expert_set: call moe_experts_alloc (or moe_experts_init) first");
         if (e.session) fail(Status::Usage, "expert_set: a decode session is active (its HBM slots hold copies)");
-        set_expert_weights(*e.experts, layer, expert, w1, w3, w2);
+        set_expert_weights(e, *e.experts, layer, expert, w1, w3, w2);
     });
 }
 
@@ -630,7 +665,7 @@ int moe_expert_read(moe_engine_t h, int32_t layer, int32_t expert, uint16_t* out
         const ModelSpec& s = e.spec();
         if (layer < 0 || layer >= s.num_layers || expert < 0 || expert >= s.experts_per_layer)
             fail(Status::Usage, "ExpertRef out of range");
-        std::memcpy(out, e.experts->expert(layer, expert), e.experts->expert_bytes);
+        read_expert_host(*e.experts, layer, expert, out);
     });
 }
 
@@ -762,7 +797,7 @@ int moe_expert_ffn(moe_engine_t h, int32_t layer, int32_t expert, const double* 
         dout.reserve(D * sizeof(float));
         zero.reserve(D * sizeof(double));
         cudaStream_t cs = e.compute_stream();
-        MOE_CUDA(cudaMemcpyAsync(w.ptr, st.expert(layer, expert), st.expert_bytes, cudaMemcpyHostToDevice, cs));
+        upload_expert_tiles(st, layer, expert, 0, st.tiles, w.as<unsigned char>(), e.copy_staging, cs);
         MOE_CUDA(cudaMemcpyAsync(dx.ptr, x, D * sizeof(double), cudaMemcpyHostToDevice, cs));
         MOE_CUDA(cudaMemsetAsync(zero.ptr, 0, D * sizeof(double), cs));
         const size_t gate_up = static_cast<size_t>(2) * Ft * D * 2;

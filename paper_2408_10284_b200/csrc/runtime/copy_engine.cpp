@@ -17,7 +17,16 @@ void check(cudaError_t e, const char* what) {
 }
 }  // namespace
 
-CopyEngine::CopyEngine(cudaStream_t stream, int device) : stream_(stream), device_(device) {
+CopyEngine::CopyEngine(cudaStream_t stream, int device, size_t staging_bytes)
+    : stream_(stream), device_(device), staging_bytes_(staging_bytes) {
+    if (staging_bytes_) {
+        check(cudaStreamCreateWithFlags(&decode_stream_, cudaStreamNonBlocking), "cudaStreamCreate (xb12 decode)");
+        for (int k = 0; k < kStaging; ++k) {
+            check(cudaMalloc(&staging_[k], staging_bytes_), "cudaMalloc (xb12 staging)");
+            check(cudaEventCreateWithFlags(&staging_landed_[k], cudaEventDisableTiming), "cudaEventCreate");
+            check(cudaEventCreateWithFlags(&staging_free_[k], cudaEventDisableTiming), "cudaEventCreate");
+        }
+    }
     thread_ = std::thread([this] { loop(); });
 }
 
@@ -36,6 +45,15 @@ CopyEngine::~CopyEngine() {
     for (cudaEvent_t e : inflight_) cudaEventDestroy(e);
     for (cudaEvent_t e : free_sync_) cudaEventDestroy(e);
     for (cudaEvent_t e : free_timing_) cudaEventDestroy(e);
+    if (decode_stream_) {
+        cudaStreamSynchronize(decode_stream_);
+        for (int k = 0; k < kStaging; ++k) {
+            cudaFree(staging_[k]);
+            cudaEventDestroy(staging_landed_[k]);
+            cudaEventDestroy(staging_free_[k]);
+        }
+        cudaStreamDestroy(decode_stream_);
+    }
 }
 
 cudaEvent_t CopyEngine::take_event(bool timing) {
@@ -50,12 +68,17 @@ cudaEvent_t CopyEngine::take_event(bool timing) {
     return e;
 }
 
-std::shared_ptr<CopyJob> CopyEngine::make_job(unsigned char* dst, const unsigned char* src, size_t tile_bytes, int tiles) {
+std::shared_ptr<CopyJob> CopyEngine::make_job(unsigned char* dst, size_t tile_bytes, std::vector<TileSource> srcs) {
     auto j = std::make_shared<CopyJob>();
     j->dst = dst;
-    j->src = src;
     j->tile_bytes = tile_bytes;
-    j->tiles = tiles;
+    j->tiles = static_cast<int>(srcs.size());
+    j->srcs = std::move(srcs);
+    const int tiles = j->tiles;
+    j->issue_seq.assign(tiles, -1);
+    for (const TileSource& t : j->srcs)
+        if (t.meta.format == 1 && (!staging_bytes_ || t.bytes > staging_bytes_))
+            fail(Status::Internal, "copy engine: XB12 record larger than the staging buffers");
     std::lock_guard<std::mutex> g(mu_);
     for (int t = 0; t < tiles; ++t) {
         j->done.push_back(take_event(false));
@@ -125,7 +148,10 @@ bool CopyEngine::fully_issued(const std::shared_ptr<CopyJob>& job) {
 bool CopyEngine::idle(const std::shared_ptr<CopyJob>& job) {
     std::lock_guard<std::mutex> g(mu_);
     if (job->next_tile != job->issued_tiles) return false;  // the copy thread is issuing a tile
-    return job->issued_tiles == 0 || cudaEventQuery(job->t_end[job->issued_tiles - 1]) == cudaSuccess;
+    // `done` follows the tile's decode (XB12) and its copy: once it completed, no stream still records
+    // or waits on this job's events
+    return job->issued_tiles == 0 || (cudaEventQuery(job->t_end[job->issued_tiles - 1]) == cudaSuccess &&
+                                      cudaEventQuery(job->done[job->issued_tiles - 1]) == cudaSuccess);
 }
 
 bool CopyEngine::landed(const std::shared_ptr<CopyJob>& job) {
@@ -139,6 +165,7 @@ void CopyEngine::drain() {
     throw_if_failed();
     lk.unlock();
     check(cudaStreamSynchronize(stream_), "copy stream sync");
+    if (decode_stream_) check(cudaStreamSynchronize(decode_stream_), "xb12 decode stream sync");
 }
 
 double CopyEngine::busy_ms() {
@@ -255,6 +282,7 @@ void CopyEngine::run() {
             auto& q = !od_.empty() ? od_ : pf_;
             job = q.front();
             tile = job->next_tile++;
+            job->issue_seq[tile] = issue_counter_++;
             if (job->next_tile == job->tiles) {
                 q.pop_front();
                 job->queued = false;
@@ -263,17 +291,25 @@ void CopyEngine::run() {
         }
         if (fault_after >= 0 && tiles_copied_.load() >= fault_after) throw std::runtime_error("injected copy fault");
         NvtxRange copy_range("copy L%d E%d tile %d (%s)", job->layer, job->expert, tile, job->on_demand ? "od" : "pf");
+        const TileSource& src = job->srcs[tile];
+        unsigned char* out = job->dst + static_cast<size_t>(tile) * job->tile_bytes;
+        const bool coded = src.meta.format == 1;
+        const int k = coded ? staging_next_ : -1;
+        if (coded) {  // the staging buffer is free once the decode that last read it has run
+            staging_next_ = (staging_next_ + 1) % kStaging;
+            ck(cudaStreamWaitEvent(stream_, staging_free_[k], 0), "cudaStreamWaitEvent");
+        }
+        unsigned char* land = coded ? static_cast<unsigned char*>(staging_[k]) : out;
         ck(cudaEventRecord(job->t_start[tile], stream_), "cudaEventRecord");
-        const size_t base = static_cast<size_t>(tile) * job->tile_bytes;
-        for (size_t off = 0; off < job->tile_bytes; off += kChunkBytes) {
+        for (size_t off = 0; off < src.bytes; off += kChunkBytes) {
             while (static_cast<int>(inflight_.size()) >= kWindow) {
                 ck(cudaEventSynchronize(inflight_.front()), "tile copy");
                 std::lock_guard<std::mutex> g(mu_);
                 free_sync_.push_back(inflight_.front());
                 inflight_.pop_front();
             }
-            const size_t n = std::min(kChunkBytes, job->tile_bytes - off);
-            ck(cudaMemcpyAsync(job->dst + base + off, job->src + base + off, n, cudaMemcpyHostToDevice, stream_),
+            const size_t n = std::min(kChunkBytes, src.bytes - off);
+            ck(cudaMemcpyAsync(land + off, src.src + off, n, cudaMemcpyHostToDevice, stream_),
                "cudaMemcpyAsync (expert tile)");
             cudaEvent_t e;
             {
@@ -283,10 +319,20 @@ void CopyEngine::run() {
             ck(cudaEventRecord(e, stream_), "cudaEventRecord");
             inflight_.push_back(e);
         }
-        ck(cudaEventRecord(job->done[tile], stream_), "cudaEventRecord");
         ck(cudaEventRecord(job->t_end[tile], stream_), "cudaEventRecord");
+        if (coded) {  // decode on its own stream so the link never waits for it
+            ck(cudaEventRecord(staging_landed_[k], stream_), "cudaEventRecord");
+            ck(cudaStreamWaitEvent(decode_stream_, staging_landed_[k], 0), "cudaStreamWaitEvent");
+            ck(xb12_decode(static_cast<const std::uint8_t*>(staging_[k]), src.meta, reinterpret_cast<std::uint16_t*>(out),
+                           decode_stream_),
+               "xb12 decode");
+            ck(cudaEventRecord(job->done[tile], decode_stream_), "cudaEventRecord");
+            ck(cudaEventRecord(staging_free_[k], decode_stream_), "cudaEventRecord");
+        } else {
+            ck(cudaEventRecord(job->done[tile], stream_), "cudaEventRecord");
+        }
         tiles_copied_ += 1;
-        bytes_copied_ += static_cast<long long>(job->tile_bytes);
+        bytes_copied_ += static_cast<long long>(src.bytes);
         {
             std::lock_guard<std::mutex> g(mu_);
             job->issued_tiles = tile + 1;

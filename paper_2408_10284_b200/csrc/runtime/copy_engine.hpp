@@ -19,13 +19,23 @@
 #include <thread>
 #include <vector>
 
+#include "../kernels/xb12.hpp"
+
 namespace adapmoe {
+
+// One tile's source in the pinned store: raw bf16 (format 0, copied straight into the slot) or an
+// XB12 record (copied into an HBM staging buffer, then decoded into the slot, kernels/xb12.hpp).
+struct TileSource {
+    const unsigned char* src = nullptr;
+    size_t bytes = 0;
+    Xb12Tile meta;
+};
 
 struct CopyJob {
     unsigned char* dst = nullptr;
-    const unsigned char* src = nullptr;
-    size_t tile_bytes = 0;
+    size_t tile_bytes = 0;  // destination stride (decoded bf16 tile)
     int tiles = 0;
+    std::vector<TileSource> srcs;  // per tile
     bool on_demand = false;
     bool logical_prefetch = false;  // a prefetch the logical engine never promoted (accounting class)
     bool consumed = false;          // the compute stream waited on (used) its tiles
@@ -43,6 +53,7 @@ struct CopyJob {
     int token = -1, layer = -1, expert = -1, evicts = -1;
     bool requested_on_demand = false, promoted = false;
     int recorded_tiles = 0;  // tiles already appended to the timeline records
+    std::vector<long long> issue_seq;  // per tile: global issue order on the (serial) link, -1 = not issued
 };
 
 // One landed tile copy, for the physical timeline (times in ms from the recorder's origin event).
@@ -58,10 +69,12 @@ public:
     static constexpr size_t kChunkBytes = 32ull << 20;
     static constexpr int kWindow = 2;
 
-    CopyEngine(cudaStream_t stream, int device);
+    // staging_bytes > 0: XB12 records land in kStaging HBM buffers of that size and a decode stream
+    // expands them into the destination (the tile's `done` event follows the decode)
+    CopyEngine(cudaStream_t stream, int device, size_t staging_bytes = 0);
     ~CopyEngine();
 
-    std::shared_ptr<CopyJob> make_job(unsigned char* dst, const unsigned char* src, size_t tile_bytes, int tiles);
+    std::shared_ptr<CopyJob> make_job(unsigned char* dst, size_t tile_bytes, std::vector<TileSource> srcs);
     void submit(const std::shared_ptr<CopyJob>& job, bool on_demand);
     void promote(const std::shared_ptr<CopyJob>& job, bool to_front);
     // Drop tiles not yet handed to the DMA engine (their data is no longer needed).
@@ -104,6 +117,12 @@ private:
 
     cudaStream_t stream_;
     int device_;
+    static constexpr int kStaging = 3;
+    cudaStream_t decode_stream_ = nullptr;
+    void* staging_[kStaging] = {};
+    size_t staging_bytes_ = 0;
+    cudaEvent_t staging_landed_[kStaging] = {}, staging_free_[kStaging] = {};
+    int staging_next_ = 0;
     std::mutex mu_;
     std::condition_variable cv_work_, cv_issued_;
     std::deque<std::shared_ptr<CopyJob>> od_, pf_;
@@ -114,6 +133,7 @@ private:
     bool busy_ = false;
     std::string error_;  // first error of the copy thread (it stops issuing)
     std::atomic<long long> tiles_copied_{0}, bytes_copied_{0};
+    long long issue_counter_ = 0;  // guarded by mu_
     double busy_ms_ = 0.0, busy_pf_ms_ = 0.0, busy_pf_used_ms_ = 0.0;
     long long pf_tiles_ = 0;
     cudaEvent_t origin_ = nullptr;

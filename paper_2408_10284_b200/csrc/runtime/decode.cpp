@@ -159,7 +159,8 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
         // gate-decided layers (free-running, moe_decode_layer without scores) emit their scores here
         d_free_scores_.reserve(static_cast<size_t>(4) * batch_ * N * sizeof(double));
     }
-    copier_ = std::make_unique<CopyEngine>(eng.copy_stream(), eng.device());
+    copier_ = std::make_unique<CopyEngine>(eng.copy_stream(), eng.device(),
+                                           store_.format == kStoreXb12 ? store_.max_record_bytes() : 0);
     // last: the constructor performs the initial fill through on_insert
     policy_ = std::make_unique<PolicyEngine>(spec_, cfg_, caps_, seed, total_tokens, this, true);
     MOE_CUDA(cudaDeviceSynchronize());
@@ -331,7 +332,12 @@ void DecodeSession::on_request(int id, ExpertRef ref, bool on_demand) {
     }
     const int s = take_slot();
     req_slot_[id] = s;
-    auto job = copier_->make_job(slot_ptr(s), store_.expert(ref.layer, ref.expert), store_.tile_bytes, store_.tiles);
+    std::vector<TileSource> srcs(store_.tiles);
+    for (int t = 0; t < store_.tiles; ++t) {
+        srcs[t].src = store_.record(ref.layer, ref.expert, t, &srcs[t].bytes);
+        srcs[t].meta = store_.meta(ref.layer, ref.expert, t);
+    }
+    auto job = copier_->make_job(slot_ptr(s), store_.tile_bytes, std::move(srcs));
     job->serial = job_serial_++;
     job->token = cur_token_;
     job->layer = ref.layer;
@@ -358,8 +364,8 @@ void DecodeSession::on_insert(ExpertRef ref, int request, std::optional<int> evi
         if (!owned(ref.layer, ref.expert)) return;
         const int s = take_slot();
         // initial residency (pinned source), ordered before any compute-stream use of the slot
-        MOE_CUDA(cudaMemcpyAsync(slot_ptr(s), store_.expert(ref.layer, ref.expert), store_.expert_bytes,
-                                 cudaMemcpyHostToDevice, eng_.compute_stream()));
+        upload_expert_tiles(store_, ref.layer, ref.expert, 0, store_.tiles, slot_ptr(s), fill_staging_,
+                            eng_.compute_stream());
         slots_[s].fill.reset();
         slots_[s].fill_done = true;
         slot_of_[key] = s;
@@ -395,7 +401,38 @@ void DecodeSession::on_tile_compute(int, ExpertRef ref, int rank, int tile, int 
     uses_.back().tiles.push_back(tile);
 }
 
+void DecodeSession::flush_waits() {
+    if (deferred_waits_.empty()) return;
+    struct W {
+        long long seq;
+        int slot, tile;
+    };
+    std::vector<W> ws;
+    for (const auto& [slot, tile] : deferred_waits_) {  // needed now: promote what is still queued
+        Slot& sl = slots_[slot];
+        if (sl.fill && !sl.fill_done && !copier_->fully_issued(sl.fill)) copier_->promote(sl.fill, true);
+    }
+    for (const auto& [slot, tile] : deferred_waits_) {
+        Slot& sl = slots_[slot];
+        if (!sl.fill || sl.fill_done) continue;
+        const int t0 = tile < 0 ? 0 : tile, t1 = tile < 0 ? sl.fill->tiles : tile + 1;
+        for (int t = t0; t < t1; ++t) {
+            copier_->wait_issued(sl.fill, t);
+            ws.push_back(W{sl.fill->issue_seq[t], slot, t});
+        }
+    }
+    deferred_waits_.clear();
+    std::sort(ws.begin(), ws.end(), [](const W& a, const W& b) { return a.seq < b.seq; });
+    defer_waits_ = false;
+    for (const W& w : ws) wait_fill(w.slot, w.tile);
+    defer_waits_ = true;
+}
+
 void DecodeSession::wait_fill(int slot, int tile) {
+    if (defer_waits_) {
+        deferred_waits_.emplace_back(slot, tile);
+        return;
+    }
     Slot& sl = slots_[slot];
     if (!sl.fill || sl.fill_done) return;
     const int t0 = tile < 0 ? 0 : tile, t1 = tile < 0 ? sl.fill->tiles : tile + 1;
@@ -447,6 +484,7 @@ void DecodeSession::ep_exchange(float* out, long long rows, long long row_stride
 void DecodeSession::timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int>>& seg_meta,
                               std::vector<std::tuple<int, int, FfnPartialRef>>& refs) {
     cudaStream_t cs = eng_.compute_stream();
+    flush_waits();
     const size_t region = static_cast<size_t>(kFfnMaxCtas) * kFfnSlotsPerCta * spec_.hidden_dim;
     if (partial_next_ >= partial_regions_) fail(Status::Internal, "decode: FFN partial pool exhausted");
     p.partial = d_partials_.as<float>() + region * partial_next_++;
@@ -470,10 +508,13 @@ void DecodeSession::timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int
 }
 
 void DecodeSession::on_layer_done(int, int, const RouteDecision& d) {
+    defer_waits_ = layer_launch();
     if (batch_ > 1)
         layer_ffn_grouped(d);
     else
         layer_ffn_single(d);
+    flush_waits();  // (nothing left unless the layer launched nothing)
+    defer_waits_ = false;
     uses_.clear();
     cudaEvent_t ev;
     if (layer_event_pool_.empty()) {
@@ -701,6 +742,7 @@ void DecodeSession::layer_ffn_single(const RouteDecision& d) {
 
 void DecodeSession::timed_grouped(GroupedLaunch& p, bool down, const RouteDecision& u) {
     cudaStream_t cs = eng_.compute_stream();
+    flush_waits();
     cudaEvent_t e0 = take_timing(), e1 = take_timing();
     MOE_CUDA(cudaEventRecord(e0, cs));
     MOE_CUDA(down ? launch_grouped_down(p, sm_count_, cs) : launch_grouped_gate_up(p, sm_count_, cs));

@@ -114,6 +114,12 @@ private:
     void release_slot(int s);
     void release_pending(bool all);
     void wait_fill(int slot, int tile);  // compute stream waits for tile (or all tiles if -1)
+    // "layer" launches wait for every tile of the layer before one launch: the waits are collected
+    // and enqueued in the order the tiles cross the (serial) link, so each wait's stall is the gap
+    // to the next landing and is charged to the tile that really gates the launch
+    bool defer_waits_ = false;
+    std::vector<std::pair<int, int>> deferred_waits_;
+    void flush_waits();
     // launch + time + clear the segment list; records where each (rank, tile) partial lives
     void timed_ffn(FfnLaunch& p, const std::vector<std::pair<int, int>>& seg_meta,
                    std::vector<std::tuple<int, int, FfnPartialRef>>& refs);
@@ -200,6 +206,7 @@ private:
 
     // slots
     DeviceBuffer pool_;
+    DeviceBuffer fill_staging_;  // XB12 records of the initial residency (decoded on the compute stream)
     size_t slot_stride_ = 0;
     int n_slots_ = 0;
     int resident_slots_ = 0;

@@ -53,7 +53,11 @@ Engine::Engine(const ModelSpec& spec, int device) : spec_(spec), device_(device)
     cudaDeviceProp prop{};
     MOE_CUDA(cudaGetDeviceProperties(&prop, device));
     if (prop.major != 10) fail(Status::Device, std::string("built for sm_100a (B200); found ") + prop.name);
-    MOE_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
+    // the compute stream (router, FFN, combine) outranks background work (the XB12 decode stream)
+    // when both want SMs
+    int least = 0, greatest = 0;
+    MOE_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    MOE_CUDA(cudaStreamCreateWithPriority(&compute_, cudaStreamNonBlocking, greatest));
     MOE_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
 }
 

@@ -118,6 +118,8 @@ public:
     std::unique_ptr<ExpertStore> experts;
     std::unique_ptr<DecodeSession> session;
     DeviceBuffer ffn_scratch;  // K2 partials of moe_expert_ffn_async (stream-ordered reuse)
+    DeviceBuffer copy_staging; // XB12 records of moe_copy_tiles / moe_expert_ffn (stream-ordered reuse)
+    int store_format = 0;      // format of the next expert store (moe_experts_set_format)
 
 private:
     ModelSpec spec_;

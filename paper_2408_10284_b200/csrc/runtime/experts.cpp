@@ -16,9 +16,23 @@
 #include <thread>
 
 #include "../kernels/expert_ffn.hpp"
+#include "../kernels/xb12.hpp"
 #include "engine.hpp"
 
 namespace adapmoe {
+
+const unsigned char* ExpertStore::record(int layer, int expert, int tile, size_t* bytes) const {
+    const int b = stored_index(layer, expert);
+    const size_t k = static_cast<size_t>(b) * tiles + tile;
+    if (bytes) *bytes = tile_meta[k].format == 1 ? tile_meta[k].bytes : tile_bytes;
+    return blocks[b] + tile_off[k];
+}
+
+size_t ExpertStore::max_record_bytes() const {
+    size_t m = 0;
+    for (const Xb12Tile& t : tile_meta) m = std::max(m, t.format == 1 ? static_cast<size_t>(t.bytes) : tile_bytes);
+    return m;
+}
 
 int ExpertStore::stored_index(int layer, int expert) const {
     const int b = index[static_cast<size_t>(layer) * experts + expert];
@@ -82,8 +96,118 @@ void expert_init_constants(std::uint64_t seed, int layer, int expert, int d, int
     scale[2] = static_cast<float>(1.0 / (37837.22 * std::sqrt(static_cast<double>(ffn))));
 }
 
+namespace {
+
+// The raw layout: tile t of every block at t * tile_bytes (kStoreBf16, and an XB12 store before
+// its experts are encoded).
+void raw_tile_layout(ExpertStore& st) {
+    const size_t nb = st.blocks.size();
+    st.tile_meta.assign(nb * st.tiles, Xb12Tile{});
+    st.tile_off.assign(nb * st.tiles, 0);
+    for (size_t b = 0; b < nb; ++b)
+        for (int t = 0; t < st.tiles; ++t) {
+            Xb12Tile& m = st.tile_meta[b * st.tiles + t];
+            m.format = 0;
+            m.n = st.tile_bytes / 2;
+            m.bytes = st.tile_bytes;
+            st.tile_off[b * st.tiles + t] = static_cast<size_t>(t) * st.tile_bytes;
+        }
+    st.link_bytes = nb * st.expert_bytes;
+}
+
+// Encode one expert (raw tile-major bf16 in device memory) into stored block b as XB12 records;
+// a tile whose escapes exceed n / 64 stays raw.  Synchronous on `s`.
+struct Xb12Scratch {
+    DeviceBuffer rec, work;
+};
+void encode_block(ExpertStore& st, int b, const std::uint16_t* d_raw, Xb12Scratch& x, cudaStream_t s) {
+    const std::uint64_t n = st.tile_bytes / 2, cap = n / 64;
+    const size_t lo_nib = xb12_align(xb12_align(n) + n / 2);
+    const size_t region = lo_nib + cap * 8;
+    x.rec.reserve(region * st.tiles);
+    x.work.reserve(static_cast<size_t>(kXb12WorkWords) * st.tiles * sizeof(std::uint32_t));
+    for (int t = 0; t < st.tiles; ++t) {
+        unsigned char* r = x.rec.as<unsigned char>() + region * t;
+        MOE_CUDA(xb12_encode(d_raw + n * t, n, r, r + xb12_align(n), reinterpret_cast<std::uint64_t*>(r + lo_nib), cap,
+                             x.work.as<std::uint32_t>() + static_cast<size_t>(kXb12WorkWords) * t, s));
+    }
+    std::vector<std::uint32_t> work(static_cast<size_t>(kXb12WorkWords) * st.tiles);
+    MOE_CUDA(cudaMemcpyAsync(work.data(), x.work.ptr, work.size() * sizeof(std::uint32_t), cudaMemcpyDeviceToHost, s));
+    MOE_CUDA(cudaStreamSynchronize(s));
+    size_t off = 0;
+    std::vector<std::uint64_t> exc;
+    for (int t = 0; t < st.tiles; ++t) {
+        Xb12Tile& m = st.tile_meta[static_cast<size_t>(b) * st.tiles + t];
+        const std::uint32_t* w = work.data() + static_cast<size_t>(kXb12WorkWords) * t;
+        m = Xb12Tile{};
+        m.n = n;
+        m.base = w[256];
+        m.n_exc = w[257];
+        unsigned char* dst = st.blocks[b] + off;
+        st.tile_off[static_cast<size_t>(b) * st.tiles + t] = off;
+        if (m.n_exc > cap) {  // does not pay: keep the raw tile
+            m.format = 0;
+            m.bytes = st.tile_bytes;
+            MOE_CUDA(cudaMemcpyAsync(dst, d_raw + n * t, st.tile_bytes, cudaMemcpyDeviceToHost, s));
+        } else {
+            m.format = 1;
+            xb12_layout(m);
+            const unsigned char* r = x.rec.as<unsigned char>() + region * t;
+            MOE_CUDA(cudaMemcpyAsync(dst, r, m.exc_off, cudaMemcpyDeviceToHost, s));
+            exc.resize(m.n_exc);
+            if (m.n_exc) {
+                MOE_CUDA(cudaMemcpyAsync(exc.data(), r + lo_nib, m.n_exc * 8, cudaMemcpyDeviceToHost, s));
+                MOE_CUDA(cudaStreamSynchronize(s));
+                std::sort(exc.begin(), exc.end());  // ascending index (the escapes arrive unordered)
+                std::memcpy(dst + m.exc_off, exc.data(), m.n_exc * 8);
+            }
+        }
+        off += m.format == 1 ? m.bytes : st.tile_bytes;
+        if (off > st.expert_bytes) fail(Status::Internal, "xb12: records exceed the expert block");
+    }
+    MOE_CUDA(cudaStreamSynchronize(s));
+}
+
+void recount_link_bytes(ExpertStore& st) {
+    st.link_bytes = 0;
+    for (const Xb12Tile& m : st.tile_meta) st.link_bytes += m.format == 1 ? m.bytes : st.tile_bytes;
+}
+
+}  // namespace
+
+void upload_expert_tiles(const ExpertStore& st, int layer, int expert, int t0, int t1, unsigned char* dst,
+                         DeviceBuffer& staging, cudaStream_t stream, cudaEvent_t const* tile_done) {
+    for (int t = t0; t < t1; ++t) {
+        size_t bytes = 0;
+        const unsigned char* rec = st.record(layer, expert, t, &bytes);
+        unsigned char* out = dst + static_cast<size_t>(t) * st.tile_bytes;
+        const Xb12Tile& m = st.meta(layer, expert, t);
+        if (m.format == 0) {
+            MOE_CUDA(cudaMemcpyAsync(out, rec, bytes, cudaMemcpyHostToDevice, stream));
+        } else {
+            staging.reserve(st.max_record_bytes());
+            MOE_CUDA(cudaMemcpyAsync(staging.ptr, rec, bytes, cudaMemcpyHostToDevice, stream));
+            MOE_CUDA(xb12_decode(staging.as<std::uint8_t>(), m, reinterpret_cast<std::uint16_t*>(out), stream));
+        }
+        if (tile_done && tile_done[t - t0]) MOE_CUDA(cudaEventRecord(tile_done[t - t0], stream));
+    }
+}
+
+void read_expert_host(const ExpertStore& st, int layer, int expert, std::uint16_t* out) {
+    for (int t = 0; t < st.tiles; ++t) {
+        size_t bytes = 0;
+        const unsigned char* rec = st.record(layer, expert, t, &bytes);
+        std::uint16_t* o = out + st.tile_bytes / 2 * t;
+        const Xb12Tile& m = st.meta(layer, expert, t);
+        if (m.format == 0)
+            std::memcpy(o, rec, st.tile_bytes);
+        else
+            xb12_decode_host(rec, m, o, 0, m.n);
+    }
+}
+
 void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::uint64_t seed, int alias,
-                        bool init_values, const int* owner, int rank) {
+                        bool init_values, const int* owner, int rank, int format) {
     const ModelSpec& spec = eng.spec();
     if (ffn <= 0 || tiles < 1 || ffn % tiles) fail(Status::Usage, "experts_init: ffn must be a positive multiple of tiles");
     const int ft = ffn / tiles;
@@ -150,7 +274,30 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
         if (!e.empty()) fail(Status::Device, "experts_init: " + e);
     auto t1 = std::chrono::steady_clock::now();
     st.pin_seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (format != kStoreBf16 && format != kStoreXb12) fail(Status::Usage, "experts_init: unknown store format");
+    if (format == kStoreXb12 && (st.tile_bytes / 2) % 16) fail(Status::Usage, "xb12 store: tile values must be a multiple of 16");
+    st.format = format;
+    raw_tile_layout(st);
     if (!init_values) return;
+    if (format == kStoreXb12) {  // GPU init kernel -> XB12 encode on the device -> D2H records
+        DeviceBuffer raw;
+        raw.reserve(st.expert_bytes);
+        Xb12Scratch x;
+        cudaStream_t s;
+        MOE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        for (int i = 0; i < stored; ++i) {
+            const int layer = first_id[i] / spec.experts_per_layer, expert = first_id[i] % spec.experts_per_layer;
+            std::uint64_t base[3];
+            float scale[3];
+            expert_init_constants(seed, layer, expert, spec.hidden_dim, ffn, base, scale);
+            MOE_CUDA(launch_expert_init(raw.as<std::uint16_t>(), spec.hidden_dim, ffn, tiles, base, scale, s));
+            encode_block(st, i, raw.as<std::uint16_t>(), x, s);
+        }
+        cudaStreamDestroy(s);
+        recount_link_bytes(st);
+        st.fill_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+        return;
+    }
     // fill: GPU init kernel into two device scratch blocks, D2H into the pinned store
     DeviceBuffer scratch[2];
     cudaStream_t s[2];
@@ -177,13 +324,16 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
     st.fill_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
 }
 
-void set_expert_weights(ExpertStore& st, int layer, int expert, const std::uint16_t* w1, const std::uint16_t* w3,
-                        const std::uint16_t* w2) {
+void set_expert_weights(Engine& eng, ExpertStore& st, int layer, int expert, const std::uint16_t* w1,
+                        const std::uint16_t* w3, const std::uint16_t* w2) {
     if (layer < 0 || layer >= st.layers || expert < 0 || expert >= st.experts) fail(Status::Usage, "ExpertRef out of range");
     if (st.alias > 0) fail(Status::Usage, "expert_set: the store aliases experts (host_alias); allocate it without");
     if (!st.has(layer, expert)) fail(Status::Usage, "expert_set: this store (an expert-parallel shard) does not hold the expert");
     const size_t D = st.d, F = st.ffn, Ft = F / st.tiles;
-    std::uint16_t* dst = reinterpret_cast<std::uint16_t*>(st.blocks[st.stored_index(layer, expert)]);
+    const int b = st.stored_index(layer, expert);
+    std::vector<std::uint16_t> packed;  // XB12: pack here, then encode into the block
+    if (st.format == kStoreXb12) packed.resize(st.expert_bytes / 2);
+    std::uint16_t* dst = st.format == kStoreXb12 ? packed.data() : reinterpret_cast<std::uint16_t*>(st.blocks[b]);
     const size_t tile_elems = 3 * Ft * D;
     auto pack_rows = [&](size_t f0, size_t f1) {
         constexpr size_t kB = 64;  // W2 transposed in kB x kB blocks (both sides cache friendly)
@@ -206,6 +356,16 @@ void set_expert_weights(ExpertStore& st, int layer, int expert, const std::uint1
     for (size_t k = 1; k < n; ++k) pool.emplace_back(pack_rows, F * k / n, F * (k + 1) / n);
     pack_rows(0, F / n);
     for (auto& th : pool) th.join();
+    if (st.format == kStoreXb12) {
+        eng.activate();
+        DeviceBuffer raw;
+        raw.reserve(st.expert_bytes);
+        Xb12Scratch x;
+        cudaStream_t s = eng.copy_stream();
+        MOE_CUDA(cudaMemcpyAsync(raw.ptr, packed.data(), st.expert_bytes, cudaMemcpyHostToDevice, s));
+        encode_block(st, b, raw.as<std::uint16_t>(), x, s);
+        recount_link_bytes(st);
+    }
 }
 
 }  // namespace adapmoe

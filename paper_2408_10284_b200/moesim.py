@@ -330,18 +330,38 @@ class Engine:
         return w
 
     # -- physical decode -----------------------------------------------------------------------
+    STORE_FORMATS = {"bf16": 0, "xb12": 1}
+
     def experts_init(self, ffn_dim: int, tiles: int, seed: int = 0, host_alias: int = 0, expert_owner=None,
-                     rank: int = 0):
+                     rank: int = 0, store_format: str = "bf16"):
         """Pinned host expert store with the deterministic init.  expert_owner ([L][N] shard table) +
-        rank: an expert-parallel shard's store, holding only the experts it owns."""
+        rank: an expert-parallel shard's store, holding only the experts it owns.  store_format
+        "xb12": lossless exponent-coded tiles (moe_experts_set_format)."""
+        check(load().moe_experts_set_format(self._h, self.STORE_FORMATS[store_format]))
         if expert_owner is None:
             check(load().moe_experts_init(self._h, ffn_dim, tiles, seed, host_alias))
         else:
             own = np.ascontiguousarray(expert_owner, dtype=np.int32).reshape(-1)
             check(load().moe_experts_init_shard(self._h, ffn_dim, tiles, seed, host_alias, _p(own, _capi._i32), rank))
 
-    def experts_alloc(self, ffn_dim: int, tiles: int, expert_owner=None, rank: int = 0):
+    def experts_format(self) -> tuple[str, int]:
+        """(store format, bytes a copy of every stored record moves over the host link)."""
+        f, b = C.c_int32(), C.c_int64()
+        check(load().moe_experts_format(self._h, C.byref(f), C.byref(b)))
+        return {v: k for k, v in self.STORE_FORMATS.items()}[f.value], b.value
+
+    def expert_tile_record(self, layer: int, expert: int, tile: int) -> dict:
+        """Host address and XB12 metadata of one stored tile record (moe_expert_tile_record)."""
+        r, b, f, base, m, nib, esc = (C.c_void_p(), C.c_int64(), C.c_int32(), C.c_uint32(), C.c_int64(), C.c_int64(),
+                                      C.c_int64())
+        check(load().moe_expert_tile_record(self._h, layer, expert, tile, C.byref(r), C.byref(b), C.byref(f),
+                                            C.byref(base), C.byref(m), C.byref(nib), C.byref(esc)))
+        return {"ptr": int(r.value), "bytes": b.value, "format": f.value, "base": base.value, "n_escapes": m.value,
+                "nib_offset": nib.value, "esc_offset": esc.value}
+
+    def experts_alloc(self, ffn_dim: int, tiles: int, expert_owner=None, rank: int = 0, store_format: str = "bf16"):
         """Pinned store for real weights (moe_experts_alloc); fill it with expert_set."""
+        check(load().moe_experts_set_format(self._h, self.STORE_FORMATS[store_format]))
         if expert_owner is None:
             check(load().moe_experts_alloc(self._h, ffn_dim, tiles))
         else:

@@ -348,6 +348,29 @@ def cpu_ffn_baseline(eng, wl, trace, tau, cfg, tok0: int, n_tok: int, gpu_out):
             "host_read_gbs": moved / dt / 1e9, "max_rel_diff_vs_gpu": rel}
 
 
+def static_config(args, wl, ws):
+    """The bench line's `config`: everything fixed by the command line and the workload (shape, batch,
+    budget, mode, store format, parallelism) — identical in both arms.  Values the pipeline derives
+    (tau, DP capacities, store sizes) go to the line's `derived` object."""
+    B = args.batch
+    ep_world = ws if ((args.ep or ws > 1) and not args.replicas) else 1
+    if ep_world > 1:
+        place = ("experts placed by a calibration trace (ep.balanced_owners)" if args.ep_owner == "balanced"
+                 else f"expert e on rank e % {ws}")
+        comb = "P2P stores into peer memory from the combine epilogue" if args.ep_exchange == "p2p" else "all_gather"
+        par = f"ep{ws} ({place}; combine: {comb})"
+    else:
+        par = f"replicas x{ws}"
+    return {"workload": f"{wl.name} batch-{B} decode, HBM expert cache {wl.budget}/{wl.layers * wl.experts} experts "
+                        f"(DP), experts offloaded to pinned host memory" +
+                        (f"; {B} token streams share the cache (union policy), grouped tcgen05 FFN" if B > 1 else ""),
+            "batch": B, "mode": "free-running" if args.free_running else "trace-replay",
+            "layers": wl.layers, "experts": wl.experts, "top_k": wl.top_k, "hidden": wl.hidden, "ffn": wl.ffn,
+            "budget": wl.budget, "tiles": wl.tiles, "lookahead": wl.lookahead, "trace_tokens": wl.tokens,
+            "store_format": args.store_format, "parallelism": par,
+            "l2": "no flush needed: resident experts (>=22 GB) >> 126 MB L2"}
+
+
 def reference_arm(args):
     ws, rank, _ = dist_init()
     if rank != 0:
@@ -365,8 +388,9 @@ def reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * per_rep / r["tokens"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp64", "data": "synthetic",
-        "config": {"workload": wl.name, "layers": wl.layers, "experts": wl.experts, "hidden": wl.hidden,
-                   "budget": wl.budget, "tokens": r["tokens"]},
+        "config": static_config(args, wl, ws),
+        "reference_sample": {"tokens": r["tokens"], "what": "the reference simulate_trace over the same trace "
+                             "(stream 0 at batch > 1: the reference is batch-1)"},
         "on_demand_loads_per_token": r["on_demand_loads"] / r["tokens"],
         "cpu_baseline": {"value": value, "unit": "tok/s", "cores": 1, "kind": "reference",
                          "sample": f"moesim simulate_trace over the {r['tokens']}-token trace, best of "
@@ -647,21 +671,11 @@ def ours(args):
         "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic: reference generator (demo8 settings) trace + counter-based random-init "
                                  "bf16 experts",
-        "config": {"workload": f"{wl.name} batch-{B} decode, HBM expert cache {wl.budget}/{wl.layers * wl.experts} experts "
-                               f"(DP), experts offloaded to pinned host memory" +
-                               (f"; {B} token streams share the cache (union policy), grouped tcgen05 FFN" if B > 1 else ""),
-                   "batch": B, "mode": "free-running" if args.free_running else "trace-replay",
-                   "layers": wl.layers, "experts": wl.experts, "top_k": wl.top_k, "hidden": wl.hidden, "ffn": wl.ffn,
-                   "budget": wl.budget, "tiles": wl.tiles, "lookahead": wl.lookahead, "trace_tokens": wl.tokens,
-                   "tau": tau, "realized_single_ratio": realized, "capacities": [int(c) for c in caps],
-                   "dp_expected_loads_per_token": exp_loads, "host_alias": alias,
-                   "expert_store_per_rank": per_rank_store,
-                   "store_format": store_fmt,
-                   "store_link_bytes_per_expert": store_link_bytes / max(1, held),
-                   "parallelism": (f"ep{ws} ({'experts placed by a calibration trace (ep.balanced_owners)' if owners is not None else f'expert e on rank e % {ws}'}; combine: "
-                                   f"{'P2P stores into peer memory from the combine epilogue' if p2p else 'all_gather'})"
-                                   if ep_world > 1 else f"replicas x{ws}"),
-                   "l2": "no flush needed: resident experts (>=22 GB) >> 126 MB L2"},
+        "config": static_config(args, wl, ws),
+        "derived": {"tau": tau, "realized_single_ratio": realized, "capacities": [int(c) for c in caps],
+                    "dp_expected_loads_per_token": exp_loads, "host_alias": alias,
+                    "expert_store_per_rank": per_rank_store, "store_format": store_fmt,
+                    "store_link_bytes_per_expert": store_link_bytes / max(1, held)},
         "on_demand_loads_per_token": od_timed / K,
         "experts_activated_per_token": act_timed / K,
         "on_demand_loads_per_token_session": res.metrics["on_demand_loads"] / decoded,

@@ -22,29 +22,60 @@ static inline float bf16(uint16_t v) {
     return c.f;
 }
 
-/* XB12 records (paper_2408_10284_b200/csrc/kernels/xb12.hpp) decoded on the fly: values
+/* XB12 / XBH records (paper_2408_10284_b200/csrc/kernels/xb12.hpp, xbh.hpp) decoded on the fly: values
  * [i0, i0 + n) of one tile record into bf16 (pairs share a nibble byte: vectorisable), then the
  * escapes that fall in the range (ascending list, binary search). */
 typedef struct {
     const uint8_t* rec;
-    int32_t format; /* 0 raw bf16, 1 XB12 */
+    int32_t format; /* 0 raw bf16, 1 XB12, 2 XBH */
     uint32_t base;
     int64_t n_exc, nib_off, exc_off;
+    int64_t n; /* values in the tile */
 } tile_rec;
+
+/* XBH (kernels/xbh.hpp): sections at offsets derived from n; segments of 512 values, each walked
+ * from its bit offset with a 12-bit peek into the decode table. */
+#define XBH_SEG 512
+#define XBH_MAXLEN 12
+static int64_t al16(int64_t v) { return (v + 15) / 16 * 16; }
+static void decode_xbh(const tile_rec* t, int64_t i0, int64_t n, uint16_t* dst) {
+    const int64_t N = t->n, lut_off = al16(N), seg_off = lut_off + 2 * (1 << XBH_MAXLEN);
+    const int64_t bits_off = al16(seg_off + 4 * ((N + XBH_SEG - 1) / XBH_SEG + 1));
+    const uint16_t* lut = (const uint16_t*)(t->rec + lut_off);
+    const uint32_t* seg = (const uint32_t*)(t->rec + seg_off);
+    const uint32_t* w = (const uint32_t*)(t->rec + bits_off);
+    const int64_t end = i0 + n;
+    for (int64_t s = i0 / XBH_SEG; s * XBH_SEG < end; ++s) {
+        uint64_t pos = seg[s];
+        const int64_t v1 = end < (s + 1) * XBH_SEG ? end : (s + 1) * XBH_SEG;
+        for (int64_t i = s * XBH_SEG; i < v1; ++i) {
+            const uint64_t win = ((uint64_t)w[pos >> 5] << 32) | w[(pos >> 5) + 1];
+            const uint32_t e = lut[(win << (pos & 31)) >> (64 - XBH_MAXLEN)];
+            pos += e >> 8;
+            if (i < i0) continue;
+            const uint32_t b = t->rec[i];
+            dst[i - i0] = (uint16_t)(((b & 0x80u) << 8) | ((e & 0xffu) << 7) | (b & 0x7fu));
+        }
+    }
+}
 
 static void decode_range(const tile_rec* t, int64_t i0, int64_t n, uint16_t* dst) {
     if (t->format == 0) {
         memcpy(dst, (const uint16_t*)t->rec + i0, (size_t)n * 2);
         return;
     }
-    const uint8_t* lo = t->rec + i0;
-    const uint8_t* nib = t->rec + t->nib_off + i0 / 2; /* i0 even */
-    const uint32_t base = t->base;
-    for (int64_t j = 0; j < n / 2; ++j) {
-        const uint32_t c = nib[j], b0 = lo[2 * j], b1 = lo[2 * j + 1];
-        const uint32_t e0 = (base + (c & 15u)) & 0xffu, e1 = (base + (c >> 4)) & 0xffu;
-        dst[2 * j] = (uint16_t)(((b0 & 0x80u) << 8) | (e0 << 7) | (b0 & 0x7fu));
-        dst[2 * j + 1] = (uint16_t)(((b1 & 0x80u) << 8) | (e1 << 7) | (b1 & 0x7fu));
+    if (t->format == 2) {
+        decode_xbh(t, i0, n, dst);
+    } else {
+        const uint8_t* lo = t->rec + i0;
+        const uint8_t* nib = t->rec + t->nib_off + i0 / 2; /* i0 even */
+        const uint32_t base = t->base;
+        for (int64_t j = 0; j < n / 2; ++j) {
+            const uint32_t c = nib[j], b0 = lo[2 * j], b1 = lo[2 * j + 1];
+            const uint32_t e0 = (base + (c & 15u)) & 0xffu, e1 = (base + (c >> 4)) & 0xffu;
+            dst[2 * j] = (uint16_t)(((b0 & 0x80u) << 8) | (e0 << 7) | (b0 & 0x7fu));
+            dst[2 * j + 1] = (uint16_t)(((b1 & 0x80u) << 8) | (e1 << 7) | (b1 & 0x7fu));
+        }
     }
     const uint64_t* exc = (const uint64_t*)(t->rec + t->exc_off);
     int64_t a = 0, b = t->n_exc;
@@ -55,7 +86,8 @@ static void decode_range(const tile_rec* t, int64_t i0, int64_t n, uint16_t* dst
     for (; a < t->n_exc && (int64_t)(exc[a] >> 16) < i0 + n; ++a) dst[(exc[a] >> 16) - i0] = (uint16_t)(exc[a] & 0xffffu);
 }
 
-/* The same layer as cpu_moe_layer over XB12 stores: recs[k * tiles + t] = tile t of selected expert k. */
+/* The same layer as cpu_moe_layer over coded stores (XB12 / XBH records, or raw tiles):
+ * recs[k * tiles + t] = tile t of selected expert k. */
 int cpu_moe_layer_xb12(const void* const* recs, const int32_t* formats, const uint32_t* bases, const int64_t* n_exc,
                        const int64_t* nib_off, const int64_t* exc_off, const double* weights, int n_experts, int D,
                        int F, int tiles, const double* x_in, float* out, int threads) {
@@ -80,7 +112,8 @@ int cpu_moe_layer_xb12(const void* const* recs, const int32_t* formats, const ui
             for (int r = r0; r < r1; ++r) {
                 const int ti = r / Ft, rr = r % Ft;
                 const size_t q = (size_t)k * tiles + ti;
-                const tile_rec tr = {(const uint8_t*)recs[q], formats[q], bases[q], n_exc[q], nib_off[q], exc_off[q]};
+                const tile_rec tr = {(const uint8_t*)recs[q], formats[q], bases[q], n_exc[q], nib_off[q], exc_off[q],
+                                     (int64_t)3 * Ft * D};
                 decode_range(&tr, (int64_t)rr * 2 * D, 2 * (int64_t)D, w1); /* W1 row then W3 row */
                 decode_range(&tr, (int64_t)2 * Ft * D + (int64_t)rr * D, D, w2);
                 float a = 0.0f, b = 0.0f;

@@ -77,9 +77,10 @@ def parse():
     ap.add_argument("--timeline", default=None,
                     help="record the physical timeline (CUDA-event tile copies, FFN launches, waits, router) over the "
                          "e2e window, write it as JSONL to this path and run the reference's timeline validators")
-    ap.add_argument("--store-format", default="xb12", choices=["bf16", "xb12"],
-                    help="pinned expert store: raw bf16 tiles, or XB12 (lossless exponent-coded bf16: 75 %% of the "
-                         "bytes over the host link, decoded into the HBM slot on arrival; identical outputs)")
+    ap.add_argument("--store-format", default="xbh", choices=["bf16", "xb12", "xbh"],
+                    help="pinned expert store: raw bf16 tiles, XB12 (lossless exponent-coded bf16, 4-bit window "
+                         "codes: 75 %% of the bytes over the host link) or XBH (per-tile Huffman-coded exponents: "
+                         "~66 %%); coded tiles are decoded into the HBM slot on arrival; identical outputs")
     ap.add_argument("--host-alias", type=int, default=None,
                     help="store only this many distinct experts in host memory (profiling runs; same bytes moved)")
     return ap.parse_args()

@@ -296,14 +296,20 @@ int moe_experts_alloc_shard(moe_engine_t engine, int32_t ffn_dim, int32_t tiles,
  * weights.  Lossless: tiles land in an HBM staging buffer and a decode kernel restores the exact bf16
  * bits in the slot before anything reads them, so every output and trace is bit-identical to the
  * bf16 store; the host link moves 25 % fewer bytes.  A tile that would not shrink (> n/64 escapes)
- * stays raw.  moe_expert_read decodes; moe_expert_host_ptr needs a bf16 store. */
+ * stays raw.  MOE_STORE_XBH keeps each tile as an XBH record (kernels/xbh.hpp): the same sign +
+ * mantissa bytes, the exponents Huffman-coded per tile (canonical, length-limited to 12 bits,
+ * 512-value independently decodable segments), ~66 % of the bytes — same lossless contract, same
+ * raw fallback.  moe_expert_read decodes; moe_expert_host_ptr needs a bf16 store. */
 #define MOE_STORE_BF16 0
 #define MOE_STORE_XB12 1
+#define MOE_STORE_XBH 2
 int moe_experts_set_format(moe_engine_t engine, int32_t format);
 /* Format of the current store and the bytes a copy of all its records moves over the host link. */
 int moe_experts_format(moe_engine_t engine, int32_t* format, int64_t* link_bytes);
-/* One tile's record in the pinned store: host address, bytes, format (0 raw bf16, 1 XB12), and for
- * XB12 the window base exponent, escape count and section offsets (lo at 0, nibbles, escapes). */
+/* One tile's record in the pinned store: host address, bytes, format (0 raw bf16, 1 XB12, 2 XBH), and
+ * for XB12 the window base exponent, escape count and section offsets (lo at 0, nibbles, escapes);
+ * for XBH the window base, escape count, the segment table's offset (nib_offset; the decode table
+ * and the code bits sit at the offsets xbh.hpp derives from the tile's value count) and the escapes'. */
 int moe_expert_tile_record(moe_engine_t engine, int32_t layer, int32_t expert, int32_t tile, const void** record,
                            int64_t* bytes, int32_t* format, uint32_t* base, int64_t* n_escapes, int64_t* nib_offset,
                            int64_t* esc_offset);

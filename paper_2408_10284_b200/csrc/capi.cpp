@@ -586,7 +586,8 @@ int moe_expert_ffn_async(moe_engine_t h, const void* expert, const double* x, fl
 int moe_experts_set_format(moe_engine_t h, int32_t format) {
     return guarded([&] {
         Engine& e = eng(h);
-        if (format != kStoreBf16 && format != kStoreXb12) fail(Status::Usage, "experts_set_format: unknown format");
+        if (format != kStoreBf16 && format != kStoreXb12 && format != kStoreXbh)
+            fail(Status::Usage, "experts_set_format: unknown format");
         e.store_format = format;
     });
 }
@@ -630,7 +631,7 @@ int moe_expert_host_ptr(moe_engine_t h, int32_t layer, int32_t expert, const voi
         if (layer < 0 || layer >= e.experts->layers || expert < 0 || expert >= e.experts->experts)
             fail(Status::Usage, "ExpertRef out of range");
         if (e.experts->format != kStoreBf16)
-            fail(Status::Usage, "expert_host_ptr: the store is XB12-coded (moe_expert_tile_record gives its records)");
+            fail(Status::Usage, "expert_host_ptr: the store is coded (XB12 / XBH; moe_expert_tile_record gives its records)");
         *ptr = e.experts->expert(layer, expert);
     });
 }

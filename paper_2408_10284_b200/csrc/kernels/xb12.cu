@@ -132,6 +132,14 @@ cudaError_t xb12_encode(const std::uint16_t* src, std::uint64_t n, std::uint8_t*
     return cudaGetLastError();
 }
 
+cudaError_t xb12_histogram(const std::uint16_t* src, std::uint64_t n, std::uint32_t* hist, cudaStream_t stream) {
+    if (n % 8 || !src || !hist) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(hist, 0, 256 * sizeof(std::uint32_t), stream);
+    if (e != cudaSuccess) return e;
+    hist_kernel<<<grid_for(n / 8), kThreads, 0, stream>>>(reinterpret_cast<const uint4*>(src), n / 8, hist);
+    return cudaGetLastError();
+}
+
 cudaError_t xb12_decode(const std::uint8_t* record, const Xb12Tile& t, std::uint16_t* dst, cudaStream_t stream) {
     if (t.format != 1 || t.n % 16) return cudaErrorInvalidValue;
     decode_kernel<<<grid_for(t.n / 16), kThreads, 0, stream>>>(reinterpret_cast<const uint4*>(record),

@@ -20,20 +20,26 @@
 
 #include <cstdint>
 
+#ifdef __CUDACC__
+#define XB_HD __host__ __device__
+#else
+#define XB_HD
+#endif
+
 namespace adapmoe {
 
 struct Xb12Tile {
-    int format = 0;               // 0 raw bf16 (the record is the tile), 1 XB12
+    int format = 0;               // 0 raw bf16 (the record is the tile), 1 XB12, 2 XBH (xbh.hpp)
     std::uint32_t base = 0;       // first exponent of the 15-exponent window
     std::uint64_t n = 0;          // values in the tile
     std::uint64_t n_exc = 0;      // escaped values
-    std::uint64_t nib_off = 0;    // byte offsets inside the record (lo at 0)
+    std::uint64_t nib_off = 0;    // byte offsets inside the record (lo at 0); XBH: the segment table
     std::uint64_t exc_off = 0;
     std::uint64_t bytes = 0;      // record bytes (256-aligned)
 };
 
 constexpr std::uint64_t kXb12Align = 256;
-inline std::uint64_t xb12_align(std::uint64_t v, std::uint64_t a = 16) { return (v + a - 1) / a * a; }
+XB_HD inline std::uint64_t xb12_align(std::uint64_t v, std::uint64_t a = 16) { return (v + a - 1) / a * a; }
 // record layout for n values with m escapes
 inline void xb12_layout(Xb12Tile& t) {
     t.nib_off = xb12_align(t.n);
@@ -47,6 +53,9 @@ inline void xb12_layout(Xb12Tile& t) {
 cudaError_t xb12_encode(const std::uint16_t* src, std::uint64_t n, std::uint8_t* lo, std::uint8_t* nib,
                         std::uint64_t* exc, std::uint64_t exc_cap, std::uint32_t* work, cudaStream_t stream);
 constexpr int kXb12WorkWords = 258;  // hist[256], base, escape count
+
+// Exponent histogram of n bf16 values (n % 8 == 0) into hist[256] (zeroed here).
+cudaError_t xb12_histogram(const std::uint16_t* src, std::uint64_t n, std::uint32_t* hist, cudaStream_t stream);
 
 // Decode (device): dst[i] = bf16 of (lo, nib) for every i, then the escapes patched.
 cudaError_t xb12_decode(const std::uint8_t* record, const Xb12Tile& t, std::uint16_t* dst, cudaStream_t stream);

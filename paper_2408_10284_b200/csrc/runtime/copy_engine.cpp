@@ -77,8 +77,8 @@ std::shared_ptr<CopyJob> CopyEngine::make_job(unsigned char* dst, size_t tile_by
     const int tiles = j->tiles;
     j->issue_seq.assign(tiles, -1);
     for (const TileSource& t : j->srcs)
-        if (t.meta.format == 1 && (!staging_bytes_ || t.bytes > staging_bytes_))
-            fail(Status::Internal, "copy engine: XB12 record larger than the staging buffers");
+        if (t.meta.format != 0 && (!staging_bytes_ || t.bytes > staging_bytes_))
+            fail(Status::Internal, "copy engine: coded record larger than the staging buffers");
     std::lock_guard<std::mutex> g(mu_);
     for (int t = 0; t < tiles; ++t) {
         j->done.push_back(take_event(false));
@@ -293,7 +293,7 @@ void CopyEngine::run() {
         NvtxRange copy_range("copy L%d E%d tile %d (%s)", job->layer, job->expert, tile, job->on_demand ? "od" : "pf");
         const TileSource& src = job->srcs[tile];
         unsigned char* out = job->dst + static_cast<size_t>(tile) * job->tile_bytes;
-        const bool coded = src.meta.format == 1;
+        const bool coded = src.meta.format != 0;
         const int k = coded ? staging_next_ : -1;
         if (coded) {  // the staging buffer is free once the decode that last read it has run
             staging_next_ = (staging_next_ + 1) % kStaging;
@@ -323,9 +323,11 @@ void CopyEngine::run() {
         if (coded) {  // decode on its own stream so the link never waits for it
             ck(cudaEventRecord(staging_landed_[k], stream_), "cudaEventRecord");
             ck(cudaStreamWaitEvent(decode_stream_, staging_landed_[k], 0), "cudaStreamWaitEvent");
-            ck(xb12_decode(static_cast<const std::uint8_t*>(staging_[k]), src.meta, reinterpret_cast<std::uint16_t*>(out),
-                           decode_stream_),
-               "xb12 decode");
+            const std::uint8_t* rec = static_cast<const std::uint8_t*>(staging_[k]);
+            std::uint16_t* dec = reinterpret_cast<std::uint16_t*>(out);
+            ck(src.meta.format == 2 ? xbh_decode(rec, src.meta, dec, decode_stream_)
+                                    : xb12_decode(rec, src.meta, dec, decode_stream_),
+               "tile record decode");
             ck(cudaEventRecord(job->done[tile], decode_stream_), "cudaEventRecord");
             ck(cudaEventRecord(staging_free_[k], decode_stream_), "cudaEventRecord");
         } else {

@@ -20,11 +20,13 @@
 #include <vector>
 
 #include "../kernels/xb12.hpp"
+#include "../kernels/xbh.hpp"
 
 namespace adapmoe {
 
 // One tile's source in the pinned store: raw bf16 (format 0, copied straight into the slot) or an
-// XB12 record (copied into an HBM staging buffer, then decoded into the slot, kernels/xb12.hpp).
+// XB12 / XBH record (copied into an HBM staging buffer, then decoded into the slot,
+// kernels/xb12.hpp, kernels/xbh.hpp).
 struct TileSource {
     const unsigned char* src = nullptr;
     size_t bytes = 0;

@@ -160,7 +160,7 @@ DecodeSession::DecodeSession(Engine& eng, std::span<const int> capacities, int s
         d_free_scores_.reserve(static_cast<size_t>(4) * batch_ * N * sizeof(double));
     }
     copier_ = std::make_unique<CopyEngine>(eng.copy_stream(), eng.device(),
-                                           store_.format == kStoreXb12 ? store_.max_record_bytes() : 0);
+                                           store_.format != kStoreBf16 ? store_.max_record_bytes() : 0);
     // last: the constructor performs the initial fill through on_insert
     policy_ = std::make_unique<PolicyEngine>(spec_, cfg_, caps_, seed, total_tokens, this, true);
     MOE_CUDA(cudaDeviceSynchronize());

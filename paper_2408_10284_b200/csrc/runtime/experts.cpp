@@ -17,6 +17,7 @@
 
 #include "../kernels/expert_ffn.hpp"
 #include "../kernels/xb12.hpp"
+#include "../kernels/xbh.hpp"
 #include "engine.hpp"
 
 namespace adapmoe {
@@ -24,13 +25,13 @@ namespace adapmoe {
 const unsigned char* ExpertStore::record(int layer, int expert, int tile, size_t* bytes) const {
     const int b = stored_index(layer, expert);
     const size_t k = static_cast<size_t>(b) * tiles + tile;
-    if (bytes) *bytes = tile_meta[k].format == 1 ? tile_meta[k].bytes : tile_bytes;
+    if (bytes) *bytes = tile_meta[k].format != 0 ? tile_meta[k].bytes : tile_bytes;
     return blocks[b] + tile_off[k];
 }
 
 size_t ExpertStore::max_record_bytes() const {
     size_t m = 0;
-    for (const Xb12Tile& t : tile_meta) m = std::max(m, t.format == 1 ? static_cast<size_t>(t.bytes) : tile_bytes);
+    for (const Xb12Tile& t : tile_meta) m = std::max(m, t.format != 0 ? static_cast<size_t>(t.bytes) : tile_bytes);
     return m;
 }
 
@@ -168,9 +169,90 @@ void encode_block(ExpertStore& st, int b, const std::uint16_t* d_raw, Xb12Scratc
     MOE_CUDA(cudaStreamSynchronize(s));
 }
 
+// The same for XBH records: exponent histograms -> per-tile Huffman codes (host) -> device encode
+// -> records D2H; a tile whose escapes exceed n / 64 or whose record would not shrink stays raw.
+struct XbhScratch {
+    DeviceBuffer rec, exc, seglen, work, code;
+};
+void encode_block_xbh(ExpertStore& st, int b, const std::uint16_t* d_raw, XbhScratch& x, cudaStream_t s) {
+    const std::uint64_t n = st.tile_bytes / 2, cap = n / 64, nseg = xbh_segments(n);
+    const size_t region = xbh_region_bytes(n);
+    const int T = st.tiles;
+    x.rec.reserve(region * T);
+    x.exc.reserve(cap * 8 * T);
+    x.seglen.reserve(4 * (nseg + 1) * T);
+    x.work.reserve(sizeof(std::uint32_t) * (256 + kXbhWorkWords) * T);
+    x.code.reserve(sizeof(XbhCode) * T);
+    std::uint32_t* hist = x.work.as<std::uint32_t>();
+    std::uint32_t* work = hist + 256 * T;
+    for (int t = 0; t < T; ++t) MOE_CUDA(xb12_histogram(d_raw + n * t, n, hist + 256 * t, s));
+    std::vector<std::uint32_t> h(256 * static_cast<size_t>(T));
+    MOE_CUDA(cudaMemcpyAsync(h.data(), hist, h.size() * 4, cudaMemcpyDeviceToHost, s));
+    MOE_CUDA(cudaStreamSynchronize(s));
+    std::vector<XbhCode> codes(T);
+    for (int t = 0; t < T; ++t) xbh_build_code(h.data() + 256 * t, codes[t]);
+    MOE_CUDA(cudaMemcpyAsync(x.code.ptr, codes.data(), sizeof(XbhCode) * T, cudaMemcpyHostToDevice, s));
+    XbhCode* dcode = x.code.as<XbhCode>();
+    for (int t = 0; t < T; ++t)
+        MOE_CUDA(xbh_encode(d_raw + n * t, n, dcode + t, x.rec.as<std::uint8_t>() + region * t,
+                            x.exc.as<std::uint64_t>() + cap * t, cap, x.seglen.as<std::uint32_t>() + (nseg + 1) * t,
+                            work + kXbhWorkWords * t, s));
+    std::vector<std::uint32_t> wk(kXbhWorkWords * static_cast<size_t>(T));
+    MOE_CUDA(cudaMemcpyAsync(wk.data(), work, wk.size() * 4, cudaMemcpyDeviceToHost, s));
+    MOE_CUDA(cudaStreamSynchronize(s));
+    size_t off = 0;
+    std::vector<std::uint64_t> exc;
+    for (int t = 0; t < T; ++t) {
+        Xb12Tile& m = st.tile_meta[static_cast<size_t>(b) * T + t];
+        m = Xb12Tile{};
+        m.n = n;
+        m.base = codes[t].base;
+        m.n_exc = wk[kXbhWorkWords * t];
+        if (m.n_exc <= cap) xbh_layout(m, wk[kXbhWorkWords * t + 1]);
+        unsigned char* dst = st.blocks[b] + off;
+        st.tile_off[static_cast<size_t>(b) * T + t] = off;
+        if (m.n_exc > cap || m.bytes >= st.tile_bytes) {  // does not pay: keep the raw tile
+            m.format = 0;
+            m.bytes = st.tile_bytes;
+            MOE_CUDA(cudaMemcpyAsync(dst, d_raw + n * t, st.tile_bytes, cudaMemcpyDeviceToHost, s));
+        } else {
+            m.format = 2;
+            const unsigned char* r = x.rec.as<unsigned char>() + region * t;
+            const size_t head = xbh_bits_off(n) + 4 * xbh_words(wk[kXbhWorkWords * t + 1]);
+            MOE_CUDA(cudaMemcpyAsync(dst, r, head, cudaMemcpyDeviceToHost, s));
+            // alignment gaps are zero (a record is a pure function of the tile, even over an old block)
+            std::memset(dst + head, 0, m.exc_off - head);
+            std::memset(dst + m.exc_off + m.n_exc * 8, 0, m.bytes - m.exc_off - m.n_exc * 8);
+            exc.resize(m.n_exc);
+            if (m.n_exc) {
+                MOE_CUDA(cudaMemcpyAsync(exc.data(), x.exc.as<std::uint64_t>() + cap * t, m.n_exc * 8,
+                                         cudaMemcpyDeviceToHost, s));
+                MOE_CUDA(cudaStreamSynchronize(s));
+                std::sort(exc.begin(), exc.end());
+                std::memcpy(dst + m.exc_off, exc.data(), m.n_exc * 8);
+            }
+        }
+        off += m.bytes;
+        if (off > st.expert_bytes) fail(Status::Internal, "xbh: records exceed the expert block");
+    }
+    MOE_CUDA(cudaStreamSynchronize(s));
+}
+
+// the store's encoder for one block
+struct StoreScratch {
+    Xb12Scratch xb12;
+    XbhScratch xbh;
+};
+void encode_store_block(ExpertStore& st, int b, const std::uint16_t* d_raw, StoreScratch& x, cudaStream_t s) {
+    if (st.format == kStoreXbh)
+        encode_block_xbh(st, b, d_raw, x.xbh, s);
+    else
+        encode_block(st, b, d_raw, x.xb12, s);
+}
+
 void recount_link_bytes(ExpertStore& st) {
     st.link_bytes = 0;
-    for (const Xb12Tile& m : st.tile_meta) st.link_bytes += m.format == 1 ? m.bytes : st.tile_bytes;
+    for (const Xb12Tile& m : st.tile_meta) st.link_bytes += m.format != 0 ? m.bytes : st.tile_bytes;
 }
 
 }  // namespace
@@ -187,7 +269,10 @@ void upload_expert_tiles(const ExpertStore& st, int layer, int expert, int t0, i
         } else {
             staging.reserve(st.max_record_bytes());
             MOE_CUDA(cudaMemcpyAsync(staging.ptr, rec, bytes, cudaMemcpyHostToDevice, stream));
-            MOE_CUDA(xb12_decode(staging.as<std::uint8_t>(), m, reinterpret_cast<std::uint16_t*>(out), stream));
+            if (m.format == 2)
+                MOE_CUDA(xbh_decode(staging.as<std::uint8_t>(), m, reinterpret_cast<std::uint16_t*>(out), stream));
+            else
+                MOE_CUDA(xb12_decode(staging.as<std::uint8_t>(), m, reinterpret_cast<std::uint16_t*>(out), stream));
         }
         if (tile_done && tile_done[t - t0]) MOE_CUDA(cudaEventRecord(tile_done[t - t0], stream));
     }
@@ -201,6 +286,8 @@ void read_expert_host(const ExpertStore& st, int layer, int expert, std::uint16_
         const Xb12Tile& m = st.meta(layer, expert, t);
         if (m.format == 0)
             std::memcpy(o, rec, st.tile_bytes);
+        else if (m.format == 2)
+            xbh_decode_host(rec, m, o, 0, m.n);
         else
             xb12_decode_host(rec, m, o, 0, m.n);
     }
@@ -274,15 +361,18 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
         if (!e.empty()) fail(Status::Device, "experts_init: " + e);
     auto t1 = std::chrono::steady_clock::now();
     st.pin_seconds = std::chrono::duration<double>(t1 - t0).count();
-    if (format != kStoreBf16 && format != kStoreXb12) fail(Status::Usage, "experts_init: unknown store format");
-    if (format == kStoreXb12 && (st.tile_bytes / 2) % 16) fail(Status::Usage, "xb12 store: tile values must be a multiple of 16");
+    if (format != kStoreBf16 && format != kStoreXb12 && format != kStoreXbh)
+        fail(Status::Usage, "experts_init: unknown store format");
+    if (format != kStoreBf16 && (st.tile_bytes / 2) % 16) fail(Status::Usage, "coded store: tile values must be a multiple of 16");
+    if (format == kStoreXbh && st.tile_bytes / 2 * kXbhMaxLen >= (1ull << 32))
+        fail(Status::Usage, "xbh store: tiles of at most 357M values (use more tiles)");
     st.format = format;
     raw_tile_layout(st);
     if (!init_values) return;
-    if (format == kStoreXb12) {  // GPU init kernel -> XB12 encode on the device -> D2H records
+    if (format != kStoreBf16) {  // GPU init kernel -> XB12 / XBH encode on the device -> D2H records
         DeviceBuffer raw;
         raw.reserve(st.expert_bytes);
-        Xb12Scratch x;
+        StoreScratch x;
         cudaStream_t s;
         MOE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         for (int i = 0; i < stored; ++i) {
@@ -291,7 +381,7 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
             float scale[3];
             expert_init_constants(seed, layer, expert, spec.hidden_dim, ffn, base, scale);
             MOE_CUDA(launch_expert_init(raw.as<std::uint16_t>(), spec.hidden_dim, ffn, tiles, base, scale, s));
-            encode_block(st, i, raw.as<std::uint16_t>(), x, s);
+            encode_store_block(st, i, raw.as<std::uint16_t>(), x, s);
         }
         cudaStreamDestroy(s);
         recount_link_bytes(st);
@@ -331,9 +421,9 @@ void set_expert_weights(Engine& eng, ExpertStore& st, int layer, int expert, con
     if (!st.has(layer, expert)) fail(Status::Usage, "expert_set: this store (an expert-parallel shard) does not hold the expert");
     const size_t D = st.d, F = st.ffn, Ft = F / st.tiles;
     const int b = st.stored_index(layer, expert);
-    std::vector<std::uint16_t> packed;  // XB12: pack here, then encode into the block
-    if (st.format == kStoreXb12) packed.resize(st.expert_bytes / 2);
-    std::uint16_t* dst = st.format == kStoreXb12 ? packed.data() : reinterpret_cast<std::uint16_t*>(st.blocks[b]);
+    std::vector<std::uint16_t> packed;  // coded stores: pack here, then encode into the block
+    if (st.format != kStoreBf16) packed.resize(st.expert_bytes / 2);
+    std::uint16_t* dst = st.format != kStoreBf16 ? packed.data() : reinterpret_cast<std::uint16_t*>(st.blocks[b]);
     const size_t tile_elems = 3 * Ft * D;
     auto pack_rows = [&](size_t f0, size_t f1) {
         constexpr size_t kB = 64;  // W2 transposed in kB x kB blocks (both sides cache friendly)
@@ -356,14 +446,14 @@ void set_expert_weights(Engine& eng, ExpertStore& st, int layer, int expert, con
     for (size_t k = 1; k < n; ++k) pool.emplace_back(pack_rows, F * k / n, F * (k + 1) / n);
     pack_rows(0, F / n);
     for (auto& th : pool) th.join();
-    if (st.format == kStoreXb12) {
+    if (st.format != kStoreBf16) {
         eng.activate();
         DeviceBuffer raw;
         raw.reserve(st.expert_bytes);
-        Xb12Scratch x;
+        StoreScratch x;
         cudaStream_t s = eng.copy_stream();
         MOE_CUDA(cudaMemcpyAsync(raw.ptr, packed.data(), st.expert_bytes, cudaMemcpyHostToDevice, s));
-        encode_block(st, b, raw.as<std::uint16_t>(), x, s);
+        encode_store_block(st, b, raw.as<std::uint16_t>(), x, s);
         recount_link_bytes(st);
     }
 }

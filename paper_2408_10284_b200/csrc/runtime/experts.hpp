@@ -8,13 +8,14 @@
 #include <vector>
 
 #include "../kernels/xb12.hpp"
+#include "../kernels/xbh.hpp"
 
 namespace adapmoe {
 
 class Engine;
 struct DeviceBuffer;
 
-enum StoreFormat : int { kStoreBf16 = 0, kStoreXb12 = 1 };
+enum StoreFormat : int { kStoreBf16 = 0, kStoreXb12 = 1, kStoreXbh = 2 };
 
 struct ExpertStore {
     int layers = 0, experts = 0, d = 0, ffn = 0, tiles = 0, alias = 0;
@@ -27,8 +28,9 @@ struct ExpertStore {
     std::vector<int> index;
     int numa_node = -1;  // host NUMA node the blocks were placed on (-1: no binding)
     double pin_seconds = 0.0, fill_seconds = 0.0;
-    // kStoreXb12: every tile is an XB12 record (kernels/xb12.hpp) or, if it would not shrink, raw
-    // bf16; records are packed in tile order (tile_off) inside the expert's block
+    // kStoreXb12 / kStoreXbh: every tile is an XB12 (kernels/xb12.hpp) / XBH (kernels/xbh.hpp)
+    // record or, if it would not shrink, raw bf16; records are packed in tile order (tile_off)
+    // inside the expert's block
     int format = kStoreBf16;
     std::vector<Xb12Tile> tile_meta;   // [stored block][tile]
     std::vector<size_t> tile_off;      // [stored block][tile] byte offset of the record in the block

@@ -330,13 +330,14 @@ class Engine:
         return w
 
     # -- physical decode -----------------------------------------------------------------------
-    STORE_FORMATS = {"bf16": 0, "xb12": 1}
+    STORE_FORMATS = {"bf16": 0, "xb12": 1, "xbh": 2}
 
     def experts_init(self, ffn_dim: int, tiles: int, seed: int = 0, host_alias: int = 0, expert_owner=None,
                      rank: int = 0, store_format: str = "bf16"):
         """Pinned host expert store with the deterministic init.  expert_owner ([L][N] shard table) +
         rank: an expert-parallel shard's store, holding only the experts it owns.  store_format
-        "xb12": lossless exponent-coded tiles (moe_experts_set_format)."""
+        "xb12" / "xbh": lossless exponent-coded tiles (4-bit window codes / per-tile Huffman codes;
+        moe_experts_set_format)."""
         check(load().moe_experts_set_format(self._h, self.STORE_FORMATS[store_format]))
         if expert_owner is None:
             check(load().moe_experts_init(self._h, ffn_dim, tiles, seed, host_alias))
@@ -351,7 +352,7 @@ class Engine:
         return {v: k for k, v in self.STORE_FORMATS.items()}[f.value], b.value
 
     def expert_tile_record(self, layer: int, expert: int, tile: int) -> dict:
-        """Host address and XB12 metadata of one stored tile record (moe_expert_tile_record)."""
+        """Host address and XB12 / XBH metadata of one stored tile record (moe_expert_tile_record)."""
         r, b, f, base, m, nib, esc = (C.c_void_p(), C.c_int64(), C.c_int32(), C.c_uint32(), C.c_int64(), C.c_int64(),
                                       C.c_int64())
         check(load().moe_expert_tile_record(self._h, layer, expert, tile, C.byref(r), C.byref(b), C.byref(f),

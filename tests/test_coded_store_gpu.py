@@ -1,9 +1,10 @@
-"""XB12 expert store on the B200 (MOE_STORE_XB12: lossless exponent-coded bf16 over the host link).
+"""Coded expert stores on the B200 (lossless exponent-coded bf16 over the host link): XB12
+(MOE_STORE_XB12, 4-bit window codes) and XBH (MOE_STORE_XBH, per-tile Huffman codes).
 
-* The GPU encoder produces exactly the records of the numpy restatement (tests/xb12_ref.py), and
-  the store decodes (host and device) to the bf16 store's bits.
-* A decode session over an XB12 store returns bit-identical layer outputs and the identical logical
-  trace as over a bf16 store, while the copy engine moves ~75 % of the bytes.
+* The GPU encoders produce exactly the records of the numpy restatements (tests/xb12_ref.py,
+  tests/xbh_ref.py), and the store decodes (host and device) to the bf16 store's bits.
+* A decode session over a coded store returns bit-identical layer outputs and the identical logical
+  trace as over a bf16 store, while the copy engine moves ~75 % (XB12) / ~66 % (XBH) of the bytes.
 * Real-weight uploads (moe_expert_set) encode too; tiles that would not shrink stay raw.
 """
 import ctypes as C
@@ -13,6 +14,7 @@ import pytest
 
 import paper_2408_10284_b200 as P
 import xb12_ref as X
+import xbh_ref as XH
 from conftest import load_golden
 from helpers import oracle_inputs, sim_config
 from oracle import oracle as O
@@ -26,25 +28,34 @@ def _record_bytes(eng, l, e, t):
     return bytes((C.c_uint8 * r["bytes"]).from_address(r["ptr"])), r
 
 
+# (restatement, format code, link-bytes ratio bound at Mixtral width; XBH's 8 KB decode table per
+# tile weighs more on the tiny shape's 344 KB tiles)
+FORMATS = {"xb12": (X, 1, 0.76), "xbh": (XH, 2, 0.67)}
+
+
+@pytest.mark.parametrize("store", ["xb12", "xbh"])
 @pytest.mark.parametrize("d,f,tiles", [(256, 896, 4), (4096, 14336, 4)])
-def test_store_records_match_reference_encoder(d, f, tiles):
+def test_store_records_match_reference_encoder(d, f, tiles, store):
+    ref_mod, code, ratio = FORMATS[store]
     with P.Engine(P.ModelSpec(2, 4, 2, d)) as eng:
-        eng.experts_init(f, tiles, seed=5, store_format="xb12")
+        eng.experts_init(f, tiles, seed=5, store_format=store)
         fmt, link = eng.experts_format()
-        assert fmt == "xb12" and link < 0.76 * 8 * 3 * f * d * 2
+        assert fmt == store and link < (ratio if d >= 4096 else ratio + 0.05) * 8 * 3 * f * d * 2
         n = 3 * f * d // tiles
         for l, e in [(0, 0), (1, 3)]:
             raw = O.expert_init(5, l, e, d, f, tiles)
             assert np.array_equal(eng.expert_read(l, e), raw)
             for t in range(tiles):
                 got, meta = _record_bytes(eng, l, e, t)
-                ref, rmeta = X.encode(raw[t * n:(t + 1) * n])
-                assert meta["format"] == rmeta["format"] == 1
+                ref, rmeta = ref_mod.encode(raw[t * n:(t + 1) * n])
+                assert meta["format"] == rmeta["format"] == code
                 assert (meta["base"], meta["n_escapes"]) == (rmeta["base"], rmeta["n_exc"])
+                assert meta["esc_offset"] == rmeta["exc_off"] and meta["nib_offset"] == rmeta["nib_off"]
                 assert got == ref
 
 
-def test_expert_set_real_weights_encode_and_raw_fallback():
+@pytest.mark.parametrize("store", ["xb12", "xbh"])
+def test_expert_set_real_weights_encode_and_raw_fallback(store):
     d, f, tiles = 256, 512, 2
     rng = np.random.default_rng(7)
     w1 = X_bf16(rng.standard_normal((f, d)) * 0.05)
@@ -53,7 +64,7 @@ def test_expert_set_real_weights_encode_and_raw_fallback():
     w2[:, : f // 2] = X_bf16(rng.standard_normal((d, f // 2)) * 0.05)
     with P.Engine(P.ModelSpec(1, 2, 2, d)) as raw_eng, P.Engine(P.ModelSpec(1, 2, 2, d)) as xb_eng:
         raw_eng.experts_alloc(f, tiles)
-        xb_eng.experts_alloc(f, tiles, store_format="xb12")
+        xb_eng.experts_alloc(f, tiles, store_format=store)
         for eng in (raw_eng, xb_eng):
             eng.expert_set(0, 1, w1, w3, w2)
             eng.expert_set(0, 0, w1, w3, X_bf16(np.ones((d, f)) * 0.01))
@@ -61,7 +72,7 @@ def test_expert_set_real_weights_encode_and_raw_fallback():
             assert np.array_equal(xb_eng.expert_read(0, e), raw_eng.expert_read(0, e))
         formats = [xb_eng.expert_tile_record(0, 1, t)["format"] for t in range(tiles)]
         assert 0 in formats  # the random-bit W2 columns make a tile not worth coding
-        assert xb_eng.expert_tile_record(0, 0, 0)["format"] == 1
+        assert xb_eng.expert_tile_record(0, 0, 0)["format"] == FORMATS[store][1]
 
 
 def X_bf16(a):
@@ -86,13 +97,14 @@ def _decode(g, fmt, T, batch=1, timeline=None):
     return hid, r, st, n
 
 
+@pytest.mark.parametrize("store", ["xb12", "xbh"])
 @pytest.mark.parametrize("name", ["tiny", "tiny_transfer_heavy", "tiny_budget0"])
-def test_decode_over_xb12_store_is_bit_identical(name, tmp_path):
+def test_decode_over_coded_store_is_bit_identical(name, store, tmp_path):
     g = load_golden(name)
     T = 24
     h0, r0, s0, _ = _decode(g, "bf16", T)
     path = tmp_path / "tl.jsonl"
-    h1, r1, s1, n = _decode(g, "xb12", T, timeline=str(path))
+    h1, r1, s1, n = _decode(g, store, T, timeline=str(path))
     assert np.array_equal(h0, h1)
     assert r0.metrics == r1.metrics and np.array_equal(r0.timeline, r1.timeline)
     # how many queued prefetch tiles get cancelled before issue depends on physical timing, so
@@ -105,9 +117,10 @@ def test_decode_over_xb12_store_is_bit_identical(name, tmp_path):
     assert not TL.check_conservation(ev, r1.metrics, s1)
 
 
-def test_decode_mixtral_width_xb12_vs_bf16():
-    """88 MB tiles (66 MB records) through the staging ring and the decode stream: outputs and trace
-    identical to the bf16 store, link bytes ~75 %."""
+@pytest.mark.parametrize("store,lo,hi", [("xb12", 0.74, 0.76), ("xbh", 0.65, 0.67)])
+def test_decode_mixtral_width_coded_vs_bf16(store, lo, hi):
+    """88 MB tiles (66 / 58 MB records) through the staging ring and the decode stream: outputs and
+    trace identical to the bf16 store, link bytes ~75 % (XB12) / ~66 % (XBH)."""
     from paper_2408_10284_b200 import workloads as W
     wl = W.mixtral_8x7b(tokens=4, budget=8)
     L = 3
@@ -117,7 +130,7 @@ def test_decode_mixtral_width_xb12_vs_bf16():
     caps = [2, 2, 2]
     cfg = P.SimConfig()
     outs = []
-    for fmt in ("bf16", "xb12"):
+    for fmt in ("bf16", store):
         with P.Engine(P.ModelSpec(L, 8, 2, 4096)) as eng:
             eng.load_gates(w.gates)
             eng.experts_init(wl.ffn, 4, seed=9, store_format=fmt)
@@ -130,14 +143,15 @@ def test_decode_mixtral_width_xb12_vs_bf16():
     (h0, r0, s0), (h1, r1, s1) = outs
     assert np.array_equal(h0, h1)
     assert r0.metrics == r1.metrics and np.array_equal(r0.timeline, r1.timeline)
-    assert 0.74 < s1["copy_bytes"] / s0["copy_bytes"] < 0.76
+    assert lo < s1["copy_bytes"] / s0["copy_bytes"] < hi
 
 
-def test_copy_tiles_decodes_xb12():
+@pytest.mark.parametrize("store", ["xb12", "xbh"])
+def test_copy_tiles_decodes_coded(store):
     import torch
     d, f, tiles = 4096, 14336, 4
     with P.Engine(P.ModelSpec(1, 2, 2, d)) as eng:
-        eng.experts_init(f, tiles, seed=3, store_format="xb12")
+        eng.experts_init(f, tiles, seed=3, store_format=store)
         buf = torch.empty(eng.expert_bytes() // 2, dtype=torch.int16, device="cuda")
         eng.copy_tiles(0, 1, 1, 2, buf.data_ptr())  # tiles 1..2 only
         torch.cuda.synchronize()

@@ -33,29 +33,36 @@ typedef struct {
     int64_t n; /* values in the tile */
 } tile_rec;
 
-/* XBH (kernels/xbh.hpp): sections at offsets derived from n; segments of 512 values, each walked
- * from its bit offset with a 12-bit peek into the decode table. */
-#define XBH_SEG 512
+/* XBH (kernels/xbh.hpp): sections at offsets derived from n and the header's code-bit count; the
+ * walk starts at the last block whose first code precedes i0 (block value bases + chunk gaps) and
+ * follows the single-code table. */
 #define XBH_MAXLEN 12
+#define XBH_BLOCK_BITS (256 * 128)
 static int64_t al16(int64_t v) { return (v + 15) / 16 * 16; }
 static void decode_xbh(const tile_rec* t, int64_t i0, int64_t n, uint16_t* dst) {
-    const int64_t N = t->n, lut_off = al16(N), seg_off = lut_off + 2 * (1 << XBH_MAXLEN);
-    const int64_t bits_off = al16(seg_off + 4 * ((N + XBH_SEG - 1) / XBH_SEG + 1));
+    const int64_t N = t->n, lut_off = al16(N), hdr_off = lut_off + 6 * (1 << XBH_MAXLEN); /* lut u16 + mlut u32 */
+    const int64_t bits = (int64_t)((const uint64_t*)(t->rec + hdr_off))[0];
+    const int64_t bits_off = hdr_off + 16, words = (bits + 31) / 32 + 8, chunks = (bits + 127) / 128;
+    const int64_t gap_off = al16(bits_off + 4 * words), base_off = al16(gap_off + 4 * ((chunks + 7) / 8));
+    const int64_t blocks = (bits + XBH_BLOCK_BITS - 1) / XBH_BLOCK_BITS;
     const uint16_t* lut = (const uint16_t*)(t->rec + lut_off);
-    const uint32_t* seg = (const uint32_t*)(t->rec + seg_off);
     const uint32_t* w = (const uint32_t*)(t->rec + bits_off);
+    const uint32_t* gaps = (const uint32_t*)(t->rec + gap_off);
+    const uint32_t* bases = (const uint32_t*)(t->rec + base_off);
+    int64_t lo_b = 0, hi_b = blocks; /* last block with bases[b] <= i0 */
+    while (hi_b - lo_b > 1) {
+        const int64_t m = (lo_b + hi_b) / 2;
+        if ((int64_t)bases[m] <= i0) lo_b = m; else hi_b = m;
+    }
+    uint64_t pos = (uint64_t)lo_b * XBH_BLOCK_BITS + (gaps[(lo_b * 256) >> 3] & 15u);
     const int64_t end = i0 + n;
-    for (int64_t s = i0 / XBH_SEG; s * XBH_SEG < end; ++s) {
-        uint64_t pos = seg[s];
-        const int64_t v1 = end < (s + 1) * XBH_SEG ? end : (s + 1) * XBH_SEG;
-        for (int64_t i = s * XBH_SEG; i < v1; ++i) {
-            const uint64_t win = ((uint64_t)w[pos >> 5] << 32) | w[(pos >> 5) + 1];
-            const uint32_t e = lut[(win << (pos & 31)) >> (64 - XBH_MAXLEN)];
-            pos += e >> 8;
-            if (i < i0) continue;
-            const uint32_t b = t->rec[i];
-            dst[i - i0] = (uint16_t)(((b & 0x80u) << 8) | ((e & 0xffu) << 7) | (b & 0x7fu));
-        }
+    for (int64_t i = bases[lo_b]; i < end; ++i) {
+        const uint64_t win = ((uint64_t)w[pos >> 5] << 32) | w[(pos >> 5) + 1];
+        const uint32_t e = lut[(win << (pos & 31)) >> (64 - XBH_MAXLEN)];
+        pos += e >> 8;
+        if (i < i0) continue;
+        const uint32_t b = t->rec[i];
+        dst[i - i0] = (uint16_t)(((b & 0x80u) << 8) | ((e & 0xffu) << 7) | (b & 0x7fu));
     }
 }
 

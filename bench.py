@@ -288,27 +288,30 @@ def cpu_ffn_baseline(eng, wl, trace, tau, cfg, tok0: int, n_tok: int, gpu_out):
     """the same decode's expert FFN on the host cores (baseline/cpu_ffn.c, OpenMP,
     builder-written — NOT the reference, whose CPU path does no FFN arithmetic): for each (token,
     layer) of a bounded sample, out = x + sum_e w_e SwiGLU_e(x) over the selected experts (the
-    reference rule's selections, from K1), reading the weights in place from the pinned host store.
-    Also the largest relative difference to the GPU decode's outputs of the same tokens."""
+    reference rule's selections, from K1), reading raw bf16 weights from host memory — the layout a
+    CPU-only system keeps (its DRAM is not behind a link, so it gains nothing from coding).  With a
+    bf16 store the weights are read in place from the pinned store; with a coded store (XB12 / XBH)
+    each selected expert is first expanded into a host bf16 buffer through the GPU decoder, outside
+    the timed region.  Also the largest relative difference to the GPU decode's outputs."""
     import ctypes as C
 
     import numpy as np
+    import torch
     lib = C.CDLL(os.path.join(ROOT, "baseline", "libcpu_ffn.so"))
     lib.cpu_moe_layer.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_double), C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.POINTER(C.c_double), C.POINTER(C.c_float), C.c_int]
-    lib.cpu_moe_layer_xb12.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_int32), C.POINTER(C.c_uint32),
-                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
-                                       C.POINTER(C.c_double), C.c_int, C.c_int, C.c_int, C.c_int,
-                                       C.POINTER(C.c_double), C.POINTER(C.c_float), C.c_int]
     fmt, _ = eng.experts_format()
-    recs = {}
     threads = os.cpu_count() or 1
     acts = np.ascontiguousarray(trace.acts[tok0: tok0 + n_tok])
     scores = trace.scores[tok0: tok0 + n_tok]
     dec, single, _, _ = eng.route_trace(acts, scores, trace.fisher, tau, cfg)
     out = np.zeros((n_tok, wl.layers, wl.hidden), dtype=np.float32)
+    ebytes = 3 * wl.ffn * wl.hidden * 2
+    if fmt != "bf16":  # two expert-sized staging buffers: device (decode target) and pinned host
+        d_buf = torch.empty(ebytes // 2, dtype=torch.int16, device="cuda")
+        h_bufs = [torch.empty(ebytes // 2, dtype=torch.int16).pin_memory() for _ in range(wl.top_k)]
     moved = 0
-    t0 = time.perf_counter()
+    dt = 0.0
     for t in range(n_tok):
         for l in range(wl.layers):
             sel = [int(e) for e in dec[t, l] if e >= 0]
@@ -317,35 +320,30 @@ def cpu_ffn_baseline(eng, wl, trace, tau, cfg, tok0: int, n_tok: int, gpu_out):
             x = acts[t, l]
             xp, op = x.ctypes.data_as(C.POINTER(C.c_double)), out[t, l].ctypes.data_as(C.POINTER(C.c_float))
             if fmt == "bf16":
-                ptrs = (C.c_void_p * len(sel))(*[eng.expert_host_ptr(l, e) for e in sel])
-                rc = lib.cpu_moe_layer(ptrs, wts, len(sel), wl.hidden, wl.ffn, wl.tiles, xp, op, threads)
-                moved += len(sel) * 3 * wl.ffn * wl.hidden * 2
-            else:  # XB12 records decoded on the fly (the same bytes the GPU path moves)
-                rs = []
-                for e in sel:
-                    for tt in range(wl.tiles):
-                        if (l, e, tt) not in recs:
-                            recs[(l, e, tt)] = eng.expert_tile_record(l, e, tt)
-                        rs.append(recs[(l, e, tt)])
-                n = len(rs)
-                rc = lib.cpu_moe_layer_xb12((C.c_void_p * n)(*[r["ptr"] for r in rs]),
-                                            (C.c_int32 * n)(*[r["format"] for r in rs]),
-                                            (C.c_uint32 * n)(*[r["base"] for r in rs]),
-                                            (C.c_int64 * n)(*[r["n_escapes"] for r in rs]),
-                                            (C.c_int64 * n)(*[r["nib_offset"] for r in rs]),
-                                            (C.c_int64 * n)(*[r["esc_offset"] for r in rs]),
-                                            wts, len(sel), wl.hidden, wl.ffn, wl.tiles, xp, op, threads)
-                moved += sum(r["bytes"] for r in rs)
+                ptrs = [eng.expert_host_ptr(l, e) for e in sel]
+            else:
+                ptrs = []
+                for k, e in enumerate(sel):
+                    eng.copy_tiles(l, e, 0, wl.tiles, d_buf.data_ptr())
+                    torch.cuda.synchronize()  # the engine's copy + decode stream, then a blocking D2H
+                    h_bufs[k].copy_(d_buf)
+                    ptrs.append(h_bufs[k].data_ptr())
+            t0 = time.perf_counter()
+            rc = lib.cpu_moe_layer((C.c_void_p * len(sel))(*ptrs), wts, len(sel), wl.hidden, wl.ffn, wl.tiles, xp, op,
+                                   threads)
+            dt += time.perf_counter() - t0
+            moved += len(sel) * ebytes
             assert rc == 0, rc
-    dt = time.perf_counter() - t0
     moe_gpu = gpu_out.astype(np.float64) - acts.astype(np.float32).astype(np.float64)
     moe_cpu = out.astype(np.float64) - acts.astype(np.float32).astype(np.float64)
     rel = float(np.abs(moe_cpu - moe_gpu).max() / max(np.abs(moe_gpu).max(), 1e-30))
+    where = ("in place from the pinned store" if fmt == "bf16" else
+             f"from host bf16 buffers (the {fmt} store's records expanded by the GPU decoder, untimed)")
     return {"value": n_tok / dt, "unit": "tok/s", "cores": threads, "kind": "port",
             "label": "not reference: builder-written CPU SwiGLU (baseline/cpu_ffn.c, OpenMP, fp32 accumulation); "
                      "the reference's CPU path does no FFN arithmetic (inc/simulator.hpp:446-462)",
-            "sample": f"{n_tok} tokens x {wl.layers} layers of the e2e window, selected experts read in place from the "
-                      f"pinned host store ({fmt} records, {moved / 1e9:.1f} GB)",
+            "sample": f"{n_tok} tokens x {wl.layers} layers of the e2e window, selected experts' raw bf16 weights read "
+                      f"{where} ({moved / 1e9:.1f} GB)",
             "host_read_gbs": moved / dt / 1e9, "max_rel_diff_vs_gpu": rel}
 
 

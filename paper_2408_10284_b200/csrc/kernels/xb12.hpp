@@ -36,6 +36,7 @@ struct Xb12Tile {
     std::uint64_t nib_off = 0;    // byte offsets inside the record (lo at 0); XBH: the segment table
     std::uint64_t exc_off = 0;
     std::uint64_t bytes = 0;      // record bytes (256-aligned)
+    std::uint64_t code_bits = 0;  // XBH: total bits of the exponent codes
 };
 
 constexpr std::uint64_t kXb12Align = 256;

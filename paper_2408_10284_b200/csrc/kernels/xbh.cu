@@ -3,11 +3,15 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cstddef>
 #include <vector>
 
 #include "xbh.hpp"
 
 namespace adapmoe {
+
+static_assert(offsetof(XbhCode, mlut) == offsetof(XbhCode, lut) + 2 * kXbhLut, "lut and mlut are copied as one block");
 
 // ---- host: the per-tile code --------------------------------------------------------------------
 
@@ -78,13 +82,31 @@ void xbh_build_code(const std::uint32_t* hist, XbhCode& c) {
             prev = static_cast<unsigned>(l);
             c.code[s] = static_cast<std::uint16_t>(code);
         }
+    std::vector<std::uint16_t> sym_lut(kXbhLut, 0);  // symbol | length << 8 of the 12-bit peek
     for (int s = 0; s < 16; ++s) {
         if (!c.len[s]) continue;
         const unsigned sh = kXbhMaxLen - c.len[s];
         const std::uint16_t entry =
             static_cast<std::uint16_t>(((s < 15 ? c.base + s : 0u) & 0xffu) | (static_cast<unsigned>(c.len[s]) << 8));
-        for (unsigned k = static_cast<unsigned>(c.code[s]) << sh; k < ((static_cast<unsigned>(c.code[s]) + 1) << sh); ++k)
+        for (unsigned k = static_cast<unsigned>(c.code[s]) << sh; k < ((static_cast<unsigned>(c.code[s]) + 1) << sh); ++k) {
             c.lut[k] = entry;
+            sym_lut[k] = static_cast<std::uint16_t>(s | (c.len[s] << 8));
+        }
+    }
+    // multi-code table: follow the peek through up to 3 codes that end inside its 12 bits; entry =
+    // symbols (4 bits each) | lengths (4 bits each) << 12 | count << 24 | total length << 26.  A
+    // peek without a code (length 0) never occurs in a stream and ends the walk.
+    for (unsigned i = 0; i < static_cast<unsigned>(kXbhLut); ++i) {
+        unsigned len = 0, syms = 0, lens = 0, cnt = 0;
+        for (int k = 0; k < 3 && len < static_cast<unsigned>(kXbhMaxLen); ++k) {
+            const unsigned e = sym_lut[(i << len) & (kXbhLut - 1)], l = e >> 8;
+            if (l == 0 || len + l > static_cast<unsigned>(kXbhMaxLen)) break;
+            syms |= (e & 15u) << (4 * k);
+            lens |= l << (4 * k);
+            ++cnt;
+            len += l;
+        }
+        c.mlut[i] = syms | (lens << 12) | (cnt << 24) | (len << 26);
     }
 }
 
@@ -98,7 +120,9 @@ __device__ __forceinline__ unsigned symbol_of(unsigned v, unsigned base) {
     return s < 15u ? s : 15u;
 }
 
-// bits of each segment's codes
+// ---- encode: 512 values per thread ----------------------------------------------------------------
+
+// bits of each encoder segment's codes
 __global__ void __launch_bounds__(kThreads) seglen_kernel(const uint4* src, std::uint64_t n, const XbhCode* code,
                                                           std::uint32_t* seglen) {
     __shared__ unsigned len[16];
@@ -106,10 +130,9 @@ __global__ void __launch_bounds__(kThreads) seglen_kernel(const uint4* src, std:
     if (threadIdx.x < 16) len[threadIdx.x] = code->len[threadIdx.x];
     if (threadIdx.x == 0) base = code->base;
     __syncthreads();
-    const std::uint64_t nseg = xbh_segments(n);
     const std::uint64_t s = blockIdx.x * static_cast<std::uint64_t>(kThreads) + threadIdx.x;
-    if (s >= nseg) return;
-    const std::uint64_t v0 = s * kXbhSeg, v1 = std::min<std::uint64_t>(n, v0 + kXbhSeg);
+    if (s >= xbh_enc_segments(n)) return;
+    const std::uint64_t v0 = s * kXbhEncSeg, v1 = std::min<std::uint64_t>(n, v0 + kXbhEncSeg);
     unsigned bits = 0;
     for (std::uint64_t g = v0 / 8; g < v1 / 8; ++g) {
         const uint4 q = src[g];
@@ -120,9 +143,8 @@ __global__ void __launch_bounds__(kThreads) seglen_kernel(const uint4* src, std:
     seglen[s] = bits;
 }
 
-// exclusive scan of seglen[0..nseg) into seg[0..nseg], seg[nseg] = total (one CTA)
-__global__ void __launch_bounds__(1024) scan_kernel(const std::uint32_t* seglen, std::uint64_t nseg, std::uint32_t* seg,
-                                                    std::uint32_t* work) {
+// exclusive scan of seglen[0..nseg) in place, seglen[nseg] = total = work[1] (one CTA)
+__global__ void __launch_bounds__(1024) scan_kernel(std::uint32_t* seglen, std::uint64_t nseg, std::uint32_t* work) {
     __shared__ unsigned long long part[1024];
     const std::uint64_t per = (nseg + 1023) / 1024;
     const std::uint64_t a = threadIdx.x * per, b = std::min<std::uint64_t>(nseg, a + per);
@@ -138,19 +160,22 @@ __global__ void __launch_bounds__(1024) scan_kernel(const std::uint32_t* seglen,
     }
     unsigned long long run = part[threadIdx.x] - sum;
     for (std::uint64_t i = a; i < b; ++i) {
-        seg[i] = static_cast<std::uint32_t>(run);
-        run += seglen[i];
+        const unsigned l = seglen[i];
+        seglen[i] = static_cast<std::uint32_t>(run);
+        run += l;
     }
     if (threadIdx.x == 1023) {
-        seg[nseg] = static_cast<std::uint32_t>(part[1023]);
+        seglen[nseg] = static_cast<std::uint32_t>(part[1023]);
         work[1] = static_cast<std::uint32_t>(part[1023]);
     }
 }
 
-// every segment's codes, MSB first from its bit offset (words shared with a neighbour: atomicOr
-// into the zeroed bit section), and the escapes
+// every segment's codes, MSB first from its bit offset (words shared with a neighbour: atomicOr into
+// the zeroed bit section); for each code that is the first to start in its 128-bit chunk, the
+// chunk's gap (and, for a block's first chunk, the block's base value index); the escapes
 __global__ void __launch_bounds__(kThreads) emit_kernel(const std::uint16_t* src, std::uint64_t n, const XbhCode* code,
                                                         const std::uint32_t* seg, std::uint32_t* words,
+                                                        std::uint32_t* gaps, std::uint32_t* bases,
                                                         unsigned long long* exc, std::uint64_t cap, unsigned* counter) {
     __shared__ unsigned len[16], cw[16];
     __shared__ unsigned base;
@@ -160,14 +185,15 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const std::uint16_t* src
     }
     if (threadIdx.x == 0) base = code->base;
     __syncthreads();
-    const std::uint64_t nseg = xbh_segments(n);
     const std::uint64_t s = blockIdx.x * static_cast<std::uint64_t>(kThreads) + threadIdx.x;
-    if (s >= nseg) return;
-    const std::uint64_t v0 = s * kXbhSeg, v1 = std::min<std::uint64_t>(n, v0 + kXbhSeg);
-    const std::uint32_t p = seg[s];
-    std::uint64_t w = p >> 5;
+    if (s >= xbh_enc_segments(n)) return;
+    const std::uint64_t v0 = s * kXbhEncSeg, v1 = std::min<std::uint64_t>(n, v0 + kXbhEncSeg);
+    std::uint64_t pos = seg[s];
+    // start of the previous code (the last of the previous segment); "none" before value 0
+    std::uint64_t prev = v0 ? pos - len[symbol_of(src[v0 - 1], base)] : ~0ull;
+    std::uint64_t w = pos >> 5;
     unsigned long long acc = 0;
-    unsigned nacc = p & 31u;  // bits of the first word that belong to the previous segment (zeros here)
+    unsigned nacc = pos & 31u;  // bits of the first word that belong to the previous segment (zeros here)
     for (std::uint64_t i = v0; i < v1; ++i) {
         const unsigned v = src[i];
         const unsigned sym = symbol_of(v, base), l = len[sym];
@@ -175,6 +201,13 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const std::uint16_t* src
             const unsigned slot = atomicAdd(counter, 1u);
             if (slot < cap) exc[slot] = (static_cast<unsigned long long>(i) << 16) | v;
         }
+        const std::uint64_t c = pos / kXbhChunkBits;
+        if (prev == ~0ull || prev / kXbhChunkBits != c) {  // first code starting in chunk c
+            atomicOr(&gaps[c >> 3], static_cast<unsigned>(pos - c * kXbhChunkBits) << (4 * (c & 7)));
+            if (c % kXbhBlockChunks == 0) bases[c / kXbhBlockChunks] = static_cast<std::uint32_t>(i);
+        }
+        prev = pos;
+        pos += l;
         acc |= static_cast<unsigned long long>(cw[sym]) << (64 - nacc - l);
         nacc += l;
         if (nacc >= 32) {
@@ -201,54 +234,171 @@ __global__ void __launch_bounds__(kThreads) lo_kernel(const uint4* src, std::uin
     }
 }
 
-constexpr int kDecThreads = 128;
+// ---- decode: one thread per 128-bit chunk, one CTA pass per block of 256 chunks --------------------
+//  stage: the block's 1024 code words (+8 look-ahead) into shared memory (one pad word per 32: the
+//         lanes' chunks are 4 words apart) — prefetched into registers during the previous block's
+//         merge — and the gap of each thread's chunk;
+//  count: each thread walks its chunk from its gap with the multi-code table (~3 codes per 12-bit
+//         lookup; a lookup whose codes all start inside the chunk is taken whole, the last few are
+//         split where the next chunk begins), counting codes;
+//  scan:  the CTA turns counts into positions in the block's exponent buffer;
+//  write: each thread walks again, OR-ing each lookup's (up to 3) 4-bit symbols into the block's
+//         zeroed symbol buffer at its positions (shared atomics: neighbours share boundary words);
+//  merge: the CTA joins symbols (+ the window base = exponent; escapes are patched afterwards) and
+//         lo bytes into bf16 over the block's value range with 16-byte lo loads and 32-byte stores
+//         (element stores for the two partial 16-value groups at the range ends, which the
+//         neighbouring blocks share), and zeroes the symbol buffer for the next block.
+constexpr int kDecThreads = static_cast<int>(kXbhBlockChunks);
+constexpr int kDecWords = static_cast<int>(kXbhBlockBits / 32);  // 1024
+constexpr int kDecStage = (kDecWords + 8 + (kDecWords + 8) / 32 + 1 + 3) / 4 * 4;  // padded, 16-byte multiple
+constexpr int kDecExWords = (static_cast<int>(kXbhBlockBits) + 32) / 8;  // <= 1 code per bit (+ slack), 8 per word
+constexpr size_t kDecSmem = sizeof(std::uint32_t) * (kXbhLut + kDecStage + 2 * (kDecThreads / 32) + kDecExWords);
 
-// One thread per 512-value segment: 64-bit bit buffer, 12-bit peek into the shared table, refilled
-// by a 32-bit word whenever fewer than 24 bits remain (two codes per check).
-__global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t* rec, std::uint64_t n, uint4* dst) {
-    __shared__ __align__(16) std::uint16_t lut[kXbhLut];
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(rec + xbh_lut_off(n));
-        uint4* d = reinterpret_cast<uint4*>(lut);
-        for (int i = threadIdx.x; i < kXbhLut / 8; i += kDecThreads) d[i] = __ldg(src + i);
-    }
-    __syncthreads();
-    const std::uint64_t nseg = xbh_segments(n);
-    const std::uint64_t s = blockIdx.x * static_cast<std::uint64_t>(kDecThreads) + threadIdx.x;
-    if (s >= nseg) return;
-    const std::uint32_t* seg = reinterpret_cast<const std::uint32_t*>(rec + xbh_seg_off(n));
+__device__ __forceinline__ unsigned padw(unsigned w) { return w + (w >> 5); }
+
+__global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t* rec, std::uint64_t n,
+                                                             std::uint64_t bits, unsigned base_exp, std::uint16_t* dst) {
+    extern __shared__ __align__(16) std::uint32_t sm[];
+    std::uint32_t* mlut = sm;
+    std::uint32_t* sw = sm + kXbhLut;
+    std::uint32_t* wsum = sw + kDecStage;
+    std::uint32_t* ex = wsum + 2 * (kDecThreads / 32);  // symbol nibbles, value j of the block at nibble j + (v0 & 15)
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    for (int i = t; i < kDecExWords; i += kDecThreads) ex[i] = 0;
     const std::uint32_t* words = reinterpret_cast<const std::uint32_t*>(rec + xbh_bits_off(n));
+    const std::uint32_t* gaps = reinterpret_cast<const std::uint32_t*>(rec + xbh_gap_off(n, bits));
+    const std::uint32_t* bases = reinterpret_cast<const std::uint32_t*>(rec + xbh_base_off(n, bits));
     const uint4* lo = reinterpret_cast<const uint4*>(rec);
-    const std::uint32_t p = __ldg(seg + s);
-    std::uint64_t nx = (p >> 5) + 2;
-    unsigned long long buf =
-        ((static_cast<unsigned long long>(__ldg(words + nx - 2)) << 32) | __ldg(words + nx - 1)) << (p & 31u);
-    int nb = 64 - static_cast<int>(p & 31u);
-    const std::uint64_t g0 = s * (kXbhSeg / 16), g1 = std::min<std::uint64_t>(n, (s + 1) * kXbhSeg) / 16;
-    for (std::uint64_t g = g0; g < g1; ++g) {
-        const uint4 l = __ldg(lo + g);
-        const unsigned lw[4] = {l.x, l.y, l.z, l.w};
-        unsigned out[8];
-#pragma unroll
-        for (int k = 0; k < 16; k += 2) {
-            if (nb < 24) {
-                buf |= static_cast<unsigned long long>(__ldg(words + nx++)) << (32 - nb);
-                nb += 32;
+    const std::uint64_t chunks = xbh_chunks(bits), blocks = xbh_blocks(bits);
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(rec + xbh_mlut_off(n));
+        for (int i = t; i < kXbhLut / 4; i += kDecThreads) reinterpret_cast<uint4*>(mlut)[i] = __ldg(src + i);
+    }
+    const unsigned base4 = (base_exp & 0xffu) * 0x01010101u;
+    const std::uint64_t nwords = xbh_words(bits);  // the bit section's words (codes + zero padding)
+    uint4 pw, px = make_uint4(0, 0, 0, 0);
+    std::uint32_t pg = 0;
+    auto prefetch = [&](std::uint64_t b) {
+        const std::uint64_t q = b * (kDecWords / 4) + t;  // uint4 index in the bit section
+        const uint4* src = reinterpret_cast<const uint4*>(words);
+        pw = 4 * q + 4 <= nwords ? __ldg(src + q) : make_uint4(0, 0, 0, 0);
+        if (t < 2) px = 4 * (q + kDecThreads) + 4 <= nwords ? __ldg(src + q + kDecThreads) : make_uint4(0, 0, 0, 0);
+        const std::uint64_t c = b * kXbhBlockChunks + t;
+        pg = c < chunks ? __ldg(gaps + (c >> 3)) : 0u;
+    };
+    auto peek = [&](unsigned pos) {  // 12 bits at `pos` of the staged block
+        const unsigned w = pos >> 5;
+        return __funnelshift_l(sw[padw(w + 1)], sw[padw(w)], pos & 31u) >> (32 - kXbhMaxLen);
+    };
+    std::uint64_t b = blockIdx.x;
+    if (b < blocks) prefetch(b);
+    for (; b < blocks; b += gridDim.x) {
+        __syncthreads();  // the previous block's merge is done with sw / ex
+        {
+            const unsigned w = 4u * t;  // 4 words, none crossing a pad (w % 32 <= 28)
+            sw[padw(w)] = pw.x, sw[padw(w) + 1] = pw.y, sw[padw(w) + 2] = pw.z, sw[padw(w) + 3] = pw.w;
+            if (t < 2) {
+                const unsigned x = 4u * (kDecThreads + t);
+                sw[padw(x)] = px.x, sw[padw(x) + 1] = px.y, sw[padw(x) + 2] = px.z, sw[padw(x) + 3] = px.w;
             }
-            unsigned pair = 0;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const unsigned e = lut[buf >> (64 - kXbhMaxLen)];
-                const unsigned len = e >> 8;
-                buf <<= len;
-                nb -= static_cast<int>(len);
-                const unsigned b = (lw[(k + h) >> 2] >> (8 * ((k + h) & 3))) & 0xffu;
-                pair |= (((b & 0x80u) << 8) | ((e & 0xffu) << 7) | (b & 0x7fu)) << (16 * h);
-            }
-            out[k >> 1] = pair;
         }
-        dst[2 * g] = make_uint4(out[0], out[1], out[2], out[3]);
-        dst[2 * g + 1] = make_uint4(out[4], out[5], out[6], out[7]);
+        const std::uint64_t c = b * kXbhBlockChunks + t;
+        const unsigned end = static_cast<unsigned>(t + 1) * static_cast<unsigned>(kXbhChunkBits);
+        const std::uint64_t rem = bits - b * kXbhBlockBits;  // codes start below this in the block
+        const unsigned stop = c < chunks ? (end < rem ? end : static_cast<unsigned>(rem)) : 0u;
+        const unsigned start =
+            static_cast<unsigned>(t) * static_cast<unsigned>(kXbhChunkBits) + ((pg >> (4 * (c & 7))) & 15u);
+        const std::uint64_t v0 = __ldg(bases + b), v1 = __ldg(bases + b + 1);
+        __syncthreads();
+        // count
+        auto partial = [&](unsigned e, unsigned pos, unsigned& k, unsigned& adv) {
+            const unsigned n3 = (e >> 24) & 3u, l0 = (e >> 12) & 15u, l1 = (e >> 16) & 15u;
+            k = 1u + (n3 > 1u && pos + l0 < stop) + (n3 > 2u && pos + l0 + l1 < stop);
+            adv = k == n3 ? e >> 26 : (k == 1u ? l0 : l0 + l1);
+        };
+        unsigned cnt = 0, pos = start;
+        for (; pos + kXbhMaxLen <= stop;) {  // every code of the lookup starts inside the chunk
+            const unsigned e = mlut[peek(pos)];
+            cnt += (e >> 24) & 3u;
+            pos += e >> 26;
+        }
+        for (; pos < stop;) {
+            unsigned k, adv;
+            partial(mlut[peek(pos)], pos, k, adv);
+            cnt += k;
+            pos += adv;
+        }
+        // exclusive scan of the counts over the CTA
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        unsigned before = 0;
+#pragma unroll
+        for (int w = 0; w < kDecThreads / 32; ++w) before += w < warp ? wsum[w] : 0u;
+        // write: symbols of the block's j-th value at nibble j + (v0 & 15) (16-value groups stay aligned)
+        {
+            unsigned o = before + incl - cnt + static_cast<unsigned>(v0 & 15);
+            auto put = [&](unsigned syms) {  // up to 3 symbols (12 bits) at nibble o
+                const unsigned sh = 4 * (o & 7);
+                atomicOr(ex + (o >> 3), syms << sh);
+                if (sh > 20) atomicOr(ex + (o >> 3) + 1, syms >> (32 - sh));
+            };
+            for (pos = start; pos + kXbhMaxLen <= stop;) {
+                const unsigned e = mlut[peek(pos)];
+                put(e & 0xfffu);  // a lookup's unused symbol nibbles are zero
+                o += (e >> 24) & 3u;
+                pos += e >> 26;
+            }
+            for (; pos < stop;) {
+                const unsigned e = mlut[peek(pos)];
+                unsigned k, adv;
+                partial(e, pos, k, adv);
+                put(e & ((1u << (4 * k)) - 1u));
+                o += k;
+                pos += adv;
+            }
+        }
+        __syncthreads();
+        // merge
+        const std::uint64_t gs = v0 >> 4, ge = (v1 + 15) >> 4;  // 16-value groups touching [v0, v1)
+        if (b + gridDim.x < blocks) prefetch(b + gridDim.x);
+        for (std::uint64_t g = gs + t; g < ge; g += kDecThreads) {
+            const uint4 l = __ldg(lo + g);
+            const uint2 sy = *reinterpret_cast<const uint2*>(ex + 2 * (g - gs));
+            ex[2 * (g - gs)] = 0;
+            ex[2 * (g - gs) + 1] = 0;
+            const unsigned lw[4] = {l.x, l.y, l.z, l.w};
+            // nibbles -> bytes (+ base): symbols 4q..4q+3 of the group
+            const unsigned ew[4] = {
+                __vadd4(__byte_perm(sy.x & 0x0f0f0f0fu, (sy.x >> 4) & 0x0f0f0f0fu, 0x5140), base4),
+                __vadd4(__byte_perm(sy.x & 0x0f0f0f0fu, (sy.x >> 4) & 0x0f0f0f0fu, 0x7362), base4),
+                __vadd4(__byte_perm(sy.y & 0x0f0f0f0fu, (sy.y >> 4) & 0x0f0f0f0fu, 0x5140), base4),
+                __vadd4(__byte_perm(sy.y & 0x0f0f0f0fu, (sy.y >> 4) & 0x0f0f0f0fu, 0x7362), base4)};
+            unsigned out[8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const unsigned lp0 = __byte_perm(lw[q], 0, 0x4140), ep0 = __byte_perm(ew[q], 0, 0x4140);
+                const unsigned lp1 = __byte_perm(lw[q], 0, 0x4342), ep1 = __byte_perm(ew[q], 0, 0x4342);
+                out[2 * q] = ((lp0 & 0x00800080u) << 8) | (ep0 << 7) | (lp0 & 0x007f007fu);
+                out[2 * q + 1] = ((lp1 & 0x00800080u) << 8) | (ep1 << 7) | (lp1 & 0x007f007fu);
+            }
+            if (g * 16 >= v0 && g * 16 + 16 <= v1) {
+                uint4* d = reinterpret_cast<uint4*>(dst + g * 16);
+                d[0] = make_uint4(out[0], out[1], out[2], out[3]);
+                d[1] = make_uint4(out[4], out[5], out[6], out[7]);
+            } else {  // a range end: only this block's values
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const std::uint64_t v = g * 16 + k;
+                    if (v >= v0 && v < v1) dst[v] = static_cast<std::uint16_t>(out[k >> 1] >> (16 * (k & 1)));
+                }
+            }
+        }
     }
 }
 
@@ -271,23 +421,23 @@ int grid_all(std::uint64_t items, int threads) {  // one thread per item
 }  // namespace
 
 cudaError_t xbh_encode(const std::uint16_t* src, std::uint64_t n, const XbhCode* dcode, std::uint8_t* record,
-                       std::uint64_t* exc, std::uint64_t exc_cap, std::uint32_t* seglen, std::uint32_t* work,
-                       cudaStream_t stream) {
-    if (n % 16 || !src || !dcode || !record || !seglen || !work) return cudaErrorInvalidValue;
+                       std::uint32_t* gaps, std::uint32_t* bases, std::uint64_t* exc, std::uint64_t exc_cap,
+                       std::uint32_t* seglen, std::uint32_t* work, cudaStream_t stream) {
+    if (n % 16 || !src || !dcode || !record || !gaps || !bases || !seglen || !work) return cudaErrorInvalidValue;
     if (n * kXbhMaxLen >= (1ull << 32)) return cudaErrorInvalidValue;  // u32 bit offsets
-    const std::uint64_t nseg = xbh_segments(n);
+    const std::uint64_t nseg = xbh_enc_segments(n);
     std::uint32_t* words = reinterpret_cast<std::uint32_t*>(record + xbh_bits_off(n));
     cudaError_t e = cudaMemsetAsync(words, 0, 4 * xbh_words(n * kXbhMaxLen), stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(gaps, 0, 4 * xbh_gap_words(n * kXbhMaxLen), stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(work, 0, kXbhWorkWords * sizeof(std::uint32_t), stream);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(record + xbh_lut_off(n), dcode->lut, 2 * kXbhLut, cudaMemcpyDeviceToDevice, stream);
+        e = cudaMemcpyAsync(record + xbh_lut_off(n), dcode->lut, 6 * kXbhLut, cudaMemcpyDeviceToDevice, stream);
     if (e != cudaSuccess) return e;
     lo_kernel<<<grid_for(n / 16), kThreads, 0, stream>>>(reinterpret_cast<const uint4*>(src), n / 16,
                                                           reinterpret_cast<uint4*>(record));
     seglen_kernel<<<grid_all(nseg, kThreads), kThreads, 0, stream>>>(reinterpret_cast<const uint4*>(src), n, dcode, seglen);
-    std::uint32_t* seg = reinterpret_cast<std::uint32_t*>(record + xbh_seg_off(n));
-    scan_kernel<<<1, 1024, 0, stream>>>(seglen, nseg, seg, work);
-    emit_kernel<<<grid_all(nseg, kThreads), kThreads, 0, stream>>>(src, n, dcode, seg, words,
+    scan_kernel<<<1, 1024, 0, stream>>>(seglen, nseg, work);
+    emit_kernel<<<grid_all(nseg, kThreads), kThreads, 0, stream>>>(src, n, dcode, seglen, words, gaps, bases,
                                                                     reinterpret_cast<unsigned long long*>(exc), exc_cap,
                                                                     work);
     return cudaGetLastError();
@@ -295,8 +445,23 @@ cudaError_t xbh_encode(const std::uint16_t* src, std::uint64_t n, const XbhCode*
 
 cudaError_t xbh_decode(const std::uint8_t* record, const Xb12Tile& t, std::uint16_t* dst, cudaStream_t stream) {
     if (t.format != 2 || t.n % 16) return cudaErrorInvalidValue;
-    decode_kernel<<<grid_all(xbh_segments(t.n), kDecThreads), kDecThreads, 0, stream>>>(record, t.n,
-                                                                                         reinterpret_cast<uint4*>(dst));
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static std::atomic<unsigned long long> configured{0};  // one bit per device: > 48 KB dynamic smem opted in
+    static std::atomic<int> sms[64];
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    if (!(configured.load() >> dev & 1ull)) {
+        e = cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDecSmem));
+        int v = 0;
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+        sms[dev].store(v);
+        configured.fetch_or(1ull << dev);
+    }
+    const std::uint64_t blocks = xbh_blocks(t.code_bits);
+    const int grid = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(blocks, 6ull * sms[dev].load())));
+    decode_kernel<<<grid, kDecThreads, kDecSmem, stream>>>(record, t.n, t.code_bits, t.base, dst);
     if (t.n_exc)
         patch_kernel<<<grid_for(t.n_exc), kThreads, 0, stream>>>(
             reinterpret_cast<const unsigned long long*>(record + t.exc_off), t.n_exc, dst);
@@ -305,22 +470,24 @@ cudaError_t xbh_decode(const std::uint8_t* record, const Xb12Tile& t, std::uint1
 
 void xbh_decode_host(const std::uint8_t* record, const Xb12Tile& t, std::uint16_t* dst, std::uint64_t i0,
                      std::uint64_t count) {
+    if (!count) return;
     const std::uint16_t* lut = reinterpret_cast<const std::uint16_t*>(record + xbh_lut_off(t.n));
-    const std::uint32_t* seg = reinterpret_cast<const std::uint32_t*>(record + xbh_seg_off(t.n));
     const std::uint32_t* words = reinterpret_cast<const std::uint32_t*>(record + xbh_bits_off(t.n));
+    const std::uint32_t* gaps = reinterpret_cast<const std::uint32_t*>(record + xbh_gap_off(t.n, t.code_bits));
+    const std::uint32_t* bases = reinterpret_cast<const std::uint32_t*>(record + xbh_base_off(t.n, t.code_bits));
+    const std::uint64_t blocks = xbh_blocks(t.code_bits);
+    // the last block whose first code is at or before value i0
+    const std::uint64_t b = static_cast<std::uint64_t>(std::upper_bound(bases, bases + blocks, i0) - bases) - 1;
+    std::uint64_t pos = b * kXbhBlockBits + (gaps[(b * kXbhBlockChunks) >> 3] & 15u);
     const std::uint64_t end = i0 + count;
-    for (std::uint64_t s = i0 / kXbhSeg; s * kXbhSeg < end; ++s) {
-        std::uint64_t pos = seg[s];
-        const std::uint64_t v1 = std::min<std::uint64_t>(end, (s + 1) * kXbhSeg);
-        for (std::uint64_t i = s * kXbhSeg; i < v1; ++i) {
-            const std::uint64_t w = pos >> 5;
-            const unsigned long long win = (static_cast<unsigned long long>(words[w]) << 32) | words[w + 1];
-            const unsigned e = lut[(win << (pos & 31)) >> (64 - kXbhMaxLen)];
-            pos += e >> 8;
-            if (i < i0) continue;
-            const unsigned b = record[i];
-            dst[i - i0] = static_cast<std::uint16_t>(((b & 0x80u) << 8) | ((e & 0xffu) << 7) | (b & 0x7fu));
-        }
+    for (std::uint64_t i = bases[b]; i < end; ++i) {
+        const std::uint64_t w = pos >> 5;
+        const unsigned long long win = (static_cast<unsigned long long>(words[w]) << 32) | words[w + 1];
+        const unsigned e = lut[(win << (pos & 31)) >> (64 - kXbhMaxLen)];
+        pos += e >> 8;
+        if (i < i0) continue;
+        const unsigned lb = record[i];
+        dst[i - i0] = static_cast<std::uint16_t>(((lb & 0x80u) << 8) | ((e & 0xffu) << 7) | (lb & 0x7fu));
     }
     const std::uint64_t* exc = reinterpret_cast<const std::uint64_t*>(record + t.exc_off);
     const std::uint64_t* it = std::lower_bound(exc, exc + t.n_exc, i0 << 16);

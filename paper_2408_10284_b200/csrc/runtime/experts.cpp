@@ -172,13 +172,16 @@ void encode_block(ExpertStore& st, int b, const std::uint16_t* d_raw, Xb12Scratc
 // The same for XBH records: exponent histograms -> per-tile Huffman codes (host) -> device encode
 // -> records D2H; a tile whose escapes exceed n / 64 or whose record would not shrink stays raw.
 struct XbhScratch {
-    DeviceBuffer rec, exc, seglen, work, code;
+    DeviceBuffer rec, gaps, bases, exc, seglen, work, code;
 };
 void encode_block_xbh(ExpertStore& st, int b, const std::uint16_t* d_raw, XbhScratch& x, cudaStream_t s) {
-    const std::uint64_t n = st.tile_bytes / 2, cap = n / 64, nseg = xbh_segments(n);
-    const size_t region = xbh_region_bytes(n);
+    const std::uint64_t n = st.tile_bytes / 2, cap = n / 64, nseg = xbh_enc_segments(n);
+    const std::uint64_t max_bits = n * kXbhMaxLen;
+    const size_t region = xbh_region_bytes(n), gw = xbh_gap_words(max_bits), bw = xbh_blocks(max_bits) + 1;
     const int T = st.tiles;
     x.rec.reserve(region * T);
+    x.gaps.reserve(4 * gw * T);
+    x.bases.reserve(4 * bw * T);
     x.exc.reserve(cap * 8 * T);
     x.seglen.reserve(4 * (nseg + 1) * T);
     x.work.reserve(sizeof(std::uint32_t) * (256 + kXbhWorkWords) * T);
@@ -195,6 +198,7 @@ void encode_block_xbh(ExpertStore& st, int b, const std::uint16_t* d_raw, XbhScr
     XbhCode* dcode = x.code.as<XbhCode>();
     for (int t = 0; t < T; ++t)
         MOE_CUDA(xbh_encode(d_raw + n * t, n, dcode + t, x.rec.as<std::uint8_t>() + region * t,
+                            x.gaps.as<std::uint32_t>() + gw * t, x.bases.as<std::uint32_t>() + bw * t,
                             x.exc.as<std::uint64_t>() + cap * t, cap, x.seglen.as<std::uint32_t>() + (nseg + 1) * t,
                             work + kXbhWorkWords * t, s));
     std::vector<std::uint32_t> wk(kXbhWorkWords * static_cast<size_t>(T));
@@ -208,29 +212,39 @@ void encode_block_xbh(ExpertStore& st, int b, const std::uint16_t* d_raw, XbhScr
         m.n = n;
         m.base = codes[t].base;
         m.n_exc = wk[kXbhWorkWords * t];
-        if (m.n_exc <= cap) xbh_layout(m, wk[kXbhWorkWords * t + 1]);
+        const std::uint64_t bits = wk[kXbhWorkWords * t + 1];
+        if (m.n_exc <= cap) xbh_layout(m, bits);
         unsigned char* dst = st.blocks[b] + off;
         st.tile_off[static_cast<size_t>(b) * T + t] = off;
         if (m.n_exc > cap || m.bytes >= st.tile_bytes) {  // does not pay: keep the raw tile
+            m = Xb12Tile{};
             m.format = 0;
+            m.n = n;
             m.bytes = st.tile_bytes;
             MOE_CUDA(cudaMemcpyAsync(dst, d_raw + n * t, st.tile_bytes, cudaMemcpyDeviceToHost, s));
         } else {
             m.format = 2;
+            // every byte of the record is written (alignment gaps zero): a pure function of the tile
+            std::memset(dst, 0, m.bytes);
             const unsigned char* r = x.rec.as<unsigned char>() + region * t;
-            const size_t head = xbh_bits_off(n) + 4 * xbh_words(wk[kXbhWorkWords * t + 1]);
-            MOE_CUDA(cudaMemcpyAsync(dst, r, head, cudaMemcpyDeviceToHost, s));
-            // alignment gaps are zero (a record is a pure function of the tile, even over an old block)
-            std::memset(dst + head, 0, m.exc_off - head);
-            std::memset(dst + m.exc_off + m.n_exc * 8, 0, m.bytes - m.exc_off - m.n_exc * 8);
+            const size_t hdr = xbh_hdr_off(n), bo = xbh_bits_off(n), go = xbh_gap_off(n, bits), so = xbh_base_off(n, bits);
+            const std::uint64_t blocks = xbh_blocks(bits);
+            MOE_CUDA(cudaMemcpyAsync(dst, r, hdr, cudaMemcpyDeviceToHost, s));
+            MOE_CUDA(cudaMemcpyAsync(dst + bo, r + bo, 4 * xbh_words(bits), cudaMemcpyDeviceToHost, s));
+            MOE_CUDA(cudaMemcpyAsync(dst + go, x.gaps.as<std::uint32_t>() + gw * t, 4 * xbh_gap_words(bits),
+                                     cudaMemcpyDeviceToHost, s));
+            MOE_CUDA(cudaMemcpyAsync(dst + so, x.bases.as<std::uint32_t>() + bw * t, 4 * blocks, cudaMemcpyDeviceToHost, s));
+            const std::uint64_t hv[2] = {bits, m.n_exc};
+            std::memcpy(dst + hdr, hv, sizeof hv);
+            const std::uint32_t last = static_cast<std::uint32_t>(n);
+            std::memcpy(dst + so + 4 * blocks, &last, 4);
             exc.resize(m.n_exc);
-            if (m.n_exc) {
+            if (m.n_exc)
                 MOE_CUDA(cudaMemcpyAsync(exc.data(), x.exc.as<std::uint64_t>() + cap * t, m.n_exc * 8,
                                          cudaMemcpyDeviceToHost, s));
-                MOE_CUDA(cudaStreamSynchronize(s));
-                std::sort(exc.begin(), exc.end());
-                std::memcpy(dst + m.exc_off, exc.data(), m.n_exc * 8);
-            }
+            MOE_CUDA(cudaStreamSynchronize(s));
+            std::sort(exc.begin(), exc.end());  // ascending index (the escapes arrive unordered)
+            if (m.n_exc) std::memcpy(dst + m.exc_off, exc.data(), m.n_exc * 8);
         }
         off += m.bytes;
         if (off > st.expert_bytes) fail(Status::Internal, "xbh: records exceed the expert block");

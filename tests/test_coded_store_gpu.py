@@ -28,9 +28,9 @@ def _record_bytes(eng, l, e, t):
     return bytes((C.c_uint8 * r["bytes"]).from_address(r["ptr"])), r
 
 
-# (restatement, format code, link-bytes ratio bound at Mixtral width; XBH's 8 KB decode table per
-# tile weighs more on the tiny shape's 344 KB tiles)
-FORMATS = {"xb12": (X, 1, 0.76), "xbh": (XH, 2, 0.67)}
+# (restatement, format code, link-bytes ratio bound at Mixtral width; XBH's 24 KB of decode tables
+# per tile weigh more on the tiny shape's 344 KB tiles)
+FORMATS = {"xb12": (X, 1, 0.76), "xbh": (XH, 2, 0.675)}
 
 
 @pytest.mark.parametrize("store", ["xb12", "xbh"])
@@ -40,7 +40,7 @@ def test_store_records_match_reference_encoder(d, f, tiles, store):
     with P.Engine(P.ModelSpec(2, 4, 2, d)) as eng:
         eng.experts_init(f, tiles, seed=5, store_format=store)
         fmt, link = eng.experts_format()
-        assert fmt == store and link < (ratio if d >= 4096 else ratio + 0.05) * 8 * 3 * f * d * 2
+        assert fmt == store and link < (ratio if d >= 4096 else ratio + 0.08) * 8 * 3 * f * d * 2
         n = 3 * f * d // tiles
         for l, e in [(0, 0), (1, 3)]:
             raw = O.expert_init(5, l, e, d, f, tiles)
@@ -117,7 +117,7 @@ def test_decode_over_coded_store_is_bit_identical(name, store, tmp_path):
     assert not TL.check_conservation(ev, r1.metrics, s1)
 
 
-@pytest.mark.parametrize("store,lo,hi", [("xb12", 0.74, 0.76), ("xbh", 0.65, 0.67)])
+@pytest.mark.parametrize("store,lo,hi", [("xb12", 0.74, 0.76), ("xbh", 0.655, 0.675)])
 def test_decode_mixtral_width_coded_vs_bf16(store, lo, hi):
     """88 MB tiles (66 / 58 MB records) through the staging ring and the decode stream: outputs and
     trace identical to the bf16 store, link bytes ~75 % (XB12) / ~66 % (XBH)."""
@@ -143,7 +143,8 @@ def test_decode_mixtral_width_coded_vs_bf16(store, lo, hi):
     (h0, r0, s0), (h1, r1, s1) = outs
     assert np.array_equal(h0, h1)
     assert r0.metrics == r1.metrics and np.array_equal(r0.timeline, r1.timeline)
-    assert lo < s1["copy_bytes"] / s0["copy_bytes"] < hi
+    # bytes per issued tile (how many queued prefetches get cancelled depends on physical timing)
+    assert lo < (s1["copy_bytes"] / s1["tile_copies"]) / (s0["copy_bytes"] / s0["tile_copies"]) < hi
 
 
 @pytest.mark.parametrize("store", ["xb12", "xbh"])

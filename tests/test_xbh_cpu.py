@@ -43,13 +43,13 @@ def test_roundtrip_gaussian_and_escapes():
     assert np.array_equal(X.decode(rec, meta, w.size), w)
 
 
-def test_partial_last_segment_and_single_symbol():
+def test_ragged_blocks_and_single_symbol():
     rng = np.random.default_rng(3)
-    w = _bf16(rng.standard_normal(512 * 40 + 48) * 0.02)  # last segment: 48 values
+    w = _bf16(rng.standard_normal(3 * 12800 + 48) * 0.02)  # ~3 decode blocks, the last one partial
     rec, meta = X.encode(w)
     assert meta["format"] == 2 and np.array_equal(X.decode(rec, meta, w.size), w)
-    one = np.full(1 << 16, 0x3F80, dtype=np.uint16)  # every exponent equal: one 1-bit code
-    base, ln, code, lut = X.build_code(np.bincount((one >> 7) & 0xFF, minlength=256))
+    one = np.full(1 << 17, 0x3F80, dtype=np.uint16)  # every exponent equal: one 1-bit code
+    base, ln, code, lut, _ = X.build_code(np.bincount((one >> 7) & 0xFF, minlength=256))
     assert sorted(x for x in ln if x) == [1]
     rec, meta = X.encode(one)
     assert meta["total_bits"] == one.size and np.array_equal(X.decode(rec, meta, one.size), one)
@@ -66,7 +66,7 @@ def test_code_is_prefix_free_optimal_and_length_limited():
             hist[start:start + k] = (rng.random(k) ** 8 * 1e6).astype(np.int64) + 1
         else:
             hist[start:start + k] = (2.0 ** -np.arange(k) * 1e7).astype(np.int64) + 1
-        base, ln, code, lut = X.build_code(hist)
+        base, ln, code, lut, mlut = X.build_code(hist)
         used = [s for s in range(16) if ln[s]]
         assert max(ln) <= X.MAX_LEN
         assert abs(sum(2.0 ** -ln[s] for s in used) - 1.0) < 1e-12  # complete prefix code
@@ -74,6 +74,18 @@ def test_code_is_prefix_free_optimal_and_length_limited():
             sh = X.MAX_LEN - ln[s]
             ent = lut[code[s] << sh: (code[s] + 1) << sh]
             assert np.all(ent >> 8 == ln[s])
+        # the multi-code table decodes the same symbols and lengths as the single-code walk
+        sym_of = {((base + k) & 0xFF): k for k in range(15)}
+        for i in rng.integers(0, 1 << X.MAX_LEN, 64):
+            m = int(mlut[i])
+            pos = 0
+            for q in range((m >> 24) & 3):
+                p12 = (int(i) << pos) & ((1 << X.MAX_LEN) - 1)
+                e = int(lut[p12])
+                s_ = 15 if (ln[15] and p12 >> (X.MAX_LEN - ln[15]) == code[15]) else sym_of[e & 0xFF]
+                assert (m >> (4 * q)) & 15 == s_ and (m >> (12 + 4 * q)) & 15 == e >> 8
+                pos += e >> 8
+            assert pos == m >> 26
         counts = list(hist[base:base + 15]) + [int(hist.sum() - hist[base:base + 15].sum())]
         cost = sum(counts[s] * ln[s] for s in used)
         ref = _huffman_cost(counts)
@@ -85,7 +97,7 @@ def test_code_is_prefix_free_optimal_and_length_limited():
 
 def test_mixtral_like_tile_size():
     rng = np.random.default_rng(5)
-    n = 1 << 20
+    n = 1 << 22  # 8 MB of bf16: the 24 KB of tables are ~0.05 bits per value
     x = (rng.integers(0, 65536, (4, n)).sum(0) - 4 * 32767.5) / (37837.22 * 64)
     w = (x.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
     rec, meta = X.encode(w)

@@ -1,12 +1,13 @@
 """numpy restatement of the XBH tile record (paper_2408_10284_b200/csrc/kernels/xbh.hpp) — test
 infrastructure: encodes a bf16 tile the way the store's encoder must (XB12's 15-exponent window,
 package-merge code lengths <= 12 over the 16 symbol counts with leaves before packages on equal
-weight, canonical codes by (length, symbol), 512-value segments, escapes ascending) and decodes
-records."""
+weight, canonical codes by (length, symbol), single- and multi-code tables, 128-bit chunk gaps and
+per-block value bases, escapes ascending) and decodes records."""
 import numpy as np
 
 MAX_LEN = 12
-SEG = 512
+CHUNK = 128           # bits per independently decodable chunk
+BLOCK = 256 * CHUNK   # bits per output-base entry
 
 
 def align(v, a=16):
@@ -17,24 +18,40 @@ def lut_off(n):
     return align(n)
 
 
-def seg_off(n):
+def mlut_off(n):
     return lut_off(n) + 2 * (1 << MAX_LEN)
 
 
-def segments(n):
-    return (n + SEG - 1) // SEG
+def hdr_off(n):
+    return mlut_off(n) + 4 * (1 << MAX_LEN)
 
 
 def bits_off(n):
-    return align(seg_off(n) + 4 * (segments(n) + 1))
+    return hdr_off(n) + 16
 
 
 def words(total_bits):
-    return (total_bits + 31) // 32 + 2
+    return (total_bits + 31) // 32 + 8
+
+
+def chunks(bits):
+    return (bits + CHUNK - 1) // CHUNK
+
+
+def blocks(bits):
+    return (bits + BLOCK - 1) // BLOCK
+
+
+def gap_off(n, bits):
+    return align(bits_off(n) + 4 * words(bits))
+
+
+def base_off(n, bits):
+    return align(gap_off(n, bits) + 4 * ((chunks(bits) + 7) // 8))
 
 
 def build_code(hist):
-    """hist[256] exponent counts -> (base, len[16], code[16], lut[4096])."""
+    """hist[256] exponent counts -> (base, len[16], code[16], lut[4096], mlut[4096])."""
     hist = [int(h) for h in hist]
     total = sum(hist)
     best, base = 0, 0
@@ -86,7 +103,29 @@ def build_code(hist):
         if ln[s]:
             sh = MAX_LEN - ln[s]
             lut[code[s] << sh:(code[s] + 1) << sh] = (((base + s) if s < 15 else 0) & 0xFF) | (ln[s] << 8)
-    return base, ln, code, lut
+    sym_lut = np.zeros(1 << MAX_LEN, dtype=np.int64)  # symbol | length << 8
+    for s in range(16):
+        if ln[s]:
+            sh = MAX_LEN - ln[s]
+            sym_lut[code[s] << sh:(code[s] + 1) << sh] = s | (ln[s] << 8)
+    # multi-code table: up to 3 consecutive codes ending inside the 12-bit peek: symbols (4 bits
+    # each) | lengths (4 bits each) << 12 | count << 24 | total length << 26
+    mlut = np.zeros(1 << MAX_LEN, dtype=np.uint32)
+    for i in range(1 << MAX_LEN):
+        L = syms = lens = cnt = 0
+        for k in range(3):
+            if L >= MAX_LEN:
+                break
+            e = int(sym_lut[(i << L) & ((1 << MAX_LEN) - 1)])
+            l2 = e >> 8
+            if l2 == 0 or L + l2 > MAX_LEN:
+                break
+            syms |= (e & 15) << (4 * k)
+            lens |= l2 << (4 * k)
+            cnt += 1
+            L += l2
+        mlut[i] = syms | (lens << 12) | (cnt << 24) | (L << 26)
+    return base, ln, code, lut, mlut
 
 
 def encode(bits: np.ndarray):
@@ -94,7 +133,7 @@ def encode(bits: np.ndarray):
     v = np.ascontiguousarray(bits, dtype=np.uint16).astype(np.uint32)
     n = v.size
     e = (v >> 7) & 0xFF
-    base, ln, code, lut = build_code(np.bincount(e, minlength=256))
+    base, ln, code, lut, mlut = build_code(np.bincount(e, minlength=256))
     s = e.astype(np.int64) - base
     esc = (s < 0) | (s >= 15)
     sym = np.where(esc, 15, s)
@@ -105,57 +144,90 @@ def encode(bits: np.ndarray):
     end = np.cumsum(L)
     pos = end - L
     total = int(end[-1])
-    seg = np.append(pos[::SEG], total).astype(np.uint32)
     nw = words(total)
-    exc_off = align(bits_off(n) + 4 * nw)
+    nb = blocks(total)
+    exc_off = align(base_off(n, total) + 4 * (nb + 1))
     nbytes = align(exc_off + 8 * n_exc, 256)
     if n_exc > n // 64 or nbytes >= 2 * n:
         return bits.tobytes(), {"format": 0, "base": base, "n_exc": n_exc, "bytes": 2 * n}
+    # chunk gaps: the first code starting in each 128-bit chunk; block bases: its value index
+    c = pos // CHUNK
+    first = np.ones(n, dtype=bool)
+    first[1:] = c[1:] != c[:-1]
+    gaps = np.zeros(chunks(total), dtype=np.uint32)
+    gaps[c[first]] = (pos[first] - c[first] * CHUNK).astype(np.uint32)
+    gw = np.zeros((chunks(total) + 7) // 8, dtype=np.uint32)
+    for k in range(8):
+        part = gaps[k::8]
+        gw[:part.size] |= part << np.uint32(4 * k)
+    idx_first = np.nonzero(first)[0]
+    blk_first = (c[first] % 256) == 0
+    bases = np.append(idx_first[blk_first], n).astype(np.uint32)
+    assert bases.size == nb + 1
     bitarr = np.zeros(32 * nw, dtype=np.uint8)
     for j in range(MAX_LEN):
         m = L > j
         bitarr[pos[m] + j] = (C[m] >> (L[m] - 1 - j)) & 1
-    wbytes = np.packbits(bitarr)  # MSB first; a word's 4 bytes big-endian
-    wds = wbytes.view(">u4").astype("<u4")
+    wds = np.packbits(bitarr).view(">u4").astype("<u4")  # MSB first; a word's 4 bytes big-endian
     lo = (((v >> 8) & 0x80) | (v & 0x7F)).astype(np.uint8)
     idx = np.nonzero(esc)[0].astype(np.uint64)
     exc = (idx << np.uint64(16)) | v[esc].astype(np.uint64)
     rec = np.zeros(nbytes, dtype=np.uint8)
     rec[:n] = lo
     rec[lut_off(n):lut_off(n) + 2 * lut.size] = lut.view(np.uint8)
-    rec[seg_off(n):seg_off(n) + 4 * seg.size] = seg.view(np.uint8)
+    rec[mlut_off(n):mlut_off(n) + 4 * mlut.size] = mlut.view(np.uint8)
+    rec[hdr_off(n):hdr_off(n) + 16] = np.array([total, n_exc], dtype=np.uint64).view(np.uint8)
     rec[bits_off(n):bits_off(n) + 4 * nw] = wds.view(np.uint8)
+    rec[gap_off(n, total):gap_off(n, total) + 4 * gw.size] = gw.view(np.uint8)
+    rec[base_off(n, total):base_off(n, total) + 4 * bases.size] = bases.view(np.uint8)
     rec[exc_off:exc_off + 8 * n_exc] = exc.view(np.uint8)
-    return rec.tobytes(), {"format": 2, "base": base, "n_exc": n_exc, "nib_off": seg_off(n), "exc_off": exc_off,
+    return rec.tobytes(), {"format": 2, "base": base, "n_exc": n_exc, "nib_off": hdr_off(n), "exc_off": exc_off,
                            "bytes": nbytes, "total_bits": total, "len": ln}
 
 
 def decode(rec: bytes, meta: dict, n: int) -> np.ndarray:
+    """The GPU decoder's scheme: every chunk walks the multi-code table from its gap, keeping the
+    codes that start inside it; chunk outputs are concatenated in order (value positions = prefix
+    sums of the chunk counts, checked against the block bases)."""
     r = np.frombuffer(rec, dtype=np.uint8)
     if meta["format"] == 0:
         return r[:2 * n].view(np.uint16).copy()
-    lut = r[lut_off(n):lut_off(n) + 2 * (1 << MAX_LEN)].view(np.uint16)
-    seg = r[seg_off(n):seg_off(n) + 4 * (segments(n) + 1)].view(np.uint32)
-    total = int(seg[-1])
+    mlut = r[mlut_off(n):mlut_off(n) + 4 * (1 << MAX_LEN)].view(np.uint32).astype(np.int64)
+    total, n_exc = (int(x) for x in r[hdr_off(n):hdr_off(n) + 16].view(np.uint64))
     nw = words(total)
-    wds = r[bits_off(n):bits_off(n) + 4 * nw].view(np.uint32).astype(">u4")
-    bitarr = np.unpackbits(wds.view(np.uint8))
-    # walk the codes value by value (vectorised over segments: each segment's position advances
-    # independently, one value per step)
-    nseg = segments(n)
-    p = seg[:-1].astype(np.int64)
-    ex = np.zeros(nseg * SEG, dtype=np.uint32)
+    bitarr = np.unpackbits(r[bits_off(n):bits_off(n) + 4 * nw].view(np.uint32).astype(">u4").view(np.uint8))
+    nc = chunks(total)
+    gw = r[gap_off(n, total):gap_off(n, total) + 4 * ((nc + 7) // 8)].view(np.uint32)
+    gaps = np.array([(int(gw[c >> 3]) >> (4 * (c & 7))) & 15 for c in range(nc)], dtype=np.int64)
+    bases = r[base_off(n, total):base_off(n, total) + 4 * (blocks(total) + 1)].view(np.uint32)
+    base = meta["base"]
+    cid = np.arange(nc, dtype=np.int64)
+    pos = cid * CHUNK + gaps
+    stop = np.minimum((cid + 1) * CHUNK, total)
     weights = (1 << np.arange(MAX_LEN - 1, -1, -1)).astype(np.int64)
-    for k in range(SEG):
-        idx = p[:, None] + np.arange(MAX_LEN)[None, :]
-        peek = (bitarr[np.minimum(idx, bitarr.size - 1)].astype(np.int64) * weights).sum(axis=1)
-        ent = lut[peek]
-        ex[np.arange(nseg) * SEG + k] = ent & 0xFF
-        p += ent >> 8
-    ex = ex[:n]
+    out_syms = [[] for _ in range(nc)]
+    active = pos < stop
+    while active.any():
+        ids = np.nonzero(active)[0]
+        p = pos[ids]
+        peek = (bitarr[p[:, None] + np.arange(MAX_LEN)[None, :]].astype(np.int64) * weights).sum(axis=1)
+        e = mlut[peek]
+        cnt, l0, l1 = (e >> 24) & 3, (e >> 12) & 15, (e >> 16) & 15
+        k = 1 + ((cnt > 1) & (p + l0 < stop[ids])) + ((cnt > 2) & (p + l0 + l1 < stop[ids]))
+        adv = np.where(k == cnt, e >> 26, np.where(k == 1, l0, l0 + l1))
+        for j, i in enumerate(ids):
+            for q in range(int(k[j])):
+                out_syms[i].append((int(e[j]) >> (4 * q)) & 15)
+        pos[ids] = p + adv
+        active = pos < stop
+    counts = np.array([len(x) for x in out_syms], dtype=np.int64)
+    starts = np.concatenate([[0], np.cumsum(counts)])
+    assert starts[-1] == n
+    assert np.array_equal(starts[::256][: bases.size - 1], bases[:-1].astype(np.int64))
+    syms = np.concatenate([np.array(x, dtype=np.uint32) for x in out_syms])
+    ex = (base + syms) & 0xFF
     lo = r[:n].astype(np.uint32)
     out = (((lo & 0x80) << 8) | (ex << 7) | (lo & 0x7F)).astype(np.uint16)
-    m = meta["n_exc"]
-    exc = r[meta["exc_off"]:meta["exc_off"] + 8 * m].view(np.uint64)
+    exc = r[meta["exc_off"]:meta["exc_off"] + 8 * n_exc].view(np.uint64)
     out[(exc >> np.uint64(16)).astype(np.int64)] = (exc & np.uint64(0xFFFF)).astype(np.uint16)
     return out

@@ -1,0 +1,151 @@
+// Microbenchmark of the XBH / XB12 tile decoders (kernels/xbh.cu, kernels/xb12.cu) on one 8x7B-sized
+// tile (88 MB of bf16, 44M values, random-init-like weights): encode on the device, then time the
+// decode with CUDA events, L2 flushed between launches, and check the bits.
+//   nvcc -std=c++20 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo --expt-relaxed-constexpr -fmad=false -I paper_2408_10284_b200/csrc \
+//        tools/xbh_bench.cu paper_2408_10284_b200/csrc/kernels/xbh.cu paper_2408_10284_b200/csrc/kernels/xb12.cu \
+//        -o tools/bin/xbh_bench
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include "kernels/xb12.hpp"
+#include "kernels/xbh.hpp"
+
+using namespace adapmoe;
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess) {                                                           \
+            std::fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+            std::exit(1);                                                                  \
+        }                                                                                  \
+    } while (0)
+
+int main(int argc, char** argv) {
+    const std::uint64_t n = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 3ull * 3584 * 4096;
+    std::vector<std::uint16_t> h(n);
+    std::mt19937_64 rng(1);
+    for (std::uint64_t i = 0; i < n; ++i) {  // sum of 4 uniform 16-bit lanes ~ N(0, 1 / sqrt(4096))
+        const std::uint64_t r = rng();
+        double s = 0;
+        for (int k = 0; k < 4; ++k) s += static_cast<double>((r >> (16 * k)) & 0xffff);
+        const float f = static_cast<float>((s - 4 * 32767.5) / (37837.22 * 64.0));
+        std::uint32_t u;
+        std::memcpy(&u, &f, 4);
+        h[i] = static_cast<std::uint16_t>(u >> 16);
+    }
+    std::uint16_t *d_raw, *d_out;
+    CK(cudaMalloc(&d_raw, n * 2));
+    CK(cudaMalloc(&d_out, n * 2));
+    CK(cudaMemcpy(d_raw, h.data(), n * 2, cudaMemcpyHostToDevice));
+    // encode (XBH)
+    std::uint32_t* hist;
+    CK(cudaMalloc(&hist, 256 * 4));
+    CK(xb12_histogram(d_raw, n, hist, 0));
+    std::vector<std::uint32_t> hh(256);
+    CK(cudaMemcpy(hh.data(), hist, 1024, cudaMemcpyDeviceToHost));
+    XbhCode code;
+    xbh_build_code(hh.data(), code);
+    XbhCode* dcode;
+    CK(cudaMalloc(&dcode, sizeof(XbhCode)));
+    CK(cudaMemcpy(dcode, &code, sizeof(XbhCode), cudaMemcpyHostToDevice));
+    std::uint8_t* region_buf;
+    const std::uint64_t region = xbh_region_bytes(n), cap = n / 64, max_bits = n * kXbhMaxLen;
+    CK(cudaMalloc(&region_buf, region));
+    std::uint64_t* exc;
+    CK(cudaMalloc(&exc, cap * 8));
+    std::uint32_t *seglen, *work, *gaps, *bases;
+    CK(cudaMalloc(&seglen, 4 * (xbh_enc_segments(n) + 1)));
+    CK(cudaMalloc(&work, 64));
+    CK(cudaMalloc(&gaps, 4 * xbh_gap_words(max_bits)));
+    CK(cudaMalloc(&bases, 4 * (xbh_blocks(max_bits) + 1)));
+    CK(xbh_encode(d_raw, n, dcode, region_buf, gaps, bases, exc, cap, seglen, work, 0));
+    std::uint32_t wk[2];
+    CK(cudaMemcpy(wk, work, 8, cudaMemcpyDeviceToHost));
+    Xb12Tile t;
+    t.format = 2;
+    t.n = n;
+    t.base = code.base;
+    t.n_exc = wk[0];
+    xbh_layout(t, wk[1]);
+    // assemble the record the way the store does (escapes unsorted: the patch kernel does not care)
+    std::uint8_t* rec;
+    CK(cudaMalloc(&rec, t.bytes));
+    CK(cudaMemset(rec, 0, t.bytes));
+    CK(cudaMemcpy(rec, region_buf, xbh_bits_off(n) + 4 * xbh_words(wk[1]), cudaMemcpyDeviceToDevice));
+    CK(cudaMemcpy(rec + xbh_gap_off(n, wk[1]), gaps, 4 * xbh_gap_words(wk[1]), cudaMemcpyDeviceToDevice));
+    const std::uint64_t nb = xbh_blocks(wk[1]);
+    CK(cudaMemcpy(rec + xbh_base_off(n, wk[1]), bases, 4 * nb, cudaMemcpyDeviceToDevice));
+    const std::uint32_t last = static_cast<std::uint32_t>(n);
+    CK(cudaMemcpy(rec + xbh_base_off(n, wk[1]) + 4 * nb, &last, 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(rec + t.exc_off, exc, t.n_exc * 8, cudaMemcpyDeviceToDevice));
+    std::printf("n %llu values: record %.1f MB (%.2f bits/value, codes %.3f bits/value), %llu escapes\n",
+                (unsigned long long)n, t.bytes / 1e6, 8.0 * t.bytes / n, double(wk[1]) / n, (unsigned long long)t.n_exc);
+    // L2 flush buffer
+    void* flush;
+    const size_t fb = 256ull << 20;
+    CK(cudaMalloc(&flush, fb));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    float best = 1e30f, sum = 0;
+    const int reps = 20;
+    for (int r = 0; r < reps + 3; ++r) {
+        CK(cudaMemset(flush, r, fb));
+        CK(cudaMemset(d_out, 0, n * 2));
+        CK(cudaEventRecord(a));
+        CK(xbh_decode(rec, t, d_out, 0));
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        if (r >= 3) {
+            best = std::min(best, ms);
+            sum += ms;
+        }
+    }
+    std::vector<std::uint16_t> o(n);
+    CK(cudaMemcpy(o.data(), d_out, n * 2, cudaMemcpyDeviceToHost));
+    std::uint64_t bad = 0;
+    for (std::uint64_t i = 0; i < n; ++i) bad += o[i] != h[i];
+    const double bytes = static_cast<double>(t.bytes) + 2.0 * n;
+    std::printf("XBH decode: best %.1f us, mean %.1f us, %.0f GB/s (record read + bf16 written), mismatches %llu\n",
+                best * 1e3, sum / reps * 1e3, bytes / (best * 1e-3) / 1e9, (unsigned long long)bad);
+    // XB12 for comparison
+    std::uint32_t* work12;
+    CK(cudaMalloc(&work12, kXb12WorkWords * 4));
+    std::uint8_t* rec12;
+    const std::uint64_t lo_nib = xb12_align(xb12_align(n) + n / 2);
+    CK(cudaMalloc(&rec12, lo_nib + cap * 8));
+    CK(xb12_encode(d_raw, n, rec12, rec12 + xb12_align(n), reinterpret_cast<std::uint64_t*>(rec12 + lo_nib), cap, work12, 0));
+    std::vector<std::uint32_t> w12(kXb12WorkWords);
+    CK(cudaMemcpy(w12.data(), work12, kXb12WorkWords * 4, cudaMemcpyDeviceToHost));
+    Xb12Tile t12;
+    t12.format = 1;
+    t12.n = n;
+    t12.base = w12[256];
+    t12.n_exc = w12[257];
+    xb12_layout(t12);
+    best = 1e30f;
+    for (int r = 0; r < reps + 3; ++r) {
+        CK(cudaMemset(flush, r, fb));
+        CK(cudaEventRecord(a));
+        CK(xb12_decode(rec12, t12, d_out, 0));
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        if (r >= 3) best = std::min(best, ms);
+    }
+    CK(cudaMemcpy(o.data(), d_out, n * 2, cudaMemcpyDeviceToHost));
+    bad = 0;
+    for (std::uint64_t i = 0; i < n; ++i) bad += o[i] != h[i];
+    std::printf("XB12 decode: best %.1f us, %.0f GB/s, mismatches %llu\n", best * 1e3,
+                (static_cast<double>(t12.bytes) + 2.0 * n) / (best * 1e-3) / 1e9, (unsigned long long)bad);
+    return 0;
+}

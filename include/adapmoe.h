@@ -483,6 +483,9 @@ typedef struct {
     int64_t router_launches;      /* K1 launches: one per layer (free-running), one per token window (trace replay) */
     int64_t spec_launches;        /* free-running batch 1: speculative next-layer FFN launches (pre-gate top-1) */
     int64_t spec_hits;            /* ... whose expert the layer's decision selected (partials reused) */
+    double record_decode_ms;      /* coded stores (XB12 / XBH): summed duration of the tile decode kernels */
+    int64_t record_decodes;       /* ... launches (one per coded tile copied) */
+    double record_decode_bytes;   /* ... bytes: records read + bf16 tiles written */
 } moe_decode_stats;
 
 /* Counters so far without ending the session. */

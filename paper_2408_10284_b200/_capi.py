@@ -74,7 +74,8 @@ class DecodeStatsC(C.Structure):
                 ("router_exact_items", C.c_int64), ("host_sync_ms", C.c_double), ("host_step_ms", C.c_double), ("slots_total", C.c_int32), ("staging_high_water", C.c_int32),
                 ("prefetch_copy_ms", C.c_double), ("prefetch_stall_ms", C.c_double),
                 ("prefetch_tile_copies", C.c_int64), ("prefetch_used_copy_ms", C.c_double),
-                ("router_launches", C.c_int64), ("spec_launches", C.c_int64), ("spec_hits", C.c_int64)]
+                ("router_launches", C.c_int64), ("spec_launches", C.c_int64), ("spec_hits", C.c_int64),
+                ("record_decode_ms", C.c_double), ("record_decodes", C.c_int64), ("record_decode_bytes", C.c_double)]
 
 
 _d = C.POINTER(C.c_double)

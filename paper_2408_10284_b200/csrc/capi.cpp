@@ -462,6 +462,9 @@ void export_stats(const DecodeStats& s, moe_decode_stats* out) {
     out->router_launches = s.router_launches;
     out->spec_launches = s.spec_launches;
     out->spec_hits = s.spec_hits;
+    out->record_decode_ms = s.decode_ms;
+    out->record_decodes = s.decode_launches;
+    out->record_decode_bytes = s.decode_bytes;
 }
 }  // namespace
 

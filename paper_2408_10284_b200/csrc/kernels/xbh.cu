@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(kThreads) lo_kernel(const uint4* src, std::uin
 //         (element stores for the two partial 16-value groups at the range ends, which the
 //         neighbouring blocks share), and zeroes the symbol buffer for the next block.
 constexpr int kDecThreads = static_cast<int>(kXbhBlockChunks);
+constexpr std::uint64_t kDecBlocksPerCta = 2;
 constexpr int kDecWords = static_cast<int>(kXbhBlockBits / 32);  // 1024
 constexpr int kDecStage = (kDecWords + 8 + (kDecWords + 8) / 32 + 1 + 3) / 4 * 4;  // padded, 16-byte multiple
 constexpr int kDecExWords = (static_cast<int>(kXbhBlockBits) + 32) / 8;  // <= 1 code per bit (+ slack), 8 per word
@@ -290,9 +291,12 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
         const unsigned w = pos >> 5;
         return __funnelshift_l(sw[padw(w + 1)], sw[padw(w)], pos & 31u) >> (32 - kXbhMaxLen);
     };
-    std::uint64_t b = blockIdx.x;
-    if (b < blocks) prefetch(b);
-    for (; b < blocks; b += gridDim.x) {
+    // kDecBlocksPerCta consecutive blocks per CTA: short-lived CTAs, so a higher-priority kernel (the
+    // FFN on the compute stream) waiting for SM space gets it within one CTA's lifetime
+    std::uint64_t b = static_cast<std::uint64_t>(blockIdx.x) * kDecBlocksPerCta;
+    const std::uint64_t b_end = std::min<std::uint64_t>(blocks, b + kDecBlocksPerCta);
+    if (b < b_end) prefetch(b);
+    for (; b < b_end; ++b) {
         __syncthreads();  // the previous block's merge is done with sw / ex
         {
             const unsigned w = 4u * t;  // 4 words, none crossing a pad (w % 32 <= 28)
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
         __syncthreads();
         // merge
         const std::uint64_t gs = v0 >> 4, ge = (v1 + 15) >> 4;  // 16-value groups touching [v0, v1)
-        if (b + gridDim.x < blocks) prefetch(b + gridDim.x);
+        if (b + 1 < b_end) prefetch(b + 1);
         for (std::uint64_t g = gs + t; g < ge; g += kDecThreads) {
             const uint4 l = __ldg(lo + g);
             const uint2 sy = *reinterpret_cast<const uint2*>(ex + 2 * (g - gs));
@@ -460,7 +464,7 @@ cudaError_t xbh_decode(const std::uint8_t* record, const Xb12Tile& t, std::uint1
         configured.fetch_or(1ull << dev);
     }
     const std::uint64_t blocks = xbh_blocks(t.code_bits);
-    const int grid = static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(blocks, 6ull * sms[dev].load())));
+    const int grid = static_cast<int>(std::max<std::uint64_t>(1, (blocks + kDecBlocksPerCta - 1) / kDecBlocksPerCta));
     decode_kernel<<<grid, kDecThreads, kDecSmem, stream>>>(record, t.n, t.code_bits, t.base, dst);
     if (t.n_exc)
         patch_kernel<<<grid_for(t.n_exc), kThreads, 0, stream>>>(

@@ -196,6 +196,29 @@ double CopyEngine::busy_ms_total(double* prefetch_ms, long long* prefetch_tiles,
     return total;
 }
 
+void CopyEngine::harvest_decodes() {
+    while (!dec_pending_.empty() && cudaEventQuery(dec_pending_.front().end) == cudaSuccess) {
+        const DecodeTiming& d = dec_pending_.front();
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, d.start, d.end) == cudaSuccess) {
+            dec_ms_ += ms;
+            dec_bytes_ += d.bytes;
+            ++dec_launches_;
+        }
+        free_timing_.push_back(d.start);
+        free_timing_.push_back(d.end);
+        dec_pending_.pop_front();
+    }
+}
+
+void CopyEngine::decode_totals(double* ms, long long* launches, double* bytes) {
+    std::lock_guard<std::mutex> g(mu_);
+    harvest_decodes();
+    if (ms) *ms = dec_ms_;
+    if (launches) *launches = dec_launches_;
+    if (bytes) *bytes = dec_bytes_;
+}
+
 void CopyEngine::retire(const std::shared_ptr<CopyJob>& job) {
     std::lock_guard<std::mutex> g(mu_);
     for (int t = 0; t < job->issued_tiles; ++t) {
@@ -325,9 +348,23 @@ void CopyEngine::run() {
             ck(cudaStreamWaitEvent(decode_stream_, staging_landed_[k], 0), "cudaStreamWaitEvent");
             const std::uint8_t* rec = static_cast<const std::uint8_t*>(staging_[k]);
             std::uint16_t* dec = reinterpret_cast<std::uint16_t*>(out);
+            DecodeTiming dt{};
+            {
+                std::lock_guard<std::mutex> g(mu_);
+                harvest_decodes();
+                dt.start = take_event(true);
+                dt.end = take_event(true);
+            }
+            dt.bytes = static_cast<double>(src.bytes) + 2.0 * static_cast<double>(src.meta.n);
+            ck(cudaEventRecord(dt.start, decode_stream_), "cudaEventRecord");
             ck(src.meta.format == 2 ? xbh_decode(rec, src.meta, dec, decode_stream_)
                                     : xb12_decode(rec, src.meta, dec, decode_stream_),
                "tile record decode");
+            ck(cudaEventRecord(dt.end, decode_stream_), "cudaEventRecord");
+            {
+                std::lock_guard<std::mutex> g(mu_);
+                dec_pending_.push_back(dt);
+            }
             ck(cudaEventRecord(job->done[tile], decode_stream_), "cudaEventRecord");
             ck(cudaEventRecord(staging_free_[k], decode_stream_), "cudaEventRecord");
         } else {

@@ -99,6 +99,9 @@ public:
     double busy_ms_total(double* prefetch_ms = nullptr, long long* prefetch_tiles = nullptr,
                          double* prefetch_used_ms = nullptr);
     void retire(const std::shared_ptr<CopyJob>& job);  // accumulate timing + recycle events
+    // Coded-tile decode kernels so far (CUDA events around each decode on the decode stream):
+    // summed duration, launches, and bytes (record read + bf16 tile written).  Waits for none.
+    void decode_totals(double* ms, long long* launches, double* bytes);
     // Physical timeline: from now on every retired tile is appended to `out` with its copy interval
     // relative to `origin` (a timed event recorded on the device); nullptr stops recording.
     // Append the landed, not yet recorded tiles of jobs that have not retired (they still hold slots).
@@ -124,6 +127,14 @@ private:
     void* staging_[kStaging] = {};
     size_t staging_bytes_ = 0;
     cudaEvent_t staging_landed_[kStaging] = {}, staging_free_[kStaging] = {};
+    struct DecodeTiming {
+        cudaEvent_t start, end;
+        double bytes;
+    };
+    std::deque<DecodeTiming> dec_pending_;  // guarded by mu_
+    double dec_ms_ = 0.0, dec_bytes_ = 0.0;
+    long long dec_launches_ = 0;
+    void harvest_decodes();  // caller holds mu_: fold completed decode timings into the totals
     int staging_next_ = 0;
     std::mutex mu_;
     std::condition_variable cv_work_, cv_issued_;

@@ -1263,6 +1263,7 @@ DecodeStats DecodeSession::snapshot() {
     s.tile_copies = copier_->tiles_copied();
     s.copy_bytes = copier_->bytes_copied();
     s.copy_busy_ms = copier_->busy_ms_total(&s.prefetch_copy_ms, &s.prefetch_tiles, &s.prefetch_used_copy_ms);
+    copier_->decode_totals(&s.decode_ms, &s.decode_launches, &s.decode_bytes);
     return s;
 }
 

@@ -49,6 +49,8 @@ struct DecodeStats {
     long long router_exact = 0;  // look-ahead items that needed the exact fp64 path
     double host_sync_ms = 0, host_step_ms = 0;  // host wall time: waiting on K1 / policy step + launches
     int slots_total = 0, staging_high_water = 0;
+    double decode_ms = 0, decode_bytes = 0;  // coded-tile decode kernels (XB12 / XBH): time, bytes
+    long long decode_launches = 0;
 };
 
 class DecodeSession : public DecodeListener {

@@ -453,14 +453,10 @@ cudaError_t xbh_decode(const std::uint8_t* record, const Xb12Tile& t, std::uint1
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     static std::atomic<unsigned long long> configured{0};  // one bit per device: > 48 KB dynamic smem opted in
-    static std::atomic<int> sms[64];
     if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     if (!(configured.load() >> dev & 1ull)) {
         e = cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kDecSmem));
-        int v = 0;
-        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess) return e;
-        sms[dev].store(v);
         configured.fetch_or(1ull << dev);
     }
     const std::uint64_t blocks = xbh_blocks(t.code_bits);

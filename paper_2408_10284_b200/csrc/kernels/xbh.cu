@@ -238,22 +238,25 @@ __global__ void __launch_bounds__(kThreads) lo_kernel(const uint4* src, std::uin
 //  stage: the block's 1024 code words (+8 look-ahead) into shared memory (one pad word per 32: the
 //         lanes' chunks are 4 words apart) — prefetched into registers during the previous block's
 //         merge — and the gap of each thread's chunk;
-//  count: each thread walks its chunk from its gap with the multi-code table (~3 codes per 12-bit
-//         lookup; a lookup whose codes all start inside the chunk is taken whole, the last few are
-//         split where the next chunk begins), counting codes;
-//  scan:  the CTA turns counts into positions in the block's exponent buffer;
-//  write: each thread walks again, OR-ing each lookup's (up to 3) 4-bit symbols into the block's
-//         zeroed symbol buffer at its positions (shared atomics: neighbours share boundary words);
-//  merge: the CTA joins symbols (+ the window base = exponent; escapes are patched afterwards) and
-//         lo bytes into bf16 over the block's value range with 16-byte lo loads and 32-byte stores
-//         (element stores for the two partial 16-value groups at the range ends, which the
-//         neighbouring blocks share), and zeroes the symbol buffer for the next block.
+//  walk:  each thread walks its chunk once from its gap with the multi-code table (~3 codes per
+//         12-bit lookup; a lookup whose codes all start inside the chunk is taken whole, the last few
+//         are split where the next chunk begins), queueing 4-bit symbols in a 64-bit fifo that
+//         spills 8 at a time into the thread's slot (17-word stride: conflict-free spills);
+//  scan:  the CTA turns code counts into the first block-relative value index of every chunk;
+//  merge: per 16-value group of the block's value range, a binary search over those prefix sums
+//         finds the chunk holding the group's first value, the group's 16 symbols are gathered
+//         from one to three slots with funnel shifts, and symbols (+ the window base = exponent;
+//         escapes are patched afterwards) join the lo bytes into bf16: 16-byte lo loads, 32-byte
+//         stores (element stores for the two partial groups at the range ends, which the
+//         neighbouring blocks share).
 constexpr int kDecThreads = static_cast<int>(kXbhBlockChunks);
 constexpr std::uint64_t kDecBlocksPerCta = 2;
 constexpr int kDecWords = static_cast<int>(kXbhBlockBits / 32);  // 1024
 constexpr int kDecStage = (kDecWords + 8 + (kDecWords + 8) / 32 + 1 + 3) / 4 * 4;  // padded, 16-byte multiple
-constexpr int kDecExWords = (static_cast<int>(kXbhBlockBits) + 32) / 8;  // <= 1 code per bit (+ slack), 8 per word
-constexpr size_t kDecSmem = sizeof(std::uint32_t) * (kXbhLut + kDecStage + 2 * (kDecThreads / 32) + kDecExWords);
+constexpr int kDecSlot = static_cast<int>(kXbhChunkBits) / 8 + 1;  // <= 128 codes per chunk, 8 per word, + pad
+constexpr int kDecSlotWords = kDecThreads * kDecSlot + 4;         // + the gather's read-ahead past the last slot
+constexpr size_t kDecSmem = sizeof(std::uint32_t) * (kXbhLut + kDecStage + (kDecThreads + 1) + 2 * (kDecThreads / 32) +
+                                                     kDecSlotWords);
 
 __device__ __forceinline__ unsigned padw(unsigned w) { return w + (w >> 5); }
 
@@ -262,10 +265,10 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
     extern __shared__ __align__(16) std::uint32_t sm[];
     std::uint32_t* mlut = sm;
     std::uint32_t* sw = sm + kXbhLut;
-    std::uint32_t* wsum = sw + kDecStage;
-    std::uint32_t* ex = wsum + 2 * (kDecThreads / 32);  // symbol nibbles, value j of the block at nibble j + (v0 & 15)
+    std::uint32_t* pre = sw + kDecStage;              // [kDecThreads + 1] first value of each chunk (block-relative)
+    std::uint32_t* wsum = pre + kDecThreads + 1;
+    std::uint32_t* slots = wsum + 2 * (kDecThreads / 32);  // [thread][kDecSlot] symbol nibbles
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    for (int i = t; i < kDecExWords; i += kDecThreads) ex[i] = 0;
     const std::uint32_t* words = reinterpret_cast<const std::uint32_t*>(rec + xbh_bits_off(n));
     const std::uint32_t* gaps = reinterpret_cast<const std::uint32_t*>(rec + xbh_gap_off(n, bits));
     const std::uint32_t* bases = reinterpret_cast<const std::uint32_t*>(rec + xbh_base_off(n, bits));
@@ -291,13 +294,14 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
         const unsigned w = pos >> 5;
         return __funnelshift_l(sw[padw(w + 1)], sw[padw(w)], pos & 31u) >> (32 - kXbhMaxLen);
     };
+    std::uint32_t* slot = slots + t * kDecSlot;
     // kDecBlocksPerCta consecutive blocks per CTA: short-lived CTAs, so a higher-priority kernel (the
     // FFN on the compute stream) waiting for SM space gets it within one CTA's lifetime
     std::uint64_t b = static_cast<std::uint64_t>(blockIdx.x) * kDecBlocksPerCta;
     const std::uint64_t b_end = std::min<std::uint64_t>(blocks, b + kDecBlocksPerCta);
     if (b < b_end) prefetch(b);
     for (; b < b_end; ++b) {
-        __syncthreads();  // the previous block's merge is done with sw / ex
+        __syncthreads();  // the previous block's merge is done with sw / slots / pre
         {
             const unsigned w = 4u * t;  // 4 words, none crossing a pad (w % 32 <= 28)
             sw[padw(w)] = pw.x, sw[padw(w) + 1] = pw.y, sw[padw(w) + 2] = pw.z, sw[padw(w) + 3] = pw.w;
@@ -310,29 +314,41 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
         const unsigned end = static_cast<unsigned>(t + 1) * static_cast<unsigned>(kXbhChunkBits);
         const std::uint64_t rem = bits - b * kXbhBlockBits;  // codes start below this in the block
         const unsigned stop = c < chunks ? (end < rem ? end : static_cast<unsigned>(rem)) : 0u;
-        const unsigned start =
+        unsigned pos =
             static_cast<unsigned>(t) * static_cast<unsigned>(kXbhChunkBits) + ((pg >> (4 * (c & 7))) & 15u);
         const std::uint64_t v0 = __ldg(bases + b), v1 = __ldg(bases + b + 1);
         __syncthreads();
-        // count
-        auto partial = [&](unsigned e, unsigned pos, unsigned& k, unsigned& adv) {
-            const unsigned n3 = (e >> 24) & 3u, l0 = (e >> 12) & 15u, l1 = (e >> 16) & 15u;
-            k = 1u + (n3 > 1u && pos + l0 < stop) + (n3 > 2u && pos + l0 + l1 < stop);
-            adv = k == n3 ? e >> 26 : (k == 1u ? l0 : l0 + l1);
+        // walk: symbols into the slot
+        unsigned cnt = 0, nf = 0, sp = 0;
+        unsigned long long fifo = 0;
+        auto spill = [&]() {
+            if (nf >= 8) {
+                slot[sp++] = static_cast<std::uint32_t>(fifo);
+                fifo >>= 32;
+                nf -= 8;
+            }
         };
-        unsigned cnt = 0, pos = start;
-        for (; pos + kXbhMaxLen <= stop;) {  // every code of the lookup starts inside the chunk
+        while (pos + kXbhMaxLen <= stop) {  // every code of the lookup starts inside the chunk
             const unsigned e = mlut[peek(pos)];
-            cnt += (e >> 24) & 3u;
-            pos += e >> 26;
-        }
-        for (; pos < stop;) {
-            unsigned k, adv;
-            partial(mlut[peek(pos)], pos, k, adv);
+            const unsigned k = (e >> 24) & 3u;
+            fifo |= static_cast<unsigned long long>(e & 0xfffu) << (4 * nf);  // unused symbol nibbles are zero
+            nf += k;
             cnt += k;
-            pos += adv;
+            pos += e >> 26;
+            spill();
         }
-        // exclusive scan of the counts over the CTA
+        while (pos < stop) {  // the chunk's last codes: stop where the next chunk's first code starts
+            const unsigned e = mlut[peek(pos)];
+            const unsigned n3 = (e >> 24) & 3u, l0 = (e >> 12) & 15u, l1 = (e >> 16) & 15u;
+            const unsigned k = 1u + (n3 > 1u && pos + l0 < stop) + (n3 > 2u && pos + l0 + l1 < stop);
+            fifo |= static_cast<unsigned long long>(e & ((1u << (4 * k)) - 1u)) << (4 * nf);
+            nf += k;
+            cnt += k;
+            pos += k == n3 ? e >> 26 : (k == 1u ? l0 : l0 + l1);
+            spill();
+        }
+        if (nf) slot[sp] = static_cast<std::uint32_t>(fifo);
+        // scan: pre[t] = first block-relative value of chunk t, pre[256] = the block's value count
         unsigned incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -344,45 +360,44 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
         unsigned before = 0;
 #pragma unroll
         for (int w = 0; w < kDecThreads / 32; ++w) before += w < warp ? wsum[w] : 0u;
-        // write: symbols of the block's j-th value at nibble j + (v0 & 15) (16-value groups stay aligned)
-        {
-            unsigned o = before + incl - cnt + static_cast<unsigned>(v0 & 15);
-            auto put = [&](unsigned syms) {  // up to 3 symbols (12 bits) at nibble o
-                const unsigned sh = 4 * (o & 7);
-                atomicOr(ex + (o >> 3), syms << sh);
-                if (sh > 20) atomicOr(ex + (o >> 3) + 1, syms >> (32 - sh));
-            };
-            for (pos = start; pos + kXbhMaxLen <= stop;) {
-                const unsigned e = mlut[peek(pos)];
-                put(e & 0xfffu);  // a lookup's unused symbol nibbles are zero
-                o += (e >> 24) & 3u;
-                pos += e >> 26;
-            }
-            for (; pos < stop;) {
-                const unsigned e = mlut[peek(pos)];
-                unsigned k, adv;
-                partial(e, pos, k, adv);
-                put(e & ((1u << (4 * k)) - 1u));
-                o += k;
-                pos += adv;
-            }
-        }
+        pre[t] = before + incl - cnt;
+        if (t == kDecThreads - 1) pre[kDecThreads] = before + incl;
         __syncthreads();
         // merge
+        const unsigned total = static_cast<unsigned>(v1 - v0);
         const std::uint64_t gs = v0 >> 4, ge = (v1 + 15) >> 4;  // 16-value groups touching [v0, v1)
         if (b + 1 < b_end) prefetch(b + 1);
         for (std::uint64_t g = gs + t; g < ge; g += kDecThreads) {
             const uint4 l = __ldg(lo + g);
-            const uint2 sy = *reinterpret_cast<const uint2*>(ex + 2 * (g - gs));
-            ex[2 * (g - gs)] = 0;
-            ex[2 * (g - gs) + 1] = 0;
+            // the group's symbols: block-relative values j0 .. j0 + 15 (j0 < 0 in the first group)
+            const int j0 = static_cast<int>(g * 16 - v0);
+            unsigned have = j0 < 0 ? static_cast<unsigned>(-j0) : 0u;  // leading values of another block
+            unsigned j = j0 < 0 ? 0u : static_cast<unsigned>(j0);
+            unsigned long long sy = 0;
+            // chunk holding value j: the last c with pre[c] <= j (pre[] ascending, pre[0] = 0)
+            unsigned ch = 0;
+#pragma unroll
+            for (unsigned step = kDecThreads / 2; step; step >>= 1)
+                if (pre[ch + step] <= j) ch += step;
+            while (have < 16 && j < total) {
+                while (pre[ch + 1] <= j) ++ch;  // skip chunks without codes
+                const unsigned off = j - pre[ch], take = min(pre[ch + 1] - j, 16u - have);
+                const std::uint32_t* sl = slots + ch * kDecSlot + (off >> 3);
+                const unsigned sh = 4 * (off & 7);
+                const unsigned x0 = __funnelshift_r(sl[0], sl[1], sh), x1 = __funnelshift_r(sl[1], sl[2], sh);
+                unsigned long long v = (static_cast<unsigned long long>(x1) << 32) | x0;
+                if (take < 16) v &= (1ull << (4 * take)) - 1ull;
+                sy |= v << (4 * have);
+                have += take;
+                j += take;
+            }
+            const unsigned sx = static_cast<unsigned>(sy), sz = static_cast<unsigned>(sy >> 32);
+            const unsigned ew[4] = {  // nibbles -> bytes + window base: symbols 4q .. 4q+3
+                __vadd4(__byte_perm(sx & 0x0f0f0f0fu, (sx >> 4) & 0x0f0f0f0fu, 0x5140), base4),
+                __vadd4(__byte_perm(sx & 0x0f0f0f0fu, (sx >> 4) & 0x0f0f0f0fu, 0x7362), base4),
+                __vadd4(__byte_perm(sz & 0x0f0f0f0fu, (sz >> 4) & 0x0f0f0f0fu, 0x5140), base4),
+                __vadd4(__byte_perm(sz & 0x0f0f0f0fu, (sz >> 4) & 0x0f0f0f0fu, 0x7362), base4)};
             const unsigned lw[4] = {l.x, l.y, l.z, l.w};
-            // nibbles -> bytes (+ base): symbols 4q..4q+3 of the group
-            const unsigned ew[4] = {
-                __vadd4(__byte_perm(sy.x & 0x0f0f0f0fu, (sy.x >> 4) & 0x0f0f0f0fu, 0x5140), base4),
-                __vadd4(__byte_perm(sy.x & 0x0f0f0f0fu, (sy.x >> 4) & 0x0f0f0f0fu, 0x7362), base4),
-                __vadd4(__byte_perm(sy.y & 0x0f0f0f0fu, (sy.y >> 4) & 0x0f0f0f0fu, 0x5140), base4),
-                __vadd4(__byte_perm(sy.y & 0x0f0f0f0fu, (sy.y >> 4) & 0x0f0f0f0fu, 0x7362), base4)};
             unsigned out[8];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {

@@ -164,3 +164,42 @@ def test_copy_tiles_decodes_coded(store):
         y = eng.expert_ffn(0, 1, x)  # host helper uploads through the decode path too
         yr = O.swiglu(ref, d, f, tiles, x.astype(np.float32))
         assert np.abs(y - yr).max() / np.abs(yr).max() < 1e-4
+
+
+@pytest.mark.parametrize("store", ["xb12", "xbh"])
+def test_degenerate_exponent_tiles(store):
+    """Edge cases of the codes: a tile with a single exponent (XBH: one 1-bit code, 128 codes per
+    128-bit chunk — the decoder's slot capacity), two exponents, and exponents far outside any window
+    (escapes past the raw-fallback cap): records match the restatement, decodes are exact."""
+    d, f, tiles = 256, 512, 2
+    rng = np.random.default_rng(11)
+    one = np.full((f, d), 0x3F80, dtype=np.uint16)                       # every weight 1.0
+    two = np.where(rng.random((f, d)) < 0.5, 0x3F80, 0x4000).astype(np.uint16)  # 1.0 / 2.0
+    w2_one = np.full((d, f), 0xBF80, dtype=np.uint16)                    # -1.0
+    spread = rng.integers(0, 1 << 16, (d, f), dtype=np.uint16)           # all exponents: raw fallback
+    ref_mod, code, _ = FORMATS[store]
+    with P.Engine(P.ModelSpec(1, 3, 2, d)) as raw_eng, P.Engine(P.ModelSpec(1, 3, 2, d)) as eng:
+        raw_eng.experts_alloc(f, tiles)
+        eng.experts_alloc(f, tiles, store_format=store)
+        for e_ in (raw_eng, eng):
+            e_.expert_set(0, 0, one, one, w2_one)
+            e_.expert_set(0, 1, two, one, two.T.copy())
+            e_.expert_set(0, 2, two, one, spread)
+        n = 3 * f * d // tiles
+        for e in range(3):
+            raw = raw_eng.expert_read(0, e)
+            assert np.array_equal(eng.expert_read(0, e), raw)
+            for t in range(tiles):
+                got, meta = _record_bytes(eng, 0, e, t)
+                ref, rmeta = ref_mod.encode(raw[t * n:(t + 1) * n])
+                assert meta["format"] == rmeta["format"]
+                if meta["format"]:
+                    assert got == ref
+        assert eng.expert_tile_record(0, 0, 0)["format"] == code
+        # the device decode path (copy_tiles: staging + decode kernels) on every tile
+        import torch
+        buf = torch.empty(eng.expert_bytes() // 2, dtype=torch.int16, device="cuda")
+        for e in range(3):
+            eng.copy_tiles(0, e, 0, tiles, buf.data_ptr())
+            torch.cuda.synchronize()
+            assert np.array_equal(buf.cpu().numpy().view(np.uint16), raw_eng.expert_read(0, e))

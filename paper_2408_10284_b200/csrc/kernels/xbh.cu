@@ -217,6 +217,15 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const std::uint16_t* src
         }
     }
     if (nacc) atomicOr(&words[w], static_cast<unsigned>(acc >> 32));
+    if (v1 == n) {  // the last code may run into a final chunk where no code starts: its gap points at
+                    // the end of the codes (a decode walk from there takes nothing); a block opening
+                    // there holds no values (base n)
+        const std::uint64_t cl = (pos + kXbhChunkBits - 1) / kXbhChunkBits - 1;
+        if (prev / kXbhChunkBits != cl) {
+            atomicOr(&gaps[cl >> 3], static_cast<unsigned>(pos - cl * kXbhChunkBits) << (4 * (cl & 7)));
+            if (cl % kXbhBlockChunks == 0) bases[cl / kXbhBlockChunks] = static_cast<std::uint32_t>(n);
+        }
+    }
 }
 
 __global__ void __launch_bounds__(kThreads) lo_kernel(const uint4* src, std::uint64_t n16, uint4* lo) {

@@ -13,9 +13,11 @@
 //   hdr             2 u64: total code bits, escapes                                  at hdr_off = mlut_off + 16 KB
 //   bits [words]    u32 : the codes, MSB first, back to back (+8 zero words)         at bits_off = hdr_off + 16
 //   gaps [chunks]   4 bit: per 128-bit chunk of `bits`, the offset of the first code starting in it
-//                         (<= 11: a code is <= 12 bits), 8 per u32, low nibble first  at gap_off
+//                         (<= 11: a code is <= 12 bits; a final chunk that only holds the end of the
+//                         last code points at the end of the codes), 8 per u32, low nibble first
+//                                                                                   at gap_off
 //   base [blocks+1] u32 : per block of 256 chunks, the index of the value whose code starts first in
-//                         it; [blocks] = n                                            at base_off
+//                         it (n for a final block without one); [blocks] = n          at base_off
 //   exc  [m]        u64 : (index << 16) | bf16 bits of each escaped value, index ascending   at exc_off
 // Symbols: exponent base + s for s < 15 (the tile's best 15-exponent window, as XB12), s = 15 =
 // escape (the value's bits are patched from `exc`).  Code lengths are length-limited Huffman

@@ -203,3 +203,28 @@ def test_degenerate_exponent_tiles(store):
             eng.copy_tiles(0, e, 0, tiles, buf.data_ptr())
             torch.cuda.synchronize()
             assert np.array_equal(buf.cpu().numpy().view(np.uint16), raw_eng.expert_read(0, e))
+
+
+def test_xbh_last_code_straddles_into_a_new_block():
+    """The sweep's seed-90427 failure mode, pinned: a tile whose last code runs into a final chunk
+    that opens a new decode block without a code start (gap -> end of codes, block base n)."""
+    import torch
+    from test_xbh_cpu import straddle_tile
+    d, f = 256, 160
+    n = 3 * f * d
+    w, total = straddle_tile(n=n)
+    # invert the tile-major packing (one tile): rows (W1 r, W3 r) for r < f, then W2^T rows
+    w1 = np.stack([w[r * 2 * d: r * 2 * d + d] for r in range(f)])
+    w3 = np.stack([w[r * 2 * d + d: (r + 1) * 2 * d] for r in range(f)])
+    w2 = np.ascontiguousarray(w[2 * f * d:].reshape(f, d).T)
+    with P.Engine(P.ModelSpec(1, 2, 2, d)) as eng:
+        eng.experts_alloc(f, 1, store_format="xbh")
+        eng.expert_set(0, 1, w1, w3, w2)
+        assert np.array_equal(eng.expert_read(0, 1), w)
+        got, meta = _record_bytes(eng, 0, 1, 0)
+        ref, rmeta = XH.encode(w)
+        assert meta["format"] == 2 and got == ref
+        buf = torch.empty(n, dtype=torch.int16, device="cuda")
+        eng.copy_tiles(0, 1, 0, 1, buf.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(buf.cpu().numpy().view(np.uint16), w)

@@ -159,3 +159,25 @@ def test_cpu_baseline_xbh_equals_bf16(lib, D, F, T):
                                 wts, 2, D, F, T, xp, out_x.ctypes.data_as(C.POINTER(C.c_float)), 3)
     assert rc == 0
     assert np.array_equal(out_raw, out_x)
+
+
+def straddle_tile(n=122880, blocks=5, seed=9):
+    """n values (a multiple of 16) whose codes total blocks * 32768 + 1 bits and whose last code runs
+    into a final 128-bit chunk that starts a new decode block and holds no code start: exponent 120
+    (1-bit code) first, then alternating 121 / 119 (2-bit codes)."""
+    total = blocks * X.BLOCK + 1
+    x = total - n  # 2-bit codes
+    na = n - x
+    assert n % 16 == 0 and na > 2 * x // 2
+    rng = np.random.default_rng(seed)
+    ex = np.concatenate([np.full(na, 120), np.tile([121, 119], x // 2 + 1)[:x]]).astype(np.uint16)
+    return ((rng.integers(0, 2, n).astype(np.uint16) << 15) | (ex << 7) |
+            rng.integers(0, 128, n).astype(np.uint16)).astype(np.uint16), total
+
+
+def test_last_code_straddles_into_a_new_block():
+    w, total = straddle_tile()
+    rec, meta = X.encode(w)
+    assert meta["format"] == 2 and meta["total_bits"] == total
+    assert X.chunks(total) - 1 == 5 * 256  # the final chunk opens block 5
+    assert np.array_equal(X.decode(rec, meta, w.size), w)  # decode asserts the block bases too

@@ -162,7 +162,14 @@ def encode(bits: np.ndarray):
         gw[:part.size] |= part << np.uint32(4 * k)
     idx_first = np.nonzero(first)[0]
     blk_first = (c[first] % 256) == 0
-    bases = np.append(idx_first[blk_first], n).astype(np.uint32)
+    bases = list(idx_first[blk_first])
+    cl = chunks(total) - 1
+    if c[-1] != cl:  # the last code runs into a final chunk where no code starts
+        gaps[cl] = total - cl * CHUNK
+        gw[cl >> 3] |= np.uint32(gaps[cl]) << np.uint32(4 * (cl & 7))
+        if cl % 256 == 0:
+            bases.append(n)
+    bases = np.array(bases + [n], dtype=np.uint32)
     assert bases.size == nb + 1
     bitarr = np.zeros(32 * nw, dtype=np.uint8)
     for j in range(MAX_LEN):

@@ -1,7 +1,8 @@
 """Randomized physical-decode parity sweep (tools/, evidence run): random shapes, capacities,
-look-ahead, batch 1 (K2, tolerance 1e-4) and batched (K3, 2e-2), tile grouping forced on or off;
-the decode's trace must equal the oracle's and every sampled layer output must match the fp64
-oracle SwiGLU within tolerance."""
+look-ahead, batch 1 (K2, tolerance 1e-4) and batched (K3, 2e-2), tile grouping forced on or off,
+expert store bf16 / XB12 / XBH (ADAPMOE_SWEEP_STORE=all, the default, picks one at random per case;
+or a fixed format); the decode's trace must equal the oracle's and every sampled layer output must
+match the fp64 oracle SwiGLU within tolerance."""
 import os
 import sys
 import time
@@ -23,6 +24,9 @@ def run(seed):
     F = 64 * tiles * int(r.integers(1, 4))
     T = int(r.integers(1, 6))
     os.environ["ADAPMOE_TILE_MERGE"] = str(int(r.integers(0, 3)))
+    store = os.environ.get("ADAPMOE_SWEEP_STORE", "all")
+    if store == "all":
+        store = str(r.choice(["bf16", "xb12", "xbh"]))
     ws = [O.generate_trace(L, N, K, D, T, 0.6, 0.2, 5, 100 + b) for b in range(B)]
     tau = O.calibrate_threshold(ws[0], 0.24)
     caps = [int(x) for x in r.integers(0, N + 1, size=L)]
@@ -31,7 +35,7 @@ def run(seed):
     cfg = P.SimConfig(tiles, 2, 1, 8, 1, lookahead, P.PolicyFlags(True, True, True))
     with P.Engine(P.ModelSpec(L, N, K, D)) as eng:
         eng.load_gates(ws[0].gates)
-        eng.experts_init(F, tiles, seed=seed)
+        eng.experts_init(F, tiles, seed=seed, store_format=store)
         eng.decode_begin(caps, ws[0].fisher, tau, cfg, 0, T, batch=B)
         if B == 1:
             hid = np.zeros((T, L, D), dtype=np.float32)
@@ -44,7 +48,7 @@ def run(seed):
             eng.decode_tokens(acts, scores, hid)
         res = eng.decode_end(cfg, T)
     if res.metrics != ref.metrics or not np.array_equal(res.timeline, ref.timeline):
-        return False, "trace"
+        return False, f"trace ({store} store)"
     tol = 1e-4 if B == 1 else 2e-2
     worst = 0.0
     for t in range(T):
@@ -59,14 +63,18 @@ def run(seed):
                     moe += wgt * O.swiglu(O.expert_init(seed, l, e, D, F, tiles), D, F, tiles, x32)
                 got = hid[t, b, l].astype(np.float64) - x32.astype(np.float64)
                 worst = max(worst, np.abs(got - moe).max() / max(np.abs(moe).max(), 1e-30))
-    return worst <= tol, f"worst rel err {worst:.2e} (tol {tol})"
+    return worst <= tol, f"{store} store: worst rel err {worst:.2e} (tol {tol})"
 
 
 def main():
     lo, hi = int(sys.argv[1]), int(sys.argv[2])
     t0, bad = time.time(), []
     for s in range(lo, hi):
-        ok, why = run(s)
+        try:
+            ok, why = run(s)
+        except Exception as e:  # noqa: BLE001  (a device error poisons the process: report the seed, stop)
+            print("ERROR", s, repr(e)[:300], flush=True)
+            raise
         if (s - lo + 1) % 1000 == 0:  # progress: a run cut short by a timeout still counts
             print(f"progress seeds {lo}..{s}: {s - lo + 1 - len(bad)} / {s - lo + 1} pass", flush=True)
         if not ok:

@@ -1,7 +1,8 @@
 """Randomized expert-parallel parity sweep (tools/, evidence run): random shapes / capacities /
 batch, random world size and random placement tables; the G shard sessions (run one after another
 on one GPU) must replay the single-GPU trace bit for bit, move / compute disjoint expert sets, and
-their partial outputs must sum to the single-GPU output (fp32: 1e-5; bf16 batched: 2e-3)."""
+their partial outputs must sum to the single-GPU output (fp32: 1e-5; bf16 batched: 2e-3).  The
+expert store is drawn from bf16 / XB12 / XBH per case (ADAPMOE_SWEEP_STORE fixes it)."""
 import os
 import sys
 import time
@@ -23,6 +24,9 @@ def run(seed):
     F = 64 * tiles * int(r.integers(1, 3))
     T = int(r.integers(1, 5))
     G = int(r.choice([2, 3, 4, 8]))
+    store = os.environ.get("ADAPMOE_SWEEP_STORE", "all")
+    if store == "all":
+        store = str(r.choice(["bf16", "xb12", "xbh"]))
     owners = r.integers(0, G, size=(L, N)).astype(np.int32) if r.integers(0, 2) else None
     ws = [O.generate_trace(L, N, K, D, T, 0.6, 0.2, 5, 100 + b) for b in range(B)]
     tau = O.calibrate_threshold(ws[0], 0.24)
@@ -38,7 +42,7 @@ def run(seed):
     for rank, world in [(0, 1)] + [(g, G) for g in range(G)]:
         with P.Engine(P.ModelSpec(L, N, K, D)) as eng:
             eng.load_gates(ws[0].gates)
-            eng.experts_init(F, tiles, seed=seed)
+            eng.experts_init(F, tiles, seed=seed, store_format=store)
             eng.decode_begin(caps, ws[0].fisher, tau, cfg, 0, T, batch=B, ep_rank=rank, ep_world=world,
                              expert_owner=owners if world > 1 else None)
             h = np.zeros(shape, dtype=np.float32)
@@ -61,7 +65,11 @@ def main():
     lo, hi = int(sys.argv[1]), int(sys.argv[2])
     t0, bad = time.time(), []
     for s in range(lo, hi):
-        ok, why = run(s)
+        try:
+            ok, why = run(s)
+        except Exception as e:  # noqa: BLE001  (a device error poisons the process: report the seed, stop)
+            print("ERROR", s, repr(e)[:300], flush=True)
+            raise
         if (s - lo + 1) % 1000 == 0:  # progress: a run cut short by a timeout still counts
             print(f"progress seeds {lo}..{s}: {s - lo + 1 - len(bad)} / {s - lo + 1} pass", flush=True)
         if not ok:

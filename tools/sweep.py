@@ -26,7 +26,8 @@ def main():
     ap.add_argument("--targets", default="0,0.12,0.24,0.36,0.48")
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--steps", type=int, default=4)
-    ap.add_argument("--out", default="gpurun_out/sweep_r1.jsonl")
+    ap.add_argument("--out", default="gpurun_out/sweep_r2.jsonl")
+    ap.add_argument("--store-format", default="xbh", choices=["bf16", "xb12", "xbh"])
     args = ap.parse_args()
 
     import numpy as np
@@ -42,7 +43,7 @@ def main():
     trace = eng.generate_trace(P.SynthConfig(spec, wl0.tokens, wl0.concentration, wl0.drift, wl0.gate_seed,
                                              wl0.token_seed, False, wl0.fisher_scales, wl0.drift_scales))
     t0 = time.time()
-    eng.experts_init(wl0.ffn, wl0.tiles, seed=1234)
+    eng.experts_init(wl0.ffn, wl0.tiles, seed=1234, store_format=args.store_format)
     store_s = time.time() - t0
     W_, K = args.warmup, args.steps
     n = W_ + K
@@ -77,7 +78,7 @@ def main():
             od = int(((tl[:, 1] == 3) & (tl[:, 7] == 0) & win).sum())
             m = res.metrics
             dd = {k: s1[k] - s0[k] for k in s0}
-            line = {"target_single_ratio": target, "tau": tau, "realized_single_ratio": realized, "budget": budget,
+            line = {"store_format": args.store_format, "target_single_ratio": target, "tau": tau, "realized_single_ratio": realized, "budget": budget,
                     "capacities": [int(c) for c in caps], "dp_expected_loads_per_token": exp_loads,
                     "mean_beta": float(np.mean(beta)), "mean_alpha": float(np.mean(alpha)),
                     "tok_s": K / (ms * 1e-3), "ms_per_token": ms / K,
@@ -97,15 +98,22 @@ def main():
                     "k2_gbs": (dd["ffn_gate_up_bytes"] + dd["ffn_down_bytes"]) / max(1e-9, dd["ffn_ms"] * 1e-3) / 1e9}
             r = bench.run_reference_driver(W.mixtral_8x7b(tokens=64, budget=budget, target_single_ratio=target), n, 1)
             if r is not None:
+                # the whole SimMetrics struct and the event timeline's FNV-1a hash vs the unmodified
+                # reference over the same tokens (as bench.py's parity object)
+                rm = r["metrics"]
+                ours = dict(m)
+                ours["on_demand_loads_per_layer"] = [int(v) for v in res.on_demand_loads_per_layer]
+                ours["latency_per_token"] = [int(v) for v in res.latency_per_token[:n]]
                 line["reference_on_demand"] = r["on_demand_loads"]
-                line["parity"] = r["on_demand_loads"] == m["on_demand_loads"]
+                line["metrics_differ"] = sorted(k for k in rm if rm[k] != ours.get(k))
+                line["parity"] = (not line["metrics_differ"] and r.get("hash_timeline") == bench.fnv1a_i64(res.timeline))
             out.write(json.dumps(line) + "\n")
             out.flush()
             print(json.dumps({k: line[k] for k in ("target_single_ratio", "budget", "tok_s", "on_demand_loads_per_token",
                                                    "prefetch_hit_rate", "link_busy_frac", "prefetch_hidden_frac", "k2_gbs",
                                                    "parity")
                               if k in line}))
-    print(json.dumps({"expert_store_s": store_s}))
+    print(json.dumps({"expert_store_s": store_s, "store_format": args.store_format}))
 
 
 if __name__ == "__main__":

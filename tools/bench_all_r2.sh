@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 bench set on one B200 (XBH store by default): headline, free-running, batched, 8x22B
 # rehearsal, and the bf16 / XB12 stores for the A/B.  Output: gpurun_out/${TAG}_*.jsonl
-TAG=${TAG:-r2h}
+TAG=${TAG:-r2k}
 mkdir -p gpurun_out
 run() { local name=$1; shift; timeout 900 python bench.py "$@" > gpurun_out/${TAG}_$name.jsonl 2> gpurun_out/${TAG}_$name.err; echo "$name rc=$?"; }
 run default

@@ -647,7 +647,7 @@ def ours(args):
     # mean launch size (traffic / algorithmic bytes is a property of the kernel's access pattern)
     traffic, traffic_src = None, None
     try:
-        src = "ncu_r1_traffic.json" if B > 1 else "ncu_r2_traffic.json"
+        src = "ncu_r2_traffic.json"
         prof = json.load(open(os.path.join(ROOT, "profiles", src)))
         keys = ["grouped_kernel<0>", "grouped_kernel<1>"] if B > 1 else ["ffn_ring_kernel<1>"]
         alg = sum(prof[k]["algorithmic_bytes"] for k in keys)

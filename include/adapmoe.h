@@ -459,7 +459,7 @@ int moe_decode_timeline_write(moe_engine_t engine, const char* path, int64_t* n_
 /* Physical counters of the session so far (CUDA-event timed on the engine's streams). */
 typedef struct {
     int64_t tokens;
-    int64_t kernels_launched;     /* our kernels: router, FFN passes, combine */
+    int64_t kernels_launched;     /* our kernels: router, FFN passes, combine, coded-tile decode + patch */
     int64_t ffn_launches;         /* FFN pass launches (gate/up + down) */
     int64_t tile_copies;          /* expert tile copies issued host -> HBM */
     int64_t copy_bytes;           /* expert bytes moved host -> HBM */

@@ -211,9 +211,10 @@ void CopyEngine::harvest_decodes() {
     }
 }
 
-void CopyEngine::decode_totals(double* ms, long long* launches, double* bytes) {
+void CopyEngine::decode_totals(double* ms, long long* launches, double* bytes, long long* kernels) {
     std::lock_guard<std::mutex> g(mu_);
     harvest_decodes();
+    if (kernels) *kernels = dec_kernels_.load();
     if (ms) *ms = dec_ms_;
     if (launches) *launches = dec_launches_;
     if (bytes) *bytes = dec_bytes_;
@@ -360,6 +361,7 @@ void CopyEngine::run() {
             ck(src.meta.format == 2 ? xbh_decode(rec, src.meta, dec, decode_stream_)
                                     : xb12_decode(rec, src.meta, dec, decode_stream_),
                "tile record decode");
+            dec_kernels_ += src.meta.n_exc ? 2 : 1;
             ck(cudaEventRecord(dt.end, decode_stream_), "cudaEventRecord");
             {
                 std::lock_guard<std::mutex> g(mu_);

@@ -101,7 +101,7 @@ public:
     void retire(const std::shared_ptr<CopyJob>& job);  // accumulate timing + recycle events
     // Coded-tile decode kernels so far (CUDA events around each decode on the decode stream):
     // summed duration, launches, and bytes (record read + bf16 tile written).  Waits for none.
-    void decode_totals(double* ms, long long* launches, double* bytes);
+    void decode_totals(double* ms, long long* launches, double* bytes, long long* kernels = nullptr);
     // Physical timeline: from now on every retired tile is appended to `out` with its copy interval
     // relative to `origin` (a timed event recorded on the device); nullptr stops recording.
     // Append the landed, not yet recorded tiles of jobs that have not retired (they still hold slots).
@@ -134,6 +134,7 @@ private:
     std::deque<DecodeTiming> dec_pending_;  // guarded by mu_
     double dec_ms_ = 0.0, dec_bytes_ = 0.0;
     long long dec_launches_ = 0;
+    std::atomic<long long> dec_kernels_{0};  // decode + escape-patch kernel launches
     void harvest_decodes();  // caller holds mu_: fold completed decode timings into the totals
     int staging_next_ = 0;
     std::mutex mu_;

@@ -1263,7 +1263,9 @@ DecodeStats DecodeSession::snapshot() {
     s.tile_copies = copier_->tiles_copied();
     s.copy_bytes = copier_->bytes_copied();
     s.copy_busy_ms = copier_->busy_ms_total(&s.prefetch_copy_ms, &s.prefetch_tiles, &s.prefetch_used_copy_ms);
-    copier_->decode_totals(&s.decode_ms, &s.decode_launches, &s.decode_bytes);
+    long long dec_kernels = 0;
+    copier_->decode_totals(&s.decode_ms, &s.decode_launches, &s.decode_bytes, &dec_kernels);
+    s.kernels += dec_kernels;  // the coded-tile decode and escape-patch kernels count as ours too
     return s;
 }
 

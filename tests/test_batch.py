@@ -83,7 +83,7 @@ def _moe_ref(ws, decisions, t, l, b, ffn, tiles, seed, cache):
     return acc
 
 
-def _run_batch(ws, caps, tau, fg, ffn, tiles, seed, calls):
+def _run_batch(ws, caps, tau, fg, ffn, tiles, seed, calls, store="bf16"):
     import paper_2408_10284_b200 as P
     w0 = ws[0]
     B, T = len(ws), w0.T
@@ -92,7 +92,7 @@ def _run_batch(ws, caps, tau, fg, ffn, tiles, seed, calls):
     cfg = P.SimConfig()
     with P.Engine(P.ModelSpec(w0.L, w0.N, w0.K, w0.D)) as eng:
         eng.load_gates(w0.gates, fg)
-        eng.experts_init(ffn, tiles, seed=seed)
+        eng.experts_init(ffn, tiles, seed=seed, store_format=store)
         eng.decode_begin(caps, w0.fisher, tau, cfg, 0, T, batch=B)
         hid = np.zeros((T, B, w0.L, w0.D), dtype=np.float32)
         for a, b in zip(calls, calls[1:]):
@@ -102,18 +102,20 @@ def _run_batch(ws, caps, tau, fg, ffn, tiles, seed, calls):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("store", ["bf16", "xbh"])
 @pytest.mark.parametrize("merge", ["0", "1", "2"])
 @pytest.mark.parametrize("B,caps", [(4, [3, 2, 2, 1]), (16, [8, 4, 2, 0]), (64, [2, 2, 2, 2])])
-def test_batched_decode_tiny(B, caps, merge, monkeypatch):
+def test_batched_decode_tiny(B, caps, merge, store, monkeypatch):
     """merge: ADAPMOE_TILE_MERGE — on-demand tiles (and the resident experts) grouped into fewer
-    grouped launches off the critical path, or one launch per landed tile."""
+    grouped launches off the critical path, or one launch per landed tile; store: bf16 or the
+    Huffman-coded XBH store (tiles decoded on the copy engine's stream before K3 reads them)."""
     monkeypatch.setenv("ADAPMOE_TILE_MERGE", merge)
     ws = _streams(B, T=8)
     fg = O.train_first_gate(ws[0], steps=50)
     tau = O.calibrate_threshold(ws[0], 0.24)
     ffn, tiles, seed = 1024, 4, 7
     ref = O.simulate_batch(ws, caps, tau, first_gate=fg)
-    r, hid = _run_batch(ws, caps, tau, fg, ffn, tiles, seed, [0, 3, 8])
+    r, hid = _run_batch(ws, caps, tau, fg, ffn, tiles, seed, [0, 3, 8], store=store)
     assert r.metrics == ref.metrics
     assert np.array_equal(r.timeline, ref.timeline)
     assert r.stats["tokens"] == 8 * B

@@ -34,7 +34,7 @@ def _whole_token_outputs(g, w, fg, cfg, ffn, seed, T):
     return hid, r
 
 
-def _per_layer(g, w, fg, cfg, ffn, seed, T, with_scores=True, timeline_path=None):
+def _per_layer(g, w, fg, cfg, ffn, seed, T, with_scores=True, timeline_path=None, store="bf16"):
     """Caller-owned loop: stand-in attention on a side stream writes x_l, then the MoE layer."""
     dev = torch.device("cuda")
     user = torch.cuda.Stream()
@@ -46,7 +46,7 @@ def _per_layer(g, w, fg, cfg, ffn, seed, T, with_scores=True, timeline_path=None
     torch.cuda.synchronize()
     with P.Engine(P.ModelSpec(w.L, w.N, w.K, w.D)) as eng:
         eng.load_gates(w.gates, fg)
-        eng.experts_init(ffn, cfg.tile_count_per_expert, seed=seed)
+        eng.experts_init(ffn, cfg.tile_count_per_expert, seed=seed, store_format=store)
         eng.decode_begin(g["sim_capacities"], w.fisher, g["tau"], cfg, int(g["workload"]["seed"]), T)
         if timeline_path:
             eng.decode_record_timeline(True)
@@ -64,14 +64,17 @@ def _per_layer(g, w, fg, cfg, ffn, seed, T, with_scores=True, timeline_path=None
     return outs.cpu().numpy(), r, n
 
 
+@pytest.mark.parametrize("store", ["bf16", "xbh"])
 @pytest.mark.parametrize("name", ["tiny", "tiny_transfer_heavy", "tiny_budget0"])
-def test_decode_layer_matches_whole_token_and_reference(name):
+def test_decode_layer_matches_whole_token_and_reference(name, store):
+    """Per-layer calls on the caller's stream reproduce the whole-token decode (bf16 store) bit for
+    bit — also over the Huffman-coded store, whose tiles are decoded on the copy engine's stream."""
     g = load_golden(name)
     w, fg = oracle_inputs(g)
     cfg = sim_config(g)
     ffn, seed, T = 224 * cfg.tile_count_per_expert, 6, 16
     ref_hid, ref = _whole_token_outputs(g, w, fg, cfg, ffn, seed, T)
-    hid, r, _ = _per_layer(g, w, fg, cfg, ffn, seed, T)
+    hid, r, _ = _per_layer(g, w, fg, cfg, ffn, seed, T, store=store)
     assert r.metrics == ref.metrics and np.array_equal(r.timeline, ref.timeline)
     assert np.array_equal(hid, ref_hid)
     assert r.stats["router_launches"] == T * w.L  # one K1 launch per layer call

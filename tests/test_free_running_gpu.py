@@ -40,7 +40,7 @@ def rmsnorm_like_gpu(x):
     return np.array([v / rms for v in xs])
 
 
-def run_and_check(batch, tol, caps=None, T=10):
+def run_and_check(batch, tol, caps=None, T=10, store="bf16"):
     """Free-running decode of the tiny case; asserts per-step parity with the oracle; returns
     (result, hidden, decode stats)."""
     g = load_golden("tiny")
@@ -56,7 +56,7 @@ def run_and_check(batch, tol, caps=None, T=10):
     scores = np.ascontiguousarray(np.stack([w.scores[:T] for w in ws], axis=1))
     with P.Engine(P.ModelSpec(L, N, K, D)) as eng:
         eng.load_gates(w0.gates, fg)
-        eng.experts_init(ffn, tiles, seed=seed)
+        eng.experts_init(ffn, tiles, seed=seed, store_format=store)
         eng.decode_begin(caps, w0.fisher, tau, cfg, 0, T, batch=batch, free_running=True, concentration=CONC)
         hid = np.zeros((T, batch, L, D), dtype=np.float32)
         if batch == 1:
@@ -108,9 +108,10 @@ def run_and_check(batch, tol, caps=None, T=10):
     return r, hid, stats
 
 
+@pytest.mark.parametrize("store", ["bf16", "xbh"])
 @pytest.mark.parametrize("batch,tol", [(1, 1e-4), (4, 2e-2)])
-def test_free_running_decode_matches_oracle_per_step(batch, tol):
-    run_and_check(batch, tol)
+def test_free_running_decode_matches_oracle_per_step(batch, tol, store):
+    run_and_check(batch, tol, store=store)
 
 
 @pytest.mark.parametrize("all_resident", [False, True])

@@ -252,20 +252,21 @@ __global__ void __launch_bounds__(kThreads) lo_kernel(const uint4* src, std::uin
 //         are split where the next chunk begins), queueing 4-bit symbols in a 64-bit fifo that
 //         spills 8 at a time into the thread's slot (17-word stride: conflict-free spills);
 //  scan:  the CTA turns code counts into the first block-relative value index of every chunk;
-//  merge: per 16-value group of the block's value range, a binary search over those prefix sums
-//         finds the chunk holding the group's first value, the group's 16 symbols are gathered
-//         from one to three slots with funnel shifts, and symbols (+ the window base = exponent;
-//         escapes are patched afterwards) join the lo bytes into bf16: 16-byte lo loads, 32-byte
-//         stores (element stores for the two partial groups at the range ends, which the
-//         neighbouring blocks share).
+//  compact: each thread ORs its slot's symbols into a zeroed block-wide nibble buffer at its
+//         position (value j at nibble j + (v0 & 15): 16-value groups stay word-aligned);
+//  merge: per 16-value group of the block's value range, 8 bytes of symbols (+ the window base =
+//         exponent; escapes are patched afterwards) join the lo bytes into bf16: 16-byte lo loads,
+//         32-byte stores (element stores for the two partial groups at the range ends, which the
+//         neighbouring blocks share); the merge zeroes the nibble words it read.
 constexpr int kDecThreads = static_cast<int>(kXbhBlockChunks);
 constexpr std::uint64_t kDecBlocksPerCta = 2;
 constexpr int kDecWords = static_cast<int>(kXbhBlockBits / 32);  // 1024
 constexpr int kDecStage = (kDecWords + 8 + (kDecWords + 8) / 32 + 1 + 3) / 4 * 4;  // padded, 16-byte multiple
 constexpr int kDecSlot = static_cast<int>(kXbhChunkBits) / 8 + 1;  // <= 128 codes per chunk, 8 per word, + pad
 constexpr int kDecSlotWords = kDecThreads * kDecSlot + 4;         // + the gather's read-ahead past the last slot
-constexpr size_t kDecSmem = sizeof(std::uint32_t) * (kXbhLut + kDecStage + (kDecThreads + 1) + 2 * (kDecThreads / 32) +
-                                                     kDecSlotWords);
+constexpr int kDecNibWords = (static_cast<int>(kXbhBlockBits) + 32) / 8 + 2;  // the block's symbols, 8 per word
+constexpr size_t kDecSmem = sizeof(std::uint32_t) * (kXbhLut + kDecStage + 2 * (kDecThreads / 32) + kDecSlotWords +
+                                                     kDecNibWords);
 
 __device__ __forceinline__ unsigned padw(unsigned w) { return w + (w >> 5); }
 
@@ -274,9 +275,10 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
     extern __shared__ __align__(16) std::uint32_t sm[];
     std::uint32_t* mlut = sm;
     std::uint32_t* sw = sm + kXbhLut;
-    std::uint32_t* pre = sw + kDecStage;              // [kDecThreads + 1] first value of each chunk (block-relative)
-    std::uint32_t* wsum = pre + kDecThreads + 1;
+    std::uint32_t* wsum = sw + kDecStage;
     std::uint32_t* slots = wsum + 2 * (kDecThreads / 32);  // [thread][kDecSlot] symbol nibbles
+    std::uint32_t* nib = slots + kDecSlotWords;  // compacted: block-relative value j at nibble j + (v0 & 15)
+    for (int i = threadIdx.x; i < kDecNibWords; i += kDecThreads) nib[i] = 0;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const std::uint32_t* words = reinterpret_cast<const std::uint32_t*>(rec + xbh_bits_off(n));
     const std::uint32_t* gaps = reinterpret_cast<const std::uint32_t*>(rec + xbh_gap_off(n, bits));
@@ -310,7 +312,7 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
     const std::uint64_t b_end = std::min<std::uint64_t>(blocks, b + kDecBlocksPerCta);
     if (b < b_end) prefetch(b);
     for (; b < b_end; ++b) {
-        __syncthreads();  // the previous block's merge is done with sw / slots / pre
+        __syncthreads();  // the previous block's merge is done with sw / slots / nib
         {
             const unsigned w = 4u * t;  // 4 words, none crossing a pad (w % 32 <= 28)
             sw[padw(w)] = pw.x, sw[padw(w) + 1] = pw.y, sw[padw(w) + 2] = pw.z, sw[padw(w) + 3] = pw.w;
@@ -357,7 +359,7 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
             spill();
         }
         if (nf) slot[sp] = static_cast<std::uint32_t>(fifo);
-        // scan: pre[t] = first block-relative value of chunk t, pre[256] = the block's value count
+        // scan: this chunk's first block-relative value
         unsigned incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -369,37 +371,30 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
         unsigned before = 0;
 #pragma unroll
         for (int w = 0; w < kDecThreads / 32; ++w) before += w < warp ? wsum[w] : 0u;
-        pre[t] = before + incl - cnt;
-        if (t == kDecThreads - 1) pre[kDecThreads] = before + incl;
+        // compact: this chunk's cnt symbols to nibbles [o, o + cnt) of the block buffer (words shared with
+        // the neighbouring chunks: atomicOr into the zeroed buffer)
+        {
+            const unsigned o = before + incl - cnt + static_cast<unsigned>(v0 & 15);
+            const unsigned sh = 4 * (o & 7);
+            std::uint32_t* d = nib + (o >> 3);
+            for (unsigned w = 0; 8 * w < cnt; ++w) {
+                const unsigned rest = cnt - 8 * w;  // symbols left, the slot's stale tail masked off
+                const std::uint32_t x = rest >= 8 ? slot[w] : slot[w] & ((1u << (4 * rest)) - 1u);
+                atomicOr(d + w, x << sh);
+                if (sh) atomicOr(d + w + 1, x >> (32 - sh));
+            }
+        }
         __syncthreads();
         // merge
-        const unsigned total = static_cast<unsigned>(v1 - v0);
         const std::uint64_t gs = v0 >> 4, ge = (v1 + 15) >> 4;  // 16-value groups touching [v0, v1)
         if (b + 1 < b_end) prefetch(b + 1);
         for (std::uint64_t g = gs + t; g < ge; g += kDecThreads) {
             const uint4 l = __ldg(lo + g);
-            // the group's symbols: block-relative values j0 .. j0 + 15 (j0 < 0 in the first group)
-            const int j0 = static_cast<int>(g * 16 - v0);
-            unsigned have = j0 < 0 ? static_cast<unsigned>(-j0) : 0u;  // leading values of another block
-            unsigned j = j0 < 0 ? 0u : static_cast<unsigned>(j0);
-            unsigned long long sy = 0;
-            // chunk holding value j: the last c with pre[c] <= j (pre[] ascending, pre[0] = 0)
-            unsigned ch = 0;
-#pragma unroll
-            for (unsigned step = kDecThreads / 2; step; step >>= 1)
-                if (pre[ch + step] <= j) ch += step;
-            while (have < 16 && j < total) {
-                while (pre[ch + 1] <= j) ++ch;  // skip chunks without codes
-                const unsigned off = j - pre[ch], take = min(pre[ch + 1] - j, 16u - have);
-                const std::uint32_t* sl = slots + ch * kDecSlot + (off >> 3);
-                const unsigned sh = 4 * (off & 7);
-                const unsigned x0 = __funnelshift_r(sl[0], sl[1], sh), x1 = __funnelshift_r(sl[1], sl[2], sh);
-                unsigned long long v = (static_cast<unsigned long long>(x1) << 32) | x0;
-                if (take < 16) v &= (1ull << (4 * take)) - 1ull;
-                sy |= v << (4 * have);
-                have += take;
-                j += take;
-            }
+            // the group's 16 symbols (values of other blocks at the range ends are masked on store)
+            const uint2 sy2 = *reinterpret_cast<const uint2*>(nib + 2 * (g - gs));
+            nib[2 * (g - gs)] = 0;  // zeroed for the next block
+            nib[2 * (g - gs) + 1] = 0;
+            const unsigned long long sy = (static_cast<unsigned long long>(sy2.y) << 32) | sy2.x;
             const unsigned sx = static_cast<unsigned>(sy), sz = static_cast<unsigned>(sy >> 32);
             const unsigned ew[4] = {  // nibbles -> bytes + window base: symbols 4q .. 4q+3
                 __vadd4(__byte_perm(sx & 0x0f0f0f0fu, (sx >> 4) & 0x0f0f0f0fu, 0x5140), base4),

@@ -43,10 +43,14 @@ CopyEngine::~CopyEngine() {
     left.swap(active_);  // retire() edits active_
     for (auto& j : left) retire(j);
     for (cudaEvent_t e : inflight_) cudaEventDestroy(e);
+    if (decode_stream_) cudaStreamSynchronize(decode_stream_);
+    for (const DecodeTiming& d : dec_pending_) {  // decode timings never harvested
+        cudaEventDestroy(d.start);
+        cudaEventDestroy(d.end);
+    }
     for (cudaEvent_t e : free_sync_) cudaEventDestroy(e);
     for (cudaEvent_t e : free_timing_) cudaEventDestroy(e);
     if (decode_stream_) {
-        cudaStreamSynchronize(decode_stream_);
         for (int k = 0; k < kStaging; ++k) {
             cudaFree(staging_[k]);
             cudaEventDestroy(staging_landed_[k]);

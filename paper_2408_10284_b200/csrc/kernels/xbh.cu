@@ -329,8 +329,9 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
             static_cast<unsigned>(t) * static_cast<unsigned>(kXbhChunkBits) + ((pg >> (4 * (c & 7))) & 15u);
         const std::uint64_t v0 = __ldg(bases + b), v1 = __ldg(bases + b + 1);
         __syncthreads();
-        // walk: symbols into the slot
-        unsigned cnt = 0, nf = 0, sp = 0;
+        // walk: symbols into the slot (two lookups per spill check while both surely start inside
+        // the chunk; a lookup adds <= 3 symbols, so the fifo holds <= 13 before a spill)
+        unsigned nf = 0, sp = 0;
         unsigned long long fifo = 0;
         auto spill = [&]() {
             if (nf >= 8) {
@@ -339,13 +340,19 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
                 nf -= 8;
             }
         };
-        while (pos + kXbhMaxLen <= stop) {  // every code of the lookup starts inside the chunk
+        auto take_all = [&]() {
             const unsigned e = mlut[peek(pos)];
-            const unsigned k = (e >> 24) & 3u;
             fifo |= static_cast<unsigned long long>(e & 0xfffu) << (4 * nf);  // unused symbol nibbles are zero
-            nf += k;
-            cnt += k;
+            nf += (e >> 24) & 3u;
             pos += e >> 26;
+        };
+        while (pos + 2 * kXbhMaxLen <= stop) {
+            take_all();
+            take_all();
+            spill();
+        }
+        while (pos + kXbhMaxLen <= stop) {  // every code of the lookup starts inside the chunk
+            take_all();
             spill();
         }
         while (pos < stop) {  // the chunk's last codes: stop where the next chunk's first code starts
@@ -354,10 +361,10 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
             const unsigned k = 1u + (n3 > 1u && pos + l0 < stop) + (n3 > 2u && pos + l0 + l1 < stop);
             fifo |= static_cast<unsigned long long>(e & ((1u << (4 * k)) - 1u)) << (4 * nf);
             nf += k;
-            cnt += k;
             pos += k == n3 ? e >> 26 : (k == 1u ? l0 : l0 + l1);
             spill();
         }
+        const unsigned cnt = 8 * sp + nf;
         if (nf) slot[sp] = static_cast<std::uint32_t>(fifo);
         // scan: this chunk's first block-relative value
         unsigned incl = cnt;

@@ -93,20 +93,20 @@ void xbh_build_code(const std::uint32_t* hist, XbhCode& c) {
             sym_lut[k] = static_cast<std::uint16_t>(s | (c.len[s] << 8));
         }
     }
-    // multi-code table: follow the peek through up to 3 codes that end inside its 12 bits; entry =
-    // symbols (4 bits each) | lengths (4 bits each) << 12 | count << 24 | total length << 26.  A
-    // peek without a code (length 0) never occurs in a stream and ends the walk.
+    // multi-code table: follow the peek through up to 5 codes that end inside its 12 bits; entry =
+    // symbols (4 bits each, bits 0-19) | count << 20 | first code's length << 23 | total length
+    // << 27.  A peek without a code (length 0) never occurs in a stream and ends the walk.
     for (unsigned i = 0; i < static_cast<unsigned>(kXbhLut); ++i) {
-        unsigned len = 0, syms = 0, lens = 0, cnt = 0;
-        for (int k = 0; k < 3 && len < static_cast<unsigned>(kXbhMaxLen); ++k) {
+        unsigned len = 0, syms = 0, first_len = 0, cnt = 0;
+        for (int k = 0; k < kXbhMultiCodes && len < static_cast<unsigned>(kXbhMaxLen); ++k) {
             const unsigned e = sym_lut[(i << len) & (kXbhLut - 1)], l = e >> 8;
             if (l == 0 || len + l > static_cast<unsigned>(kXbhMaxLen)) break;
             syms |= (e & 15u) << (4 * k);
-            lens |= l << (4 * k);
+            if (k == 0) first_len = l;
             ++cnt;
             len += l;
         }
-        c.mlut[i] = syms | (lens << 12) | (cnt << 24) | (len << 26);
+        c.mlut[i] = syms | (cnt << 20) | (first_len << 23) | (len << 27);
     }
 }
 
@@ -247,9 +247,9 @@ __global__ void __launch_bounds__(kThreads) lo_kernel(const uint4* src, std::uin
 //  stage: the block's 1024 code words (+8 look-ahead) into shared memory (one pad word per 32: the
 //         lanes' chunks are 4 words apart) — prefetched into registers during the previous block's
 //         merge — and the gap of each thread's chunk;
-//  walk:  each thread walks its chunk once from its gap with the multi-code table (~3 codes per
-//         12-bit lookup; a lookup whose codes all start inside the chunk is taken whole, the last few
-//         are split where the next chunk begins), queueing 4-bit symbols in a 64-bit fifo that
+//  walk:  each thread walks its chunk once from its gap with the multi-code table (up to 5, ~4 codes
+//         per 12-bit lookup while the lookup's codes all start inside the chunk, then one code per
+//         lookup until the next chunk's first code), queueing 4-bit symbols in a 64-bit fifo that
 //         spills 8 at a time into the thread's slot (17-word stride: conflict-free spills);
 //  scan:  the CTA turns code counts into the first block-relative value index of every chunk;
 //  compact: each thread ORs its slot's symbols into a zeroed block-wide nibble buffer at its
@@ -329,8 +329,7 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
             static_cast<unsigned>(t) * static_cast<unsigned>(kXbhChunkBits) + ((pg >> (4 * (c & 7))) & 15u);
         const std::uint64_t v0 = __ldg(bases + b), v1 = __ldg(bases + b + 1);
         __syncthreads();
-        // walk: symbols into the slot (two lookups per spill check while both surely start inside
-        // the chunk; a lookup adds <= 3 symbols, so the fifo holds <= 13 before a spill)
+        // walk: symbols into the slot (a lookup adds <= 5 symbols: the fifo holds <= 12 before a spill)
         unsigned nf = 0, sp = 0;
         unsigned long long fifo = 0;
         auto spill = [&]() {
@@ -340,28 +339,21 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const std::uint8_t*
                 nf -= 8;
             }
         };
-        auto take_all = [&]() {
+        auto take_all = [&]() {  // every code of the lookup (<= 5) starts inside the chunk
             const unsigned e = mlut[peek(pos)];
-            fifo |= static_cast<unsigned long long>(e & 0xfffu) << (4 * nf);  // unused symbol nibbles are zero
-            nf += (e >> 24) & 3u;
-            pos += e >> 26;
+            fifo |= static_cast<unsigned long long>(e & 0xfffffu) << (4 * nf);  // unused symbol nibbles are zero
+            nf += (e >> 20) & 7u;
+            pos += e >> 27;
         };
-        while (pos + 2 * kXbhMaxLen <= stop) {
-            take_all();
-            take_all();
-            spill();
-        }
-        while (pos + kXbhMaxLen <= stop) {  // every code of the lookup starts inside the chunk
+        while (pos + kXbhMaxLen <= stop) {
             take_all();
             spill();
         }
-        while (pos < stop) {  // the chunk's last codes: stop where the next chunk's first code starts
+        while (pos < stop) {  // the chunk's last codes, one per lookup: stop where the next chunk's first code starts
             const unsigned e = mlut[peek(pos)];
-            const unsigned n3 = (e >> 24) & 3u, l0 = (e >> 12) & 15u, l1 = (e >> 16) & 15u;
-            const unsigned k = 1u + (n3 > 1u && pos + l0 < stop) + (n3 > 2u && pos + l0 + l1 < stop);
-            fifo |= static_cast<unsigned long long>(e & ((1u << (4 * k)) - 1u)) << (4 * nf);
-            nf += k;
-            pos += k == n3 ? e >> 26 : (k == 1u ? l0 : l0 + l1);
+            fifo |= static_cast<unsigned long long>(e & 15u) << (4 * nf);
+            nf += 1;
+            pos += (e >> 23) & 15u;
             spill();
         }
         const unsigned cnt = 8 * sp + nf;

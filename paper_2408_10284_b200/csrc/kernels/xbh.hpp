@@ -7,9 +7,9 @@
 // many), so XBH codes them with a per-tile canonical Huffman code.  Record of a tile of n values:
 //   lo   [n]        u8  : sign << 7 | mantissa(7)                                   at 0
 //   lut  [4096]     u16 : single-code table of the 12-bit peek: exponent | length << 8   at lut_off = align(n)
-//   mlut [4096]     u32 : multi-code table: up to 3 consecutive codes inside the peek — symbols
-//                         (4 bits each, bits 0-11), their lengths (4 bits each, 12-23), count
-//                         (24-25), total length (26-29)                              at mlut_off = lut_off + 8 KB
+//   mlut [4096]     u32 : multi-code table: up to 5 consecutive codes inside the peek — symbols
+//                         (4 bits each, bits 0-19), count (20-22), the first code's length (23-26),
+//                         total length (27-30)                                      at mlut_off = lut_off + 8 KB
 //   hdr             2 u64: total code bits, escapes                                  at hdr_off = mlut_off + 16 KB
 //   bits [words]    u32 : the codes, MSB first, back to back (+8 zero words)         at bits_off = hdr_off + 16
 //   gaps [chunks]   4 bit: per 128-bit chunk of `bits`, the offset of the first code starting in it
@@ -40,6 +40,7 @@ namespace adapmoe {
 
 constexpr int kXbhMaxLen = 12;        // longest code: the decode tables have 2^12 entries
 constexpr int kXbhLut = 1 << kXbhMaxLen;
+constexpr int kXbhMultiCodes = 5;     // codes per multi-code table entry
 constexpr std::uint64_t kXbhChunkBits = 128;  // unit of independent decoding
 constexpr std::uint64_t kXbhBlockChunks = 256;  // chunks per output-base entry (one decode CTA pass)
 constexpr std::uint64_t kXbhBlockBits = kXbhChunkBits * kXbhBlockChunks;

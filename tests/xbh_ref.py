@@ -6,6 +6,7 @@ per-block value bases, escapes ascending) and decodes records."""
 import numpy as np
 
 MAX_LEN = 12
+MULTI = 5             # codes per multi-code table entry
 CHUNK = 128           # bits per independently decodable chunk
 BLOCK = 256 * CHUNK   # bits per output-base entry
 
@@ -108,12 +109,12 @@ def build_code(hist):
         if ln[s]:
             sh = MAX_LEN - ln[s]
             sym_lut[code[s] << sh:(code[s] + 1) << sh] = s | (ln[s] << 8)
-    # multi-code table: up to 3 consecutive codes ending inside the 12-bit peek: symbols (4 bits
-    # each) | lengths (4 bits each) << 12 | count << 24 | total length << 26
+    # multi-code table: up to 5 consecutive codes ending inside the 12-bit peek: symbols (4 bits
+    # each) | count << 20 | first length << 23 | total length << 27
     mlut = np.zeros(1 << MAX_LEN, dtype=np.uint32)
     for i in range(1 << MAX_LEN):
-        L = syms = lens = cnt = 0
-        for k in range(3):
+        L = syms = first = cnt = 0
+        for k in range(MULTI):
             if L >= MAX_LEN:
                 break
             e = int(sym_lut[(i << L) & ((1 << MAX_LEN) - 1)])
@@ -121,10 +122,11 @@ def build_code(hist):
             if l2 == 0 or L + l2 > MAX_LEN:
                 break
             syms |= (e & 15) << (4 * k)
-            lens |= l2 << (4 * k)
+            if k == 0:
+                first = l2
             cnt += 1
             L += l2
-        mlut[i] = syms | (lens << 12) | (cnt << 24) | (L << 26)
+        mlut[i] = syms | (cnt << 20) | (first << 23) | (L << 27)
     return base, ln, code, lut, mlut
 
 
@@ -219,9 +221,9 @@ def decode(rec: bytes, meta: dict, n: int) -> np.ndarray:
         p = pos[ids]
         peek = (bitarr[p[:, None] + np.arange(MAX_LEN)[None, :]].astype(np.int64) * weights).sum(axis=1)
         e = mlut[peek]
-        cnt, l0, l1 = (e >> 24) & 3, (e >> 12) & 15, (e >> 16) & 15
-        k = 1 + ((cnt > 1) & (p + l0 < stop[ids])) + ((cnt > 2) & (p + l0 + l1 < stop[ids]))
-        adv = np.where(k == cnt, e >> 26, np.where(k == 1, l0, l0 + l1))
+        whole = p + MAX_LEN <= stop[ids]  # every code of the entry starts inside the chunk
+        k = np.where(whole, (e >> 20) & 7, 1)
+        adv = np.where(whole, e >> 27, (e >> 23) & 15)
         for j, i in enumerate(ids):
             for q in range(int(k[j])):
                 out_syms[i].append((int(e[j]) >> (4 * q)) & 15)

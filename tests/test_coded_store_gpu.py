@@ -228,3 +228,20 @@ def test_xbh_last_code_straddles_into_a_new_block():
         eng.copy_tiles(0, 1, 0, 1, buf.data_ptr())
         torch.cuda.synchronize()
         assert np.array_equal(buf.cpu().numpy().view(np.uint16), w)
+
+
+def test_xbh_largest_tiles_8x22b_single_tile():
+    """Mixtral-8x22B expert shape as ONE tile (d 6144, ffn 16384: 302 M values, ~3.3 G code bits —
+    near the format's u32 bit-offset limit; ~24k decode blocks): store, host and device decodes exact."""
+    import torch
+    d, f, tiles = 6144, 16384, 1
+    with P.Engine(P.ModelSpec(1, 2, 2, d)) as eng:
+        eng.experts_init(f, tiles, seed=21, store_format="xbh")
+        r = eng.expert_tile_record(0, 1, 0)
+        assert r["format"] == 2 and r["bytes"] < 0.67 * 3 * f * d * 2
+        ref = O.expert_init(21, 0, 1, d, f, tiles)
+        assert np.array_equal(eng.expert_read(0, 1), ref)
+        buf = torch.empty(ref.size, dtype=torch.int16, device="cuda")
+        eng.copy_tiles(0, 1, 0, 1, buf.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(buf.cpu().numpy().view(np.uint16), ref)

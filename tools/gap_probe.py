@@ -1,5 +1,7 @@
+"""Per-layer gap probe (tools/, not product): one 8x7B decode with ADAPMOE_GAP_TRACE-style timing of
+K1 / host step / FFN / combine per layer (profiling the free-running round trip)."""
 import os, sys, time
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2408_10284_b200 as P
 from paper_2408_10284_b200 import workloads as W

@@ -1,5 +1,7 @@
+"""generate_trace timing + cProfile (tools/, not product) at the 8x7B 64-token workload."""
+import os
 import sys, time
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2408_10284_b200 as P
 from paper_2408_10284_b200 import workloads as W

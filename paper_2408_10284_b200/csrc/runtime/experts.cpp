@@ -80,10 +80,10 @@ void prefer_node(void* p, size_t bytes, int node) {
 }  // namespace
 
 ExpertStore::~ExpertStore() {
-    for (unsigned char* b : blocks) {
-        if (!b) continue;
-        cudaHostUnregister(b);
-        std::free(b);
+    for (size_t i = 0; i < blocks.size(); ++i) {
+        if (!blocks[i]) continue;
+        if (i < pinned.size() && pinned[i]) cudaHostUnregister(blocks[i]);
+        std::free(blocks[i]);
     }
 }
 
@@ -269,6 +269,32 @@ void recount_link_bytes(ExpertStore& st) {
     for (const Xb12Tile& m : st.tile_meta) st.link_bytes += m.format != 0 ? m.bytes : st.tile_bytes;
 }
 
+// Pin every block of a coded store over its records only (host threads, after the encoder wrote them
+// into the unpinned blocks; the pages past the records were never touched).
+void pin_coded_blocks(ExpertStore& st) {
+    const size_t page = 2u << 20;
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    std::vector<std::string> errors(hw);
+    for (unsigned w = 0; w < hw; ++w)
+        pool.emplace_back([&, w] {
+            for (size_t b = w; b < st.blocks.size(); b += hw) {
+                const size_t k = b * st.tiles + st.tiles - 1;  // the last record ends the block's content
+                const size_t used = st.tile_off[k] + (st.tile_meta[k].format ? st.tile_meta[k].bytes : st.tile_bytes);
+                const size_t keep = std::min(st.expert_bytes, (used + page - 1) / page * page);
+                const cudaError_t e = cudaHostRegister(st.blocks[b], keep, cudaHostRegisterDefault);
+                if (e != cudaSuccess) {
+                    errors[w] = std::string("cudaHostRegister: ") + cudaGetErrorString(e);
+                    return;
+                }
+                st.pinned[b] = keep;
+            }
+        });
+    for (auto& t : pool) t.join();
+    for (auto& e : errors)
+        if (!e.empty()) fail(Status::Device, "experts_init: " + e);
+}
+
 }  // namespace
 
 void upload_expert_tiles(const ExpertStore& st, int layer, int expert, int t0, int t1, unsigned char* dst,
@@ -343,8 +369,12 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
     for (int i = 0; i < n_held; ++i)
         if (first_id[st.index[held[i]]] < 0) first_id[st.index[held[i]]] = held[i];
     st.blocks.assign(stored, nullptr);
+    st.pinned.assign(stored, 0);
     st.numa_node = gpu_numa_node(eng.device());
 
+    // a coded store built from the synthetic init is encoded straight into unpinned blocks (D2H through
+    // pageable memory, touching only the records' pages) and pinned afterwards, records only
+    const bool defer_pin = format != kStoreBf16 && init_values;
     // allocate + first-touch + pin in parallel: page faulting and locking dominate at 90+ GB
     auto t0 = std::chrono::steady_clock::now();
     const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
@@ -360,14 +390,17 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
                 }
                 madvise(p, st.expert_bytes, MADV_HUGEPAGE);
                 prefer_node(p, st.expert_bytes, st.numa_node);  // before first touch
+                st.blocks[i] = static_cast<unsigned char*>(p);
+                if (defer_pin) continue;  // coded synthetic store: pinned after encoding, records only
                 std::memset(p, 0, st.expert_bytes);
                 cudaError_t e = cudaHostRegister(p, st.expert_bytes, cudaHostRegisterDefault);
                 if (e != cudaSuccess) {
+                    st.blocks[i] = nullptr;
                     std::free(p);
                     errors[w] = std::string("cudaHostRegister: ") + cudaGetErrorString(e);
                     return;
                 }
-                st.blocks[i] = static_cast<unsigned char*>(p);
+                st.pinned[i] = st.expert_bytes;
             }
         });
     for (auto& t : pool) t.join();
@@ -399,6 +432,7 @@ void build_expert_store(Engine& eng, ExpertStore& st, int ffn, int tiles, std::u
         }
         cudaStreamDestroy(s);
         recount_link_bytes(st);
+        pin_coded_blocks(st);
         st.fill_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
         return;
     }
@@ -435,6 +469,12 @@ void set_expert_weights(Engine& eng, ExpertStore& st, int layer, int expert, con
     if (!st.has(layer, expert)) fail(Status::Usage, "expert_set: this store (an expert-parallel shard) does not hold the expert");
     const size_t D = st.d, F = st.ffn, Ft = F / st.tiles;
     const int b = st.stored_index(layer, expert);
+    if (st.pinned[b] < st.expert_bytes) {  // a coded block pinned over its records only: pin all of it
+        if (st.pinned[b]) MOE_CUDA(cudaHostUnregister(st.blocks[b]));
+        st.pinned[b] = 0;
+        MOE_CUDA(cudaHostRegister(st.blocks[b], st.expert_bytes, cudaHostRegisterDefault));
+        st.pinned[b] = st.expert_bytes;
+    }
     std::vector<std::uint16_t> packed;  // coded stores: pack here, then encode into the block
     if (st.format != kStoreBf16) packed.resize(st.expert_bytes / 2);
     std::uint16_t* dst = st.format != kStoreBf16 ? packed.data() : reinterpret_cast<std::uint16_t*>(st.blocks[b]);

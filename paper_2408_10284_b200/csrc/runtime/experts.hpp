@@ -23,6 +23,7 @@ struct ExpertStore {
     size_t expert_bytes = 0;  // 3 * F * d * 2
     size_t tile_bytes = 0;    // expert_bytes / tiles
     std::vector<unsigned char*> blocks;  // registered host memory, one per stored expert
+    std::vector<size_t> pinned;          // [block] bytes registered (expert_bytes, or a coded block's records)
     // [L*N] block of each (layer, expert); -1 = not held by this store (an expert-parallel shard
     // pins only the experts it owns)
     std::vector<int> index;
@@ -46,7 +47,11 @@ struct ExpertStore {
     bool has(int layer, int expert) const { return index[static_cast<size_t>(layer) * experts + expert] >= 0; }
     int stored_index(int layer, int expert) const;  // fails (Usage) for an expert the store does not hold
     const unsigned char* expert(int layer, int expert) const { return blocks[stored_index(layer, expert)]; }
-    size_t pinned_bytes() const { return blocks.size() * expert_bytes; }
+    size_t pinned_bytes() const {
+        size_t b = 0;
+        for (size_t p : pinned) b += p;
+        return b;
+    }
     ~ExpertStore();
 };
 

@@ -245,3 +245,36 @@ def test_xbh_largest_tiles_8x22b_single_tile():
         eng.copy_tiles(0, 1, 0, 1, buf.data_ptr())
         torch.cuda.synchronize()
         assert np.array_equal(buf.cpu().numpy().view(np.uint16), ref)
+
+
+def test_coded_store_pins_only_its_records():
+    """A synthetic coded store is encoded into unpinned blocks and pinned over its records only: pinned
+    bytes ~ the records (XBH ~0.67 of bf16); reads, copies and a later expert_set (which pins the
+    whole block) still work."""
+    import torch
+    d, f, tiles = 4096, 14336, 4
+    with P.Engine(P.ModelSpec(1, 4, 2, d)) as eng:
+        eng.experts_init(f, tiles, seed=8, store_format="xbh")
+        info = eng.experts_info()
+        raw_bytes = 4 * 3 * f * d * 2
+        assert info["pinned_bytes"] < 0.69 * raw_bytes, info
+        ref = O.expert_init(8, 0, 2, d, f, tiles)
+        assert np.array_equal(eng.expert_read(0, 2), ref)
+        buf = torch.empty(ref.size, dtype=torch.int16, device="cuda")
+        eng.copy_tiles(0, 2, 0, tiles, buf.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(buf.cpu().numpy().view(np.uint16), ref)
+        # overwrite one expert with real-layout weights: the block is pinned whole again
+        rng = np.random.default_rng(3)
+        w1 = X_bf16(rng.standard_normal((f, d)) * 0.02)
+        w3 = X_bf16(rng.standard_normal((f, d)) * 0.02)
+        w2 = X_bf16(rng.standard_normal((d, f)) * 0.02)
+        eng.expert_set(0, 1, w1, w3, w2)
+        assert eng.experts_info()["pinned_bytes"] > info["pinned_bytes"]
+        got = eng.expert_read(0, 1)
+        n = 3 * f * d // tiles
+        assert np.array_equal(got[:d], w1[0]) and np.array_equal(got[d:2 * d], w3[0])
+        eng.copy_tiles(0, 1, 0, tiles, buf.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(buf.cpu().numpy().view(np.uint16), got)
+        assert n % 16 == 0

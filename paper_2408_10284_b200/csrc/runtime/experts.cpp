@@ -154,6 +154,9 @@ void encode_block(ExpertStore& st, int b, const std::uint16_t* d_raw, Xb12Scratc
             m.format = 1;
             xb12_layout(m);
             const unsigned char* r = x.rec.as<unsigned char>() + region * t;
+            // the alignment padding after the escapes is zero (a record is a pure function of the tile,
+            // whatever the block held before)
+            std::memset(dst + m.exc_off, 0, m.bytes - m.exc_off);
             MOE_CUDA(cudaMemcpyAsync(dst, r, m.exc_off, cudaMemcpyDeviceToHost, s));
             exc.resize(m.n_exc);
             if (m.n_exc) {

@@ -454,14 +454,16 @@ def ours(args):
     try:
         avail = int(open("/proc/meminfo").read().split("MemAvailable:")[1].split()[0]) * 1024
         per_rank = int(0.85 * avail / max(1, int(os.environ.get("LOCAL_WORLD_SIZE", ws))))
-        if per_rank < held * expert_bytes:
-            alias = max(1, per_rank // expert_bytes)
+        # a coded store pins its records only (~0.67 / 0.75 of the bf16 bytes for XBH / XB12)
+        held_bytes = {"bf16": 1.0, "xb12": 0.76, "xbh": 0.68}[args.store_format] * expert_bytes
+        if per_rank < held * held_bytes:
+            alias = max(1, int(per_rank // held_bytes))
     except Exception:  # noqa: BLE001
         pass
     if args.host_alias is not None:
         alias = args.host_alias
     elif alias and ep_world > 1:
-        raise SystemExit(f"rank {rank}: the expert-parallel shard needs {held * expert_bytes / 1e9:.0f} GB of pinned "
+        raise SystemExit(f"rank {rank}: the expert-parallel shard needs {held * held_bytes / 1e9:.0f} GB of pinned "
                          f"host memory, {per_rank / 1e9:.0f} GB available per rank (pass --host-alias to alias blocks)")
     link_peak = h2d_peak_gbs(local)
     t0 = time.time()
